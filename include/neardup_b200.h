@@ -1,0 +1,170 @@
+/* neardup_b200 -- C-ABI of the B200-native MinHash-LSH dedup hot path.
+ *
+ * The reference (neardup, /root/reference/proj) has no FFI: its boundary is the
+ * C++ library API in include/neardup/*.hpp called by src/pipeline.cpp.  Each
+ * entry point below replaces one of those calls (cited as file:line under
+ * /root/reference/proj); include/neardup_b200.hpp re-exposes them with the
+ * reference's C++ names and types.  Plain pointers and sizes only; no
+ * allocation crosses the ABI except through the documented two-phase
+ * fetch calls.  Status codes mirror the reference's exception taxonomy
+ * (util.hpp:13-26 -> tools/main.cpp:18-21 exit codes) plus a device code.
+ */
+#ifndef NEARDUP_B200_H
+#define NEARDUP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+#define ND_OK 0
+#define ND_ERR_INTERNAL 1   /* unexpected failure (bug) */
+#define ND_ERR_CONFIG 2     /* ConfigError        util.hpp:13 */
+#define ND_ERR_IO 3         /* IoError            util.hpp:18 */
+#define ND_ERR_PREREQ 4     /* PrerequisiteError  util.hpp:23 */
+#define ND_ERR_DEVICE 5     /* CUDA / NCCL failure (new) */
+#define ND_ERR_SHORT 6      /* ShortDocumentError minhash.hpp:63 */
+
+/* HashFunctionParams (minhash.hpp:17-25), byte-identical layout (24 bytes). */
+typedef struct nd_hash_fn {
+  uint32_t modulus;      /* prime p in [2^21, 2^23) */
+  uint32_t base;         /* prime q in (256, 2^16) */
+  uint32_t base_inverse; /* q^-1 mod p */
+  uint32_t base_power;   /* q^(L-1) mod p */
+  uint64_t reduce_factor;/* floor(2^64 / p) */
+} nd_hash_fn;
+
+/* Artifact-shaping run parameters (RunConfig, pipeline.hpp:21-36). */
+typedef struct nd_params {
+  uint32_t hash_count;      /* H = bands * rows */
+  uint32_t bands;           /* b */
+  uint32_t rows;            /* r */
+  uint32_t shingle_len;     /* L */
+  uint32_t unit;            /* 0 = byte (ShingleUnit::kByte); 1 = codepoint (unsupported) */
+  uint32_t bucket_count;    /* K; 0 = choose_bucket_count(n, bucket_scale) */
+  uint64_t threshold_num;   /* SimilarityThreshold (compare.hpp:28-37) */
+  uint64_t threshold_den;
+  uint64_t scale_num;       /* bucket_scale Ratio (lsh.hpp:18) */
+  uint64_t scale_den;
+  uint64_t seed;            /* family seed (pipeline.hpp:35) */
+} nd_params;
+
+typedef struct nd_ctx nd_ctx;
+
+/* ---- host-only helpers (no device needed) -------------------------------- */
+const char* nd_version(void);
+/* last error message of the calling thread (ctx-free calls) */
+const char* nd_last_error_global(void);
+/* derive_family (minhash.hpp:42, minhash.cpp:71-105); out holds H entries */
+int nd_derive_family(uint64_t seed, uint32_t hash_count, uint32_t shingle_len, uint32_t unit,
+                     nd_hash_fn* out);
+/* choose_bucket_count (lsh.hpp:33, lsh.cpp:26-40) */
+int nd_choose_bucket_count(uint64_t doc_count, uint64_t scale_num, uint64_t scale_den,
+                           uint32_t* bucket_count_out);
+/* SimilarityThreshold::min_matches (compare.hpp:35, compare.cpp:17-22) */
+uint32_t nd_min_matches(uint32_t hash_count, uint64_t num, uint64_t den);
+/* band_partition (lsh.hpp:53, lsh.cpp:62-72): ranges[2*w], ranges[2*w+1] */
+int nd_band_partition(uint32_t bands, uint32_t workers, uint32_t* ranges);
+/* cell owner map for G shards: owner(cell) = floor(cell * G / (bands*K)); the
+ * generalisation of band_partition to cell ranges. first_cell has
+ * G+1 entries. */
+int nd_cell_partition(uint32_t bands, uint32_t bucket_count, uint32_t shards,
+                      uint64_t* first_cell);
+
+/* Seeded synthetic corpus in the reference generator's shape
+ * (synthetic.cpp:39-110).  mode 0 reproduces generate_synthetic bit for bit
+ * (single thread); mode 1 is the multi-threaded streaming variant for large
+ * corpora (same alphabet, length law, groups, edit law; different RNG
+ * stream).  len_law 0 = uniform [len_min, len_max]; 1 = lognormal with
+ * median len_min, sigma_milli/1000, clipped to [200, len_max].
+ * Two-phase: call with bytes == NULL to learn nbytes, then again to fill. */
+typedef struct nd_synth_spec {
+  uint64_t doc_count, group_count;
+  uint32_t group_size_min, group_size_max;
+  uint64_t edit_num, edit_den;
+  uint32_t len_min, len_max;
+  uint64_t seed;
+  uint32_t mode, len_law, sigma_milli, threads;
+} nd_synth_spec;
+int nd_synth_generate(const nd_synth_spec* spec, uint8_t* bytes, uint64_t* offsets,
+                      uint64_t* nbytes_out);
+
+/* ---- device context ----------------------------------------------------- */
+int nd_ctx_create(int device, nd_ctx** out);
+void nd_ctx_destroy(nd_ctx* ctx);
+const char* nd_last_error(const nd_ctx* ctx);
+/* stream all device work of this ctx is ordered on (cudaStream_t; NULL = own) */
+int nd_ctx_set_stream(nd_ctx* ctx, void* cuda_stream);
+/* Uploads the family (derive_family's output) for signature kernels. */
+int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t hash_count,
+                     uint32_t shingle_len, uint32_t unit);
+
+/* signature_of_document over a packed batch + band_bucket_ids
+ * (minhash.hpp:71-78, lsh.hpp:38-40; caller pipeline.cpp:214-218).
+ * bytes[offsets[i] .. offsets[i+1]) is document i (NFC UTF-8, byte units).
+ * sig_out: n*H u32 row-major; band_out: n*bands u32 (NULL to skip), ids mod K
+ * (K == 0 -> raw u32 band row sums, K-independent).  Every document must
+ * yield a full window (else ND_ERR_SHORT, nothing written).
+ * Host pointers; copies in and out are pipelined inside; synchronous. */
+int nd_signatures(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                  uint32_t bands, uint32_t rows, uint32_t bucket_count, uint32_t* sig_out,
+                  uint32_t* band_out);
+/* Same on device pointers, asynchronous on the ctx stream. */
+int nd_signatures_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offsets,
+                         uint64_t n, uint32_t bands, uint32_t rows, uint32_t bucket_count,
+                         uint32_t* d_sig, uint32_t* d_band);
+
+/* compare_pass (compare.hpp:52, compare.cpp:69-86) over cells given as CSR
+ * row lists into a host signature matrix sigs[nrows*H]; rows inside a cell
+ * ascend.  Result: sorted distinct (lo, hi) row pairs with match counts,
+ * fetched with nd_pairs_fetch. */
+int nd_compare_cells(nd_ctx* ctx, const uint32_t* sigs, uint64_t nrows, uint32_t hash_count,
+                     const uint64_t* cell_offsets, const uint32_t* cell_rows, uint64_t ncells,
+                     uint64_t threshold_num, uint64_t threshold_den, uint64_t* npairs_out);
+int nd_pairs_fetch(nd_ctx* ctx, uint32_t* lo, uint32_t* hi, uint32_t* match_count);
+
+/* union_pairs + components (dedup_graph.hpp:34-43) over row-index pairs;
+ * groups fetched with nd_groups_fetch. */
+int nd_union(nd_ctx* ctx, const uint32_t* lo, const uint32_t* hi, uint64_t npairs,
+             uint32_t nnodes, uint64_t* nmembers_out, uint64_t* ngroups_out);
+/* members in output order (groups by representative, members ascending);
+ * group_start[ngroups+1] offsets into members. */
+int nd_groups_fetch(nd_ctx* ctx, uint32_t* members, uint64_t* group_start);
+
+/* In-memory run_dedup (pipeline.hpp:100, pipeline.cpp:510-532): signatures
+ * -> band keys -> cell grouping -> compare -> distinct pairs -> components.
+ * doc_ids (NULL = 0..n-1) must ascend.  Stats then fetch. */
+typedef struct nd_dedup_stats {
+  uint64_t documents;        /* total_surviving */
+  uint32_t bucket_count;     /* K used */
+  uint64_t nonsingleton_cells;
+  uint64_t candidate_pairs;  /* sum n(n-1)/2 over cells (pipeline.cpp:406-411) */
+  uint64_t emitted_pairs;    /* accepted before cross-band dedup */
+  uint64_t distinct_pairs;
+  uint64_t duplicate_groups;
+  uint64_t near_duplicates;
+  uint64_t removals;
+  double seconds[6];         /* device time: sig, cells, compare, pairs, cc, d2h */
+} nd_dedup_stats;
+int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const uint64_t* doc_ids,
+             uint64_t n, const nd_params* params, nd_dedup_stats* stats);
+/* Same with the packed batch already in device memory. */
+int nd_dedup_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offsets,
+                    const uint64_t* doc_ids, uint64_t n, const nd_params* params,
+                    nd_dedup_stats* stats);
+/* distinct pairs (doc ids, sorted by (lo, hi)) of the last dedup */
+int nd_dedup_fetch_pairs(nd_ctx* ctx, uint64_t* lo, uint64_t* hi, uint32_t* match_count);
+/* groups of the last dedup as doc ids: members in output order,
+ * group_start[ngroups+1]; representative = members[group_start[g]] */
+int nd_dedup_fetch_groups(nd_ctx* ctx, uint64_t* members, uint64_t* group_start);
+/* Reference-identical report bytes (groups.jsonl, removal.txt, summary.json
+ * as written by pipeline.cpp:479-506) for the last dedup, into dir. */
+int nd_dedup_write_report(nd_ctx* ctx, const char* dir, uint64_t total_records);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEARDUP_B200_H */

@@ -1,0 +1,35 @@
+// Host-only internals (compiled by g++/nvcc host pass; no CUDA types).
+#pragma once
+
+#include <cstdint>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "neardup_b200.h"
+
+namespace ndb {
+
+// Exceptions mapped to ND_ERR_* at the C-ABI boundary (nd_capi.cu).
+struct NdError : std::runtime_error {
+  int code;
+  NdError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw NdError(code, msg); }
+
+uint64_t bounded_random(std::mt19937_64& rng, uint64_t bound);
+std::vector<nd_hash_fn> derive_family(uint64_t seed, uint32_t H, uint32_t L, uint32_t unit);
+uint32_t choose_bucket_count(uint64_t n, uint64_t num, uint64_t den);
+uint32_t min_matches(uint32_t H, uint64_t num, uint64_t den);
+
+// synthetic corpus (host_synth.cpp)
+void synth_generate(const nd_synth_spec& spec, uint8_t* bytes, uint64_t* offsets,
+                    uint64_t* nbytes_out);
+
+// report writers (host_report.cpp): groups as doc ids in output order
+void write_report(const std::string& dir, const std::vector<uint64_t>& members,
+                  const std::vector<uint64_t>& group_start, uint64_t total_documents,
+                  uint64_t total_records, uint64_t distinct_pairs);
+
+}  // namespace ndb

@@ -1,0 +1,319 @@
+// C-ABI of neardup_b200 (include/neardup_b200.h): context, family upload,
+// signature entry points (host-pipelined and device-resident), and the
+// exception -> status mapping (reference taxonomy util.hpp:13-26).
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "nd_capi_impl.cuh"
+
+namespace {
+thread_local std::string g_error;
+}
+
+namespace ndb {
+
+int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+int guarded_impl(nd_ctx* ctx, const std::function<void()>& fn) {
+  try {
+    if (ctx) ND_CUDA(cudaSetDevice(ctx->device));
+    fn();
+    return ND_OK;
+  } catch (const NdError& e) {
+    (ctx ? ctx->err : g_error) = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    (ctx ? ctx->err : g_error) = std::string("host allocation failed: ") + e.what();
+    return ND_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    (ctx ? ctx->err : g_error) = e.what();
+    return ND_ERR_INTERNAL;
+  }
+}
+
+}  // namespace ndb
+
+using ndb::fail;
+
+nd_ctx::~nd_ctx() {
+  for (auto* b : {&fam_buf, &sig_in_text, &sig_in_off}) b->release();
+  for (int i = 0; i < 2; ++i) {
+    slot[i].text.release();
+    slot[i].off.release();
+    slot[i].sig.release();
+    slot[i].band.release();
+    slot[i].scratch.release();
+    if (slot[i].h2d_done) cudaEventDestroy(slot[i].h2d_done);
+    if (slot[i].comp_done) cudaEventDestroy(slot[i].comp_done);
+    if (slot[i].d2h_done) cudaEventDestroy(slot[i].d2h_done);
+    if (slot[i].comp) cudaStreamDestroy(slot[i].comp);
+  }
+  pinned_off.release();
+  sig_scratch.release();
+  dedup.release();
+  if (h2d) cudaStreamDestroy(h2d);
+  if (d2h) cudaStreamDestroy(d2h);
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+void nd_ctx::ensure_streams() {
+  if (h2d) return;
+  ND_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+  ND_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    ND_CUDA(cudaStreamCreateWithFlags(&slot[i].comp, cudaStreamNonBlocking));
+    ND_CUDA(cudaEventCreateWithFlags(&slot[i].h2d_done, cudaEventDisableTiming));
+    ND_CUDA(cudaEventCreateWithFlags(&slot[i].comp_done, cudaEventDisableTiming));
+    ND_CUDA(cudaEventCreateWithFlags(&slot[i].d2h_done, cudaEventDisableTiming));
+  }
+}
+
+void nd_ctx::require_family() const {
+  if (!fam.q) fail(ND_ERR_PREREQ, "no hash family uploaded (call nd_family_upload first)");
+}
+
+namespace ndb {
+
+// Host-pipelined signatures: chunks of documents are copied in (h2d stream),
+// signed on alternating compute streams, and copied out (d2h stream), so the
+// PCIe transfers of chunk c+1 / c-1 overlap the kernel of chunk c (the
+// paper's double buffering; reference slab queue
+// pipeline.cpp:121-169).
+void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                     uint32_t bands, uint32_t rows, uint32_t K, uint32_t* sig_out,
+                     uint32_t* band_out) {
+  ctx->require_family();
+  const uint32_t H = ctx->fam.H;
+  const uint32_t L = ctx->fam.L;
+  if (n == 0) return;
+  if (band_out && (bands == 0 || rows == 0 || static_cast<uint64_t>(bands) * rows != H))
+    fail(ND_ERR_CONFIG, "signature has " + std::to_string(H) + " values, banding needs " +
+                            std::to_string(bands) + "*" + std::to_string(rows));
+  for (uint64_t i = 0; i < n; ++i) {
+    if (offsets[i + 1] < offsets[i]) fail(ND_ERR_CONFIG, "offsets must be non-decreasing");
+    if (offsets[i + 1] - offsets[i] < L)
+      fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has " +
+                             std::to_string(offsets[i + 1] - offsets[i]) + " units, needs " +
+                             std::to_string(L));
+  }
+  ctx->ensure_streams();
+  cudaEvent_t start;
+  ND_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  ND_CUDA(cudaEventRecord(start, ctx->stream));
+  ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
+
+  // chunking: <= kChunkBytes of text and <= kChunkDocs documents per chunk
+  constexpr uint64_t kChunkBytes = 256ull << 20;
+  constexpr uint64_t kChunkDocs = 1ull << 20;
+  std::vector<std::pair<uint64_t, uint64_t>> chunks;
+  for (uint64_t d0 = 0; d0 < n;) {
+    uint64_t d1 = d0 + 1;
+    while (d1 < n && d1 - d0 < kChunkDocs && offsets[d1 + 1] - offsets[d0] <= kChunkBytes) ++d1;
+    chunks.push_back({d0, d1});
+    d0 = d1;
+  }
+  uint64_t max_docs = 0, max_bytes = 0;
+  for (auto [a, b] : chunks) {
+    max_docs = std::max(max_docs, b - a);
+    max_bytes = std::max(max_bytes, offsets[b] - offsets[a]);
+  }
+  uint64_t* hoff = static_cast<uint64_t*>(ctx->pinned_off.get(2 * (max_docs + 1) * sizeof(uint64_t)));
+  bool first_use[2] = {true, true};
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    auto& sl = ctx->slot[c & 1];
+    const uint64_t d0 = chunks[c].first, d1 = chunks[c].second, m = d1 - d0;
+    const uint64_t tb = offsets[d1] - offsets[d0];
+    uint8_t* dtext = sl.text.as<uint8_t>(max_bytes + 16);
+    uint64_t* doff = sl.off.as<uint64_t>(max_docs + 1);
+    uint32_t* dsig = sl.sig.as<uint32_t>(max_docs * H);
+    uint32_t* dband = band_out ? sl.band.as<uint32_t>(max_docs * bands) : nullptr;
+    uint64_t* ho = hoff + (c & 1) * (max_docs + 1);
+    // the slot is free once its previous chunk's results left the device
+    if (!first_use[c & 1]) {
+      ND_CUDA(cudaEventSynchronize(sl.d2h_done));  // host offsets buffer reuse
+      ND_CUDA(cudaStreamWaitEvent(ctx->h2d, sl.d2h_done, 0));
+    }
+    first_use[c & 1] = false;
+    for (uint64_t i = 0; i <= m; ++i) ho[i] = offsets[d0 + i] - offsets[d0];
+    ND_CUDA(cudaMemcpyAsync(dtext, bytes + offsets[d0], tb, cudaMemcpyHostToDevice, ctx->h2d));
+    ND_CUDA(cudaMemcpyAsync(doff, ho, (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->h2d));
+    ND_CUDA(cudaEventRecord(sl.h2d_done, ctx->h2d));
+    ND_CUDA(cudaStreamWaitEvent(sl.comp, sl.h2d_done, 0));
+    launch_signatures(ctx->fam, dtext, doff, m, bands, rows, K, dsig, dband, sl.scratch,
+                      sl.comp, /*check_short=*/false, ho);
+    ND_CUDA(cudaEventRecord(sl.comp_done, sl.comp));
+    ND_CUDA(cudaStreamWaitEvent(ctx->d2h, sl.comp_done, 0));
+    ND_CUDA(cudaMemcpyAsync(sig_out + d0 * H, dsig, m * H * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, ctx->d2h));
+    if (band_out)
+      ND_CUDA(cudaMemcpyAsync(band_out + d0 * bands, dband, m * bands * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, ctx->d2h));
+    ND_CUDA(cudaEventRecord(sl.d2h_done, ctx->d2h));
+  }
+  cudaEvent_t end;
+  ND_CUDA(cudaEventCreateWithFlags(&end, cudaEventDisableTiming));
+  ND_CUDA(cudaEventRecord(end, ctx->d2h));
+  ND_CUDA(cudaStreamWaitEvent(ctx->stream, end, 0));
+  ND_CUDA(cudaStreamSynchronize(ctx->d2h));
+  cudaEventDestroy(start);
+  cudaEventDestroy(end);
+}
+
+}  // namespace ndb
+
+using namespace ndb;
+
+extern "C" {
+
+const char* nd_version(void) { return "neardup_b200 0.1 (sm_100a)"; }
+const char* nd_last_error_global(void) { return g_error.c_str(); }
+
+int nd_derive_family(uint64_t seed, uint32_t H, uint32_t L, uint32_t unit, nd_hash_fn* out) {
+  return guarded_impl(nullptr, [&] {
+    if (!out) fail(ND_ERR_CONFIG, "null output");
+    std::vector<nd_hash_fn> fam = derive_family(seed, H, L, unit);
+    std::memcpy(out, fam.data(), fam.size() * sizeof(nd_hash_fn));
+  });
+}
+
+int nd_choose_bucket_count(uint64_t n, uint64_t num, uint64_t den, uint32_t* out) {
+  return guarded_impl(nullptr, [&] { *out = choose_bucket_count(n, num, den); });
+}
+
+uint32_t nd_min_matches(uint32_t H, uint64_t num, uint64_t den) { return min_matches(H, num, den); }
+
+int nd_band_partition(uint32_t bands, uint32_t workers, uint32_t* ranges) {
+  return guarded_impl(nullptr, [&] {
+    if (workers == 0) fail(ND_ERR_CONFIG, "worker count must be positive");
+    uint32_t cursor = 0;
+    for (uint32_t w = 0; w < workers; ++w) {
+      uint32_t len = bands / workers + (w < bands % workers ? 1 : 0);
+      ranges[2 * w] = cursor;
+      ranges[2 * w + 1] = cursor + len;
+      cursor += len;
+    }
+  });
+}
+
+int nd_cell_partition(uint32_t bands, uint32_t K, uint32_t shards, uint64_t* first_cell) {
+  return guarded_impl(nullptr, [&] {
+    if (shards == 0) fail(ND_ERR_CONFIG, "shard count must be positive");
+    uint64_t cells = static_cast<uint64_t>(bands) * K;
+    for (uint32_t g = 0; g <= shards; ++g)
+      first_cell[g] = static_cast<uint64_t>((static_cast<unsigned __int128>(cells) * g + shards - 1) / shards);
+  });
+}
+
+int nd_synth_generate(const nd_synth_spec* spec, uint8_t* bytes, uint64_t* offsets,
+                      uint64_t* nbytes_out) {
+  return guarded_impl(nullptr, [&] { synth_generate(*spec, bytes, offsets, nbytes_out); });
+}
+
+int nd_ctx_create(int device, nd_ctx** out) {
+  return guarded_impl(nullptr, [&] {
+    int count = 0;
+    ND_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) fail(ND_ERR_DEVICE, "no such CUDA device");
+    ND_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    ND_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) fail(ND_ERR_DEVICE, "neardup_b200 requires an sm_100 (Blackwell) device");
+    auto* ctx = new nd_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete ctx;
+      fail(ND_ERR_DEVICE, cudaGetErrorString(e));
+    }
+    ctx->own_stream = true;
+    *out = ctx;
+  });
+}
+
+void nd_ctx_destroy(nd_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  delete ctx;
+}
+
+const char* nd_last_error(const nd_ctx* ctx) { return ctx ? ctx->err.c_str() : g_error.c_str(); }
+
+int nd_ctx_set_stream(nd_ctx* ctx, void* stream) {
+  return guarded_impl(ctx, [&] {
+    if (ctx->own_stream && ctx->stream) {
+      ND_CUDA(cudaStreamSynchronize(ctx->stream));
+      ND_CUDA(cudaStreamDestroy(ctx->stream));
+    }
+    if (stream) {
+      ctx->stream = static_cast<cudaStream_t>(stream);
+      ctx->own_stream = false;
+    } else {
+      ND_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      ctx->own_stream = true;
+    }
+  });
+}
+
+int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L, uint32_t unit) {
+  return guarded_impl(ctx, [&] {
+    if (H == 0 || L == 0) fail(ND_ERR_CONFIG, "hash count and shingle length must be positive");
+    if (unit != 0)
+      fail(ND_ERR_CONFIG, "codepoint shingle units are not supported on the GPU path yet");
+    if (L > 64) fail(ND_ERR_CONFIG, "shingle length above 64 is not supported on the GPU path");
+    uint32_t Hp = 32;
+    while (Hp < H) Hp *= 2;
+    if (Hp > 512) fail(ND_ERR_CONFIG, "hash count above 512 is not supported on the GPU path");
+    std::vector<uint32_t> host(4 * Hp);
+    for (uint32_t i = 0; i < Hp; ++i) {
+      const nd_hash_fn& f = fns[i < H ? i : 0];  // pad with copies of fn 0 (never stored)
+      uint64_t p = f.modulus;
+      if (p < 257 || p >= (1u << 23) || f.base == 0 || f.base >= (1u << 16))
+        fail(ND_ERR_CONFIG, "hash function outside the GPU arithmetic domain (p < 2^23, q < 2^16)");
+      uint64_t qL = static_cast<uint64_t>(f.base_power) * f.base % p;  // q^L = q^(L-1) * q
+      host[i] = f.base;
+      host[Hp + i] = static_cast<uint32_t>((p - qL) % p);
+      host[2 * Hp + i] = static_cast<uint32_t>((1ull << 40) / p);
+      host[3 * Hp + i] = static_cast<uint32_t>(0u - static_cast<uint32_t>(p));
+    }
+    uint32_t* d = ctx->fam_buf.as<uint32_t>(4 * Hp);
+    ND_CUDA(cudaMemcpy(d, host.data(), host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    ctx->fam.q = d;
+    ctx->fam.qln = d + Hp;
+    ctx->fam.m = d + 2 * Hp;
+    ctx->fam.negp = d + 3 * Hp;
+    ctx->fam.H = H;
+    ctx->fam.Hp = Hp;
+    ctx->fam.L = L;
+    ctx->family_host.assign(fns, fns + H);
+  });
+}
+
+int nd_signatures(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                  uint32_t bands, uint32_t rows, uint32_t K, uint32_t* sig_out,
+                  uint32_t* band_out) {
+  return guarded_impl(ctx, [&] {
+    signatures_host(ctx, bytes, offsets, n, bands, rows, K, sig_out, band_out);
+  });
+}
+
+int nd_signatures_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offsets,
+                         uint64_t n, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
+                         uint32_t* d_band) {
+  return guarded_impl(ctx, [&] {
+    ctx->require_family();
+    if (d_band && (bands == 0 || rows == 0 || static_cast<uint64_t>(bands) * rows != ctx->fam.H))
+      fail(ND_ERR_CONFIG, "banding shape does not match the hash count");
+    launch_signatures(ctx->fam, d_bytes, d_offsets, n, bands, rows, K, d_sig, d_band,
+                      ctx->sig_scratch, ctx->stream, /*check_short=*/true, nullptr);
+  });
+}
+
+}  // extern "C"
