@@ -5,46 +5,66 @@
 //
 // Arithmetic.  For hash function (p, q) the window value is
 //   h_w = sum_{i<L} c_{w+i} q^i mod p          (hash_window_direct, minhash.cpp:111-119)
-// Any exact evaluation gives the same bits, and the signature is the min over
-// windows, so we walk each work item BACKWARD with the Horner-shift recurrence
-//   h_w = c_w + q*h_{w+1} - c_{w+L} q^L  (mod p)
-// instead of the reference's forward Eq.5 update (minhash.cpp:121-131).  Per
-// (window, function) it costs 8 single-issue integer instructions, split
-// 4 fma-pipe / 4 alu-pipe:
-//   A  = c_out*QLn + c_in            IMAD        QLn = (p - q^L mod p) mod p
-//   u  = q*s + A          (64-bit)   IMAD.WIDE   u < 2^39 + 2^31
-//   t  = u >> 8           (32-bit)   SHF
-//   k  = hi32(t * M)                 IMAD.HI     M = floor(2^40 / p): k in {Q-1, Q}
-//   r  = lo32(u) - k*p               IMAD        r in [0, 2p)
-//   r' = min(r, r - p)  (unsigned)   IADD+IMNMX  canonical residue = next state s
-//   sig = min(sig, r')               IMNMX
+// Any exact evaluation gives the same bits and the signature is the min over
+// windows, so each work item is walked BACKWARD with the Horner-shift
+// recurrence (instead of the reference's forward Eq.5 update, minhash.cpp:121-131)
+//   u   = q*c_{w+1} + c_out*QLn + c_in,   QLn = (p - q^L mod p) mod p
+//   c_w = u mod p                          (u < 2^39 + 2^31)
 // The window state starts at 0 one position past the item's last character
 // and is warmed up over L-1 partial windows (c_out = 0 beyond the item), so no
 // separate direct evaluation of the first window is needed.
 //
-// Layout.  Lane l of the warp owns functions [l*F, l*F+F) of the padded
-// family (Hp = 32*F, pad functions are copies of function 0 and never
-// stored).  The item's characters are staged per warp in shared memory in
-// chunks of kChunk windows and read back as broadcast LDS.U8 (2 per window,
-// amortised over F functions).  Long documents are split into items of at
-// most kSeg windows; their per-item minima meet through atomicMin and their
-// band keys are computed by a follow-up pass.
+// Reduction, "fq" variant (default).  ncu on the all-integer variant showed the
+// FMA-heavy pipe (the only one that executes IMAD / IMAD.WIDE / IMAD.HI) at 90%
+// while ALU sat at 42% and FMA-lite idle.  The quotient k = floor(u/p) is
+// therefore ESTIMATED in FP32 on the FMA-lite pipe and only three plain 32-bit
+// IMADs remain on FMA-heavy (10 instructions per hash-window, 3/3/4 over
+// heavy/lite/alu):
+//   SB = c | 0x4B000000                 LOP3        float(SB) = 2^23 + c exactly
+//   t1 = fma(c_out, QLn/p, -2^23 q/p + 2^-5)   FFMA
+//   R  = fma(float(SB), q/p, t1)        FFMA        R in [u/p + 0.015, u/p + 0.048]
+//   Kb = bits(R + (2^23 - 0.5), round-down)   FADD.RM   Kb = 0x4B000000 + floor(R - 1/2)
+//   r  = q*c + (c_out*QLn + c_in) - Kb*p + 0x4B000000*p  (3 IMAD + IADD, mod 2^32)
+//   c' = min(r, r - p) (unsigned)       VIADDMNMX   r in [0, 2p) -> canonical
+//   sig = min(sig, c')                  VIMNMX
+// floor(R - 1/2) is Q or Q-1 (Q = floor(u/p)) because the FP32 error of R is
+// < 0.017 (derivation in DESIGN.md), so r = u - k*p lies in [0, 2p).
+// The "int" variant (ND_K1_KERNEL=int) keeps the all-integer Barrett
+// reduction (IMAD.WIDE + SHF + IMAD.HI) for comparison.
+//
+// Layout.  A warp owns one work item.  Its 32 lanes form Z groups of 32/Z
+// lanes; lane l of a group owns functions [l*F, l*F+F) of the padded family
+// (Hp = 32*F/Z; pad functions are copies of function 0 and never stored), and
+// group z walks the z-th of Z equal slices of the item's windows (the min
+// over a partition of windows is the min of the partial minima, so the
+// slices meet through a warp shuffle).  Characters are staged per group in
+// shared memory as (byte, float) pairs and read back as broadcast LDS.
+// Documents longer than kSeg windows are split into several work items that
+// meet through atomicMin; their band keys come from a follow-up pass.
+#include <cstdlib>
+#include <string>
+
 #include "nd_internal.cuh"
 
 namespace ndb {
 namespace {
 
-constexpr int kWarps = 8;           // warps per block
-constexpr int kChunk = 512;         // windows staged per chunk
+constexpr int kWarps = 4;           // warps per block
 constexpr int kLMax = 64;           // max shingle length
-constexpr int kBuf = kChunk + kLMax;
+// positions staged per chunk and group: (char, float) pairs, 8 B each
+__host__ __device__ constexpr int chunk_for(int Z) { return Z >= 4 ? 128 : 256; }
 constexpr uint32_t kSeg = 8192;     // max windows per work item
+constexpr uint32_t kMagicBits = 0x4B000000u;  // bits of 2^23f
 
 struct FamPtrs {
   const uint32_t* q;
   const uint32_t* qln;
   const uint32_t* m;
   const uint32_t* negp;
+  const uint32_t* c3;     // 0x4B000000 * p mod 2^32
+  const float* qp;        // fl(q / p)
+  const float* qlnp;      // fl(QLn / p)
+  const float* c1e;       // -2^23 * qp + 2^-5 (exact)
 };
 
 // ---------------------------------------------------------------------------
@@ -61,7 +81,7 @@ __global__ void k_plan(const uint64_t* __restrict__ offsets, uint64_t n, uint32_
     uint64_t nwin = len - L + 1;
     uint64_t s = (nwin + kSeg - 1) / kSeg;
     nseg = static_cast<uint32_t>(s);
-    if (s > 1) atomicAdd(&flags[1], 1u);  // multi-segment document count
+    if (s > 1) atomicAdd(&flags[1], 1u);  // multi-item document count
   }
   seg_count[d] = nseg;
 }
@@ -85,7 +105,7 @@ __global__ void k_fill_multi(const uint32_t* __restrict__ multi_docs, uint32_t n
   }
 }
 
-// band keys from finished signature rows (multi-segment documents)
+// band keys from finished signature rows (multi-item documents)
 __global__ void k_bands_from_rows(const uint32_t* __restrict__ docs, uint32_t ndocs,
                                   const uint32_t* __restrict__ sig, uint32_t H, uint32_t bands,
                                   uint32_t rows, uint32_t K, uint32_t* __restrict__ band) {
@@ -100,38 +120,99 @@ __global__ void k_bands_from_rows(const uint32_t* __restrict__ docs, uint32_t nd
 }
 
 // ---------------------------------------------------------------------------
-// one rolling step for all F functions of this lane
-template <int F, bool kMin>
-__device__ __forceinline__ void step(uint32_t cin, uint32_t cout, const uint32_t (&q)[F],
-                                     const uint32_t (&qln)[F], const uint32_t (&m)[F],
-                                     const uint32_t (&negp)[F], uint32_t (&s)[F],
-                                     uint32_t (&mn)[F]) {
-#pragma unroll
-  for (int f = 0; f < F; ++f) {
-    uint32_t a = cout * qln[f] + cin;
-    uint64_t u = static_cast<uint64_t>(q[f]) * s[f] + a;
-    uint32_t lo = static_cast<uint32_t>(u);
-    uint32_t t = __funnelshift_r(lo, static_cast<uint32_t>(u >> 32), 8);
-    uint32_t k = __umulhi(t, m[f]);
-    uint32_t r = lo + k * negp[f];
-    uint32_t r2 = r + negp[f];
-    uint32_t c = min(r, r2);
-    s[f] = c;
-    if (kMin) mn[f] = min(mn[f], c);
-  }
-}
+enum class Arith { kInt, kFq };
+
+template <Arith A, int F>
+struct Consts;
 
 template <int F>
+struct Consts<Arith::kInt, F> {
+  uint32_t q[F], qln[F], m[F], negp[F];
+  __device__ void load(const FamPtrs& fp, int base) {
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      q[f] = fp.q[base + f];
+      qln[f] = fp.qln[base + f];
+      m[f] = fp.m[base + f];
+      negp[f] = fp.negp[base + f];
+    }
+  }
+  // one rolling step for all F functions: all-integer Barrett reduction
+  template <bool kMin>
+  __device__ __forceinline__ void step(uint32_t cin, uint32_t cout, float /*cout_f*/,
+                                       uint32_t (&s)[F], uint32_t (&mn)[F]) const {
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      uint32_t a = cout * qln[f] + cin;
+      uint64_t u = static_cast<uint64_t>(q[f]) * s[f] + a;
+      uint32_t lo = static_cast<uint32_t>(u);
+      uint32_t t = __funnelshift_r(lo, static_cast<uint32_t>(u >> 32), 8);
+      uint32_t k = __umulhi(t, m[f]);  // M = floor(2^40 / p): k in {Q-1, Q}
+      uint32_t r = lo + k * negp[f];
+      uint32_t c = min(r, r + negp[f]);
+      s[f] = c;
+      if (kMin) mn[f] = min(mn[f], c);
+    }
+  }
+};
+
+template <int F>
+struct Consts<Arith::kFq, F> {
+  // integer constants pre-scaled by 256 (see step): the state is C = 256*c
+  uint32_t q256[F], qln256[F], negp256[F];
+  float qp[F], qlnp[F], c1e[F];
+  __device__ void load(const FamPtrs& fp, int base) {
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      q256[f] = fp.q[base + f] << 8;
+      qln256[f] = fp.qln[base + f] << 8;
+      negp256[f] = fp.negp[base + f] << 8;
+      qp[f] = fp.qp[base + f];
+      qlnp[f] = fp.qlnp[base + f];
+      c1e[f] = fp.c1e[base + f];
+    }
+  }
+  // One rolling step for function f; returns the new scaled state 256*c.
+  // With everything scaled by 256 the bias of the float bits (0x4B000000 =
+  // 0x4B * 2^24) vanishes mod 2^32, so the biased words feed the IMADs
+  // directly and r*256 < 2^32 comes out exact:
+  //   sb   = (C >> 8) | 0x4B000000      LEA.HI       float(sb) = 2^23 + c
+  //   R    = fma(sb, q/p, fma(c_out, QLn/p, c1e))   2 FFMA
+  //   Kb   = bits(R + 2^23 - 1/2, rd)   FADD.RM      = 0x4B000000 + k
+  //   256r = sb*256q + Kb*(-256p) + c_out*256QLn + 256c_in   3 IMAD
+  //   C'   = min(256r, 256r - 256p)     VIADDMNMX    canonical, scaled
+  __device__ __forceinline__ uint32_t roll(int f, uint32_t C, uint32_t cin256, uint32_t cout,
+                                           float cout_f) const {
+    const uint32_t sb = (C >> 8) | kMagicBits;
+    const float t1 = __fmaf_rn(cout_f, qlnp[f], c1e[f]);
+    const float R = __fmaf_rn(__uint_as_float(sb), qp[f], t1);
+    const uint32_t kb = __float_as_uint(__fadd_rd(R, 8388607.5f));
+    uint32_t x = cout * qln256[f] + cin256;
+    x = kb * negp256[f] + x;
+    x = sb * q256[f] + x;
+    return min(x, x + negp256[f]);
+  }
+};
+
+template <Arith A, int F, int Z>
 __global__ void __launch_bounds__(kWarps * 32)
     k_signature(const uint8_t* __restrict__ text, const uint64_t* __restrict__ offsets,
                 const uint32_t* __restrict__ item_doc, const uint64_t* __restrict__ item_off,
                 uint64_t n_items, FamPtrs fam, uint32_t L, uint32_t H, uint32_t bands,
                 uint32_t rows, uint32_t K, uint32_t* __restrict__ sig,
                 uint32_t* __restrict__ band) {
-  __shared__ __align__(16) uint8_t sbuf[kWarps][kBuf];
-  __shared__ __align__(16) uint32_t srow[kWarps][32 * F];
+  constexpr int G = 32 / Z;  // lanes per group
+  constexpr int Hp = G * F;
+  constexpr int kChunk = chunk_for(Z);
+  constexpr int kBuf = kChunk + kLMax;
+  __shared__ __align__(16) uint2 sbuf[kWarps][Z][kBuf];
+  __shared__ __align__(16) uint32_t sbuf256[kWarps][Z][kBuf];
+  __shared__ __align__(16) uint32_t srow[kWarps][Hp];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int gl = lane % G;
+  const unsigned gmask = Z == 1 ? 0xFFFFFFFFu : (((1u << G) - 1u) << (grp * G));
   const uint64_t item = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
   if (item >= n_items) return;
 
@@ -147,100 +228,179 @@ __global__ void __launch_bounds__(kWarps * 32)
   const uint64_t off = offsets[doc];
   const uint64_t len = offsets[doc + 1] - off;
   const uint64_t nwin = len - L + 1;
-  const uint64_t we = min(ws + kSeg, nwin);
-  const uint64_t e = we + L - 1;  // one past the last character this item reads
+  const uint64_t item_end = min(ws + kSeg, nwin);
+  // this group's slice of windows [gs, ge)
+  const uint64_t span = item_end - ws;
+  const uint64_t gs = ws + span * grp / Z;
+  const uint64_t ge = ws + span * (grp + 1) / Z;
+  const uint64_t e = ge + L - 1;  // one past the last character this slice reads
   const uint8_t* base = text + off;
 
-  uint32_t q[F], qln[F], m[F], negp[F], s[F], mn[F];
+  Consts<A, F> k;
+  k.load(fam, gl * F);
+  uint32_t s[F], mn[F];
 #pragma unroll
   for (int f = 0; f < F; ++f) {
-    int idx = lane * F + f;
-    q[f] = fam.q[idx];
-    qln[f] = fam.qln[idx];
-    m[f] = fam.m[idx];
-    negp[f] = fam.negp[idx];
     s[f] = 0;
     mn[f] = 0xFFFFFFFFu;
   }
 
-  uint8_t* buf = sbuf[warp];
-  uint64_t p_hi = e;  // positions [p_lo, p_hi) handled per chunk, descending
+  uint2* buf = sbuf[warp][grp];
+  uint32_t* buf256 = sbuf256[warp][grp];
+  uint64_t p_hi = ge > gs ? e : gs;  // positions [p_lo, p_hi) per chunk, descending
   bool first = true;
-  while (p_hi > ws) {
-    const uint64_t p_lo = (p_hi - ws > kChunk) ? p_hi - kChunk : ws;
+  while (p_hi > gs) {
+    const uint64_t p_lo = (p_hi - gs > kChunk) ? p_hi - kChunk : gs;
     const int cnt = static_cast<int>(p_hi - p_lo);
-    // stage chars [p_lo, p_hi + L), zero beyond e (virtual characters)
-    for (int j = lane; j < cnt + static_cast<int>(L); j += 32) {
+    // stage (char, float(char)) and 256*char for [p_lo, p_hi + L), zero beyond e
+    for (int j = gl; j < cnt + static_cast<int>(L); j += G) {
       uint64_t pos = p_lo + j;
-      buf[j] = pos < e ? base[pos] : 0;
+      uint32_t c = pos < e ? base[pos] : 0u;
+      buf[j] = make_uint2(c, __float_as_uint(static_cast<float>(c)));
+      buf256[j] = c << 8;
     }
-    __syncwarp();
+    __syncwarp(gmask);
     int j = cnt - 1;
-    if (first) {
-      // L-1 warm-up positions: partial windows, not part of the minimum
-      for (int w = 0; w < static_cast<int>(L) - 1; ++w, --j)
-        step<F, false>(buf[j], buf[j + L], q, qln, m, negp, s, mn);
-      first = false;
+    if constexpr (A == Arith::kFq) {
+      if (first) {
+        for (int w = 0; w < static_cast<int>(L) - 1; ++w, --j) {
+          const uint2 o = buf[j + L];
+          const uint32_t ci = buf256[j];
+#pragma unroll
+          for (int f = 0; f < F; ++f) s[f] = k.roll(f, s[f], ci, o.x, __uint_as_float(o.y));
+        }
+        first = false;
+      }
+      // two windows per iteration: one 3-way min (VIMNMX3) folds both
+      for (; j >= 1; j -= 2) {
+        const uint2 o0 = buf[j + L], o1 = buf[j - 1 + L];
+        const uint32_t c0 = buf256[j], c1 = buf256[j - 1];
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          const uint32_t a0 = k.roll(f, s[f], c0, o0.x, __uint_as_float(o0.y));
+          const uint32_t a1 = k.roll(f, a0, c1, o1.x, __uint_as_float(o1.y));
+          s[f] = a1;
+          mn[f] = __vimin3_u32(mn[f], a0, a1);
+        }
+      }
+      if (j == 0) {
+        const uint2 o = buf[L];
+        const uint32_t ci = buf256[0];
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          s[f] = k.roll(f, s[f], ci, o.x, __uint_as_float(o.y));
+          mn[f] = min(mn[f], s[f]);
+        }
+      }
+    } else {
+      if (first) {
+        // L-1 warm-up positions: partial windows, not part of the minimum
+        for (int w = 0; w < static_cast<int>(L) - 1; ++w, --j) {
+          const uint2 o = buf[j + L];
+          k.template step<false>(buf[j].x, o.x, __uint_as_float(o.y), s, mn);
+        }
+        first = false;
+      }
+#pragma unroll 2
+      for (; j >= 0; --j) {
+        const uint2 o = buf[j + L];
+        k.template step<true>(buf[j].x, o.x, __uint_as_float(o.y), s, mn);
+      }
     }
-    // main positions, unrolled by 4
-    for (; j >= 3; j -= 4) {
-      uint32_t c0 = buf[j], o0 = buf[j + L];
-      uint32_t c1 = buf[j - 1], o1 = buf[j - 1 + L];
-      uint32_t c2 = buf[j - 2], o2 = buf[j - 2 + L];
-      uint32_t c3 = buf[j - 3], o3 = buf[j - 3 + L];
-      step<F, true>(c0, o0, q, qln, m, negp, s, mn);
-      step<F, true>(c1, o1, q, qln, m, negp, s, mn);
-      step<F, true>(c2, o2, q, qln, m, negp, s, mn);
-      step<F, true>(c3, o3, q, qln, m, negp, s, mn);
-    }
-    for (; j >= 0; --j) step<F, true>(buf[j], buf[j + L], q, qln, m, negp, s, mn);
-    __syncwarp();
+    __syncwarp(gmask);
     p_hi = p_lo;
   }
 
+  if (Z > 1) {  // the slices' partial minima meet
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+#pragma unroll
+      for (int o = G; o < 32; o <<= 1) mn[f] = min(mn[f], __shfl_xor_sync(0xFFFFFFFFu, mn[f], o));
+    if (grp != 0) return;
+  }
+
+  if constexpr (A == Arith::kFq) {
+#pragma unroll
+    for (int f = 0; f < F; ++f) mn[f] >>= 8;  // scaled state -> canonical value
+  }
   uint32_t* out = sig + doc * H;
+  const int fbase = gl * F;
   if (multi) {
 #pragma unroll
-    for (int f = 0; f < F; ++f) {
-      int idx = lane * F + f;
-      if (idx < static_cast<int>(H)) atomicMin(out + idx, mn[f]);
-    }
+    for (int f = 0; f < F; ++f)
+      if (fbase + f < static_cast<int>(H)) atomicMin(out + fbase + f, mn[f]);
     return;
   }
-  uint32_t* row = srow[warp];
-  if ((H % 4) == 0 && (F % 4) == 0 && lane * F + F <= static_cast<int>(H)) {
+  if ((H % 4) == 0 && (F % 4) == 0 && fbase + F <= static_cast<int>(H)) {
 #pragma unroll
     for (int f = 0; f < F; f += 4)
-      *reinterpret_cast<uint4*>(out + lane * F + f) = make_uint4(mn[f], mn[f + 1], mn[f + 2], mn[f + 3]);
+      *reinterpret_cast<uint4*>(out + fbase + f) = make_uint4(mn[f], mn[f + 1], mn[f + 2], mn[f + 3]);
   } else {
 #pragma unroll
     for (int f = 0; f < F; ++f)
-      if (lane * F + f < static_cast<int>(H)) out[lane * F + f] = mn[f];
+      if (fbase + f < static_cast<int>(H)) out[fbase + f] = mn[f];
   }
   if (band == nullptr) return;
+  uint32_t* row = srow[warp];
 #pragma unroll
-  for (int f = 0; f < F; ++f) row[lane * F + f] = mn[f];
-  __syncwarp();
-  for (uint32_t j = lane; j < bands; j += 32) {
+  for (int f = 0; f < F; ++f) row[fbase + f] = mn[f];
+  __syncwarp(gmask);
+  for (uint32_t jb = gl; jb < bands; jb += G) {
     uint64_t sum = 0;
-    for (uint32_t r = 0; r < rows; ++r) sum += row[j * rows + r];
-    band[doc * bands + j] = K ? static_cast<uint32_t>(sum % K) : static_cast<uint32_t>(sum);
+    for (uint32_t r = 0; r < rows; ++r) sum += row[jb * rows + r];
+    band[doc * bands + jb] = K ? static_cast<uint32_t>(sum % K) : static_cast<uint32_t>(sum);
   }
 }
 
-template <int F>
+template <Arith A, int F, int Z>
 void launch_k1(const DevFamily& fam, const uint8_t* d_bytes, const uint64_t* d_offsets,
                const uint32_t* item_doc, const uint64_t* item_off, uint64_t items, uint32_t bands,
                uint32_t rows, uint32_t K, uint32_t* d_sig, uint32_t* d_band, cudaStream_t s) {
-  FamPtrs p{fam.q, fam.qln, fam.m, fam.negp};
+  FamPtrs p{fam.q, fam.qln, fam.m, fam.negp, fam.c3, fam.qp, fam.qlnp, fam.c1e};
   uint64_t blocks = (items + kWarps - 1) / kWarps;
-  k_signature<F><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
+  k_signature<A, F, Z><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
       d_bytes, d_offsets, item_doc, item_off, items, p, fam.L, fam.H, bands, rows, K, d_sig,
       d_band);
   ND_CHECK_LAUNCH();
 }
 
+using Launcher = void (*)(const DevFamily&, const uint8_t*, const uint64_t*, const uint32_t*,
+                          const uint64_t*, uint64_t, uint32_t, uint32_t, uint32_t, uint32_t*,
+                          uint32_t*, cudaStream_t);
+
+// (arith, Hp) -> instantiation; F = functions per lane, Z = window slices per
+// warp.  ND_K1_FZ="F,Z" overrides the default shape (tuning experiments).
+Launcher pick_launcher(bool int_arith, uint32_t Hp) {
+  if (int_arith) {
+    switch (Hp) {
+      case 32: return launch_k1<Arith::kInt, 1, 1>;
+      case 64: return launch_k1<Arith::kInt, 2, 1>;
+      case 128: return launch_k1<Arith::kInt, 4, 1>;
+      case 256: return launch_k1<Arith::kInt, 8, 1>;
+      case 512: return launch_k1<Arith::kInt, 16, 1>;
+    }
+    return nullptr;
+  }
+  const char* fz = getenv("ND_K1_FZ");
+  if (fz && Hp == 128) {
+    std::string v(fz);
+    if (v == "4,1") return launch_k1<Arith::kFq, 4, 1>;
+    if (v == "8,2") return launch_k1<Arith::kFq, 8, 2>;
+    if (v == "16,4") return launch_k1<Arith::kFq, 16, 4>;
+  }
+  switch (Hp) {
+    case 32: return launch_k1<Arith::kFq, 4, 4>;
+    case 64: return launch_k1<Arith::kFq, 8, 4>;
+    case 128: return launch_k1<Arith::kFq, 8, 2>;
+    case 256: return launch_k1<Arith::kFq, 8, 1>;
+    case 512: return launch_k1<Arith::kFq, 16, 1>;
+  }
+  return nullptr;
+}
+
 }  // namespace
+
 
 void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint64_t* d_offsets,
                        uint64_t n, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
@@ -296,14 +456,13 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     item_doc = idoc;
     item_off = off;
   }
-  switch (fam.Hp / 32) {
-    case 1: launch_k1<1>(fam, d_bytes, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, s); break;
-    case 2: launch_k1<2>(fam, d_bytes, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, s); break;
-    case 4: launch_k1<4>(fam, d_bytes, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, s); break;
-    case 8: launch_k1<8>(fam, d_bytes, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, s); break;
-    case 16: launch_k1<16>(fam, d_bytes, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, s); break;
-    default: fail(ND_ERR_CONFIG, "hash count must be at most 512 on the GPU path");
-  }
+  static const bool int_arith = [] {
+    const char* v = getenv("ND_K1_KERNEL");
+    return v && std::string(v) == "int";
+  }();
+  Launcher go = pick_launcher(int_arith, fam.Hp);
+  if (!go) fail(ND_ERR_CONFIG, "hash count must be at most 512 on the GPU path");
+  go(fam, d_bytes, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, s);
   if (nmulti && d_band) {
     uint64_t total = static_cast<uint64_t>(nmulti) * bands;
     k_bands_from_rows<<<static_cast<unsigned>((total + tb - 1) / tb), tb, 0, s>>>(

@@ -2,6 +2,7 @@
 // signature entry points (host-pipelined and device-resident), and the
 // exception -> status mapping (reference taxonomy util.hpp:13-26).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -271,24 +272,37 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L,
     uint32_t Hp = 32;
     while (Hp < H) Hp *= 2;
     if (Hp > 512) fail(ND_ERR_CONFIG, "hash count above 512 is not supported on the GPU path");
-    std::vector<uint32_t> host(4 * Hp);
+    // 8 arrays of Hp entries: q, QLn, M, -p, c3 (u32) and q/p, QLn/p, c1e (f32)
+    std::vector<uint32_t> host(8 * Hp);
     for (uint32_t i = 0; i < Hp; ++i) {
       const nd_hash_fn& f = fns[i < H ? i : 0];  // pad with copies of fn 0 (never stored)
       uint64_t p = f.modulus;
       if (p < 257 || p >= (1u << 23) || f.base == 0 || f.base >= (1u << 16))
         fail(ND_ERR_CONFIG, "hash function outside the GPU arithmetic domain (p < 2^23, q < 2^16)");
       uint64_t qL = static_cast<uint64_t>(f.base_power) * f.base % p;  // q^L = q^(L-1) * q
+      uint32_t qln = static_cast<uint32_t>((p - qL) % p);
+      float qp = static_cast<float>(static_cast<double>(f.base) / static_cast<double>(p));
+      float qlnp = static_cast<float>(static_cast<double>(qln) / static_cast<double>(p));
+      float c1e = -std::ldexp(qp, 23) + 0.03125f;  // exact: ulp(2^23 qp) <= 2^-6
       host[i] = f.base;
-      host[Hp + i] = static_cast<uint32_t>((p - qL) % p);
+      host[Hp + i] = qln;
       host[2 * Hp + i] = static_cast<uint32_t>((1ull << 40) / p);
       host[3 * Hp + i] = static_cast<uint32_t>(0u - static_cast<uint32_t>(p));
+      host[4 * Hp + i] = static_cast<uint32_t>(0x4B000000ull * p);
+      std::memcpy(&host[5 * Hp + i], &qp, 4);
+      std::memcpy(&host[6 * Hp + i], &qlnp, 4);
+      std::memcpy(&host[7 * Hp + i], &c1e, 4);
     }
-    uint32_t* d = ctx->fam_buf.as<uint32_t>(4 * Hp);
+    uint32_t* d = ctx->fam_buf.as<uint32_t>(8 * Hp);
     ND_CUDA(cudaMemcpy(d, host.data(), host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     ctx->fam.q = d;
     ctx->fam.qln = d + Hp;
     ctx->fam.m = d + 2 * Hp;
     ctx->fam.negp = d + 3 * Hp;
+    ctx->fam.c3 = d + 4 * Hp;
+    ctx->fam.qp = reinterpret_cast<float*>(d + 5 * Hp);
+    ctx->fam.qlnp = reinterpret_cast<float*>(d + 6 * Hp);
+    ctx->fam.c1e = reinterpret_cast<float*>(d + 7 * Hp);
     ctx->fam.H = H;
     ctx->fam.Hp = Hp;
     ctx->fam.L = L;

@@ -31,6 +31,10 @@ struct DevFamily {
   uint32_t* qln = nullptr;   // (p - q^L mod p) mod p
   uint32_t* m = nullptr;     // floor(2^40 / p)
   uint32_t* negp = nullptr;  // (uint32_t)(-p)
+  uint32_t* c3 = nullptr;    // 0x4B000000 * p mod 2^32  (fq variant)
+  float* qp = nullptr;       // fl(q / p)
+  float* qlnp = nullptr;     // fl(QLn / p)
+  float* c1e = nullptr;      // -2^23 * qp + 2^-5
   uint32_t H = 0;            // real hash count
   uint32_t Hp = 0;           // padded hash count
   uint32_t L = 0;

@@ -24,7 +24,8 @@ _lib.check(lib.nd_synth_generate(C.byref(spec), data.ctypes.data_as(_lib.u8p),
                                  offs.ctypes.data_as(_lib.u64p), C.byref(nb)))
 print(f"gen {n} docs {nb.value/1e9:.2f} GB in {time.time()-t0:.1f}s", flush=True)
 ctx = Context(0)
-stream = torch.cuda.current_stream()
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
 ctx.set_stream(stream.cuda_stream)
 fam = minhash.derive_family(5, H, 5)
 d_data = torch.from_numpy(data).cuda()
