@@ -56,6 +56,8 @@ typedef struct nd_ctx nd_ctx;
 
 /* ---- host-only helpers (no device needed) -------------------------------- */
 const char* nd_version(void);
+/* number of neardup_b200 kernel launches issued by this process so far */
+uint64_t nd_launch_count(void);
 /* last error message of the calling thread (ctx-free calls) */
 const char* nd_last_error_global(void);
 /* derive_family (minhash.hpp:42, minhash.cpp:71-105); out holds H entries */

@@ -60,6 +60,7 @@ class NdDedupStats(C.Structure):
 # name -> (restype, argtypes); every symbol include/neardup_b200.h declares
 SIGNATURES = {
     "nd_version": (C.c_char_p, []),
+    "nd_launch_count": (C.c_uint64, []),
     "nd_last_error_global": (C.c_char_p, []),
     "nd_derive_family": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                    C.POINTER(NdHashFn)]),

@@ -15,6 +15,8 @@ thread_local std::string g_error;
 
 namespace ndb {
 
+std::atomic<uint64_t> g_launches{0};
+
 int sm_count() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -174,6 +176,7 @@ using namespace ndb;
 extern "C" {
 
 const char* nd_version(void) { return "neardup_b200 0.1 (sm_100a)"; }
+uint64_t nd_launch_count(void) { return g_launches.load(); }
 const char* nd_last_error_global(void) { return g_error.c_str(); }
 
 int nd_derive_family(uint64_t seed, uint32_t H, uint32_t L, uint32_t unit, nd_hash_fn* out) {

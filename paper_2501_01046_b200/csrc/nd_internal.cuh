@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -21,7 +22,14 @@ namespace ndb {
                                      " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
   } while (0)
 
-#define ND_CHECK_LAUNCH() ND_CUDA(cudaGetLastError())
+// every kernel launch site ends with ND_CHECK_LAUNCH(); it also counts launches
+// (nd_launch_count) so benchmarks can report how many of our kernels ran.
+extern std::atomic<uint64_t> g_launches;
+#define ND_CHECK_LAUNCH()                                   \
+  do {                                                      \
+    ::ndb::g_launches.fetch_add(1, std::memory_order_relaxed); \
+    ND_CUDA(cudaGetLastError());                            \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // Device-side per-function constants for the rolling hash (see k_signature.cu).
