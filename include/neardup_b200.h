@@ -119,6 +119,11 @@ int nd_signatures_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_
                          uint64_t n, uint32_t bands, uint32_t rows, uint32_t bucket_count,
                          uint32_t* d_sig, uint32_t* d_band);
 
+/* band_bucket_ids (lsh.hpp:38-40, lsh.cpp:42-60) over host signature rows
+ * sigs[n*H] -> band ids[n*bands] (K == 0: raw u32 row sums). */
+int nd_band_keys(nd_ctx* ctx, const uint32_t* sigs, uint64_t n, uint32_t hash_count,
+                 uint32_t bands, uint32_t rows, uint32_t bucket_count, uint32_t* band_out);
+
 /* compare_pass (compare.hpp:52, compare.cpp:69-86) over cells given as CSR
  * row lists into a host signature matrix sigs[nrows*H]; rows inside a cell
  * ascend.  Result: sorted distinct (lo, hi) row pairs with match counts,

@@ -78,6 +78,8 @@ SIGNATURES = {
                                 u32p, u32p]),
     "nd_signatures_device": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_uint32, C.c_uint32,
                                        C.c_uint32, vp, vp]),
+    "nd_band_keys": (C.c_int, [vp, u32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                               C.c_uint32, u32p]),
     "nd_compare_cells": (C.c_int, [vp, u32p, C.c_uint64, C.c_uint32, u64p, u32p, C.c_uint64,
                                    C.c_uint64, C.c_uint64, u64p]),
     "nd_pairs_fetch": (C.c_int, [vp, u32p, u32p, u32p]),

@@ -29,7 +29,8 @@ void synth_generate(const nd_synth_spec& spec, uint8_t* bytes, uint64_t* offsets
 
 // report writers (host_report.cpp): groups as doc ids in output order
 void write_report(const std::string& dir, const std::vector<uint64_t>& members,
-                  const std::vector<uint64_t>& group_start, uint64_t total_documents,
+                  const std::vector<uint64_t>& group_start, const std::vector<uint64_t>& near,
+                  const std::vector<uint64_t>& removals, uint64_t total_documents,
                   uint64_t total_records, uint64_t distinct_pairs);
 
 }  // namespace ndb

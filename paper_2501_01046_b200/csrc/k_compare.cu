@@ -1,0 +1,159 @@
+// K3: all-pairs comparison inside LSH cells -- compare_bucket
+// (compare.cpp:24-67) over every non-singleton cell.
+//
+// The reference counts all H positions of every pair (i < j) and accepts iff
+// m*den > num*H (compare.hpp:31-34), i.e. m >= min_matches.  A pair can only
+// be accepted if it has at most A = H - min_matches mismatches, so a pair
+// with NO match among any fixed P >= A+1 positions is provably rejected (the
+// exact early-termination rule of the reference's own oracle,
+// oracle.cpp:81-92, proven equal to the full scan by test_oracle.cpp:96-112).
+//
+// Layout: one 128-thread CTA per (cell, tile of 128 rows).  Thread t owns row
+// i = tile*128 + t and keeps the first Pf values of its signature in
+// registers.  Columns j > i stream through shared memory in batches of 64
+// (Pf values each) and are read back as broadcast LDS.128; the prefilter is
+// an OR-chain of equality tests (ISETP.EQ.OR).  Survivors get the full H-way
+// count with the same early exit, from global memory, and accepted pairs are
+// appended with one atomic per pair.  Pairs are canonical (lo < hi) row
+// indices packed as lo << nb | hi so that sort + unique (compare.cpp:77-84)
+// is a single radix sort over 2*nb bits.
+#include "nd_internal.cuh"
+
+namespace ndb {
+namespace {
+
+constexpr int kRows = kCmpRows;  // rows per CTA (= threads)
+constexpr int kCols = 64;        // columns staged per batch
+
+__device__ __forceinline__ uint32_t full_matches(const uint32_t* __restrict__ a,
+                                                 const uint32_t* __restrict__ b, uint32_t H,
+                                                 uint32_t allowed, bool& alive) {
+  uint32_t matches = 0;
+  alive = true;
+  for (uint32_t h0 = 0; h0 < H; h0 += 32) {
+    const uint32_t hi = min(H, h0 + 32);
+    for (uint32_t h = h0; h < hi; ++h) matches += __ldg(a + h) == __ldg(b + h);
+    if (hi - matches > allowed) {  // accepting count unreachable (oracle.cpp:81-92)
+      alive = false;
+      return matches;
+    }
+  }
+  return matches;
+}
+
+__device__ __forceinline__ void emit(uint32_t ra, uint32_t rb, uint32_t m, int nb,
+                                     uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
+                                     unsigned long long* __restrict__ count, uint64_t cap) {
+  const uint32_t lo = min(ra, rb), hi = max(ra, rb);
+  unsigned long long slot = atomicAdd(count, 1ull);
+  if (slot < cap) {
+    out_key[slot] = (static_cast<uint64_t>(lo) << nb) | hi;
+    out_m[slot] = m;
+  }
+}
+
+// Pf > 0: prefilter over the first Pf positions (Pf >= H - min_matches + 1).
+// Pf == 0: no prefilter (every pair takes the full early-exit count).
+template <int Pf>
+__global__ void __launch_bounds__(kRows)
+    k_compare(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
+              const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
+              const uint32_t* __restrict__ item_cell, const uint64_t* __restrict__ item_off,
+              uint32_t min_match, int nb, uint64_t* __restrict__ out_key,
+              uint32_t* __restrict__ out_m, unsigned long long* __restrict__ count, uint64_t cap) {
+  constexpr int PS = Pf > 0 ? ((Pf + 3) / 4) * 4 : 4;
+  __shared__ __align__(16) uint32_t cols[kCols][PS];
+  __shared__ uint32_t col_row[kCols];
+  const uint32_t item = blockIdx.x;
+  const uint32_t cell = item_cell[item];
+  const uint32_t tile = static_cast<uint32_t>(item - item_off[cell]);
+  const uint64_t s = cell_start[cell];
+  const uint32_t n = cell_len[cell];
+  const uint32_t i = tile * kRows + threadIdx.x;
+  const bool valid = i < n;
+  const uint32_t my_row = valid ? rows[s + i] : 0;
+  const uint32_t* my_sig = sig + static_cast<uint64_t>(my_row) * H;
+  const uint32_t allowed = H - min_match;
+
+  uint32_t pre[Pf > 0 ? Pf : 1];
+  if constexpr (Pf > 0) {
+#pragma unroll
+    for (int k = 0; k < Pf; ++k) pre[k] = valid ? __ldg(my_sig + k) : 0xFFFFFFFFu;
+  }
+
+  for (uint32_t j0 = tile * kRows + 1; j0 < n; j0 += kCols) {
+    const uint32_t cmax = min(static_cast<uint32_t>(kCols), n - j0);
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < cmax; c += kRows) col_row[c] = rows[s + j0 + c];
+    if constexpr (Pf > 0) {
+      __syncthreads();
+      for (uint32_t idx = threadIdx.x; idx < cmax * Pf; idx += kRows) {
+        const uint32_t c = idx / Pf, k = idx % Pf;
+        cols[c][k] = __ldg(sig + static_cast<uint64_t>(col_row[c]) * H + k);
+      }
+    }
+    __syncthreads();
+    if (!valid) continue;
+    // columns j <= i are not this row's (upper triangle, compare.cpp:46)
+    uint32_t c0 = (i + 1 > j0) ? i + 1 - j0 : 0;
+    for (uint32_t c = c0; c < cmax; ++c) {
+      bool cand = true;
+      if constexpr (Pf > 0) {
+        bool any = false;
+        const uint4* col = reinterpret_cast<const uint4*>(cols[c]);
+#pragma unroll
+        for (int q = 0; q < PS / 4; ++q) {
+          const uint4 v = col[q];
+          any |= (4 * q + 0 < Pf) && pre[4 * q + 0] == v.x;
+          if (4 * q + 1 < Pf) any |= pre[4 * q + 1] == v.y;
+          if (4 * q + 2 < Pf) any |= pre[4 * q + 2] == v.z;
+          if (4 * q + 3 < Pf) any |= pre[4 * q + 3] == v.w;
+        }
+        cand = any;
+      }
+      if (cand) {
+        const uint32_t other = col_row[c];
+        bool alive;
+        const uint32_t m =
+            full_matches(my_sig, sig + static_cast<uint64_t>(other) * H, H, allowed, alive);
+        if (alive && m >= min_match) emit(my_row, other, m, nb, out_key, out_m, count, cap);
+      }
+    }
+  }
+}
+
+using CmpFn = void (*)(const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
+                       const uint32_t*, const uint32_t*, const uint64_t*, uint32_t, int,
+                       uint64_t*, uint32_t*, unsigned long long*, uint64_t);
+
+}  // namespace
+
+// Smallest compiled prefilter width >= H - min_matches + 1 that fits in H.
+int compare_prefilter_width(uint32_t H, uint32_t min_match) {
+  const uint32_t P = H - min_match + 1;
+  for (int pf : {16, 28, 32, 52, 64})
+    if (static_cast<uint32_t>(pf) >= P && static_cast<uint32_t>(pf) <= H) return pf;
+  return 0;
+}
+
+void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32_t min_match,
+                    int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,
+                    uint64_t cap, cudaStream_t s) {
+  if (cs.items == 0 || min_match > H) return;
+  CmpFn fn = nullptr;
+  switch (compare_prefilter_width(H, min_match)) {
+    case 16: fn = k_compare<16>; break;
+    case 28: fn = k_compare<28>; break;
+    case 32: fn = k_compare<32>; break;
+    case 52: fn = k_compare<52>; break;
+    case 64: fn = k_compare<64>; break;
+    default: fn = k_compare<0>; break;
+  }
+  if (cs.items > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many compare work items");
+  fn<<<static_cast<unsigned>(cs.items), kRows, 0, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start,
+                                                       cs.cell_len, cs.item_cell, cs.item_off,
+                                                       min_match, nb, out_key, out_m, count, cap);
+  ND_CHECK_LAUNCH();
+}
+
+}  // namespace ndb

@@ -105,6 +105,11 @@ __global__ void k_fill_multi(const uint32_t* __restrict__ multi_docs, uint32_t n
   }
 }
 
+__global__ void k_iota_docs(uint32_t* __restrict__ v, uint64_t n) {
+  uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) v[i] = static_cast<uint32_t>(i);
+}
+
 // band keys from finished signature rows (multi-item documents)
 __global__ void k_bands_from_rows(const uint32_t* __restrict__ docs, uint32_t ndocs,
                                   const uint32_t* __restrict__ sig, uint32_t H, uint32_t bands,
@@ -469,6 +474,19 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
         multi_docs, nmulti, d_sig, fam.H, bands, rows, K, d_band);
     ND_CHECK_LAUNCH();
   }
+}
+
+void launch_band_keys(const uint32_t* d_sig, uint64_t n, uint32_t H, uint32_t bands, uint32_t rows,
+                      uint32_t K, uint32_t* d_band, uint32_t* d_docs, cudaStream_t s) {
+  if (n == 0) return;
+  if (n > 0xFFFFFFFFull) fail(ND_ERR_CONFIG, "batch exceeds 2^32 documents");
+  const unsigned tb = 256;
+  k_iota_docs<<<static_cast<unsigned>((n + tb - 1) / tb), tb, 0, s>>>(d_docs, n);
+  ND_CHECK_LAUNCH();
+  uint64_t total = n * bands;
+  k_bands_from_rows<<<static_cast<unsigned>((total + tb - 1) / tb), tb, 0, s>>>(
+      d_docs, static_cast<uint32_t>(n), d_sig, H, bands, rows, K, d_band);
+  ND_CHECK_LAUNCH();
 }
 
 }  // namespace ndb

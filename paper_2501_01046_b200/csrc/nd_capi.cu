@@ -61,6 +61,8 @@ nd_ctx::~nd_ctx() {
   pinned_off.release();
   sig_scratch.release();
   dedup.release();
+  api.release();
+  api2.release();
   if (h2d) cudaStreamDestroy(h2d);
   if (d2h) cudaStreamDestroy(d2h);
   if (own_stream && stream) cudaStreamDestroy(stream);
@@ -310,6 +312,7 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L,
     ctx->fam.Hp = Hp;
     ctx->fam.L = L;
     ctx->family_host.assign(fns, fns + H);
+    ctx->family_derived = false;
   });
 }
 

@@ -24,7 +24,10 @@ struct nd_ctx {
   ndb::DevFamily fam;
   std::vector<nd_hash_fn> family_host;
   ndb::SigScratch sig_scratch;
-  ndb::DedupState dedup;
+  ndb::DedupState dedup;        // last nd_dedup / nd_dedup_device
+  ndb::DedupState api, api2;    // last nd_compare_cells / nd_union
+  uint64_t family_seed = 0;
+  bool family_derived = false;  // family came from derive_family(family_seed, ...)
   std::string err;
 
   ~nd_ctx();

@@ -1,41 +1,404 @@
-// C-ABI of the compare / union / dedup stages (filled in by k_cells.cu,
-// k_compare.cu, k_pairs.cu, k_components.cu).
+// In-memory dedup driver (K1 -> K2 -> K3 -> K4) and the C-ABI of the compare,
+// union and dedup stages.
+//
+// run_dedup (pipeline.cpp:510-532) chains three file-backed stages: hash
+// (.feds files), gather-compare (.pairs files) and union.  Here the same
+// stages run back to back on one device with every intermediate resident in
+// HBM: signatures + band keys (K1), stable cell grouping (K2), in-cell
+// comparison (K3), distinct pairs + components (K4).  Only the report leaves
+// the device.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
 #include "nd_capi_impl.cuh"
+
+namespace ndb {
+namespace {
+
+struct EventTimer {
+  cudaEvent_t e[8];
+  int n = 0;
+  cudaStream_t s;
+  explicit EventTimer(cudaStream_t st) : s(st) {
+    for (auto& x : e) cudaEventCreate(&x);
+  }
+  ~EventTimer() {
+    for (auto& x : e) cudaEventDestroy(x);
+  }
+  void mark() { cudaEventRecord(e[n++], s); }
+  double seconds(int a, int b) {
+    float ms = 0;
+    cudaEventSynchronize(e[b]);
+    cudaEventElapsedTime(&ms, e[a], e[b]);
+    return ms / 1e3;
+  }
+};
+
+void validate(const nd_params& p) {
+  // RunConfig::validate (pipeline.cpp:20-33), artifact-shaping fields
+  if (p.bands == 0 || p.rows == 0) fail(ND_ERR_CONFIG, "bands and rows must be positive");
+  if (static_cast<uint64_t>(p.bands) * p.rows != p.hash_count)
+    fail(ND_ERR_CONFIG, "hash count " + std::to_string(p.hash_count) + " must equal bands*rows = " +
+                            std::to_string(p.bands) + "*" + std::to_string(p.rows));
+  if (p.shingle_len == 0) fail(ND_ERR_CONFIG, "shingle length must be positive");
+  if (p.threshold_den == 0) fail(ND_ERR_CONFIG, "ratio denominator must be positive");
+  if (p.threshold_num > p.threshold_den) fail(ND_ERR_CONFIG, "threshold must be at most 1");
+  if (p.bucket_count == 0 && (p.scale_num == 0 || p.scale_den == 0))
+    fail(ND_ERR_CONFIG, "bucket scale must be positive");
+}
+
+void ensure_family(nd_ctx* ctx, const nd_params& p) {
+  const auto& fam = ctx->fam;
+  if (fam.q && fam.H == p.hash_count && fam.L == p.shingle_len && ctx->family_seed == p.seed &&
+      ctx->family_derived)
+    return;
+  std::vector<nd_hash_fn> f = derive_family(p.seed, p.hash_count, p.shingle_len, p.unit);
+  int rc = nd_family_upload(ctx, f.data(), p.hash_count, p.shingle_len, p.unit);
+  if (rc != ND_OK) fail(rc, ctx->err);
+  ctx->family_seed = p.seed;
+  ctx->family_derived = true;
+}
+
+// compare + distinct pairs over a prepared CellSet (grows the pair buffer and
+// re-runs once if the first pass overflowed it)
+void compare_and_unique(DedupState& st, const uint32_t* d_sig, uint32_t H, uint32_t mm,
+                        uint64_t nrows, cudaStream_t s) {
+  PairSet& ps = st.pairs;
+  ps.nb = std::max(1, bits_for(nrows ? nrows - 1 : 0));
+  if (2 * ps.nb > 64) fail(ND_ERR_CONFIG, "too many rows for packed pair keys");
+  ps.counter = ps.dcount.as<unsigned long long>(1);
+  if (ps.cap == 0) ps.cap = std::max<uint64_t>(1 << 20, 2 * nrows);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    ps.keys = ps.dkeys.as<uint64_t>(ps.cap);
+    ps.vals = ps.dvals.as<uint32_t>(ps.cap);
+    ND_CUDA(cudaMemsetAsync(ps.counter, 0, sizeof(unsigned long long), s));
+    launch_compare(st.cells, d_sig, H, mm, ps.nb, ps.keys, ps.vals, ps.counter, ps.cap, s);
+    unsigned long long got = 0;
+    ND_CUDA(cudaMemcpyAsync(&got, ps.counter, sizeof got, cudaMemcpyDeviceToHost, s));
+    ND_CUDA(cudaStreamSynchronize(s));
+    ps.count = got;
+    if (got <= ps.cap) break;
+    ps.cap = got + got / 4;
+  }
+  unique_pairs(ps, s);
+}
+
+template <class T>
+std::vector<T> d2h(const T* d, uint64_t n, cudaStream_t s) {
+  std::vector<T> h(n);
+  if (n) ND_CUDA(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  return h;
+}
+
+uint64_t id_of(const DedupState& st, uint32_t row) {
+  return st.doc_ids.empty() ? row : st.doc_ids[row];
+}
+
+// The shared tail of nd_dedup / nd_dedup_device: K2..K4 on the signatures and
+// band keys already in st.sig / st.band.
+void dedup_tail(nd_ctx* ctx, DedupState& st, const nd_params& p, uint64_t n, nd_dedup_stats* stats,
+                EventTimer& t) {
+  cudaStream_t s = ctx->stream;
+  const uint32_t H = p.hash_count;
+  const uint32_t mm = min_matches(H, p.threshold_num, p.threshold_den);
+  build_cells_from_bands(st.cells, st.band.as<uint32_t>(n * p.bands), n, p.bands, st.K, kCmpRows,
+                         s);
+  t.mark();  // 2
+  compare_and_unique(st, st.sig.as<uint32_t>(n * H), H, mm, n, s);
+  t.mark();  // 3
+  components(st.groups, st.pairs.lo, st.pairs.hi, st.pairs.distinct, n, s);
+  t.mark();  // 4
+  ND_CUDA(cudaStreamSynchronize(s));
+  st.documents = n;
+  st.valid = true;
+  if (stats) {
+    stats->documents = n;
+    stats->bucket_count = st.K;
+    stats->nonsingleton_cells = st.cells.ncells;
+    stats->candidate_pairs = st.cells.candidate_pairs;
+    stats->emitted_pairs = st.pairs.count;
+    stats->distinct_pairs = st.pairs.distinct;
+    stats->duplicate_groups = st.groups.groups;
+    stats->near_duplicates = st.groups.members;
+    stats->removals = st.groups.removals;
+    stats->seconds[0] = t.seconds(0, 1);
+    stats->seconds[1] = t.seconds(1, 2);
+    stats->seconds[2] = t.seconds(2, 3);
+    stats->seconds[3] = 0;  // distinct pairs are folded into [2]
+    stats->seconds[4] = t.seconds(3, 4);
+    stats->seconds[5] = 0;
+  }
+}
+
+uint32_t bucket_count_for(const nd_params& p, uint64_t n) {
+  return p.bucket_count ? p.bucket_count : choose_bucket_count(n, p.scale_num, p.scale_den);
+}
+
+void set_doc_ids(DedupState& st, const uint64_t* doc_ids, uint64_t n) {
+  st.doc_ids.clear();
+  if (!doc_ids) return;
+  for (uint64_t i = 1; i < n; ++i)
+    if (doc_ids[i] <= doc_ids[i - 1]) fail(ND_ERR_CONFIG, "doc_ids must be strictly ascending");
+  st.doc_ids.assign(doc_ids, doc_ids + n);
+}
+
+}  // namespace
+}  // namespace ndb
 
 using namespace ndb;
 
 extern "C" {
 
-int nd_compare_cells(nd_ctx* ctx, const uint32_t*, uint64_t, uint32_t, const uint64_t*,
-                     const uint32_t*, uint64_t, uint64_t, uint64_t, uint64_t*) {
-  return guarded_impl(ctx, [&] { fail(ND_ERR_INTERNAL, "not implemented"); });
+int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const uint64_t* doc_ids,
+             uint64_t n, const nd_params* params, nd_dedup_stats* stats) {
+  return guarded_impl(ctx, [&] {
+    const nd_params p = *params;
+    validate(p);
+    ensure_family(ctx, p);
+    DedupState& st = ctx->dedup;
+    st.valid = false;
+    set_doc_ids(st, doc_ids, n);
+    if (n == 0) fail(ND_ERR_CONFIG, "no documents survive preprocessing; nothing to deduplicate");
+    for (uint64_t i = 0; i < n; ++i)
+      if (offsets[i + 1] < offsets[i] || offsets[i + 1] - offsets[i] < p.shingle_len)
+        fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has fewer units than the shingle length");
+    st.K = bucket_count_for(p, n);
+    cudaStream_t s = ctx->stream;
+    ctx->ensure_streams();
+    EventTimer t(s);
+    t.mark();  // 0
+    // H2D in chunks on the copy stream, K1 per chunk as it lands
+    const uint64_t total = offsets[n] - offsets[0];
+    uint8_t* d_text = st.text.as<uint8_t>(total + 16);
+    uint64_t* d_off = st.offs.as<uint64_t>(n + 1);
+    uint32_t* d_sig = st.sig.as<uint32_t>(n * p.hash_count);
+    uint32_t* d_band = st.band.as<uint32_t>(n * p.bands);
+    std::vector<uint64_t> rebased(offsets, offsets + n + 1);
+    for (auto& o : rebased) o -= offsets[0];
+    uint64_t* h_off = static_cast<uint64_t*>(ctx->pinned_off.get((n + 1) * sizeof(uint64_t)));
+    std::memcpy(h_off, rebased.data(), (n + 1) * sizeof(uint64_t));
+    cudaEvent_t start;
+    ND_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    ND_CUDA(cudaEventRecord(start, s));
+    ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
+    ND_CUDA(cudaMemcpyAsync(d_off, h_off, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->h2d));
+    constexpr uint64_t kChunk = 256ull << 20;
+    std::vector<cudaEvent_t> evs;
+    for (uint64_t d0 = 0; d0 < n;) {
+      uint64_t d1 = d0 + 1;
+      while (d1 < n && rebased[d1 + 1] - rebased[d0] <= kChunk) ++d1;
+      ND_CUDA(cudaMemcpyAsync(d_text + rebased[d0], bytes + offsets[0] + rebased[d0],
+                              rebased[d1] - rebased[d0], cudaMemcpyHostToDevice, ctx->h2d));
+      cudaEvent_t ev;
+      ND_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      ND_CUDA(cudaEventRecord(ev, ctx->h2d));
+      ND_CUDA(cudaStreamWaitEvent(s, ev, 0));
+      evs.push_back(ev);
+      launch_signatures(ctx->fam, d_text, d_off + d0, d1 - d0, p.bands, p.rows, st.K,
+                        d_sig + d0 * p.hash_count, d_band + d0 * p.bands, st.sig_scratch, s,
+                        false, h_off + d0);
+      d0 = d1;
+    }
+    t.mark();  // 1
+    dedup_tail(ctx, st, p, n, stats, t);
+    for (auto ev : evs) cudaEventDestroy(ev);
+    cudaEventDestroy(start);
+  });
 }
-int nd_pairs_fetch(nd_ctx* ctx, uint32_t*, uint32_t*, uint32_t*) {
-  return guarded_impl(ctx, [&] { fail(ND_ERR_INTERNAL, "not implemented"); });
+
+int nd_dedup_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offsets,
+                    const uint64_t* doc_ids, uint64_t n, const nd_params* params,
+                    nd_dedup_stats* stats) {
+  return guarded_impl(ctx, [&] {
+    const nd_params p = *params;
+    validate(p);
+    ensure_family(ctx, p);
+    DedupState& st = ctx->dedup;
+    st.valid = false;
+    set_doc_ids(st, doc_ids, n);
+    if (n == 0) fail(ND_ERR_CONFIG, "no documents survive preprocessing; nothing to deduplicate");
+    st.K = bucket_count_for(p, n);
+    cudaStream_t s = ctx->stream;
+    EventTimer t(s);
+    t.mark();
+    launch_signatures(ctx->fam, d_bytes, d_offsets, n, p.bands, p.rows, st.K,
+                      st.sig.as<uint32_t>(n * p.hash_count), st.band.as<uint32_t>(n * p.bands),
+                      st.sig_scratch, s, true, nullptr);
+    t.mark();
+    dedup_tail(ctx, st, p, n, stats, t);
+  });
 }
-int nd_union(nd_ctx* ctx, const uint32_t*, const uint32_t*, uint64_t, uint32_t, uint64_t*,
-             uint64_t*) {
-  return guarded_impl(ctx, [&] { fail(ND_ERR_INTERNAL, "not implemented"); });
+
+int nd_dedup_fetch_pairs(nd_ctx* ctx, uint64_t* lo, uint64_t* hi, uint32_t* match_count) {
+  return guarded_impl(ctx, [&] {
+    DedupState& st = ctx->dedup;
+    if (!st.valid) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");
+    cudaStream_t s = ctx->stream;
+    const uint64_t d = st.pairs.distinct;
+    auto l = d2h(st.pairs.lo, d, s);
+    auto h = d2h(st.pairs.hi, d, s);
+    auto m = d2h(st.pairs.mc, d, s);
+    ND_CUDA(cudaStreamSynchronize(s));
+    for (uint64_t i = 0; i < d; ++i) {
+      if (lo) lo[i] = id_of(st, l[i]);
+      if (hi) hi[i] = id_of(st, h[i]);
+      if (match_count) match_count[i] = m[i];
+    }
+  });
 }
-int nd_groups_fetch(nd_ctx* ctx, uint32_t*, uint64_t*) {
-  return guarded_impl(ctx, [&] { fail(ND_ERR_INTERNAL, "not implemented"); });
+
+int nd_dedup_fetch_groups(nd_ctx* ctx, uint64_t* members, uint64_t* group_start) {
+  return guarded_impl(ctx, [&] {
+    DedupState& st = ctx->dedup;
+    if (!st.valid) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");
+    cudaStream_t s = ctx->stream;
+    const GroupSet& g = st.groups;
+    auto mem = d2h(g.member_rows, g.members, s);
+    auto gs = d2h(g.group_start, g.groups ? g.groups + 1 : 0, s);
+    ND_CUDA(cudaStreamSynchronize(s));
+    for (uint64_t i = 0; i < g.members; ++i) members[i] = id_of(st, mem[i]);
+    if (g.groups)
+      std::memcpy(group_start, gs.data(), (g.groups + 1) * sizeof(uint64_t));
+    else
+      group_start[0] = 0;
+  });
 }
-int nd_dedup(nd_ctx* ctx, const uint8_t*, const uint64_t*, const uint64_t*, uint64_t,
-             const nd_params*, nd_dedup_stats*) {
-  return guarded_impl(ctx, [&] { fail(ND_ERR_INTERNAL, "not implemented"); });
+
+int nd_dedup_write_report(nd_ctx* ctx, const char* dir, uint64_t total_records) {
+  return guarded_impl(ctx, [&] {
+    DedupState& st = ctx->dedup;
+    if (!st.valid) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");
+    cudaStream_t s = ctx->stream;
+    const GroupSet& g = st.groups;
+    auto mem = d2h(g.member_rows, g.members, s);
+    auto gs = d2h(g.group_start, g.groups ? g.groups + 1 : 0, s);
+    auto near = d2h(g.near, g.members, s);
+    auto rem = d2h(g.removal, g.removals, s);
+    ND_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint64_t> members(mem.size()), nearv(near.size()), remv(rem.size());
+    for (size_t i = 0; i < mem.size(); ++i) members[i] = id_of(st, mem[i]);
+    for (size_t i = 0; i < near.size(); ++i) nearv[i] = id_of(st, near[i]);
+    for (size_t i = 0; i < rem.size(); ++i) remv[i] = id_of(st, rem[i]);
+    write_report(dir, members, gs, nearv, remv, st.documents,
+                 total_records ? total_records : st.documents, st.pairs.distinct);
+  });
 }
-int nd_dedup_device(nd_ctx* ctx, const uint8_t*, const uint64_t*, const uint64_t*, uint64_t,
-                    const nd_params*, nd_dedup_stats*) {
-  return guarded_impl(ctx, [&] { fail(ND_ERR_INTERNAL, "not implemented"); });
+
+// ---- stage entry points over caller-provided signatures / cells / pairs -----
+
+int nd_band_keys(nd_ctx* ctx, const uint32_t* sigs, uint64_t n, uint32_t H, uint32_t bands,
+                 uint32_t rows, uint32_t K, uint32_t* band_out) {
+  return guarded_impl(ctx, [&] {
+    // band_bucket_ids' shape checks (lsh.cpp:45-51)
+    if (bands == 0 || rows == 0) fail(ND_ERR_CONFIG, "bands and rows must be positive");
+    if (static_cast<uint64_t>(bands) * rows != H)
+      fail(ND_ERR_CONFIG, "signature has " + std::to_string(H) + " values, banding needs " +
+                              std::to_string(bands) + "*" + std::to_string(rows));
+    if (n == 0) return;
+    DedupState& st = ctx->api;
+    cudaStream_t s = ctx->stream;
+    uint32_t* d_sig = st.sig.as<uint32_t>(n * H);
+    uint32_t* d_band = st.band.as<uint32_t>(n * bands);
+    uint32_t* d_docs = st.cells.rec_vals.as<uint32_t>(n);
+    ND_CUDA(cudaMemcpyAsync(d_sig, sigs, n * H * 4, cudaMemcpyHostToDevice, s));
+    launch_band_keys(d_sig, n, H, bands, rows, K, d_band, d_docs, s);
+    ND_CUDA(cudaMemcpyAsync(band_out, d_band, n * bands * 4, cudaMemcpyDeviceToHost, s));
+    ND_CUDA(cudaStreamSynchronize(s));
+  });
 }
-int nd_dedup_fetch_pairs(nd_ctx* ctx, uint64_t*, uint64_t*, uint32_t*) {
-  return guarded_impl(ctx, [&] { fail(ND_ERR_INTERNAL, "not implemented"); });
+
+int nd_compare_cells(nd_ctx* ctx, const uint32_t* sigs, uint64_t nrows, uint32_t H,
+                     const uint64_t* cell_offsets, const uint32_t* cell_rows, uint64_t ncells,
+                     uint64_t num, uint64_t den, uint64_t* npairs_out) {
+  return guarded_impl(ctx, [&] {
+    if (H == 0) fail(ND_ERR_CONFIG, "hash count must be positive");
+    if (den == 0) fail(ND_ERR_CONFIG, "ratio denominator must be positive");
+    DedupState& st = ctx->api;
+    cudaStream_t s = ctx->stream;
+    st.valid = false;
+    const uint64_t total = ncells ? cell_offsets[ncells] : 0;
+    for (uint64_t c = 0; c < ncells; ++c) {
+      if (cell_offsets[c + 1] < cell_offsets[c]) fail(ND_ERR_CONFIG, "cell offsets must ascend");
+      for (uint64_t k = cell_offsets[c]; k < cell_offsets[c + 1]; ++k) {
+        if (cell_rows[k] >= nrows) fail(ND_ERR_CONFIG, "cell row out of range");
+        if (k > cell_offsets[c] && cell_rows[k] <= cell_rows[k - 1])
+          fail(ND_ERR_CONFIG, "rows inside a cell must ascend");
+      }
+    }
+    uint32_t* d_sig = st.sig.as<uint32_t>(nrows * H + 1);
+    if (nrows) ND_CUDA(cudaMemcpyAsync(d_sig, sigs, nrows * H * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    // cells as records: key = cell index, value = row; stable grouping keeps the order
+    std::vector<uint32_t> keys(total), vals(cell_rows, cell_rows + total);
+    for (uint64_t c = 0; c < ncells; ++c)
+      for (uint64_t k = cell_offsets[c]; k < cell_offsets[c + 1]; ++k) keys[k] = static_cast<uint32_t>(c);
+    uint32_t* dk = st.cells.rec_keys.as<uint32_t>(total + 1);
+    uint32_t* dv = st.cells.rec_vals.as<uint32_t>(total + 1);
+    if (total) {
+      ND_CUDA(cudaMemcpyAsync(dk, keys.data(), total * 4, cudaMemcpyHostToDevice, s));
+      ND_CUDA(cudaMemcpyAsync(dv, vals.data(), total * 4, cudaMemcpyHostToDevice, s));
+    }
+    build_cells_from_records(st.cells, dk, dv, total, ncells ? ncells : 1, kCmpRows, s);
+    compare_and_unique(st, d_sig, H, min_matches(H, num, den), nrows, s);
+    ND_CUDA(cudaStreamSynchronize(s));
+    st.doc_ids.clear();
+    st.documents = nrows;
+    st.valid = true;
+    *npairs_out = st.pairs.distinct;
+  });
 }
-int nd_dedup_fetch_groups(nd_ctx* ctx, uint64_t*, uint64_t*) {
-  return guarded_impl(ctx, [&] { fail(ND_ERR_INTERNAL, "not implemented"); });
+
+int nd_pairs_fetch(nd_ctx* ctx, uint32_t* lo, uint32_t* hi, uint32_t* match_count) {
+  return guarded_impl(ctx, [&] {
+    DedupState& st = ctx->api;
+    if (!st.valid) fail(ND_ERR_PREREQ, "no compare result; run nd_compare_cells first");
+    cudaStream_t s = ctx->stream;
+    const uint64_t d = st.pairs.distinct;
+    if (d) {
+      if (lo) ND_CUDA(cudaMemcpyAsync(lo, st.pairs.lo, d * 4, cudaMemcpyDeviceToHost, s));
+      if (hi) ND_CUDA(cudaMemcpyAsync(hi, st.pairs.hi, d * 4, cudaMemcpyDeviceToHost, s));
+      if (match_count) ND_CUDA(cudaMemcpyAsync(match_count, st.pairs.mc, d * 4, cudaMemcpyDeviceToHost, s));
+    }
+    ND_CUDA(cudaStreamSynchronize(s));
+  });
 }
-int nd_dedup_write_report(nd_ctx* ctx, const char*, uint64_t) {
-  return guarded_impl(ctx, [&] { fail(ND_ERR_INTERNAL, "not implemented"); });
+
+int nd_union(nd_ctx* ctx, const uint32_t* lo, const uint32_t* hi, uint64_t npairs, uint32_t nnodes,
+             uint64_t* nmembers_out, uint64_t* ngroups_out) {
+  return guarded_impl(ctx, [&] {
+    DedupState& st = ctx->api2;
+    cudaStream_t s = ctx->stream;
+    st.valid = false;
+    for (uint64_t i = 0; i < npairs; ++i)
+      if (lo[i] >= nnodes || hi[i] >= nnodes) fail(ND_ERR_CONFIG, "pair endpoint out of range");
+    uint32_t* dlo = st.pairs.dlo.as<uint32_t>(npairs + 1);
+    uint32_t* dhi = st.pairs.dhi.as<uint32_t>(npairs + 1);
+    if (npairs) {
+      ND_CUDA(cudaMemcpyAsync(dlo, lo, npairs * 4, cudaMemcpyHostToDevice, s));
+      ND_CUDA(cudaMemcpyAsync(dhi, hi, npairs * 4, cudaMemcpyHostToDevice, s));
+    }
+    components(st.groups, dlo, dhi, npairs, nnodes, s);
+    ND_CUDA(cudaStreamSynchronize(s));
+    st.valid = true;
+    *nmembers_out = st.groups.members;
+    *ngroups_out = st.groups.groups;
+  });
+}
+
+int nd_groups_fetch(nd_ctx* ctx, uint32_t* members, uint64_t* group_start) {
+  return guarded_impl(ctx, [&] {
+    DedupState& st = ctx->api2;
+    if (!st.valid) fail(ND_ERR_PREREQ, "no union result; run nd_union first");
+    cudaStream_t s = ctx->stream;
+    const GroupSet& g = st.groups;
+    if (g.members) ND_CUDA(cudaMemcpyAsync(members, g.member_rows, g.members * 4, cudaMemcpyDeviceToHost, s));
+    if (g.groups)
+      ND_CUDA(cudaMemcpyAsync(group_start, g.group_start, (g.groups + 1) * 8, cudaMemcpyDeviceToHost, s));
+    else
+      group_start[0] = 0;
+    ND_CUDA(cudaStreamSynchronize(s));
+  });
 }
 
 }  // extern "C"

@@ -110,25 +110,114 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
                        uint32_t* d_band, SigScratch& scratch, cudaStream_t stream,
                        bool check_short, const uint64_t* h_offsets);
 
+// Scratch for radix_sort_* (k_sort.cu).
+struct SortScratch {
+  DevBuf keys_alt, vals_alt, hist, offs, scan;
+  void release() {
+    for (DevBuf* b : {&keys_alt, &vals_alt, &hist, &offs, &scan}) b->release();
+  }
+};
+// Stable LSD radix sort of (key, value) pairs by the low key_bits bits.
+void radix_sort_u32(uint32_t* keys, uint32_t* vals, uint64_t n, int key_bits, SortScratch& sc,
+                    cudaStream_t s);
+void radix_sort_u64(uint64_t* keys, uint32_t* vals, uint64_t n, int key_bits, SortScratch& sc,
+                    cudaStream_t s);
+
+int bits_for(uint64_t maxval);  // number of bits needed to hold maxval
+
+// K2 output: non-singleton LSH cells as CSR over sorted rows (k_cells.cu).
+constexpr uint32_t kCmpRows = 128;  // rows per compare work item
+struct CellSet {
+  DevBuf rec_keys, rec_vals, flag, run_idx, run_start, cstart, clen, ckey, cpairs, ctiles, pair_off,
+      ioff, icell, scan;
+  SortScratch sort;
+  uint64_t records = 0, ncells = 0, items = 0, candidate_pairs = 0;
+  const uint32_t* sorted_rows = nullptr;  // rows of all records, grouped by cell
+  uint64_t* cell_start = nullptr;         // per non-singleton cell
+  uint32_t* cell_len = nullptr;
+  uint32_t* cell_key = nullptr;           // band*K + bucket
+  uint64_t* item_off = nullptr;           // per cell: first compare item
+  uint32_t* item_cell = nullptr;          // per item: its cell
+  void release() {
+    for (DevBuf* b : {&rec_keys, &rec_vals, &flag, &run_idx, &run_start, &cstart, &clen, &ckey,
+                      &cpairs, &ctiles, &pair_off, &ioff, &icell, &scan})
+      b->release();
+    sort.release();
+  }
+};
+// records: keys = cell ids (< key_limit), vals = rows; both are permuted.
+void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint64_t m,
+                              uint64_t key_limit, uint32_t tile_rows, cudaStream_t s);
+void build_cells_from_bands(CellSet& cs, const uint32_t* band, uint64_t n, uint32_t bands,
+                            uint32_t K, uint32_t tile_rows, cudaStream_t s);
+
+// K3 output: accepted pairs, packed keys lo << nb | hi with match counts.
+struct PairSet {
+  DevBuf dkeys, dvals, dcount, flag, idx, scan, dlo, dhi, dmc;
+  SortScratch sort;
+  uint64_t* keys = nullptr;
+  uint32_t* vals = nullptr;
+  unsigned long long* counter = nullptr;
+  uint64_t cap = 0, count = 0, distinct = 0;
+  int nb = 1;
+  uint32_t *lo = nullptr, *hi = nullptr, *mc = nullptr;  // distinct, sorted by (lo, hi)
+  void release() {
+    for (DevBuf* b : {&dkeys, &dvals, &dcount, &flag, &idx, &scan, &dlo, &dhi, &dmc}) b->release();
+    sort.release();
+  }
+};
+int compare_prefilter_width(uint32_t H, uint32_t min_match);
+void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32_t min_match,
+                    int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,
+                    uint64_t cap, cudaStream_t s);
+uint64_t unique_pairs(PairSet& ps, cudaStream_t s);
+
+// K4 output: components as groups of rows (k_union.cu).
+struct GroupSet {
+  DevBuf parent, flagbuf, in_edge, idx, keys, vals, rflag, dnear, ridx, gflag, gidx, gstart, drem,
+      scan;
+  SortScratch sort;
+  uint64_t members = 0, groups = 0, removals = 0;
+  uint32_t* member_rows = nullptr;  // groups by representative, members ascending
+  uint64_t* group_start = nullptr;  // groups + 1
+  uint32_t* near = nullptr;         // all members, ascending
+  uint32_t* removal = nullptr;      // members that are not representatives, ascending
+  void release() {
+    for (DevBuf* b : {&parent, &flagbuf, &in_edge, &idx, &keys, &vals, &rflag, &dnear, &ridx,
+                      &gflag, &gidx, &gstart, &drem, &scan})
+      b->release();
+    sort.release();
+  }
+};
+void components(GroupSet& gs, const uint32_t* lo, const uint32_t* hi, uint64_t e, uint64_t n,
+                cudaStream_t s);
+
 // State of the last dedup run held by a context (results stay on device
 // until fetched).
 struct DedupState {
-  DevBuf sig, band, cell_count, cell_off, cell_docs, cand, pairs, pairs_tmp, labels, tmp, tmp2,
-      sort_tmp, stats;
-  std::vector<uint64_t> doc_ids;        // row -> doc id
-  std::vector<uint64_t> pair_lo, pair_hi;
-  std::vector<uint32_t> pair_m;
-  std::vector<uint64_t> members, group_start;
-  uint64_t documents = 0, distinct_pairs = 0;
+  DevBuf sig, band, text, offs;
+  CellSet cells;
+  PairSet pairs;
+  GroupSet groups;
+  SigScratch sig_scratch;
+  std::vector<uint64_t> doc_ids;  // row -> doc id (empty = identity)
+  uint64_t documents = 0;
+  uint32_t K = 0;
   bool valid = false;
   void release() {
-    for (DevBuf* b : {&sig, &band, &cell_count, &cell_off, &cell_docs, &cand, &pairs, &pairs_tmp,
-                      &labels, &tmp, &tmp2, &sort_tmp, &stats})
-      b->release();
+    for (DevBuf* b : {&sig, &band, &text, &offs}) b->release();
+    cells.release();
+    pairs.release();
+    groups.release();
+    sig_scratch.release();
   }
 };
 
-// exclusive scan of u64 counts (n entries) into out (n+1 entries, out[n] = total)
+// band keys for n signature rows already on the device (d_docs: n scratch words)
+void launch_band_keys(const uint32_t* d_sig, uint64_t n, uint32_t H, uint32_t bands, uint32_t rows,
+                      uint32_t K, uint32_t* d_band, uint32_t* d_docs, cudaStream_t s);
+
+// exclusive scan of counts (n entries) into out (n+1 entries, out[n] = total)
 void scan_u64(const uint64_t* d_in, uint64_t* d_out, uint64_t n, DevBuf& tmp, cudaStream_t s);
 void scan_u32_to_u64(const uint32_t* d_in, uint64_t* d_out, uint64_t n, DevBuf& tmp,
                      cudaStream_t s);

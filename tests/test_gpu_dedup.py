@@ -1,0 +1,244 @@
+"""K2-K4 parity: compare, union and full dedup vs the reference itself.
+
+Follows the reference's own tests: test_compare.cpp (tiled == naive over
+n in {2,3,31,32,33,64} x thresholds, cross-band repeat suppression),
+test_dedup_graph.cpp (transitive closure, order/repeat invariance, long
+chains, min representative), and test_pipeline.cpp / acceptance 6 for whole
+runs: groups.jsonl, removal.txt and summary.json must be byte-identical with
+the reference's run_dedup on the same corpus, and candidate_pairs must match
+the reference's compare_stage.json counter.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2501_01046_b200 import _lib, compare, dedup_graph, lsh, minhash, pipeline
+from paper_2501_01046_b200.compare import DuplicatePair, GatheredBucket, GatherResult, SimilarityThreshold
+
+pytestmark = pytest.mark.gpu
+
+
+def random_bucket(n, H, seed, alphabet=3):
+    rng = np.random.default_rng(seed)
+    b = GatheredBucket(lsh.BucketKey(0, 0), [i * 3 + 1 for i in range(n)],
+                       rng.integers(0, alphabet, size=n * H).astype(np.uint32))
+    return b
+
+
+def naive(bucket, H, thr):
+    n = len(bucket.doc_ids)
+    sig = bucket.signatures.reshape(n, H)
+    out = []
+    for i in range(n):
+        for j in range(i + 1, n):
+            m = int((sig[i] == sig[j]).sum())
+            if thr.accepts(m, H):
+                out.append(DuplicatePair(bucket.doc_ids[i], bucket.doc_ids[j], m))
+    return sorted(out, key=lambda p: (p.lo, p.hi))
+
+
+@pytest.mark.parametrize("n", [2, 3, 31, 32, 33, 64, 127, 128, 129, 300])
+@pytest.mark.parametrize("thr", [(1, 4), (1, 2), (3, 4)])
+def test_compare_bucket_equals_naive(ctx, n, thr):
+    t = SimilarityThreshold(thr)
+    b = random_bucket(n, 8, 1000 + n)
+    assert compare.compare_bucket(b, 8, t, ctx=ctx) == naive(b, 8, t)
+
+
+@pytest.mark.parametrize("H,thr", [(128, (4, 5)), (256, (4, 5)), (64, (1, 2)), (16, (9, 10)),
+                                   (128, (0, 1)), (128, (1, 1))])
+def test_compare_planted_rows_vs_reference(ctx, ref, H, thr):
+    # rows derived from a few bases with controlled mutation rates so match
+    # counts straddle the threshold; many cells, sizes across tile boundaries
+    rng = np.random.default_rng(H)
+    buckets = []
+    for c, n in enumerate([2, 5, 40, 129, 260]):
+        base = rng.integers(0, 1 << 22, size=H).astype(np.uint32)
+        sig = np.tile(base, (n, 1))
+        for r in range(n):
+            k = int(rng.integers(0, H // 3))
+            pos = rng.choice(H, size=k, replace=False)
+            sig[r, pos] = rng.integers(0, 1 << 22, size=k)
+        buckets.append(GatheredBucket(lsh.BucketKey(c, 0), list(range(c * 1000, c * 1000 + n)),
+                                      sig.reshape(-1)))
+    t = SimilarityThreshold(thr)
+    got = compare.compare_pass(GatherResult(buckets), H, t, ctx=ctx)
+    allsig = np.concatenate([b.signatures.reshape(-1, H) for b in buckets])
+    ids = np.concatenate([b.doc_ids for b in buckets]).astype(np.uint64)
+    offs = np.cumsum([0] + [len(b.doc_ids) for b in buckets]).astype(np.uint64)
+    lo, hi, m = ref.compare_cells(allsig, offs, np.arange(len(ids), dtype=np.uint32), *thr,
+                                  doc_ids=ids)
+    want = [DuplicatePair(int(a), int(b), int(c)) for a, b, c in zip(lo, hi, m)]
+    assert got == want
+    if thr != (1, 1):
+        assert got  # planted rows guarantee accepted pairs
+
+
+def test_compare_pass_drops_cross_band_repeats(ctx):
+    # test_compare.cpp:113-130
+    first = GatheredBucket(lsh.BucketKey(0, 1), [10, 20], np.array([1, 2, 3, 4, 1, 2, 3, 9], np.uint32))
+    second = GatheredBucket(lsh.BucketKey(1, 4), [10, 20], first.signatures.copy())
+    pairs = compare.compare_pass(GatherResult([first, second]), 4, SimilarityThreshold((1, 2)), ctx=ctx)
+    assert pairs == [DuplicatePair(10, 20, 3)]
+
+
+def test_compare_validates(ctx):
+    b = random_bucket(4, 8, 2)
+    t = SimilarityThreshold((1, 2))
+    with pytest.raises(_lib.ConfigError):
+        compare.compare_bucket(b, 0, t, ctx=ctx)
+    with pytest.raises(_lib.ConfigError):
+        compare.compare_bucket(b, 8, t, tile_size=0, ctx=ctx)
+    b.signatures = b.signatures[:-1]
+    with pytest.raises(_lib.ConfigError):
+        compare.compare_bucket(b, 8, t, ctx=ctx)
+
+
+def groups_of(pairs, ctx):
+    return dedup_graph.components(dedup_graph.union_pairs(
+        [DuplicatePair(a, b, 9) for a, b in pairs], ctx=ctx))
+
+
+def test_components_closure_and_representatives(ctx):
+    g = groups_of([(1, 2), (2, 3), (8, 9)], ctx)
+    assert [(x.representative, x.members) for x in g] == [(1, [1, 2, 3]), (8, [8, 9])]
+    g = groups_of([(50, 7), (99, 50), (3, 2)], ctx)
+    assert [(x.representative, x.members) for x in g] == [(2, [2, 3]), (7, [7, 50, 99])]
+    g = groups_of([(i, i + 1) for i in range(1000)], ctx)
+    assert len(g) == 1 and g[0].representative == 0 and len(g[0].members) == 1001
+    assert groups_of([], ctx) == []
+
+
+def test_components_order_and_repeats_invariant(ctx):
+    pairs = [(1, 2), (2, 3), (3, 4), (10, 11), (11, 12), (1, 4), (20, 21)]
+    want = groups_of(pairs, ctx)
+    rng = np.random.default_rng(5)
+    for trial in range(10):
+        sh = [pairs[i] for i in rng.permutation(len(pairs))]
+        if trial % 2:
+            sh = sh + pairs
+        assert groups_of(sh, ctx) == want
+
+
+def test_components_random_graphs_vs_reference(ctx, ref):
+    rng = np.random.default_rng(9)
+    for n_nodes, n_edges in [(50, 40), (2000, 1500), (100000, 60000)]:
+        lo = rng.integers(0, n_nodes, size=n_edges)
+        hi = rng.integers(0, n_nodes, size=n_edges)
+        keep = lo != hi
+        lo, hi = np.minimum(lo, hi)[keep] * 7 + 3, np.maximum(lo, hi)[keep] * 7 + 3
+        rep, mem = ref.union(lo.astype(np.uint64), hi.astype(np.uint64))
+        g = groups_of(list(zip(lo.tolist(), hi.tolist())), ctx)
+        got = [(x.representative, m) for x in g for m in x.members]
+        assert got == list(zip(rep.tolist(), mem.tolist()))
+
+
+def test_emit_report(ctx):
+    r = dedup_graph.emit_report(groups_of([(1, 2), (5, 6), (6, 7)], ctx), 100, 3)
+    assert r.near_duplicates == [1, 2, 5, 6, 7] and r.removals == [2, 6, 7]
+    assert r.ratio == pytest.approx(0.05) and r.distinct_pairs == 3
+    r = dedup_graph.emit_report([], 42, 0)
+    assert r.groups == [] and r.ratio == 0.0
+
+
+# ---- whole runs vs the reference's run_dedup ---------------------------------
+
+def _files(ws):
+    return {f: open(os.path.join(ws, f), "rb").read()
+            for f in ("groups.jsonl", "removal.txt", "summary.json")}
+
+
+def _run_both(ref, tmp_path, corpus_kwargs, cfg_kwargs, ctx):
+    corpus = str(tmp_path / "corpus.jsonl")
+    truth = str(tmp_path / "truth.jsonl")
+    ref.generate_synthetic(corpus_path=corpus, truth_path=truth, **corpus_kwargs)
+    ws_ref = str(tmp_path / "ws_ref")
+    ws_gpu = str(tmp_path / "ws_gpu")
+    os.makedirs(ws_ref)
+    H = cfg_kwargs.get("hash_count", 128)
+    bands = cfg_kwargs.get("bands", 16)
+    rows = cfg_kwargs.get("rows", 8)
+    thr = cfg_kwargs.get("threshold", (4, 5))
+    ref.run_dedup(corpus, ws_ref, H=H, bands=bands, rows=rows, thr=thr, workers=os.cpu_count())
+    cfg = pipeline.RunConfig(inputs=[corpus], workspace=ws_gpu, **cfg_kwargs)
+    rep = pipeline.run_dedup(cfg, ctx=ctx)
+    stage = json.load(open(os.path.join(ws_ref, "compare_stage.json")))
+    return _files(ws_ref), _files(ws_gpu), rep, stage
+
+
+def test_c1_dedup_byte_identical(ctx, ref, tmp_path):
+    # 10k docs, 500 planted pairs, 1600-2400 B, seed 1
+    want, got, rep, stage = _run_both(
+        ref, tmp_path, dict(doc_count=10000, group_count=500, len_min=1600, len_max=2400, seed=1),
+        {}, ctx)
+    assert got == want
+    assert rep.candidate_pairs == stage["candidate_pairs"] == 4006931
+    s = json.loads(want["summary.json"])
+    assert s["duplicate_groups"] == 500 and s["near_duplicates"] == 1000
+    assert want["groups.jsonl"].startswith(b'{"representative":14,"members":[14,549]}')
+
+
+def test_dedup_h256_groups_of_five_byte_identical(ctx, ref, tmp_path):
+    want, got, rep, stage = _run_both(
+        ref, tmp_path, dict(doc_count=4000, group_count=300, gmin=2, gmax=5, edit=(3, 100),
+                            len_min=300, len_max=900, seed=7),
+        dict(hash_count=256, bands=32, rows=8), ctx)
+    assert got == want
+    assert rep.candidate_pairs == stage["candidate_pairs"]
+
+
+@pytest.mark.parametrize("thr", [(1, 2), (9, 10)])
+def test_dedup_thresholds_byte_identical(ctx, ref, tmp_path, thr):
+    want, got, rep, stage = _run_both(
+        ref, tmp_path, dict(doc_count=3000, group_count=200, gmin=2, gmax=4, edit=(8, 100),
+                            len_min=250, len_max=700, seed=11),
+        dict(threshold=thr), ctx)
+    assert got == want
+    assert rep.candidate_pairs == stage["candidate_pairs"]
+
+
+def test_long_document_skew_vs_reference(ctx, ref, tmp_path):
+    # lognormal lengths up to 60 KB (multi-item K1 path, skewed big cells)
+    spec = _lib.NdSynthSpec(doc_count=1500, group_count=150, group_size_min=2, group_size_max=6,
+                            edit_num=1, edit_den=100, len_min=3000, len_max=60000, seed=3,
+                            mode=1, len_law=1, sigma_milli=1200)
+    import ctypes as C
+
+    lib = _lib.load()
+    nb = C.c_uint64()
+    _lib.check(lib.nd_synth_generate(C.byref(spec), None, None, C.byref(nb)))
+    data = np.empty(nb.value, np.uint8)
+    offs = np.empty(spec.doc_count + 1, np.uint64)
+    _lib.check(lib.nd_synth_generate(C.byref(spec), data.ctypes.data_as(_lib.u8p),
+                                     offs.ctypes.data_as(_lib.u64p), C.byref(nb)))
+    assert np.diff(offs).max() > 8196  # exercises multi-item documents
+    corpus = str(tmp_path / "skew.jsonl")
+    with open(corpus, "w") as f:
+        for i in range(spec.doc_count):
+            f.write(json.dumps({"text": bytes(data[offs[i]:offs[i + 1]]).decode()}) + "\n")
+    ws_ref, ws_gpu = str(tmp_path / "r"), str(tmp_path / "g")
+    os.makedirs(ws_ref)
+    ref.run_dedup(corpus, ws_ref, workers=os.cpu_count())
+    rep = pipeline.run_dedup(pipeline.RunConfig(inputs=[corpus], workspace=ws_gpu), ctx=ctx)
+    assert _files(ws_gpu) == _files(ws_ref)
+    assert rep.candidate_pairs == json.load(open(os.path.join(ws_ref, "compare_stage.json")))["candidate_pairs"]
+
+
+def test_dedup_pairs_match_reference_pair_files(ctx, ref, tmp_path):
+    # distinct pair set (lo, hi, match_count) vs the reference's .pairs files
+    corpus = str(tmp_path / "c.jsonl")
+    ref.generate_synthetic(2000, 150, gmin=2, gmax=3, len_min=300, len_max=800, seed=5,
+                           corpus_path=corpus, truth_path=str(tmp_path / "t.jsonl"))
+    ws_ref = str(tmp_path / "r")
+    os.makedirs(ws_ref)
+    ref.run_dedup(corpus, ws_ref, workers=4)
+    want = set()
+    for f in os.listdir(os.path.join(ws_ref, "pairs")):
+        for p in compare.read_pair_file(os.path.join(ws_ref, "pairs", f)):
+            want.add((p.lo, p.hi, p.match_count))
+    rep = pipeline.run_dedup(pipeline.RunConfig(inputs=[corpus], workspace=str(tmp_path / "g")),
+                             ctx=ctx)
+    got = pipeline.dedup_pairs(rep.distinct_pairs, ctx=ctx)
+    assert [(p.lo, p.hi, p.match_count) for p in got] == sorted(want)
