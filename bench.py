@@ -308,21 +308,30 @@ def main():
 
             if hasattr(pipeline, "dedup_packed") and world == 1:
                 cfg = pipeline.RunConfig()
-                pipeline.dedup_packed(data, offs, cfg, ctx=ctx)  # warm-up
+                pipeline.dedup_packed(data, offs, cfg, ctx=ctx, fetch="arrays")  # warm-up
                 barrier()
-                reps = max(1, min(3, args.steps))
+                reps = max(1, min(5, args.steps))
                 d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 d0.record(stream)
                 for _ in range(reps):
-                    rep = pipeline.dedup_packed(data, offs, cfg, ctx=ctx)
+                    rep = pipeline.dedup_packed(data, offs, cfg, ctx=ctx, fetch="arrays")
                 d1.record(stream)
                 barrier()
                 dms = d0.elapsed_time(d1) / reps
+                st = rep.stats
                 dedup = {"value": docs / (dms / 1e3), "unit": "docs/s", "ms_per_run": dms,
-                         "groups": len(rep.groups), "distinct_pairs": rep.distinct_pairs,
-                         "candidate_pairs": getattr(rep, "candidate_pairs", None),
-                         "note": "in-memory run_dedup equivalent: host packed batch -> "
-                                 "DedupReport in host memory (H2D, K1-K4, D2H)"}
+                         "groups": st["duplicate_groups"], "near_duplicates": st["near_duplicates"],
+                         "distinct_pairs": st["distinct_pairs"],
+                         "candidate_pairs": st["candidate_pairs"],
+                         "emitted_pairs": st["emitted_pairs"], "cells": st["nonsingleton_cells"],
+                         "stage_seconds": {"h2d+k1_signatures": st["seconds"][0],
+                                           "k2_cells": st["seconds"][1],
+                                           "k3_compare+k4_unique": st["seconds"][2],
+                                           "k4_components": st["seconds"][4]},
+                         "candidate_pairs_per_s": st["candidate_pairs"] / st["seconds"][2]
+                         if st["seconds"][2] else None,
+                         "note": "in-memory run_dedup equivalent per GPU shard: pinned host "
+                                 "packed batch -> groups in host memory (H2D, K1-K4, D2H)"}
         except ImportError:
             dedup = None
 
@@ -345,9 +354,11 @@ def main():
     hbm_bytes = nbytes + 8 * (docs + 1) + 4 * docs * (H + BANDS)
     hbm_gbs = hbm_bytes / (k1_ms / 1e3) / 1e9
     hbm_peak = peaks.get("hbm_gbs", 6544.3)
-    traffic = load_traffic()
+    traffic_info = load_traffic()
+    traffic = traffic_info.get("bytes_per_launch") if traffic_info else None
     roofline = {"bound": "int_alu", "achieved": achieved, "peak": peak_run,
                 "unit": "T int-ops/s", "frac": achieved / peak_run, "traffic": traffic,
+                "traffic_unit": "dram bytes per launch (ncu --set full, profiles/k1_traffic.json)",
                 "work": f"{OPS_PER_HWE} int ops x {hwe:.4g} hash-window evals per launch "
                         "(sum over docs of (len-L+1)*H)",
                 "peak_basis": f"{sms} SMs x 128 lanes x measured SM clock "

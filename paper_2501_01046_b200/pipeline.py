@@ -106,10 +106,17 @@ class RunConfig:
                         scale_num=sn, scale_den=sd, seed=self.seed)
 
 
-def _fetch_report(ctx: Context, stats: NdDedupStats) -> DedupReport:
+def _fetch_report(ctx: Context, stats: NdDedupStats, lists: bool = True) -> DedupReport:
     mem = np.empty(stats.near_duplicates, np.uint64)
     gs = np.empty(stats.duplicate_groups + 1, np.uint64)
     ctx.check(ctx.lib.nd_dedup_fetch_groups(ctx.h, mem.ctypes.data_as(u64p), gs.ctypes.data_as(u64p)))
+    if not lists:  # arrays only: members in group order + group offsets
+        rep = DedupReport(total_documents=stats.documents, distinct_pairs=stats.distinct_pairs)
+        rep.candidate_pairs = stats.candidate_pairs
+        rep.group_members, rep.group_start = mem, gs
+        rep.stats = {k: getattr(stats, k) for k, _ in NdDedupStats._fields_ if k != "seconds"}
+        rep.stats["seconds"] = list(stats.seconds)
+        return rep
     groups = []
     for g in range(stats.duplicate_groups):
         m = mem[int(gs[g]):int(gs[g + 1])].tolist()
@@ -127,10 +134,12 @@ def _fetch_report(ctx: Context, stats: NdDedupStats) -> DedupReport:
 
 def dedup_packed(data: np.ndarray, offsets: np.ndarray, config: RunConfig | None = None,
                  doc_ids: np.ndarray | None = None, bucket_count: int = 0,
-                 ctx: Context | None = None, fetch: bool = True) -> DedupReport:
+                 ctx: Context | None = None, fetch="lists") -> DedupReport:
     """In-memory run_dedup over a packed batch of surviving documents (host buffers).
 
-    doc_ids (ascending) default to 0..n-1.  bucket_count 0 = choose_bucket_count(n)."""
+    doc_ids (ascending) default to 0..n-1.  bucket_count 0 = choose_bucket_count(n).
+    fetch: "lists" (DuplicateGroup objects), "arrays" (numpy members + offsets),
+    or None (statistics only; results stay on the device)."""
     config = config or RunConfig()
     config.validate()
     ctx = ctx or default_context()
@@ -148,7 +157,7 @@ def dedup_packed(data: np.ndarray, offsets: np.ndarray, config: RunConfig | None
         rep = DedupReport(total_documents=stats.documents, distinct_pairs=stats.distinct_pairs)
         rep.candidate_pairs = stats.candidate_pairs
         return rep
-    return _fetch_report(ctx, stats)
+    return _fetch_report(ctx, stats, lists=(fetch != "arrays"))
 
 
 def dedup_pairs(distinct_pairs: int, ctx: Context | None = None):
