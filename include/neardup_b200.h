@@ -114,6 +114,11 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t hash_count,
 int nd_signatures(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
                   uint32_t bands, uint32_t rows, uint32_t bucket_count, uint32_t* sig_out,
                   uint32_t* band_out);
+/* Host text in, device outputs: the same pipelined H2D + K1 as nd_signatures
+ * but d_sig / d_band stay in HBM (input of the dedup stages).  Synchronous. */
+int nd_signatures_h2d(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                      uint32_t bands, uint32_t rows, uint32_t bucket_count, uint32_t* d_sig,
+                      uint32_t* d_band);
 /* Same on device pointers, asynchronous on the ctx stream. */
 int nd_signatures_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offsets,
                          uint64_t n, uint32_t bands, uint32_t rows, uint32_t bucket_count,
@@ -170,6 +175,30 @@ int nd_dedup_fetch_groups(nd_ctx* ctx, uint64_t* members, uint64_t* group_start)
 /* Reference-identical report bytes (groups.jsonl, removal.txt, summary.json
  * as written by pipeline.cpp:479-506) for the last dedup, into dir. */
 int nd_dedup_write_report(nd_ctx* ctx, const char* dir, uint64_t total_records);
+
+/* ---- stage entry points for the multi-GPU dedup (device pointers, async on
+ * the ctx stream unless noted).  See DESIGN.md section 7. -------------------- */
+/* (cell = band*K + bucket, doc_base + row) records of n documents' band ids,
+ * stably sorted by cell (scan_gather's grouping, sigstore.cpp:228-286);
+ * d_keys / d_vals receive n*bands entries each. */
+int nd_stage_cell_records(nd_ctx* ctx, const uint32_t* d_band, uint64_t n, uint32_t bands,
+                          uint32_t bucket_count, uint32_t doc_base, uint32_t* d_keys,
+                          uint32_t* d_vals);
+/* compare_pass over the cells of m (cell, row) records (any order; stable by
+ * arrival) against signature rows d_sig[nrows*H]; keeps the sorted distinct
+ * pairs in the ctx; synchronous; *npairs_out = their count. */
+int nd_stage_compare(nd_ctx* ctx, const uint32_t* d_sig, uint64_t nrows, uint32_t hash_count,
+                     const uint32_t* d_keys, const uint32_t* d_vals, uint64_t m,
+                     uint64_t key_limit, uint64_t threshold_num, uint64_t threshold_den,
+                     uint64_t* npairs_out, uint64_t* candidate_pairs_out);
+/* copies the pairs of the last nd_stage_compare into device buffers */
+int nd_stage_pairs_copy(nd_ctx* ctx, uint32_t* d_lo, uint32_t* d_hi, uint32_t* d_match);
+/* union stage over gathered pairs (rows < nnodes, repeats allowed): distinct
+ * pairs + components become the ctx's dedup result (nd_dedup_fetch_* and
+ * nd_dedup_write_report apply; doc ids = rows).  Synchronous. */
+int nd_stage_union(nd_ctx* ctx, const uint32_t* d_lo, const uint32_t* d_hi,
+                   const uint32_t* d_match, uint64_t npairs, uint64_t nnodes,
+                   nd_dedup_stats* stats);
 
 #ifdef __cplusplus
 }

@@ -76,6 +76,8 @@ SIGNATURES = {
     "nd_family_upload": (C.c_int, [vp, C.POINTER(NdHashFn), C.c_uint32, C.c_uint32, C.c_uint32]),
     "nd_signatures": (C.c_int, [vp, u8p, u64p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                 u32p, u32p]),
+    "nd_signatures_h2d": (C.c_int, [vp, u8p, u64p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                    C.c_uint32, vp, vp]),
     "nd_signatures_device": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_uint32, C.c_uint32,
                                        C.c_uint32, vp, vp]),
     "nd_band_keys": (C.c_int, [vp, u32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
@@ -92,6 +94,13 @@ SIGNATURES = {
     "nd_dedup_fetch_pairs": (C.c_int, [vp, u64p, u64p, u32p]),
     "nd_dedup_fetch_groups": (C.c_int, [vp, u64p, u64p]),
     "nd_dedup_write_report": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
+    "nd_stage_cell_records": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                        vp, vp]),
+    "nd_stage_compare": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, vp, C.c_uint64,
+                                   C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p]),
+    "nd_stage_pairs_copy": (C.c_int, [vp, vp, vp, vp]),
+    "nd_stage_union": (C.c_int, [vp, vp, vp, vp, C.c_uint64, C.c_uint64,
+                                 C.POINTER(NdDedupStats)]),
 }
 
 _lock = threading.Lock()

@@ -14,12 +14,13 @@ namespace ndb {
 namespace {
 
 __global__ void k_records(const uint32_t* __restrict__ band, uint64_t n, uint32_t bands,
-                          uint32_t K, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                          uint32_t K, uint32_t doc_base, uint32_t* __restrict__ keys,
+                          uint32_t* __restrict__ vals) {
   uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= n * bands) return;
   uint32_t j = static_cast<uint32_t>(i % bands);
   keys[i] = j * K + band[i];
-  vals[i] = static_cast<uint32_t>(i / bands);
+  vals[i] = doc_base + static_cast<uint32_t>(i / bands);
 }
 
 __global__ void k_heads(const uint32_t* __restrict__ keys, uint64_t m, uint32_t* __restrict__ flag) {
@@ -133,17 +134,23 @@ void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint6
   ND_CHECK_LAUNCH();
 }
 
-void build_cells_from_bands(CellSet& cs, const uint32_t* band, uint64_t n, uint32_t bands,
-                            uint32_t K, uint32_t tile_rows, cudaStream_t s) {
+void make_records(const uint32_t* band, uint64_t n, uint32_t bands, uint32_t K, uint32_t doc_base,
+                  uint32_t* keys, uint32_t* vals, cudaStream_t s) {
   const uint64_t m = n * bands;
   if (static_cast<uint64_t>(bands) * K > 0xFFFFFFFFull)
     fail(ND_ERR_CONFIG, "bands * bucket_count exceeds 2^32 cells");
-  uint32_t* keys = cs.rec_keys.as<uint32_t>(m);
-  uint32_t* vals = cs.rec_vals.as<uint32_t>(m);
   if (m) {
-    k_records<<<blocks_for(m, 256), 256, 0, s>>>(band, n, bands, K, keys, vals);
+    k_records<<<blocks_for(m, 256), 256, 0, s>>>(band, n, bands, K, doc_base, keys, vals);
     ND_CHECK_LAUNCH();
   }
+}
+
+void build_cells_from_bands(CellSet& cs, const uint32_t* band, uint64_t n, uint32_t bands,
+                            uint32_t K, uint32_t tile_rows, cudaStream_t s) {
+  const uint64_t m = n * bands;
+  uint32_t* keys = cs.rec_keys.as<uint32_t>(m);
+  uint32_t* vals = cs.rec_vals.as<uint32_t>(m);
+  make_records(band, n, bands, K, 0, keys, vals, s);
   build_cells_from_records(cs, keys, vals, m, static_cast<uint64_t>(bands) * K, tile_rows, s);
 }
 

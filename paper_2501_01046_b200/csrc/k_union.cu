@@ -114,7 +114,29 @@ __global__ void k_compact_u32(const uint32_t* __restrict__ src, const uint32_t* 
   if (i < m && flag[i]) dst[idx[i]] = src[i];
 }
 
+__global__ void k_pack_pairs(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi,
+                             const uint32_t* __restrict__ m, uint64_t count, int nb,
+                             uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= count) return;
+  uint32_t a = min(lo[i], hi[i]), b = max(lo[i], hi[i]);
+  keys[i] = (static_cast<uint64_t>(a) << nb) | b;
+  vals[i] = m ? m[i] : 0u;
+}
+
 }  // namespace
+
+void pack_pairs(PairSet& ps, const uint32_t* lo, const uint32_t* hi, const uint32_t* m,
+                uint64_t count, cudaStream_t s) {
+  ps.cap = count ? count : 1;
+  ps.keys = ps.dkeys.as<uint64_t>(ps.cap);
+  ps.vals = ps.dvals.as<uint32_t>(ps.cap);
+  ps.count = count;
+  if (count) {
+    k_pack_pairs<<<blocks_for(count, 256), 256, 0, s>>>(lo, hi, m, count, ps.nb, ps.keys, ps.vals);
+    ND_CHECK_LAUNCH();
+  }
+}
 
 uint64_t unique_pairs(PairSet& ps, cudaStream_t s) {
   const unsigned tb = 256;

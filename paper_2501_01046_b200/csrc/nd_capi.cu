@@ -63,6 +63,8 @@ nd_ctx::~nd_ctx() {
   dedup.release();
   api.release();
   api2.release();
+  h2d_state.release();
+  stage_sort.release();
   if (h2d) cudaStreamDestroy(h2d);
   if (d2h) cudaStreamDestroy(d2h);
   if (own_stream && stream) cudaStreamDestroy(stream);

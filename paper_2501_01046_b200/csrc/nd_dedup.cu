@@ -96,6 +96,47 @@ uint64_t id_of(const DedupState& st, uint32_t row) {
   return st.doc_ids.empty() ? row : st.doc_ids[row];
 }
 
+// Host text -> device signatures/band keys: chunks of <= 256 MB are copied
+// on the h2d stream and signed on the ctx stream as each lands (PCIe overlaps
+// K1).  The text stays in st.text.
+void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uint64_t* offsets,
+                    uint64_t n, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
+                    uint32_t* d_band) {
+  if (n == 0) return;
+  cudaStream_t s = ctx->stream;
+  ctx->ensure_streams();
+  const uint32_t H = ctx->fam.H;
+  const uint64_t total = offsets[n] - offsets[0];
+  uint8_t* d_text = st.text.as<uint8_t>(total + 16);
+  uint64_t* d_off = st.offs.as<uint64_t>(n + 1);
+  uint64_t* h_off = static_cast<uint64_t*>(ctx->pinned_off.get((n + 1) * sizeof(uint64_t)));
+  for (uint64_t i = 0; i <= n; ++i) h_off[i] = offsets[i] - offsets[0];
+  cudaEvent_t start;
+  ND_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  ND_CUDA(cudaEventRecord(start, s));
+  ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
+  ND_CUDA(cudaMemcpyAsync(d_off, h_off, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->h2d));
+  constexpr uint64_t kChunk = 256ull << 20;
+  std::vector<cudaEvent_t> evs;
+  for (uint64_t d0 = 0; d0 < n;) {
+    uint64_t d1 = d0 + 1;
+    while (d1 < n && h_off[d1 + 1] - h_off[d0] <= kChunk) ++d1;
+    ND_CUDA(cudaMemcpyAsync(d_text + h_off[d0], bytes + offsets[0] + h_off[d0], h_off[d1] - h_off[d0],
+                            cudaMemcpyHostToDevice, ctx->h2d));
+    cudaEvent_t ev;
+    ND_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ND_CUDA(cudaEventRecord(ev, ctx->h2d));
+    ND_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    evs.push_back(ev);
+    launch_signatures(ctx->fam, d_text, d_off + d0, d1 - d0, bands, rows, K, d_sig + d0 * H,
+                      d_band ? d_band + d0 * bands : nullptr, st.sig_scratch, s, false, h_off + d0);
+    d0 = d1;
+  }
+  // events may be destroyed once enqueued work referencing them is recorded
+  for (auto ev : evs) cudaEventDestroy(ev);
+  cudaEventDestroy(start);
+}
+
 // The shared tail of nd_dedup / nd_dedup_device: K2..K4 on the signatures and
 // band keys already in st.sig / st.band.
 void dedup_tail(nd_ctx* ctx, DedupState& st, const nd_params& p, uint64_t n, nd_dedup_stats* stats,
@@ -166,45 +207,26 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
         fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has fewer units than the shingle length");
     st.K = bucket_count_for(p, n);
     cudaStream_t s = ctx->stream;
-    ctx->ensure_streams();
     EventTimer t(s);
     t.mark();  // 0
-    // H2D in chunks on the copy stream, K1 per chunk as it lands
-    const uint64_t total = offsets[n] - offsets[0];
-    uint8_t* d_text = st.text.as<uint8_t>(total + 16);
-    uint64_t* d_off = st.offs.as<uint64_t>(n + 1);
-    uint32_t* d_sig = st.sig.as<uint32_t>(n * p.hash_count);
-    uint32_t* d_band = st.band.as<uint32_t>(n * p.bands);
-    std::vector<uint64_t> rebased(offsets, offsets + n + 1);
-    for (auto& o : rebased) o -= offsets[0];
-    uint64_t* h_off = static_cast<uint64_t*>(ctx->pinned_off.get((n + 1) * sizeof(uint64_t)));
-    std::memcpy(h_off, rebased.data(), (n + 1) * sizeof(uint64_t));
-    cudaEvent_t start;
-    ND_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-    ND_CUDA(cudaEventRecord(start, s));
-    ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
-    ND_CUDA(cudaMemcpyAsync(d_off, h_off, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->h2d));
-    constexpr uint64_t kChunk = 256ull << 20;
-    std::vector<cudaEvent_t> evs;
-    for (uint64_t d0 = 0; d0 < n;) {
-      uint64_t d1 = d0 + 1;
-      while (d1 < n && rebased[d1 + 1] - rebased[d0] <= kChunk) ++d1;
-      ND_CUDA(cudaMemcpyAsync(d_text + rebased[d0], bytes + offsets[0] + rebased[d0],
-                              rebased[d1] - rebased[d0], cudaMemcpyHostToDevice, ctx->h2d));
-      cudaEvent_t ev;
-      ND_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      ND_CUDA(cudaEventRecord(ev, ctx->h2d));
-      ND_CUDA(cudaStreamWaitEvent(s, ev, 0));
-      evs.push_back(ev);
-      launch_signatures(ctx->fam, d_text, d_off + d0, d1 - d0, p.bands, p.rows, st.K,
-                        d_sig + d0 * p.hash_count, d_band + d0 * p.bands, st.sig_scratch, s,
-                        false, h_off + d0);
-      d0 = d1;
-    }
+    h2d_signatures(ctx, st, bytes, offsets, n, p.bands, p.rows, st.K,
+                   st.sig.as<uint32_t>(n * p.hash_count), st.band.as<uint32_t>(n * p.bands));
     t.mark();  // 1
     dedup_tail(ctx, st, p, n, stats, t);
-    for (auto ev : evs) cudaEventDestroy(ev);
-    cudaEventDestroy(start);
+  });
+}
+
+int nd_signatures_h2d(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                      uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig, uint32_t* d_band) {
+  return guarded_impl(ctx, [&] {
+    ctx->require_family();
+    if (d_band && (bands == 0 || rows == 0 || static_cast<uint64_t>(bands) * rows != ctx->fam.H))
+      fail(ND_ERR_CONFIG, "banding shape does not match the hash count");
+    for (uint64_t i = 0; i < n; ++i)
+      if (offsets[i + 1] < offsets[i] || offsets[i + 1] - offsets[i] < ctx->fam.L)
+        fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has fewer units than the shingle length");
+    h2d_signatures(ctx, ctx->h2d_state, bytes, offsets, n, bands, rows, K, d_sig, d_band);
+    ND_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -283,6 +305,85 @@ int nd_dedup_write_report(nd_ctx* ctx, const char* dir, uint64_t total_records) 
     for (size_t i = 0; i < rem.size(); ++i) remv[i] = id_of(st, rem[i]);
     write_report(dir, members, gs, nearv, remv, st.documents,
                  total_records ? total_records : st.documents, st.pairs.distinct);
+  });
+}
+
+// ---- multi-GPU stage entry points (device pointers) -----------------------
+
+int nd_stage_cell_records(nd_ctx* ctx, const uint32_t* d_band, uint64_t n, uint32_t bands,
+                          uint32_t K, uint32_t doc_base, uint32_t* d_keys, uint32_t* d_vals) {
+  return guarded_impl(ctx, [&] {
+    if (bands == 0 || K == 0) fail(ND_ERR_CONFIG, "bands and bucket count must be positive");
+    cudaStream_t s = ctx->stream;
+    const uint64_t m = n * bands;
+    make_records(d_band, n, bands, K, doc_base, d_keys, d_vals, s);
+    radix_sort_u32(d_keys, d_vals, m, bits_for(static_cast<uint64_t>(bands) * K - 1),
+                   ctx->stage_sort, s);
+  });
+}
+
+int nd_stage_compare(nd_ctx* ctx, const uint32_t* d_sig, uint64_t nrows, uint32_t H,
+                     const uint32_t* d_keys, const uint32_t* d_vals, uint64_t m, uint64_t key_limit,
+                     uint64_t num, uint64_t den, uint64_t* npairs_out, uint64_t* cand_out) {
+  return guarded_impl(ctx, [&] {
+    if (H == 0) fail(ND_ERR_CONFIG, "hash count must be positive");
+    if (den == 0) fail(ND_ERR_CONFIG, "ratio denominator must be positive");
+    DedupState& st = ctx->api;
+    cudaStream_t s = ctx->stream;
+    st.valid = false;
+    uint32_t* k = st.cells.rec_keys.as<uint32_t>(m + 1);
+    uint32_t* v = st.cells.rec_vals.as<uint32_t>(m + 1);
+    if (m) {
+      ND_CUDA(cudaMemcpyAsync(k, d_keys, m * 4, cudaMemcpyDeviceToDevice, s));
+      ND_CUDA(cudaMemcpyAsync(v, d_vals, m * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    build_cells_from_records(st.cells, k, v, m, key_limit, kCmpRows, s);
+    compare_and_unique(st, d_sig, H, min_matches(H, num, den), nrows, s);
+    ND_CUDA(cudaStreamSynchronize(s));
+    st.valid = true;
+    *npairs_out = st.pairs.distinct;
+    if (cand_out) *cand_out = st.cells.candidate_pairs;
+  });
+}
+
+int nd_stage_pairs_copy(nd_ctx* ctx, uint32_t* d_lo, uint32_t* d_hi, uint32_t* d_match) {
+  return guarded_impl(ctx, [&] {
+    DedupState& st = ctx->api;
+    if (!st.valid) fail(ND_ERR_PREREQ, "no compare result; run nd_stage_compare first");
+    cudaStream_t s = ctx->stream;
+    const uint64_t d = st.pairs.distinct;
+    if (d) {
+      ND_CUDA(cudaMemcpyAsync(d_lo, st.pairs.lo, d * 4, cudaMemcpyDeviceToDevice, s));
+      ND_CUDA(cudaMemcpyAsync(d_hi, st.pairs.hi, d * 4, cudaMemcpyDeviceToDevice, s));
+      ND_CUDA(cudaMemcpyAsync(d_match, st.pairs.mc, d * 4, cudaMemcpyDeviceToDevice, s));
+    }
+  });
+}
+
+int nd_stage_union(nd_ctx* ctx, const uint32_t* d_lo, const uint32_t* d_hi, const uint32_t* d_match,
+                   uint64_t npairs, uint64_t nnodes, nd_dedup_stats* stats) {
+  return guarded_impl(ctx, [&] {
+    DedupState& st = ctx->dedup;
+    cudaStream_t s = ctx->stream;
+    st.valid = false;
+    st.doc_ids.clear();
+    st.pairs.nb = std::max(1, bits_for(nnodes ? nnodes - 1 : 0));
+    if (2 * st.pairs.nb > 64) fail(ND_ERR_CONFIG, "too many rows for packed pair keys");
+    pack_pairs(st.pairs, d_lo, d_hi, d_match, npairs, s);
+    unique_pairs(st.pairs, s);
+    components(st.groups, st.pairs.lo, st.pairs.hi, st.pairs.distinct, nnodes, s);
+    ND_CUDA(cudaStreamSynchronize(s));
+    st.documents = nnodes;
+    st.valid = true;
+    if (stats) {
+      *stats = nd_dedup_stats{};
+      stats->documents = nnodes;
+      stats->emitted_pairs = npairs;
+      stats->distinct_pairs = st.pairs.distinct;
+      stats->duplicate_groups = st.groups.groups;
+      stats->near_duplicates = st.groups.members;
+      stats->removals = st.groups.removals;
+    }
   });
 }
 

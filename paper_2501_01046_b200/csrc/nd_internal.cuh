@@ -148,6 +148,8 @@ struct CellSet {
 // records: keys = cell ids (< key_limit), vals = rows; both are permuted.
 void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint64_t m,
                               uint64_t key_limit, uint32_t tile_rows, cudaStream_t s);
+void make_records(const uint32_t* band, uint64_t n, uint32_t bands, uint32_t K, uint32_t doc_base,
+                  uint32_t* keys, uint32_t* vals, cudaStream_t s);
 void build_cells_from_bands(CellSet& cs, const uint32_t* band, uint64_t n, uint32_t bands,
                             uint32_t K, uint32_t tile_rows, cudaStream_t s);
 
@@ -171,6 +173,9 @@ void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32
                     int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,
                     uint64_t cap, cudaStream_t s);
 uint64_t unique_pairs(PairSet& ps, cudaStream_t s);
+// packs (lo, hi, m) triples (lo < hi not required) into ps.keys/ps.vals
+void pack_pairs(PairSet& ps, const uint32_t* lo, const uint32_t* hi, const uint32_t* m,
+                uint64_t count, cudaStream_t s);
 
 // K4 output: components as groups of rows (k_union.cu).
 struct GroupSet {

@@ -1,0 +1,195 @@
+"""Multi-GPU dedup: one process per GPU, documents sharded by contiguous ranges
+(SURVEY 8e).  The reference partitions bands over worker threads
+(band_partition, lsh.cpp:62-72; paper: "process j is in charge of
+N_band/N_GPU bands"); here cells (band*K + bucket) are owned by
+contiguous ranges so that any number of GPUs is balanced (nd_cell_partition).
+
+  1. N = all-reduce(n_r); K = choose_bucket_count(N); doc_base = exclusive
+     prefix of n_r (global row = doc_base + local row, ascending doc order).
+  2. K1 on the local shard (rank-local, no collective).
+  3. (cell, row) records of the shard, stably sorted by cell on the device;
+     split by owner range -> all-to-all (counts, then records).  Records
+     arrive grouped by source rank = ascending rows, so a stable regroup keeps
+     each cell's rows ascending, like the reference's file scan.
+  4. All-gather of the signature rows (every owner compares against any row).
+  5. K2+K3 on the owned cells -> distinct pairs (global rows).
+  6. All-gather of the pairs; K4 (distinct + components) on every rank
+     (cheap, identical everywhere); rank 0 writes / returns the report.
+Outputs are identical for any number of ranks (tests/test_distributed.py).
+
+The per-rank compute steps go through a "stages" object; GpuStages (the
+product) calls the C-ABI on device tensors.  torch.distributed is plumbing:
+NCCL over NVLink on GPUs, gloo on CPU for the protocol tests.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import NdDedupStats
+from .lsh import cell_partition, choose_bucket_count, _ratio
+
+
+@dataclass
+class ShardResult:
+    report: object | None  # DedupReport on rank 0 (fetch="lists"/"arrays"), else None
+    candidate_pairs: int
+    emitted_pairs: int
+    distinct_pairs: int
+    bucket_count: int
+    documents: int
+
+
+class GpuStages:
+    """Per-rank device stages over torch CUDA tensors (C-ABI entry points)."""
+
+    def __init__(self, ctx, device):
+        import torch
+
+        self.torch = torch
+        self.ctx = ctx
+        self.device = device
+
+    def tensor(self, shape, dtype):
+        return self.torch.empty(shape, dtype=dtype, device=self.device)
+
+    def signatures(self, data, offsets, family, bands, rows, K):
+        """Pinned host text -> device signatures/band keys (pipelined H2D + K1)."""
+        t = self.torch
+        n = len(offsets) - 1
+        data = np.ascontiguousarray(data, np.uint8)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        sig = self.tensor((n, family.hash_count), t.int32)
+        band = self.tensor((n, bands), t.int32)
+        self.ctx.upload_family(family)
+        self.ctx.check(self.ctx.lib.nd_signatures_h2d(
+            self.ctx.h, data.ctypes.data_as(_lib.u8p), offsets.ctypes.data_as(_lib.u64p), n, bands,
+            rows, K, C.c_void_p(sig.data_ptr()), C.c_void_p(band.data_ptr())))
+        return sig, band
+
+    def ctx_sync(self):
+        self.torch.cuda.synchronize(self.device)
+
+    def cell_records(self, band, bands, K, doc_base):
+        t = self.torch
+        n = band.shape[0]
+        keys = self.tensor((n * bands,), t.int32)
+        vals = self.tensor((n * bands,), t.int32)
+        self.ctx.check(self.ctx.lib.nd_stage_cell_records(
+            self.ctx.h, C.c_void_p(band.data_ptr()), n, bands, K, doc_base,
+            C.c_void_p(keys.data_ptr()), C.c_void_p(vals.data_ptr())))
+        self.ctx_sync()
+        return keys, vals
+
+    def compare(self, sig_all, keys, vals, key_limit, H, threshold):
+        """K2 + K3 + distinct pairs of the owned cells; returns (lo, hi, m, candidates)."""
+        t = self.torch
+        num, den = threshold
+        npairs, cand = C.c_uint64(), C.c_uint64()
+        self.ctx.check(self.ctx.lib.nd_stage_compare(
+            self.ctx.h, C.c_void_p(sig_all.data_ptr()), sig_all.shape[0], H,
+            C.c_void_p(keys.data_ptr()), C.c_void_p(vals.data_ptr()), keys.shape[0], key_limit,
+            num, den, C.byref(npairs), C.byref(cand)))
+        k = npairs.value
+        lo, hi, m = (self.tensor((max(k, 1),), t.int32) for _ in range(3))
+        self.ctx.check(self.ctx.lib.nd_stage_pairs_copy(
+            self.ctx.h, C.c_void_p(lo.data_ptr()), C.c_void_p(hi.data_ptr()),
+            C.c_void_p(m.data_ptr())))
+        self.ctx_sync()
+        return lo[:k], hi[:k], m[:k], cand.value
+
+    def union(self, lo, hi, m, nnodes):
+        st = NdDedupStats()
+        ptr = (lambda x: C.c_void_p(x.data_ptr()) if x.numel() else None)
+        self.ctx.check(self.ctx.lib.nd_stage_union(self.ctx.h, ptr(lo), ptr(hi), ptr(m),
+                                                   lo.numel(), nnodes, C.byref(st)))
+        return st
+
+    def report(self, stats, fetch):
+        from .pipeline import _fetch_report
+
+        return _fetch_report(self.ctx, stats, lists=(fetch != "arrays"))
+
+
+def _all_gather_var(dist, t, group, torch):
+    """all_gather of a 1-D/2-D tensor whose first dimension differs per rank."""
+    world = dist.get_world_size(group)
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(sizes) if sizes else 0
+    pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[: t.shape[0]] = t
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    return torch.cat([o[:s] for o, s in zip(outs, sizes)]), sizes
+
+
+def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists") -> ShardResult:
+    """Distributed in-memory dedup of this rank's shard (see module doc)."""
+    import torch
+    import torch.distributed as dist
+
+    from .minhash import derive_family
+
+    config.validate()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = stages.device
+    n_local = len(offsets) - 1
+    # 1. global N, K, doc_base
+    cnt = torch.tensor([n_local], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    N = sum(counts)
+    doc_base = sum(counts[:rank])
+    if N == 0:
+        raise _lib.ConfigError(_lib.ND_ERR_CONFIG,
+                               "no documents survive preprocessing; nothing to deduplicate")
+    if N >= 2**32:
+        raise _lib.ConfigError(_lib.ND_ERR_CONFIG, "more than 2^32 documents")
+    K = choose_bucket_count(N, config.bucket_scale)
+    b = config.bands
+    fam = derive_family(config.seed, config.hash_count, config.shingle_len, config.unit)
+    # 2. K1 on the shard
+    sig, band = stages.signatures(data, offsets, fam, b, config.rows, K)
+    # 3. records -> owners
+    keys, vals = stages.cell_records(band, b, K, doc_base)
+    first = cell_partition(b, K, world)
+    bounds = torch.tensor(first[1:-1], dtype=torch.int64, device=dev)
+    splits = torch.searchsorted(keys.to(torch.int64), bounds) if world > 1 else \
+        torch.zeros(0, dtype=torch.int64, device=dev)
+    edges = [0] + [int(x) for x in splits.tolist()] + [keys.shape[0]]
+    send = [edges[i + 1] - edges[i] for i in range(world)]
+    send_t = torch.tensor(send, dtype=torch.int64, device=dev)
+    recv_t = torch.empty_like(send_t)
+    dist.all_to_all_single(recv_t, send_t, group=group)
+    recv = [int(x) for x in recv_t.tolist()]
+    rkeys = torch.empty(sum(recv), dtype=keys.dtype, device=dev)
+    rvals = torch.empty(sum(recv), dtype=vals.dtype, device=dev)
+    dist.all_to_all_single(rkeys, keys, recv, send, group=group)
+    dist.all_to_all_single(rvals, vals, recv, send, group=group)
+    # 4. all signature rows on every rank
+    sig_all, _ = _all_gather_var(dist, sig, group, torch)
+    # 5. compare the owned cells
+    thr = _ratio(config.threshold)
+    lo, hi, m, cand_local = stages.compare(sig_all, rkeys, rvals, b * K, config.hash_count, thr)
+    emitted = torch.tensor([lo.shape[0]], dtype=torch.int64, device=dev)
+    # candidate pairs of the owned cells (sum n(n-1)/2, pipeline.cpp:406-411)
+    cand = torch.tensor([cand_local], dtype=torch.int64, device=dev)
+    dist.all_reduce(cand, group=group)
+    dist.all_reduce(emitted, group=group)
+    # 6. edges everywhere, union stage
+    trip = torch.stack([lo, hi, m], dim=1) if lo.numel() else torch.zeros((0, 3), dtype=lo.dtype, device=dev)
+    all_trip, _ = _all_gather_var(dist, trip, group, torch)
+    st = stages.union(all_trip[:, 0].contiguous(), all_trip[:, 1].contiguous(),
+                      all_trip[:, 2].contiguous(), N)
+    rep = stages.report(st, fetch) if (rank == 0 and fetch) else None
+    if rep is not None:
+        rep.candidate_pairs = int(cand.item())
+    return ShardResult(rep, int(cand.item()), int(emitted.item()), st.distinct_pairs, K, N)
