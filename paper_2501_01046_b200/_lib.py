@@ -11,7 +11,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libneardup_b200.so")
+LIB_PATH = os.environ.get("ND_LIB_PATH") or os.path.join(PKG, "libneardup_b200.so")
 
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)

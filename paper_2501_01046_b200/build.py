@@ -65,6 +65,10 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
         objs = list(ex.map(lambda s: _compile(s, force, digest), srcs))
+    for stale in set(glob.glob(os.path.join(OBJ, "*.o"))) - set(objs):
+        os.remove(stale)  # objects of older header digests / removed sources
+    with open(os.path.join(OBJ, "current.txt"), "w") as f:
+        f.write("\n".join(objs) + "\n")
     if (force or not os.path.exists(LIB)
             or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs)):
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lpthread"]

@@ -12,9 +12,11 @@
 // i = tile*128 + t and keeps the first Pf values of its signature in
 // registers.  Columns j > i stream through shared memory in batches of 64
 // (Pf values each) and are read back as broadcast LDS.128; the prefilter is
-// an OR-chain of equality tests (ISETP.EQ.OR).  Survivors get the full H-way
-// count with the same early exit, from global memory, and accepted pairs are
-// appended with one atomic per pair.  Pairs are canonical (lo < hi) row
+// an OR-chain of equality tests (ISETP.EQ.OR).  Survivors are queued in
+// shared memory and, after each column batch, counted exactly by whole warps
+// (32 positions per step, ballot/popc, the same early exit) so a rare
+// survivor does not stall its warp; accepted pairs are appended with one
+// atomic per pair.  Pairs are canonical (lo < hi) row
 // indices packed as lo << nb | hi so that sort + unique (compare.cpp:77-84)
 // is a single radix sort over 2*nb bits.
 #include "nd_internal.cuh"
@@ -52,8 +54,32 @@ __device__ __forceinline__ void emit(uint32_t ra, uint32_t rb, uint32_t m, int n
   }
 }
 
-// Pf > 0: prefilter over the first Pf positions (Pf >= H - min_matches + 1).
-// Pf == 0: no prefilter (every pair takes the full early-exit count).
+// Warp-cooperative exact count of one candidate pair: lanes compare 32
+// consecutive positions per step (coalesced 128-byte row reads) and a
+// ballot/popc reduces them; the early exit of oracle.cpp:81-92 is applied per
+// 32-position chunk.  Returns true when accepted (m >= min_match).
+__device__ __forceinline__ bool warp_count(const uint32_t* __restrict__ a,
+                                           const uint32_t* __restrict__ b, uint32_t H,
+                                           uint32_t allowed, uint32_t min_match, uint32_t& m) {
+  const int lane = threadIdx.x & 31;
+  uint32_t matches = 0;
+  for (uint32_t h0 = 0; h0 < H; h0 += 32) {
+    const uint32_t h = h0 + lane;
+    const bool eq = h < H && __ldg(a + h) == __ldg(b + h);
+    matches += __popc(__ballot_sync(0xFFFFFFFFu, eq));
+    const uint32_t seen = min(H, h0 + 32);
+    if (seen - matches > allowed) return false;
+  }
+  m = matches;
+  return matches >= min_match;
+}
+
+// Pf > 0: prefilter over the first Pf positions (Pf >= H - min_matches + 1);
+// prefilter survivors are queued in shared memory and counted exactly by
+// whole warps after each column batch, so one survivor no longer stalls its
+// warp's 31 other lanes.  Pf == 0: no prefilter (every pair is a survivor).
+constexpr int kQueue = 1024;  // survivor slots per CTA (flushed every batch)
+
 template <int Pf>
 __global__ void __launch_bounds__(kRows)
     k_compare(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
@@ -64,6 +90,8 @@ __global__ void __launch_bounds__(kRows)
   constexpr int PS = Pf > 0 ? ((Pf + 3) / 4) * 4 : 4;
   __shared__ __align__(16) uint32_t cols[kCols][PS];
   __shared__ uint32_t col_row[kCols];
+  __shared__ uint2 queue[kQueue];
+  __shared__ uint32_t qn;
   const uint32_t item = blockIdx.x;
   const uint32_t cell = item_cell[item];
   const uint32_t tile = static_cast<uint32_t>(item - item_off[cell]);
@@ -72,14 +100,17 @@ __global__ void __launch_bounds__(kRows)
   const uint32_t i = tile * kRows + threadIdx.x;
   const bool valid = i < n;
   const uint32_t my_row = valid ? rows[s + i] : 0;
-  const uint32_t* my_sig = sig + static_cast<uint64_t>(my_row) * H;
   const uint32_t allowed = H - min_match;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarpsPerBlock = kRows / 32;
 
   uint32_t pre[Pf > 0 ? Pf : 1];
   if constexpr (Pf > 0) {
+    const uint32_t* my_sig = sig + static_cast<uint64_t>(my_row) * H;
 #pragma unroll
     for (int k = 0; k < Pf; ++k) pre[k] = valid ? __ldg(my_sig + k) : 0xFFFFFFFFu;
   }
+  if (threadIdx.x == 0) qn = 0;
 
   for (uint32_t j0 = tile * kRows + 1; j0 < n; j0 += kCols) {
     const uint32_t cmax = min(static_cast<uint32_t>(kCols), n - j0);
@@ -93,32 +124,72 @@ __global__ void __launch_bounds__(kRows)
       }
     }
     __syncthreads();
-    if (!valid) continue;
-    // columns j <= i are not this row's (upper triangle, compare.cpp:46)
-    uint32_t c0 = (i + 1 > j0) ? i + 1 - j0 : 0;
-    for (uint32_t c = c0; c < cmax; ++c) {
-      bool cand = true;
-      if constexpr (Pf > 0) {
-        bool any = false;
-        const uint4* col = reinterpret_cast<const uint4*>(cols[c]);
+    if (valid) {
+      // columns j <= i are not this row's (upper triangle, compare.cpp:46)
+      const uint32_t c0 = (i + 1 > j0) ? i + 1 - j0 : 0;
+      for (uint32_t c = c0; c < cmax; ++c) {
+        bool cand = true;
+        if constexpr (Pf > 0) {
+          bool any = false;
+          const uint4* col = reinterpret_cast<const uint4*>(cols[c]);
 #pragma unroll
-        for (int q = 0; q < PS / 4; ++q) {
-          const uint4 v = col[q];
-          any |= (4 * q + 0 < Pf) && pre[4 * q + 0] == v.x;
-          if (4 * q + 1 < Pf) any |= pre[4 * q + 1] == v.y;
-          if (4 * q + 2 < Pf) any |= pre[4 * q + 2] == v.z;
-          if (4 * q + 3 < Pf) any |= pre[4 * q + 3] == v.w;
+          for (int q = 0; q < PS / 4; ++q) {
+            const uint4 v = col[q];
+            if (4 * q + 0 < Pf) any |= pre[4 * q + 0] == v.x;
+            if (4 * q + 1 < Pf) any |= pre[4 * q + 1] == v.y;
+            if (4 * q + 2 < Pf) any |= pre[4 * q + 2] == v.z;
+            if (4 * q + 3 < Pf) any |= pre[4 * q + 3] == v.w;
+          }
+          cand = any;
         }
-        cand = any;
-      }
-      if (cand) {
-        const uint32_t other = col_row[c];
-        bool alive;
-        const uint32_t m =
-            full_matches(my_sig, sig + static_cast<uint64_t>(other) * H, H, allowed, alive);
-        if (alive && m >= min_match) emit(my_row, other, m, nb, out_key, out_m, count, cap);
+        if (cand) {
+          const uint32_t slot = atomicAdd(&qn, 1u);
+          if (slot < kQueue) queue[slot] = make_uint2(my_row, col_row[c]);
+        }
       }
     }
+    __syncthreads();
+    // drain the survivors: one warp per candidate pair
+    uint32_t qcount = qn;
+    for (uint32_t base = 0; base < qcount; base += kQueue) {
+      const uint32_t lim = min(qcount - base, static_cast<uint32_t>(kQueue));
+      for (uint32_t t = warp; t < lim; t += kWarpsPerBlock) {
+        const uint2 pr = queue[t];
+        uint32_t m;
+        if (warp_count(sig + static_cast<uint64_t>(pr.x) * H, sig + static_cast<uint64_t>(pr.y) * H,
+                       H, allowed, min_match, m) && lane == 0)
+          emit(pr.x, pr.y, m, nb, out_key, out_m, count, cap);
+      }
+      if (lim == static_cast<uint32_t>(kQueue) && qcount > kQueue) {
+        // overflow (only when > kQueue survivors in one batch): recompute this
+        // batch's survivors beyond the queue directly, thread by thread
+        __syncthreads();
+        if (valid) {
+          const uint32_t c0 = (i + 1 > j0) ? i + 1 - j0 : 0;
+          for (uint32_t c = c0; c < cmax; ++c) {
+            bool cand = true;
+            if constexpr (Pf > 0) {
+              bool any = false;
+#pragma unroll
+              for (int k = 0; k < Pf; ++k) any |= pre[k] == cols[c][k];
+              cand = any;
+            }
+            if (cand) {
+              bool alive;
+              const uint32_t other = col_row[c];
+              const uint32_t mm = full_matches(sig + static_cast<uint64_t>(my_row) * H,
+                                               sig + static_cast<uint64_t>(other) * H, H,
+                                               allowed, alive);
+              if (alive && mm >= min_match) emit(my_row, other, mm, nb, out_key, out_m, count, cap);
+            }
+          }
+        }
+        qcount = 0;  // the thread-by-thread pass covered every survivor of the batch
+        break;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) qn = 0;
   }
 }
 

@@ -49,7 +49,24 @@
 namespace ndb {
 namespace {
 
-constexpr int kWarps = 4;           // warps per block
+#ifndef ND_K1_WARPS
+#define ND_K1_WARPS 4
+#endif
+#ifndef ND_K1_MINBLOCKS
+#define ND_K1_MINBLOCKS 0  // 0: no min-blocks hint (ptxas chose 96 registers)
+#endif
+#if ND_K1_MINBLOCKS > 0
+#define ND_K1_BOUNDS __launch_bounds__(ND_K1_WARPS * 32, ND_K1_MINBLOCKS)
+#else
+#define ND_K1_BOUNDS __launch_bounds__(ND_K1_WARPS * 32)
+#endif
+#ifndef ND_K1_UNROLL4
+#define ND_K1_UNROLL4 1
+#endif
+#ifndef ND_K1_ASM_ORDER
+#define ND_K1_ASM_ORDER 0
+#endif
+constexpr int kWarps = ND_K1_WARPS;  // warps per block
 constexpr int kLMax = 64;           // max shingle length
 // positions staged per chunk and group: (char, float) pairs, 8 B each
 __host__ __device__ constexpr int chunk_for(int Z) { return Z >= 4 ? 128 : 256; }
@@ -192,15 +209,19 @@ struct Consts<Arith::kFq, F> {
     const float t1 = __fmaf_rn(cout_f, qlnp[f], c1e[f]);
     const float R = __fmaf_rn(__uint_as_float(sb), qp[f], t1);
     const uint32_t kb = __float_as_uint(__fadd_rd(R, 8388607.5f));
+    // the integer side only waits for kb in its last IMAD (shorter chain)
     uint32_t x = cout * qln256[f] + cin256;
-    x = kb * negp256[f] + x;
     x = sb * q256[f] + x;
+#if ND_K1_ASM_ORDER
+    asm volatile("" : "+r"(x));  // keep the association: kb is consumed last
+#endif
+    x = kb * negp256[f] + x;
     return min(x, x + negp256[f]);
   }
 };
 
 template <Arith A, int F, int Z>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void ND_K1_BOUNDS
     k_signature(const uint8_t* __restrict__ text, const uint64_t* __restrict__ offsets,
                 const uint32_t* __restrict__ item_doc, const uint64_t* __restrict__ item_off,
                 uint64_t n_items, FamPtrs fam, uint32_t L, uint32_t H, uint32_t bands,
@@ -276,6 +297,22 @@ __global__ void __launch_bounds__(kWarps * 32)
         }
         first = false;
       }
+#if ND_K1_UNROLL4
+      for (; j >= 3; j -= 4) {
+        const uint2 o0 = buf[j + L], o1 = buf[j - 1 + L], o2 = buf[j - 2 + L], o3 = buf[j - 3 + L];
+        const uint32_t c0 = buf256[j], c1 = buf256[j - 1], c2 = buf256[j - 2], c3 = buf256[j - 3];
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          const uint32_t a0 = k.roll(f, s[f], c0, o0.x, __uint_as_float(o0.y));
+          const uint32_t a1 = k.roll(f, a0, c1, o1.x, __uint_as_float(o1.y));
+          const uint32_t a2 = k.roll(f, a1, c2, o2.x, __uint_as_float(o2.y));
+          const uint32_t a3 = k.roll(f, a2, c3, o3.x, __uint_as_float(o3.y));
+          s[f] = a3;
+          mn[f] = __vimin3_u32(mn[f], a0, a1);
+          mn[f] = __vimin3_u32(mn[f], a2, a3);
+        }
+      }
+#endif
       // two windows per iteration: one 3-way min (VIMNMX3) folds both
       for (; j >= 1; j -= 2) {
         const uint2 o0 = buf[j + L], o1 = buf[j - 1 + L];

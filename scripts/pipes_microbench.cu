@@ -1,0 +1,242 @@
+// Integer / FP32 pipe throughput on this B200 (used to set the K1 roofline).
+// Each thread runs 8 independent dependency chains of one instruction class
+// for ITERS iterations; throughput = lane-ops / (SMs * clock * time).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/pipes scripts/pipes_microbench.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int ITERS = 4096;
+
+__global__ void k_imad(unsigned* out, unsigned a, unsigned b) {
+  unsigned x[8];
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(a), "r"(b));
+  unsigned s = 0;
+  for (int i = 0; i < 8; ++i) s ^= x[i];
+  if (s == 0x12345) out[0] = s;
+}
+
+__global__ void k_imadwide(unsigned* out, unsigned a, unsigned b) {
+  unsigned long long x[8];
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(x[i]) : "r"((unsigned)x[i]), "r"(a));
+  unsigned long long s = 0;
+  for (int i = 0; i < 8; ++i) s ^= x[i];
+  if (s == 0x12345) out[0] = (unsigned)s;
+}
+
+__global__ void k_imadhi(unsigned* out, unsigned a, unsigned b) {
+  unsigned x[8];
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(a), "r"(b));
+  unsigned s = 0;
+  for (int i = 0; i < 8; ++i) s ^= x[i];
+  if (s == 0x12345) out[0] = s;
+}
+
+__global__ void k_ffma(unsigned* out, float a, float b) {
+  float x[8];
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[i]) : "f"(a), "f"(b));
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 1234.5f) out[0] = 1;
+}
+
+__global__ void k_ffma3(unsigned* out, float a, float b) {  // 3 distinct register sources
+  float x[8], y[8];
+  for (int i = 0; i < 8; ++i) { x[i] = threadIdx.x + i; y[i] = i * a; }
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[i]) : "f"(y[i]), "f"(y[(i + 1) & 7]));
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 1234.5f) out[0] = 1;
+}
+
+__global__ void k_alu(unsigned* out, unsigned a, unsigned b) {
+  unsigned x[8];
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("shf.l.wrap.b32 %0, %0, %0, %1;" : "+r"(x[i]) : "r"(a + i));
+  unsigned s = 0;
+  for (int i = 0; i < 8; ++i) s ^= x[i];
+  if (s == 0x12345) out[0] = s;
+}
+
+__global__ void k_mix(unsigned* out, unsigned a, unsigned b) {  // 1 IMAD : 1 FFMA : 1 ALU
+  unsigned x[8];
+  float f[8];
+  for (int i = 0; i < 8; ++i) { x[i] = threadIdx.x + i; f[i] = i; }
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(a), "r"(b));
+      asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(f[i]) : "f"(1.0001f), "f"(0.5f));
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(x[i]) : "r"(b));
+    }
+  unsigned s = 0;
+  for (int i = 0; i < 8; ++i) s ^= x[i] ^ __float_as_uint(f[i]);
+  if (s == 0x12345) out[0] = s;
+}
+
+// ---- the K1 roll sequence: per-lane constants (registers) vs warp-uniform
+// constants (constant bank), same instruction sequence otherwise
+struct RollC {
+  unsigned q256, qln256, negp256;
+  float qp, qlnp, c1e;
+};
+__constant__ RollC g_rc[8];
+
+__device__ __forceinline__ unsigned roll(unsigned C, unsigned cin256, unsigned cout, float cout_f,
+                                         unsigned q256, unsigned qln256, unsigned negp256,
+                                         float qp, float qlnp, float c1e) {
+  const unsigned sb = (C >> 8) | 0x4B000000u;
+  const float t1 = __fmaf_rn(cout_f, qlnp, c1e);
+  const float R = __fmaf_rn(__uint_as_float(sb), qp, t1);
+  const unsigned kb = __float_as_uint(__fadd_rd(R, 8388607.5f));
+  unsigned x = cout * qln256 + cin256;
+  x = kb * negp256 + x;
+  x = sb * q256 + x;
+  return min(x, x + negp256);
+}
+
+__global__ void k_roll_reg(unsigned* out, const RollC* rc, unsigned seed) {
+  RollC c[8];
+  for (int f = 0; f < 8; ++f) c[f] = rc[(threadIdx.x * 8 + f) & 63];  // lane-varying
+  unsigned s[8], mn[8];
+  for (int f = 0; f < 8; ++f) { s[f] = 0; mn[f] = ~0u; }
+  unsigned ch = seed + threadIdx.x;
+  for (int it = 0; it < ITERS; ++it) {
+    ch = ch * 1664525u + 1013904223u;
+    unsigned cin = (ch >> 8) & 0xFF00u, cout = ch >> 24;
+    float cf = (float)cout;
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      s[f] = roll(s[f], cin, cout, cf, c[f].q256, c[f].qln256, c[f].negp256, c[f].qp, c[f].qlnp, c[f].c1e);
+      mn[f] = min(mn[f], s[f]);
+    }
+  }
+  unsigned r = 0;
+  for (int f = 0; f < 8; ++f) r ^= mn[f];
+  if (r == 0x12345) out[0] = r;
+}
+
+__global__ void k_roll_uni(unsigned* out, const RollC* rc, unsigned seed) {
+  unsigned s[8], mn[8];
+  for (int f = 0; f < 8; ++f) { s[f] = 0; mn[f] = ~0u; }
+  unsigned ch = seed + threadIdx.x;
+  for (int it = 0; it < ITERS; ++it) {
+    ch = ch * 1664525u + 1013904223u;
+    unsigned cin = (ch >> 8) & 0xFF00u, cout = ch >> 24;
+    float cf = (float)cout;
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      s[f] = roll(s[f], cin, cout, cf, g_rc[f].q256, g_rc[f].qln256, g_rc[f].negp256, g_rc[f].qp,
+                  g_rc[f].qlnp, g_rc[f].c1e);
+      mn[f] = min(mn[f], s[f]);
+    }
+  }
+  unsigned r = 0;
+  for (int f = 0; f < 8; ++f) r ^= mn[f];
+  if (r == 0x12345) out[0] = r;
+}
+
+// constants as immediates (what a family-specialised JIT kernel would see)
+__global__ void k_roll_imm(unsigned* out, const RollC* rc, unsigned seed) {
+  unsigned s[8], mn[8];
+  for (int f = 0; f < 8; ++f) { s[f] = 0; mn[f] = ~0u; }
+  unsigned ch = seed + threadIdx.x;
+  for (int it = 0; it < ITERS; ++it) {
+    ch = ch * 1664525u + 1013904223u;
+    unsigned cin = (ch >> 8) & 0xFF00u, cout = ch >> 24;
+    float cf = (float)cout;
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      const unsigned p = 2097143u + 2 * f, q = 257 + 2 * f;
+      s[f] = roll(s[f], cin, cout, cf, q << 8, ((p - 7) % p) << 8, (0u - p) << 8, (float)q / p, 0.3f,
+                  -8388608.0f * ((float)q / p) + 0.03125f);
+      mn[f] = min(mn[f], s[f]);
+    }
+  }
+  unsigned r = 0;
+  for (int f = 0; f < 8; ++f) r ^= mn[f];
+  if (r == 0x12345) out[0] = r;
+}
+
+void run_roll(const char* name, void (*k)(unsigned*, const RollC*, unsigned), int sms, int clk) {
+  RollC h[64];
+  for (int i = 0; i < 64; ++i) {
+    unsigned p = 2097143u + 2 * i, q = 257 + 2 * i;
+    h[i] = {q << 8, ((p - 7) % p) << 8, (0u - p) << 8, (float)q / p, 0.3f, -8388608.0f * ((float)q / p) + 0.03125f};
+  }
+  RollC* d_rc;
+  cudaMalloc(&d_rc, sizeof h);
+  cudaMemcpy(d_rc, h, sizeof h, cudaMemcpyHostToDevice);
+  cudaMemcpyToSymbol(g_rc, h, sizeof(RollC) * 8);
+  unsigned* d;
+  cudaMalloc(&d, 4);
+  int blocks = sms * 8, threads = 128;
+  k<<<blocks, threads>>>(d, d_rc, 1);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 5; ++r) k<<<blocks, threads>>>(d, d_rc, r);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  double hwe = 5.0 * blocks * threads * (double)ITERS * 8;
+  printf("%-12s %8.3f ms  %.3f T HWE/s  %.2f HWE/clk/SM\n", name, ms / 5, hwe / (ms * 1e-3) / 1e12,
+         hwe / (ms * 1e-3) / (sms * (double)clk * 1e3));
+}
+
+template <class Kern, class T>
+void run(const char* name, Kern k, T a, T b, int ops_per_inner, int sms, int clk_khz) {
+  unsigned* d;
+  cudaMalloc(&d, 4);
+  int blocks = sms * 8, threads = 256;
+  k<<<blocks, threads>>>(d, a, b);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 5; ++r) k<<<blocks, threads>>>(d, a, b);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  double lane_ops = 5.0 * blocks * threads * (double)ITERS * 8 * ops_per_inner;
+  double per_clk_sm = lane_ops / (ms * 1e-3) / (sms * (double)clk_khz * 1e3);
+  printf("%-12s %8.3f ms  %7.1f lane-ops/clk/SM (at max clock)  %.3f Tops/s\n", name, ms / 5,
+         per_clk_sm, lane_ops / (ms * 1e-3) / 1e12);
+  cudaFree(d);
+}
+
+int main() {
+  int sms, clk;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  printf("SMs %d, max clock %d kHz\n", sms, clk);
+  run("IMAD", k_imad, 3u, 7u, 1, sms, clk);
+  run("IMAD.WIDE", k_imadwide, 3u, 7u, 1, sms, clk);
+  run("IMAD.HI", k_imadhi, 3u, 7u, 1, sms, clk);
+  run("FFMA(imm)", k_ffma, 1.0001f, 0.5f, 1, sms, clk);
+  run("FFMA(3reg)", k_ffma3, 1.0001f, 0.5f, 1, sms, clk);
+  run("ALU", k_alu, 3u, 7u, 1, sms, clk);
+  run("mix 1:1:1", k_mix, 3u, 7u, 3, sms, clk);
+  run_roll("roll(reg)", k_roll_reg, sms, clk);
+  run_roll("roll(uniform)", k_roll_uni, sms, clk);
+  run_roll("roll(imm)", k_roll_imm, sms, clk);
+  return 0;
+}
