@@ -93,6 +93,11 @@ typedef struct nd_synth_spec {
 } nd_synth_spec;
 int nd_synth_generate(const nd_synth_spec* spec, uint8_t* bytes, uint64_t* offsets,
                       uint64_t* nbytes_out);
+/* mode-1 corpus text generated directly in device memory (identical bytes to
+ * nd_synth_generate); d_offsets = the offsets nd_synth_generate(spec, NULL,
+ * offsets, &n) returned, already copied to the device.  Synchronous. */
+int nd_synth_text_device(nd_ctx* ctx, const nd_synth_spec* spec, const uint64_t* d_offsets,
+                         uint8_t* d_bytes);
 
 /* ---- device context ----------------------------------------------------- */
 int nd_ctx_create(int device, nd_ctx** out);

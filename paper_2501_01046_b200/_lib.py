@@ -69,6 +69,7 @@ SIGNATURES = {
     "nd_band_partition": (C.c_int, [C.c_uint32, C.c_uint32, u32p]),
     "nd_cell_partition": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, u64p]),
     "nd_synth_generate": (C.c_int, [C.POINTER(NdSynthSpec), u8p, u64p, u64p]),
+    "nd_synth_text_device": (C.c_int, [vp, C.POINTER(NdSynthSpec), vp, vp]),
     "nd_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
     "nd_ctx_destroy": (None, [vp]),
     "nd_last_error": (C.c_char_p, [vp]),

@@ -23,7 +23,7 @@ std::vector<nd_hash_fn> derive_family(uint64_t seed, uint32_t H, uint32_t L, uin
 uint32_t choose_bucket_count(uint64_t n, uint64_t num, uint64_t den);
 uint32_t min_matches(uint32_t H, uint64_t num, uint64_t den);
 
-// synthetic corpus (host_synth.cpp)
+// synthetic corpus (synth.cu)
 void synth_generate(const nd_synth_spec& spec, uint8_t* bytes, uint64_t* offsets,
                     uint64_t* nbytes_out);
 

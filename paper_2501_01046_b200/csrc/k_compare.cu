@@ -8,9 +8,9 @@
 // exact early-termination rule of the reference's own oracle,
 // oracle.cpp:81-92, proven equal to the full scan by test_oracle.cpp:96-112).
 //
-// Layout: one 128-thread CTA per (cell, tile of 128 rows).  Thread t owns row
-// i = tile*128 + t and keeps the first Pf values of its signature in
-// registers.  Columns j > i stream through shared memory in batches of 64
+// Layout: one 128-thread CTA per (cell, tile of kCmpRows = 256 rows).  Thread t
+// owns rows tile*256 + t and + 128 and keeps the first Pf values of both
+// signatures in registers.  Columns j > i stream through shared memory in batches of 64
 // (Pf values each) and are read back as broadcast LDS.128; the prefilter is
 // an OR-chain of equality tests (ISETP.EQ.OR).  Survivors are queued in
 // shared memory and, after each column batch, counted exactly by whole warps
@@ -24,8 +24,7 @@
 namespace ndb {
 namespace {
 
-constexpr int kRows = kCmpRows;  // rows per CTA (= threads)
-constexpr int kCols = 64;        // columns staged per batch
+constexpr int kCols = 64;  // columns staged per batch
 
 __device__ __forceinline__ uint32_t full_matches(const uint32_t* __restrict__ a,
                                                  const uint32_t* __restrict__ b, uint32_t H,
@@ -77,11 +76,15 @@ __device__ __forceinline__ bool warp_count(const uint32_t* __restrict__ a,
 // Pf > 0: prefilter over the first Pf positions (Pf >= H - min_matches + 1);
 // prefilter survivors are queued in shared memory and counted exactly by
 // whole warps after each column batch, so one survivor no longer stalls its
-// warp's 31 other lanes.  Pf == 0: no prefilter (every pair is a survivor).
-constexpr int kQueue = 1024;  // survivor slots per CTA (flushed every batch)
+// warp's 31 other lanes (a full queue falls back to an inline count).
+// Pf == 0: no prefilter (every pair is a survivor).  Each thread owns kR rows
+// (i and i + kThreads), so every broadcast LDS.128 feeds 4*kR comparisons.
+constexpr int kThreads = 128;
+constexpr int kR = kCmpRows / kThreads;  // rows per thread
+constexpr int kQueue = 1024;             // survivor slots per CTA (drained every batch)
 
 template <int Pf>
-__global__ void __launch_bounds__(kRows)
+__global__ void __launch_bounds__(kThreads)
     k_compare(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
               const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
               const uint32_t* __restrict__ item_cell, const uint64_t* __restrict__ item_off,
@@ -97,96 +100,90 @@ __global__ void __launch_bounds__(kRows)
   const uint32_t tile = static_cast<uint32_t>(item - item_off[cell]);
   const uint64_t s = cell_start[cell];
   const uint32_t n = cell_len[cell];
-  const uint32_t i = tile * kRows + threadIdx.x;
-  const bool valid = i < n;
-  const uint32_t my_row = valid ? rows[s + i] : 0;
   const uint32_t allowed = H - min_match;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kWarpsPerBlock = kRows / 32;
+  constexpr int kWarpsPerBlock = kThreads / 32;
 
-  uint32_t pre[Pf > 0 ? Pf : 1];
-  if constexpr (Pf > 0) {
-    const uint32_t* my_sig = sig + static_cast<uint64_t>(my_row) * H;
+  uint32_t ri[kR], row[kR];
+  bool valid[kR];
+  uint32_t pre[kR][Pf > 0 ? Pf : 1];
 #pragma unroll
-    for (int k = 0; k < Pf; ++k) pre[k] = valid ? __ldg(my_sig + k) : 0xFFFFFFFFu;
+  for (int r = 0; r < kR; ++r) {
+    ri[r] = tile * kCmpRows + r * kThreads + threadIdx.x;
+    valid[r] = ri[r] < n;
+    row[r] = valid[r] ? rows[s + ri[r]] : 0;
+    if constexpr (Pf > 0) {
+      const uint32_t* my_sig = sig + static_cast<uint64_t>(row[r]) * H;
+#pragma unroll
+      for (int k = 0; k < Pf; ++k) pre[r][k] = valid[r] ? __ldg(my_sig + k) : 0xFFFFFFFFu;
+    }
   }
   if (threadIdx.x == 0) qn = 0;
 
-  for (uint32_t j0 = tile * kRows + 1; j0 < n; j0 += kCols) {
+  for (uint32_t j0 = tile * kCmpRows + 1; j0 < n; j0 += kCols) {
     const uint32_t cmax = min(static_cast<uint32_t>(kCols), n - j0);
     __syncthreads();
-    for (uint32_t c = threadIdx.x; c < cmax; c += kRows) col_row[c] = rows[s + j0 + c];
+    for (uint32_t c = threadIdx.x; c < cmax; c += kThreads) col_row[c] = rows[s + j0 + c];
     if constexpr (Pf > 0) {
       __syncthreads();
-      for (uint32_t idx = threadIdx.x; idx < cmax * Pf; idx += kRows) {
+      for (uint32_t idx = threadIdx.x; idx < cmax * Pf; idx += kThreads) {
         const uint32_t c = idx / Pf, k = idx % Pf;
         cols[c][k] = __ldg(sig + static_cast<uint64_t>(col_row[c]) * H + k);
       }
     }
     __syncthreads();
-    if (valid) {
-      // columns j <= i are not this row's (upper triangle, compare.cpp:46)
-      const uint32_t c0 = (i + 1 > j0) ? i + 1 - j0 : 0;
-      for (uint32_t c = c0; c < cmax; ++c) {
-        bool cand = true;
-        if constexpr (Pf > 0) {
-          bool any = false;
-          const uint4* col = reinterpret_cast<const uint4*>(cols[c]);
+    // columns j <= i are not row i's (upper triangle, compare.cpp:46)
+    const uint32_t c0 = valid[0] ? ((ri[0] + 1 > j0) ? ri[0] + 1 - j0 : 0) : cmax;
+    for (uint32_t c = c0; c < cmax; ++c) {
+      const uint32_t j = j0 + c;
+      bool cand[kR];
+      if constexpr (Pf > 0) {
+        bool any[kR];
 #pragma unroll
-          for (int q = 0; q < PS / 4; ++q) {
-            const uint4 v = col[q];
-            if (4 * q + 0 < Pf) any |= pre[4 * q + 0] == v.x;
-            if (4 * q + 1 < Pf) any |= pre[4 * q + 1] == v.y;
-            if (4 * q + 2 < Pf) any |= pre[4 * q + 2] == v.z;
-            if (4 * q + 3 < Pf) any |= pre[4 * q + 3] == v.w;
+        for (int r = 0; r < kR; ++r) any[r] = false;
+        const uint4* col = reinterpret_cast<const uint4*>(cols[c]);
+#pragma unroll
+        for (int q = 0; q < PS / 4; ++q) {
+          const uint4 v = col[q];
+#pragma unroll
+          for (int r = 0; r < kR; ++r) {
+            if (4 * q + 0 < Pf) any[r] |= pre[r][4 * q + 0] == v.x;
+            if (4 * q + 1 < Pf) any[r] |= pre[r][4 * q + 1] == v.y;
+            if (4 * q + 2 < Pf) any[r] |= pre[r][4 * q + 2] == v.z;
+            if (4 * q + 3 < Pf) any[r] |= pre[r][4 * q + 3] == v.w;
           }
-          cand = any;
         }
-        if (cand) {
+#pragma unroll
+        for (int r = 0; r < kR; ++r) cand[r] = any[r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < kR; ++r) cand[r] = true;
+      }
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        if (cand[r] && valid[r] && j > ri[r]) {
+          const uint32_t other = col_row[c];
           const uint32_t slot = atomicAdd(&qn, 1u);
-          if (slot < kQueue) queue[slot] = make_uint2(my_row, col_row[c]);
+          if (slot < kQueue) {
+            queue[slot] = make_uint2(row[r], other);
+          } else {  // queue full: count inline
+            bool alive;
+            const uint32_t m = full_matches(sig + static_cast<uint64_t>(row[r]) * H,
+                                            sig + static_cast<uint64_t>(other) * H, H, allowed, alive);
+            if (alive && m >= min_match) emit(row[r], other, m, nb, out_key, out_m, count, cap);
+          }
         }
       }
     }
     __syncthreads();
     // drain the survivors: one warp per candidate pair
-    uint32_t qcount = qn;
-    for (uint32_t base = 0; base < qcount; base += kQueue) {
-      const uint32_t lim = min(qcount - base, static_cast<uint32_t>(kQueue));
-      for (uint32_t t = warp; t < lim; t += kWarpsPerBlock) {
-        const uint2 pr = queue[t];
-        uint32_t m;
-        if (warp_count(sig + static_cast<uint64_t>(pr.x) * H, sig + static_cast<uint64_t>(pr.y) * H,
-                       H, allowed, min_match, m) && lane == 0)
-          emit(pr.x, pr.y, m, nb, out_key, out_m, count, cap);
-      }
-      if (lim == static_cast<uint32_t>(kQueue) && qcount > kQueue) {
-        // overflow (only when > kQueue survivors in one batch): recompute this
-        // batch's survivors beyond the queue directly, thread by thread
-        __syncthreads();
-        if (valid) {
-          const uint32_t c0 = (i + 1 > j0) ? i + 1 - j0 : 0;
-          for (uint32_t c = c0; c < cmax; ++c) {
-            bool cand = true;
-            if constexpr (Pf > 0) {
-              bool any = false;
-#pragma unroll
-              for (int k = 0; k < Pf; ++k) any |= pre[k] == cols[c][k];
-              cand = any;
-            }
-            if (cand) {
-              bool alive;
-              const uint32_t other = col_row[c];
-              const uint32_t mm = full_matches(sig + static_cast<uint64_t>(my_row) * H,
-                                               sig + static_cast<uint64_t>(other) * H, H,
-                                               allowed, alive);
-              if (alive && mm >= min_match) emit(my_row, other, mm, nb, out_key, out_m, count, cap);
-            }
-          }
-        }
-        qcount = 0;  // the thread-by-thread pass covered every survivor of the batch
-        break;
-      }
+    const uint32_t lim = min(qn, static_cast<uint32_t>(kQueue));
+    for (uint32_t t = warp; t < lim; t += kWarpsPerBlock) {
+      const uint2 pr = queue[t];
+      uint32_t m;
+      if (warp_count(sig + static_cast<uint64_t>(pr.x) * H, sig + static_cast<uint64_t>(pr.y) * H, H,
+                     allowed, min_match, m) && lane == 0)
+        emit(pr.x, pr.y, m, nb, out_key, out_m, count, cap);
     }
     __syncthreads();
     if (threadIdx.x == 0) qn = 0;
@@ -221,7 +218,7 @@ void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32
     default: fn = k_compare<0>; break;
   }
   if (cs.items > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many compare work items");
-  fn<<<static_cast<unsigned>(cs.items), kRows, 0, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start,
+  fn<<<static_cast<unsigned>(cs.items), kThreads, 0, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start,
                                                        cs.cell_len, cs.item_cell, cs.item_off,
                                                        min_match, nb, out_key, out_m, count, cap);
   ND_CHECK_LAUNCH();

@@ -59,6 +59,7 @@ nd_ctx::~nd_ctx() {
     if (slot[i].comp) cudaStreamDestroy(slot[i].comp);
   }
   pinned_off.release();
+  synth_buf.release();
   sig_scratch.release();
   dedup.release();
   api.release();
@@ -222,6 +223,11 @@ int nd_cell_partition(uint32_t bands, uint32_t K, uint32_t shards, uint64_t* fir
 int nd_synth_generate(const nd_synth_spec* spec, uint8_t* bytes, uint64_t* offsets,
                       uint64_t* nbytes_out) {
   return guarded_impl(nullptr, [&] { synth_generate(*spec, bytes, offsets, nbytes_out); });
+}
+
+int nd_synth_text_device(nd_ctx* ctx, const nd_synth_spec* spec, const uint64_t* d_offsets,
+                         uint8_t* d_bytes) {
+  return guarded_impl(ctx, [&] { synth_text_device(*spec, d_offsets, d_bytes, ctx->synth_buf, ctx->stream); });
 }
 
 int nd_ctx_create(int device, nd_ctx** out) {

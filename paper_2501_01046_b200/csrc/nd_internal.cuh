@@ -126,7 +126,7 @@ void radix_sort_u64(uint64_t* keys, uint32_t* vals, uint64_t n, int key_bits, So
 int bits_for(uint64_t maxval);  // number of bits needed to hold maxval
 
 // K2 output: non-singleton LSH cells as CSR over sorted rows (k_cells.cu).
-constexpr uint32_t kCmpRows = 128;  // rows per compare work item
+constexpr uint32_t kCmpRows = 128;  // rows per compare work item (128 threads x kR)
 struct CellSet {
   DevBuf rec_keys, rec_vals, flag, run_idx, run_start, cstart, clen, ckey, cpairs, ctiles, pair_off,
       ioff, icell, scan;
@@ -226,6 +226,10 @@ void launch_band_keys(const uint32_t* d_sig, uint64_t n, uint32_t H, uint32_t ba
 void scan_u64(const uint64_t* d_in, uint64_t* d_out, uint64_t n, DevBuf& tmp, cudaStream_t s);
 void scan_u32_to_u64(const uint32_t* d_in, uint64_t* d_out, uint64_t n, DevBuf& tmp,
                      cudaStream_t s);
+
+// mode-1 synthetic text into device memory (synth.cu)
+void synth_text_device(const nd_synth_spec& s, const uint64_t* d_offsets, uint8_t* d_bytes,
+                       DevBuf& scratch, cudaStream_t stream);
 
 int sm_count();
 

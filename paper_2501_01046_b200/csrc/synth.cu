@@ -19,13 +19,21 @@
 #include <thread>
 #include <vector>
 
-#include "host_internal.hpp"
+#include "nd_internal.cuh"
+
+#define ND_HD __host__ __device__
 
 namespace ndb {
 namespace {
 
 constexpr char kAlphabet[] = "abcdefghijklmnopqrstuvwxyz0123456789 ";
+__device__ __constant__ char kAlphaDev[] = "abcdefghijklmnopqrstuvwxyz0123456789 ";
 constexpr uint64_t kAlpha = 37;
+#ifdef __CUDA_ARCH__
+#define kAlphaChars kAlphaDev
+#else
+#define kAlphaChars kAlphabet
+#endif
 
 uint64_t gcd_u64(uint64_t a, uint64_t b) {
   while (b) {
@@ -99,69 +107,89 @@ std::vector<std::string> generate_mode0(const nd_synth_spec& s) {
 }
 
 // ---------------------------------------------------------------- mode 1
-inline uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
+// Counter-based and random-access: draw(key, i) = mix64(mix64(key) + i*C), so
+// any character of any document can be produced independently -- on the host
+// (threads) or on the device (k_synth_text, one warp per document), with
+// identical bytes.  Lengths (which use libm for the lognormal law) are always
+// computed on the host.
+ND_HD inline uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
+ND_HD inline uint64_t draw(uint64_t mixed_key, uint64_t i) {
+  return mix64(mixed_key + i * 0xD1B54A32D192ED03ull);
+}
 
-struct Stream {  // counter-based stream: x_i = mix64(key + i * golden)
+struct Stream {  // sequential view of the same counter-based draws
   uint64_t key, ctr = 0;
   explicit Stream(uint64_t k) : key(mix64(k)) {}
-  uint64_t next() { return mix64(key + (ctr++) * 0xD1B54A32D192ED03ull); }
+  uint64_t next() { return draw(key, ctr++); }
   uint64_t below(uint64_t b) { return static_cast<uint64_t>((static_cast<unsigned __int128>(next()) * b) >> 64); }
   double unit() { return (next() >> 11) * (1.0 / 9007199254740992.0); }
 };
 
-// bijection on [0, n) (Feistel on 2*half bits + cycle walking)
-struct Perm {
-  uint64_t n, half_mask;
+// POD view shared by host and device
+struct M1 {
+  uint64_t n, seed, grouped, ngroups, perm_key, half_mask;
   int half_bits;
-  uint64_t key;
-  Perm(uint64_t n_, uint64_t seed) : n(n_), key(seed) {
-    int bits = 2;
-    while ((1ull << bits) < n) bits += 2;
-    half_bits = bits / 2;
-    half_mask = (1ull << half_bits) - 1;
-  }
-  uint64_t round_f(uint64_t x, int r) const { return mix64(x ^ (key + 0x100000001B3ull * r)) & half_mask; }
-  uint64_t enc(uint64_t x) const {
-    uint64_t l = x >> half_bits, rr = x & half_mask;
-    for (int r = 0; r < 4; ++r) {
-      uint64_t t = l ^ round_f(rr, r);
-      l = rr;
-      rr = t;
-    }
-    return (l << half_bits) | rr;
-  }
-  uint64_t dec(uint64_t y) const {
-    uint64_t l = y >> half_bits, rr = y & half_mask;
-    for (int r = 3; r >= 0; --r) {
-      uint64_t t = rr ^ round_f(l, r);
-      rr = l;
-      l = t;
-    }
-    return (l << half_bits) | rr;
-  }
-  uint64_t fwd(uint64_t x) const {
-    do x = enc(x);
-    while (x >= n);
-    return x;
-  }
-  uint64_t inv(uint64_t y) const {
-    do y = dec(y);
-    while (y >= n);
-    return y;
-  }
+  uint32_t edit_thresh;  // P(edit) * 2^32
+  uint32_t len_draws;    // draws consumed by the length law (1 uniform, 2 lognormal)
 };
+
+ND_HD inline uint64_t perm_dec(const M1& m, uint64_t y) {
+  uint64_t l = y >> m.half_bits, rr = y & m.half_mask;
+  for (int r = 3; r >= 0; --r) {
+    uint64_t t = rr ^ (mix64(l ^ (m.perm_key + 0x100000001B3ull * r)) & m.half_mask);
+    rr = l;
+    l = t;
+  }
+  return (l << m.half_bits) | rr;
+}
+ND_HD inline uint64_t perm_inv(const M1& m, uint64_t y) {  // Feistel + cycle walking
+  do y = perm_dec(m, y);
+  while (y >= m.n);
+  return y;
+}
+
+// logical index -> (text stream key, edit stream key or 0)
+ND_HD inline void m1_source(const M1& m, const uint64_t* group_first, uint64_t logical,
+                            uint64_t& text_key, uint64_t& edit_key) {
+  if (logical < m.grouped) {
+    uint64_t lo = 0, hi = m.ngroups;  // last g with group_first[g] <= logical
+    while (hi - lo > 1) {
+      uint64_t mid = (lo + hi) / 2;
+      if (group_first[mid] <= logical) lo = mid; else hi = mid;
+    }
+    const uint64_t g = lo, k = logical - group_first[g];
+    text_key = m.seed * 0x632BE59BD9B4E019ull + 0x7777 + g;
+    edit_key = k == 0 ? 0 : (m.seed * 0x8CB92BA72F3D8DD7ull + (g << 8) + k + 1);
+  } else {
+    text_key = m.seed * 0x632BE59BD9B4E019ull + 0x3333333333ull + logical;
+    edit_key = 0;
+  }
+}
+
+// character i of a document (text stream mixed key tkm, edit stream mixed keys
+// ekm / ekm2 or 0)
+ND_HD inline uint8_t m1_char(const M1& m, uint64_t tkm, uint64_t ekm, uint64_t ekm2, uint64_t i) {
+  const uint64_t x = draw(tkm, m.len_draws + i / 2);
+  const uint32_t h = static_cast<uint32_t>(x >> (32 * (i & 1)));
+  uint32_t idx = static_cast<uint32_t>((static_cast<uint64_t>(h) * kAlpha) >> 32);
+  if (ekm) {
+    const uint32_t e = static_cast<uint32_t>(draw(ekm, i / 2) >> (32 * (i & 1)));
+    if (e < m.edit_thresh)  // substitution by a different letter
+      idx = (idx + 1 + static_cast<uint32_t>(draw(ekm2, i) % (kAlpha - 1))) % kAlpha;
+  }
+  return static_cast<uint8_t>(kAlphaChars[idx]);
+}
 
 struct Mode1 {
   const nd_synth_spec& s;
   std::vector<uint64_t> group_first;  // logical index of each group's first member (+ total)
-  Perm perm;
-  uint64_t edit_thresh;  // P(edit) * 2^32
-  explicit Mode1(const nd_synth_spec& spec) : s(spec), perm(spec.doc_count, mix64(spec.seed ^ 0xABCDEF)) {
+  M1 m;
+  explicit Mode1(const nd_synth_spec& spec) : s(spec) {
     group_first.resize(s.group_count + 1);
     uint64_t acc = 0;
     for (uint64_t g = 0; g < s.group_count; ++g) {
@@ -171,19 +199,18 @@ struct Mode1 {
     }
     group_first[s.group_count] = acc;
     if (acc > s.doc_count) fail(ND_ERR_CONFIG, "doc count cannot hold the grouped documents");
-    edit_thresh = static_cast<uint64_t>((static_cast<long double>(s.edit_num) / s.edit_den) * 4294967296.0L);
-  }
-  // logical index -> (text stream key, edit stream key or 0)
-  void source(uint64_t logical, uint64_t& text_key, uint64_t& edit_key) const {
-    if (logical < group_first[s.group_count]) {
-      uint64_t g = std::upper_bound(group_first.begin(), group_first.end(), logical) - group_first.begin() - 1;
-      uint64_t m = logical - group_first[g];
-      text_key = s.seed * 0x632BE59BD9B4E019ull + 0x7777 + g;
-      edit_key = m == 0 ? 0 : (s.seed * 0x8CB92BA72F3D8DD7ull + (g << 8) + m + 1);
-    } else {
-      text_key = s.seed * 0x632BE59BD9B4E019ull + 0x3333333333ull + logical;
-      edit_key = 0;
-    }
+    m.n = s.doc_count;
+    m.seed = s.seed;
+    m.grouped = acc;
+    m.ngroups = s.group_count;
+    m.perm_key = mix64(s.seed ^ 0xABCDEF);
+    int bits = 2;
+    while ((1ull << bits) < m.n) bits += 2;
+    m.half_bits = bits / 2;
+    m.half_mask = (1ull << m.half_bits) - 1;
+    m.edit_thresh = s.edit_num == 0 ? 0u : static_cast<uint32_t>(std::min<long double>(
+        4294967295.0L, (static_cast<long double>(s.edit_num) / s.edit_den) * 4294967296.0L));
+    m.len_draws = s.len_law == 0 ? 1 : 2;
   }
   uint64_t length(Stream& st) const {
     if (s.len_law == 0) return s.len_min + st.below(static_cast<uint64_t>(s.len_max) - s.len_min + 1);
@@ -197,41 +224,33 @@ struct Mode1 {
   }
   uint64_t doc_len(uint64_t position) const {
     uint64_t tk, ek;
-    source(perm.inv(position), tk, ek);
+    m1_source(m, group_first.data(), perm_inv(m, position), tk, ek);
     Stream st(tk);
     return length(st);
   }
-  void doc_text(uint64_t position, uint8_t* out) const {
+  void doc_text(uint64_t position, uint8_t* out, uint64_t len) const {
     uint64_t tk, ek;
-    source(perm.inv(position), tk, ek);
-    Stream st(tk);
-    uint64_t len = length(st);
-    uint64_t i = 0;
-    while (i < len) {
-      uint64_t x = st.next();
-      for (int k = 0; k < 2 && i < len; ++k, ++i) {
-        uint32_t h = static_cast<uint32_t>(x >> (32 * k));
-        out[i] = static_cast<uint8_t>(kAlphabet[(static_cast<uint64_t>(h) * kAlpha) >> 32]);
-      }
-    }
-    if (ek && s.edit_num) {
-      Stream ed(ek);
-      for (uint64_t j = 0; j < len; j += 2) {
-        uint64_t x = ed.next();
-        for (int k = 0; k < 2 && j + k < len; ++k) {
-          uint32_t h = static_cast<uint32_t>(x >> (32 * k));
-          if (h < edit_thresh) {
-            uint8_t c = out[j + k];
-            uint8_t r;
-            do r = static_cast<uint8_t>(kAlphabet[ed.below(kAlpha)]);
-            while (r == c);
-            out[j + k] = r;
-          }
-        }
-      }
-    }
+    m1_source(m, group_first.data(), perm_inv(m, position), tk, ek);
+    const uint64_t tkm = mix64(tk);
+    const uint64_t ekm = (ek && m.edit_thresh) ? mix64(ek) : 0;
+    const uint64_t ekm2 = ekm ? mix64(ek ^ 0x5A5A5A5A5A5A5A5Aull) : 0;
+    for (uint64_t i = 0; i < len; ++i) out[i] = m1_char(m, tkm, ekm, ekm2, i);
   }
 };
+
+__global__ void k_synth_text(M1 m, const uint64_t* __restrict__ group_first,
+                             const uint64_t* __restrict__ offsets, uint8_t* __restrict__ out) {
+  const uint64_t doc = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (doc >= m.n) return;
+  uint64_t tk, ek;
+  m1_source(m, group_first, perm_inv(m, doc), tk, ek);
+  const uint64_t tkm = mix64(tk);
+  const uint64_t ekm = (ek && m.edit_thresh) ? mix64(ek) : 0;
+  const uint64_t ekm2 = ekm ? mix64(ek ^ 0x5A5A5A5A5A5A5A5Aull) : 0;
+  const uint64_t b = offsets[doc], len = offsets[doc + 1] - b;
+  for (uint64_t i = lane; i < len; i += 32) out[b + i] = m1_char(m, tkm, ekm, ekm2, i);
+}
 
 template <class F>
 void parallel_range(uint64_t n, unsigned threads, F&& fn) {
@@ -295,8 +314,24 @@ void synth_generate(const nd_synth_spec& s, uint8_t* bytes, uint64_t* offsets,
   *nbytes_out = offs[s.doc_count];
   if (!bytes) return;
   parallel_range(s.doc_count, threads, [&](uint64_t b, uint64_t e) {
-    for (uint64_t i = b; i < e; ++i) gen.doc_text(i, bytes + offs[i]);
+    for (uint64_t i = b; i < e; ++i) gen.doc_text(i, bytes + offs[i], offs[i + 1] - offs[i]);
   });
+}
+
+void synth_text_device(const nd_synth_spec& s, const uint64_t* d_offsets, uint8_t* d_bytes,
+                       DevBuf& scratch, cudaStream_t stream) {
+  validate(s);
+  if (s.mode != 1) fail(ND_ERR_CONFIG, "device generation supports mode 1 only");
+  Mode1 gen(s);
+  uint64_t* d_gf = scratch.as<uint64_t>(gen.group_first.size());
+  ND_CUDA(cudaMemcpyAsync(d_gf, gen.group_first.data(), gen.group_first.size() * sizeof(uint64_t),
+                          cudaMemcpyHostToDevice, stream));
+  const uint64_t threads = s.doc_count * 32;
+  if (threads == 0) return;
+  k_synth_text<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(gen.m, d_gf, d_offsets,
+                                                                              d_bytes);
+  ND_CHECK_LAUNCH();
+  ND_CUDA(cudaStreamSynchronize(stream));
 }
 
 }  // namespace ndb
