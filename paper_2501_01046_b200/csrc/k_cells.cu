@@ -8,6 +8,8 @@
 // (sigstore.cpp:271-284), and the work list for K3 is built: one item per
 // (cell, tile of kCmpRows rows).  candidate_pairs = sum n(n-1)/2 is the
 // reference's own counter (pipeline.cpp:406-411).
+#include <cstdlib>
+
 #include "nd_internal.cuh"
 
 namespace ndb {
@@ -49,7 +51,8 @@ __global__ void k_cells_compact(const uint64_t* __restrict__ run_start, const ui
                                 const uint32_t* __restrict__ sorted_keys, uint32_t tile_rows,
                                 uint64_t* __restrict__ cell_start, uint32_t* __restrict__ cell_len,
                                 uint32_t* __restrict__ cell_key, uint64_t* __restrict__ cell_pairs,
-                                uint32_t* __restrict__ cell_tiles) {
+                                uint32_t* __restrict__ cell_tiles, uint32_t join_max,
+                                unsigned long long* __restrict__ max_len) {
   uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (r >= runs || !keep[r]) return;
   uint64_t c = keep_idx[r];
@@ -59,7 +62,9 @@ __global__ void k_cells_compact(const uint64_t* __restrict__ run_start, const ui
   cell_len[c] = static_cast<uint32_t>(len);
   cell_key[c] = sorted_keys[s];
   cell_pairs[c] = len * (len - 1) / 2;
-  cell_tiles[c] = static_cast<uint32_t>((len + tile_rows - 1) / tile_rows);
+  // cells the hash join takes (k_join) need no all-pairs tiles
+  cell_tiles[c] = len > join_max ? static_cast<uint32_t>((len + tile_rows - 1) / tile_rows) : 0u;
+  atomicMax(max_len, static_cast<unsigned long long>(len));
 }
 
 __global__ void k_item_cells(const uint64_t* __restrict__ item_off, uint64_t cells,
@@ -82,6 +87,10 @@ int bits_for(uint64_t maxval) {
 void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint64_t m,
                               uint64_t key_limit, uint32_t tile_rows, cudaStream_t s) {
   const unsigned tb = 256;
+  {  // ND_JOIN=0 routes every cell through the all-pairs kernel (A/B tests)
+    const char* j = getenv("ND_JOIN");
+    cs.join_enabled = !(j && j[0] == '0');
+  }
   cs.records = m;
   cs.ncells = 0;
   cs.items = 0;
@@ -115,22 +124,28 @@ void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint6
   cs.cell_key = cs.ckey.as<uint32_t>(cells);
   uint64_t* cpairs = cs.cpairs.as<uint64_t>(cells + 1);
   uint32_t* ctiles = cs.ctiles.as<uint32_t>(cells);
+  unsigned long long* dmax = reinterpret_cast<unsigned long long*>(cs.maxbuf.as<uint64_t>(1));
+  ND_CUDA(cudaMemsetAsync(dmax, 0, sizeof(uint64_t), s));
   k_cells_compact<<<blocks_for(runs, tb), tb, 0, s>>>(run_start, keep, keep_idx, runs, keys,
                                                       tile_rows, cs.cell_start, cs.cell_len,
-                                                      cs.cell_key, cpairs, ctiles);
+                                                      cs.cell_key, cpairs, ctiles,
+                                                      cs.join_enabled ? kJoinMax : 0u, dmax);
   ND_CHECK_LAUNCH();
   uint64_t* pair_off = cs.pair_off.as<uint64_t>(cells + 1);
   scan_u64(cpairs, pair_off, cells, cs.scan, s);
   cs.item_off = cs.ioff.as<uint64_t>(cells + 1);
   scan_u32_to_u64(ctiles, cs.item_off, cells, cs.scan, s);
-  uint64_t tail[2];
+  uint64_t tail[3];
   ND_CUDA(cudaMemcpyAsync(&tail[0], pair_off + cells, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   ND_CUDA(cudaMemcpyAsync(&tail[1], cs.item_off + cells, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  ND_CUDA(cudaMemcpyAsync(&tail[2], dmax, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   ND_CUDA(cudaStreamSynchronize(s));
   cs.candidate_pairs = tail[0];
   cs.items = tail[1];
-  cs.item_cell = cs.icell.as<uint32_t>(cs.items);
-  k_item_cells<<<blocks_for(cells, tb), tb, 0, s>>>(cs.item_off, cells, cs.item_cell);
+  cs.max_len = cs.join_enabled ? tail[2] : 0;
+  cs.item_cell = cs.icell.as<uint32_t>(cs.items + 1);
+  if (cs.items)
+    k_item_cells<<<blocks_for(cells, tb), tb, 0, s>>>(cs.item_off, cells, cs.item_cell);
   ND_CHECK_LAUNCH();
 }
 

@@ -19,6 +19,8 @@
 // atomic per pair.  Pairs are canonical (lo < hi) row
 // indices packed as lo << nb | hi so that sort + unique (compare.cpp:77-84)
 // is a single radix sort over 2*nb bits.
+#include <algorithm>
+
 #include "nd_internal.cuh"
 
 namespace ndb {
@@ -190,6 +192,109 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact hash-join candidate generation for cells of up to kJoinMax documents.
+//
+// A pair with no match among positions [0, P) (P = H - min_matches + 1) is
+// provably rejected (see the header), so the pairs worth counting are exactly
+// the pairs that share a value at some position k < P.  Instead of testing
+// all n(n-1)/2 pairs, one CTA per cell builds, for each k, a hash table of
+// value -> chain of documents in shared memory (tagged entries, so tables are
+// never cleared between positions) and enumerates the pairs inside each
+// chain: O(n*P) work per cell instead of O(n^2*P).  Each candidate (d, e)
+// found at position k is checked by one thread: the first P' = min(H, 32)
+// positions of both rows are compared, the candidate is dropped unless k is
+// its FIRST matching position (each pair is checked once per cell) and unless
+// it has at most H - min_matches mismatches so far; survivors get the full
+// early-exit count (oracle.cpp:81-92) and accepted pairs are emitted.
+constexpr int kJoinThreads = 256;
+
+__device__ __forceinline__ void join_check(const uint32_t* __restrict__ sig, uint32_t H,
+                                           uint32_t ra, uint32_t rb, uint32_t k, uint32_t P,
+                                           uint32_t min_match, int nb,
+                                           uint64_t* __restrict__ out_key,
+                                           uint32_t* __restrict__ out_m,
+                                           unsigned long long* __restrict__ count, uint64_t cap) {
+  const uint32_t* a = sig + static_cast<uint64_t>(ra) * H;
+  const uint32_t* b = sig + static_cast<uint64_t>(rb) * H;
+  const uint32_t allowed = H - min_match;
+  const uint32_t pc = min(H, 32u);
+  uint32_t matches = 0, first = 0xFFFFFFFFu;
+  if ((H & 3) == 0) {
+    for (uint32_t h = 0; h < pc; h += 4) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(a + h));
+      const uint4 y = __ldg(reinterpret_cast<const uint4*>(b + h));
+      const bool e0 = x.x == y.x, e1 = x.y == y.y, e2 = x.z == y.z, e3 = x.w == y.w;
+      matches += e0 + e1 + e2 + e3;
+      if (first == 0xFFFFFFFFu)
+        first = e0 ? h : e1 ? h + 1 : e2 ? h + 2 : e3 ? h + 3 : 0xFFFFFFFFu;
+    }
+  } else {
+    for (uint32_t h = 0; h < pc; ++h) {
+      const bool e = __ldg(a + h) == __ldg(b + h);
+      matches += e;
+      if (e && first == 0xFFFFFFFFu) first = h;
+    }
+  }
+  if (first != k) return;                 // found (and checked) at an earlier position
+  if (pc - matches > allowed) return;     // accepting count already unreachable
+  bool alive;
+  const uint32_t m = full_matches(a, b, H, allowed, alive);
+  if (alive && m >= min_match) emit(ra, rb, m, nb, out_key, out_m, count, cap);
+  (void)P;
+}
+
+__global__ void __launch_bounds__(kJoinThreads)
+    k_join(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
+           const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
+           uint32_t join_max, uint32_t tbits, uint32_t P, uint32_t min_match, int nb,
+           uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
+           unsigned long long* __restrict__ count, uint64_t cap) {
+  extern __shared__ uint32_t jsm[];
+  const uint32_t n = cell_len[blockIdx.x];
+  if (n > join_max) return;  // big cells go to k_compare
+  const uint32_t T = 1u << tbits;
+  uint32_t* keys = jsm;                // T   (tag << 23 | value), tag 0 = empty
+  uint32_t* head = keys + T;           // T   (tag << 16 | doc)
+  uint32_t* next = head + T;           // join_max
+  uint32_t* rowsm = next + join_max;   // join_max
+  const uint64_t s = cell_start[blockIdx.x];
+  for (uint32_t i = threadIdx.x; i < n; i += kJoinThreads) rowsm[i] = rows[s + i];
+  for (uint32_t i = threadIdx.x; i < T; i += kJoinThreads) {
+    keys[i] = 0;
+    head[i] = 0;
+  }
+  __syncthreads();
+  const uint32_t mask = T - 1;
+  for (uint32_t k = 0; k < P; ++k) {
+    const uint32_t tag = k + 1;
+    for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads) {
+      const uint32_t v = __ldg(sig + static_cast<uint64_t>(rowsm[d]) * H + k);
+      const uint32_t key = (tag << 23) | v;
+      uint32_t h = (v * 0x9E3779B1u) >> (32 - tbits);
+      for (;;) {
+        const uint32_t cur = keys[h];
+        if (cur == key) break;
+        if ((cur >> 23) == tag) {  // another value of this position: probe on
+          h = (h + 1) & mask;
+          continue;
+        }
+        const uint32_t old = atomicCAS(&keys[h], cur, key);
+        if (old == cur || old == key) break;
+        // lost a race for this slot: look at it again
+      }
+      const uint32_t prev = atomicExch(&head[h], (tag << 16) | d);
+      next[d] = (prev >> 16) == tag ? (prev & 0xFFFFu) : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads) {
+      for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e])
+        join_check(sig, H, rowsm[d], rowsm[e], k, P, min_match, nb, out_key, out_m, count, cap);
+    }
+    __syncthreads();
+  }
+}
+
 using CmpFn = void (*)(const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
                        const uint32_t*, const uint32_t*, const uint64_t*, uint32_t, int,
                        uint64_t*, uint32_t*, unsigned long long*, uint64_t);
@@ -207,7 +312,27 @@ int compare_prefilter_width(uint32_t H, uint32_t min_match) {
 void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32_t min_match,
                     int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,
                     uint64_t cap, cudaStream_t s) {
-  if (cs.items == 0 || min_match > H) return;
+  if (cs.ncells == 0 || min_match > H) return;
+  // cells of <= kJoinMax documents: hash join (one CTA per cell)
+  const uint32_t P = H - min_match + 1;
+  const uint32_t join_max = static_cast<uint32_t>(std::min<uint64_t>(cs.max_len, kJoinMax));
+  if (join_max >= 2 && P <= 510) {
+    uint32_t tbits = 4;
+    while ((1u << tbits) < 2 * join_max) ++tbits;
+    const size_t smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      ND_CUDA(cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+      configured = smem;
+    }
+    if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
+    k_join<<<static_cast<unsigned>(cs.ncells), kJoinThreads, smem, s>>>(
+        d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len, join_max, tbits, P, min_match, nb,
+        out_key, out_m, count, cap);
+    ND_CHECK_LAUNCH();
+  }
+  if (cs.items == 0) return;  // no cell above kJoinMax
   CmpFn fn = nullptr;
   switch (compare_prefilter_width(H, min_match)) {
     case 16: fn = k_compare<16>; break;

@@ -127,9 +127,12 @@ int bits_for(uint64_t maxval);  // number of bits needed to hold maxval
 
 // K2 output: non-singleton LSH cells as CSR over sorted rows (k_cells.cu).
 constexpr uint32_t kCmpRows = 128;  // rows per compare work item (128 threads x kR)
+constexpr uint32_t kJoinMax = 4096;  // largest cell the hash join (k_join) takes
 struct CellSet {
   DevBuf rec_keys, rec_vals, flag, run_idx, run_start, cstart, clen, ckey, cpairs, ctiles, pair_off,
-      ioff, icell, scan;
+      ioff, icell, scan, maxbuf;
+  bool join_enabled = true;     // cells <= kJoinMax use the hash join
+  uint64_t max_len = 0;         // largest non-singleton cell
   SortScratch sort;
   uint64_t records = 0, ncells = 0, items = 0, candidate_pairs = 0;
   const uint32_t* sorted_rows = nullptr;  // rows of all records, grouped by cell
@@ -140,7 +143,7 @@ struct CellSet {
   uint32_t* item_cell = nullptr;          // per item: its cell
   void release() {
     for (DevBuf* b : {&rec_keys, &rec_vals, &flag, &run_idx, &run_start, &cstart, &clen, &ckey,
-                      &cpairs, &ctiles, &pair_off, &ioff, &icell, &scan})
+                      &cpairs, &ctiles, &pair_off, &ioff, &icell, &scan, &maxbuf})
       b->release();
     sort.release();
   }

@@ -242,3 +242,45 @@ def test_dedup_pairs_match_reference_pair_files(ctx, ref, tmp_path):
                              ctx=ctx)
     got = pipeline.dedup_pairs(rep.distinct_pairs, ctx=ctx)
     assert [(p.lo, p.hi, p.match_count) for p in got] == sorted(want)
+
+
+def test_join_and_all_pairs_paths_agree(ctx, ref, tmp_path, monkeypatch):
+    # the same corpus through the hash join (default) and the all-pairs kernel
+    corpus = str(tmp_path / "c.jsonl")
+    ref.generate_synthetic(3000, 250, gmin=2, gmax=4, edit=(4, 100), len_min=300, len_max=900,
+                           seed=23, corpus_path=corpus, truth_path=str(tmp_path / "t.jsonl"))
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ND_JOIN", mode)
+        ws = str(tmp_path / f"g{mode}")
+        rep = pipeline.run_dedup(pipeline.RunConfig(inputs=[corpus], workspace=ws), ctx=ctx)
+        outs[mode] = (_files(ws), pipeline.dedup_pairs(rep.distinct_pairs, ctx=ctx))
+    assert outs["1"] == outs["0"]
+    assert outs["1"][1]
+
+
+def test_giant_cells_mix_join_and_all_pairs(ctx, ref, tmp_path):
+    # 4500 near-copies of one text put > kJoinMax (4096) documents into cells
+    # (all-pairs kernel) while the random documents' cells go through the join
+    rng = np.random.default_rng(31)
+    alpha = np.frombuffer(b"abcdefghijklmnopqrstuvwxyz0123456789 ", np.uint8)
+    base = alpha[rng.integers(0, 37, size=700)]
+    docs = []
+    for i in range(4500):
+        t = base.copy()
+        pos = rng.integers(0, 700, size=int(rng.integers(0, 4)))
+        t[pos] = alpha[rng.integers(0, 37, size=len(pos))]
+        docs.append(t)
+    docs += [alpha[rng.integers(0, 37, size=int(n))] for n in rng.integers(300, 900, size=1500)]
+    order = rng.permutation(len(docs))
+    corpus = str(tmp_path / "g.jsonl")
+    with open(corpus, "w") as f:
+        for i in order:
+            f.write(json.dumps({"text": bytes(docs[i]).decode()}) + "\n")
+    ws_ref, ws_gpu = str(tmp_path / "r"), str(tmp_path / "g")
+    os.makedirs(ws_ref)
+    ref.run_dedup(corpus, ws_ref, workers=os.cpu_count())
+    rep = pipeline.run_dedup(pipeline.RunConfig(inputs=[corpus], workspace=ws_gpu), ctx=ctx)
+    assert _files(ws_gpu) == _files(ws_ref)
+    assert rep.stats is None or rep.candidate_pairs == json.load(
+        open(os.path.join(ws_ref, "compare_stage.json")))["candidate_pairs"]
