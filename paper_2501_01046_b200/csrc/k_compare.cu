@@ -244,6 +244,9 @@ __device__ __forceinline__ void join_check(const uint32_t* __restrict__ sig, uin
   (void)P;
 }
 
+constexpr int kJoinQueue = 2048;  // candidate slots (drained when >= kJoinDrain are waiting)
+constexpr int kJoinDrain = 512;
+
 __global__ void __launch_bounds__(kJoinThreads)
     k_join(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
            const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
@@ -251,6 +254,8 @@ __global__ void __launch_bounds__(kJoinThreads)
            uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
            unsigned long long* __restrict__ count, uint64_t cap) {
   extern __shared__ uint32_t jsm[];
+  __shared__ uint2 queue[kJoinQueue];
+  __shared__ uint32_t qn;
   const uint32_t n = cell_len[blockIdx.x];
   if (n > join_max) return;  // big cells go to k_compare
   const uint32_t T = 1u << tbits;
@@ -264,6 +269,7 @@ __global__ void __launch_bounds__(kJoinThreads)
     keys[i] = 0;
     head[i] = 0;
   }
+  if (threadIdx.x == 0) qn = 0;
   __syncthreads();
   const uint32_t mask = T - 1;
   for (uint32_t k = 0; k < P; ++k) {
@@ -287,11 +293,29 @@ __global__ void __launch_bounds__(kJoinThreads)
       next[d] = (prev >> 16) == tag ? (prev & 0xFFFFu) : 0xFFFFFFFFu;
     }
     __syncthreads();
+    // enumerate the pairs of every chain into the queue (checked by whole CTAs,
+    // one candidate per thread, so a candidate never idles 31 lanes)
     for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads) {
-      for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e])
-        join_check(sig, H, rowsm[d], rowsm[e], k, P, min_match, nb, out_key, out_m, count, cap);
+      for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e]) {
+        const uint32_t slot = atomicAdd(&qn, 1u);
+        if (slot < kJoinQueue)
+          queue[slot] = make_uint2(d | (e << 16), k);
+        else  // queue full: check inline
+          join_check(sig, H, rowsm[d], rowsm[e], k, P, min_match, nb, out_key, out_m, count, cap);
+      }
     }
     __syncthreads();
+    const uint32_t waiting = min(qn, static_cast<uint32_t>(kJoinQueue));
+    if (waiting >= kJoinDrain || (k + 1 == P && waiting > 0)) {
+      for (uint32_t t = threadIdx.x; t < waiting; t += kJoinThreads) {
+        const uint2 c = queue[t];
+        join_check(sig, H, rowsm[c.x & 0xFFFFu], rowsm[c.x >> 16], c.y, P, min_match, nb, out_key,
+                   out_m, count, cap);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) qn = 0;
+      __syncthreads();
+    }
   }
 }
 
