@@ -218,18 +218,27 @@ __device__ __forceinline__ void join_check(const uint32_t* __restrict__ sig, uin
   const uint32_t* a = sig + static_cast<uint64_t>(ra) * H;
   const uint32_t* b = sig + static_cast<uint64_t>(rb) * H;
   const uint32_t allowed = H - min_match;
-  const uint32_t pc = min(H, 32u);
-  uint32_t matches = 0, first = 0xFFFFFFFFu;
-  if ((H & 3) == 0) {
-    for (uint32_t h = 0; h < pc; h += 4) {
-      const uint4 x = __ldg(reinterpret_cast<const uint4*>(a + h));
-      const uint4 y = __ldg(reinterpret_cast<const uint4*>(b + h));
-      const bool e0 = x.x == y.x, e1 = x.y == y.y, e2 = x.z == y.z, e3 = x.w == y.w;
+  uint32_t matches = 0, first = 0xFFFFFFFFu, pc;
+  if (H >= 32 && (H & 3) == 0) {
+    pc = 32;  // 16 independent 16-byte loads in flight
+    uint4 x[8], y[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      x[q] = __ldg(reinterpret_cast<const uint4*>(a) + q);
+      y[q] = __ldg(reinterpret_cast<const uint4*>(b) + q);
+    }
+#pragma unroll
+    for (int q = 7; q >= 0; --q) {  // descending, so `first` ends at the lowest match
+      const bool e0 = x[q].x == y[q].x, e1 = x[q].y == y[q].y, e2 = x[q].z == y[q].z,
+                 e3 = x[q].w == y[q].w;
       matches += e0 + e1 + e2 + e3;
-      if (first == 0xFFFFFFFFu)
-        first = e0 ? h : e1 ? h + 1 : e2 ? h + 2 : e3 ? h + 3 : 0xFFFFFFFFu;
+      if (e3) first = 4 * q + 3;
+      if (e2) first = 4 * q + 2;
+      if (e1) first = 4 * q + 1;
+      if (e0) first = 4 * q;
     }
   } else {
+    pc = min(H, 32u);
     for (uint32_t h = 0; h < pc; ++h) {
       const bool e = __ldg(a + h) == __ldg(b + h);
       matches += e;
@@ -244,9 +253,8 @@ __device__ __forceinline__ void join_check(const uint32_t* __restrict__ sig, uin
   (void)P;
 }
 
-constexpr int kJoinQueue = 2048;  // candidate slots (drained when >= kJoinDrain are waiting)
-constexpr int kJoinDrain = 512;
-
+// DPT = documents per thread (join_max <= DPT * kJoinThreads)
+template <int DPT>
 __global__ void __launch_bounds__(kJoinThreads)
     k_join(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
            const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
@@ -254,8 +262,6 @@ __global__ void __launch_bounds__(kJoinThreads)
            uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
            unsigned long long* __restrict__ count, uint64_t cap) {
   extern __shared__ uint32_t jsm[];
-  __shared__ uint2 queue[kJoinQueue];
-  __shared__ uint32_t qn;
   const uint32_t n = cell_len[blockIdx.x];
   if (n > join_max) return;  // big cells go to k_compare
   const uint32_t T = 1u << tbits;
@@ -269,51 +275,54 @@ __global__ void __launch_bounds__(kJoinThreads)
     keys[i] = 0;
     head[i] = 0;
   }
-  if (threadIdx.x == 0) qn = 0;
   __syncthreads();
   const uint32_t mask = T - 1;
-  for (uint32_t k = 0; k < P; ++k) {
-    const uint32_t tag = k + 1;
-    for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads) {
-      const uint32_t v = __ldg(sig + static_cast<uint64_t>(rowsm[d]) * H + k);
-      const uint32_t key = (tag << 23) | v;
-      uint32_t h = (v * 0x9E3779B1u) >> (32 - tbits);
-      for (;;) {
-        const uint32_t cur = keys[h];
-        if (cur == key) break;
-        if ((cur >> 23) == tag) {  // another value of this position: probe on
-          h = (h + 1) & mask;
-          continue;
+  const bool vec = (H & 3) == 0;
+  for (uint32_t k0 = 0; k0 < P; k0 += 4) {
+    // this thread's documents' values at positions k0..k0+3, loaded up front
+    uint4 val[DPT];
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const uint32_t d = threadIdx.x + j * kJoinThreads;
+      if (d < n) {
+        const uint32_t* r = sig + static_cast<uint64_t>(rowsm[d]) * H + k0;
+        if (vec && k0 + 4 <= H)
+          val[j] = __ldg(reinterpret_cast<const uint4*>(r));
+        else
+          val[j] = make_uint4(__ldg(r), k0 + 1 < H ? __ldg(r + 1) : 0u,
+                              k0 + 2 < H ? __ldg(r + 2) : 0u, k0 + 3 < H ? __ldg(r + 3) : 0u);
+      }
+    }
+#pragma unroll
+    for (uint32_t dk = 0; dk < 4; ++dk) {
+      const uint32_t k = k0 + dk;
+      if (k >= P) break;
+      const uint32_t tag = k + 1;
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) {
+        const uint32_t d = threadIdx.x + j * kJoinThreads;
+        if (d >= n) break;
+        const uint32_t v = dk == 0 ? val[j].x : dk == 1 ? val[j].y : dk == 2 ? val[j].z : val[j].w;
+        const uint32_t key = (tag << 23) | v;
+        uint32_t h = (v * 0x9E3779B1u) >> (32 - tbits);
+        for (;;) {
+          const uint32_t cur = keys[h];
+          if (cur == key) break;
+          if ((cur >> 23) == tag) {  // another value of this position: probe on
+            h = (h + 1) & mask;
+            continue;
+          }
+          const uint32_t old = atomicCAS(&keys[h], cur, key);
+          if (old == cur || old == key) break;
+          // lost a race for this slot: look at it again
         }
-        const uint32_t old = atomicCAS(&keys[h], cur, key);
-        if (old == cur || old == key) break;
-        // lost a race for this slot: look at it again
-      }
-      const uint32_t prev = atomicExch(&head[h], (tag << 16) | d);
-      next[d] = (prev >> 16) == tag ? (prev & 0xFFFFu) : 0xFFFFFFFFu;
-    }
-    __syncthreads();
-    // enumerate the pairs of every chain into the queue (checked by whole CTAs,
-    // one candidate per thread, so a candidate never idles 31 lanes)
-    for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads) {
-      for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e]) {
-        const uint32_t slot = atomicAdd(&qn, 1u);
-        if (slot < kJoinQueue)
-          queue[slot] = make_uint2(d | (e << 16), k);
-        else  // queue full: check inline
-          join_check(sig, H, rowsm[d], rowsm[e], k, P, min_match, nb, out_key, out_m, count, cap);
-      }
-    }
-    __syncthreads();
-    const uint32_t waiting = min(qn, static_cast<uint32_t>(kJoinQueue));
-    if (waiting >= kJoinDrain || (k + 1 == P && waiting > 0)) {
-      for (uint32_t t = threadIdx.x; t < waiting; t += kJoinThreads) {
-        const uint2 c = queue[t];
-        join_check(sig, H, rowsm[c.x & 0xFFFFu], rowsm[c.x >> 16], c.y, P, min_match, nb, out_key,
-                   out_m, count, cap);
+        const uint32_t prev = atomicExch(&head[h], (tag << 16) | d);
+        next[d] = (prev >> 16) == tag ? (prev & 0xFFFFu) : 0xFFFFFFFFu;
       }
       __syncthreads();
-      if (threadIdx.x == 0) qn = 0;
+      for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads)
+        for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e])
+          join_check(sig, H, rowsm[d], rowsm[e], k, P, min_match, nb, out_key, out_m, count, cap);
       __syncthreads();
     }
   }
@@ -344,14 +353,19 @@ void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32
     uint32_t tbits = 4;
     while ((1u << tbits) < 2 * join_max) ++tbits;
     const size_t smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      ND_CUDA(cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    using JoinFn = void (*)(const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
+                            const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, int,
+                            uint64_t*, uint32_t*, unsigned long long*, uint64_t);
+    JoinFn fn = join_max <= 2 * kJoinThreads   ? k_join<2>
+                : join_max <= 4 * kJoinThreads ? k_join<4>
+                : join_max <= 8 * kJoinThreads ? k_join<8>
+                                               : k_join<16>;
+    static_assert(16 * kJoinThreads >= kJoinMax, "k_join<16> must cover kJoinMax");
+    if (smem > 48 * 1024)
+      ND_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-      configured = smem;
-    }
     if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
-    k_join<<<static_cast<unsigned>(cs.ncells), kJoinThreads, smem, s>>>(
+    fn<<<static_cast<unsigned>(cs.ncells), kJoinThreads, smem, s>>>(
         d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len, join_max, tbits, P, min_match, nb,
         out_key, out_m, count, cap);
     ND_CHECK_LAUNCH();
