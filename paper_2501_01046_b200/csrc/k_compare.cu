@@ -245,8 +245,15 @@ __device__ __forceinline__ void join_check(const uint32_t* __restrict__ sig, uin
       if (e && first == 0xFFFFFFFFu) first = h;
     }
   }
-  if (first != k) return;                 // found (and checked) at an earlier position
   if (pc - matches > allowed) return;     // accepting count already unreachable
+  // check each pair once per cell: at its FIRST matching position
+  if (k < pc) {
+    if (first != k) return;
+  } else {
+    if (first != 0xFFFFFFFFu) return;     // matched inside the prefix already
+    for (uint32_t h = pc; h < k; ++h)
+      if (__ldg(a + h) == __ldg(b + h)) return;
+  }
   bool alive;
   const uint32_t m = full_matches(a, b, H, allowed, alive);
   if (alive && m >= min_match) emit(ra, rb, m, nb, out_key, out_m, count, cap);

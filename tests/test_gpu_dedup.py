@@ -284,3 +284,27 @@ def test_giant_cells_mix_join_and_all_pairs(ctx, ref, tmp_path):
     assert _files(ws_gpu) == _files(ws_ref)
     assert rep.stats is None or rep.candidate_pairs == json.load(
         open(os.path.join(ws_ref, "compare_stage.json")))["candidate_pairs"]
+
+
+@pytest.mark.parametrize("thr", [(1, 2), (2, 5)])
+def test_join_finds_pairs_whose_first_match_is_late(ctx, ref, thr):
+    # low thresholds make P = H - min_matches + 1 > 32: pairs whose first
+    # equal position lies beyond the 32-position prefix must still be found
+    H = 128
+    rng = np.random.default_rng(41)
+    n = 120
+    base = rng.integers(0, 1 << 22, size=H).astype(np.uint32)
+    sig = np.tile(base, (n, 1))
+    for r in range(n):
+        late = int(rng.integers(32, 60))  # positions [0, late) all differ
+        sig[r, :late] = rng.integers(0, 1 << 22, size=late)
+        k = int(rng.integers(0, 10))
+        pos = rng.choice(np.arange(late, H), size=k, replace=False)
+        sig[r, pos] = rng.integers(0, 1 << 22, size=k)
+    b = GatheredBucket(lsh.BucketKey(0, 0), list(range(n)), sig.reshape(-1))
+    t = SimilarityThreshold(thr)
+    got = compare.compare_bucket(b, H, t, ctx=ctx)
+    lo, hi, m = ref.compare_cells(sig, np.array([0, n], np.uint64), np.arange(n, dtype=np.uint32),
+                                  *thr)
+    assert got == [DuplicatePair(int(a), int(c), int(d)) for a, c, d in zip(lo, hi, m)]
+    assert got
