@@ -26,6 +26,7 @@
 #include "neardup/dedup_graph.hpp"
 #include "neardup/lsh.hpp"
 #include "neardup/minhash.hpp"
+#include "neardup/oracle.hpp"
 #include "neardup/pipeline.hpp"
 #include "neardup/sigstore.hpp"
 #include "neardup/synthetic.hpp"
@@ -147,6 +148,26 @@ int ref_compare_cells(const uint32_t* sigs, const uint64_t* doc_ids, uint32_t H,
       (*hi_out)[i] = pairs[i].hi;
       (*m_out)[i] = pairs[i].match_count;
     }
+  });
+}
+
+// all_pairs_dupset (oracle.cpp:53-108): docs with any partner above the
+// threshold; out receives the sorted doc ids, *nout their count.
+int ref_all_pairs_dupset(const uint32_t* sigs, const uint64_t* doc_ids, uint64_t n, uint32_t H,
+                         uint64_t thr_num, uint64_t thr_den, unsigned workers, uint64_t* out,
+                         uint64_t* nout) {
+  return guarded([&] {
+    std::vector<Signature> s(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      s[i].doc_id = doc_ids ? doc_ids[i] : i;
+      s[i].values.assign(sigs + i * H, sigs + (i + 1) * H);
+    }
+    OracleGuard g;
+    g.override_refusal = true;
+    g.warn_above = ~0ull;
+    NearDuplicateSet set = all_pairs_dupset(s, H, SimilarityThreshold{Ratio(thr_num, thr_den)}, g, workers);
+    for (size_t i = 0; i < set.doc_ids.size(); ++i) out[i] = set.doc_ids[i];
+    *nout = set.doc_ids.size();
   });
 }
 

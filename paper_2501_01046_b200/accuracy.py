@@ -1,0 +1,103 @@
+"""Accuracy evaluation on the GPU -- mirror of the reference's oracle.hpp and
+run_eval_accuracy (pipeline.cpp:534-585), SURVEY 8f rank 4.
+
+  exact_window_jaccard     oracle.cpp:32-51   (host; set arithmetic on windows)
+  all_pairs_dupset         oracle.cpp:53-108  -> K3 over ONE cell holding every document
+  standard_minhash_dupset  oracle.cpp:110-122 -> K1 + the above
+  dupset_jaccard           oracle.cpp:124-141 (host merge of sorted id lists)
+  run_eval_accuracy        pipeline.cpp:534-585
+The all-pairs comparison is the same exact kernel pair as the dedup's K3
+(hash join for <= 4096 documents, tiled all-pairs with the exact prefilter
+above), so the quadratic reference oracle becomes a sub-second GPU pass at
+10^5-10^6 documents.
+"""
+from __future__ import annotations
+
+import json
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import compare, minhash, pipeline
+from .compare import GatheredBucket, GatherResult, SimilarityThreshold
+from .device import Context
+from .lsh import BucketKey
+
+
+@dataclass
+class JaccardResult:
+    intersection: int = 0
+    union_size: int = 0
+
+    def value(self) -> float:
+        return 1.0 if self.union_size == 0 else self.intersection / self.union_size
+
+
+@dataclass
+class NearDuplicateSet:
+    method: str
+    doc_ids: list[int]
+
+
+def exact_window_jaccard(a: bytes, b: bytes, shingle_len: int) -> JaccardResult:
+    """|A ∩ B| / |A ∪ B| over distinct byte windows (oracle.cpp:32-51)."""
+    if shingle_len == 0:
+        raise ValueError("shingle length must be positive")
+    if len(a) < shingle_len or len(b) < shingle_len:
+        raise minhash.ShortDocumentError(6, f"document too short for a {shingle_len}-unit window")
+    sa = {a[i:i + shingle_len] for i in range(len(a) - shingle_len + 1)}
+    sb = {b[i:i + shingle_len] for i in range(len(b) - shingle_len + 1)}
+    inter = len(sa & sb)
+    return JaccardResult(inter, len(sa) + len(sb) - inter)
+
+
+def all_pairs_dupset(signatures, hash_count: int, threshold: SimilarityThreshold,
+                     ctx: Context | None = None, doc_ids=None) -> NearDuplicateSet:
+    """Every document with some partner above the threshold (exhaustive)."""
+    sig = np.ascontiguousarray(signatures, np.uint32).reshape(-1, hash_count)
+    ids = list(range(sig.shape[0])) if doc_ids is None else [int(d) for d in doc_ids]
+    order = np.argsort(np.asarray(ids, dtype=np.uint64), kind="stable")
+    bucket = GatheredBucket(BucketKey(0, 0), [ids[i] for i in order], sig[order].reshape(-1))
+    pairs = compare.compare_pass(GatherResult([bucket]), hash_count, threshold, ctx=ctx)
+    docs = sorted({p.lo for p in pairs} | {p.hi for p in pairs})
+    return NearDuplicateSet("all-pairs", docs)
+
+
+def standard_minhash_dupset(docs, family, threshold, ctx: Context | None = None) -> NearDuplicateSet:
+    sigs = minhash.signature_batch(docs, family, ctx=ctx)
+    mat = np.stack([s.values for s in sigs]) if sigs else np.zeros((0, family.hash_count), np.uint32)
+    out = all_pairs_dupset(mat, family.hash_count, threshold, ctx, [s.doc_id for s in sigs])
+    out.method = "standard-minhash"
+    return out
+
+
+def dupset_jaccard(a, b) -> JaccardResult:
+    sa, sb = set(a), set(b)
+    inter = len(sa & sb)
+    return JaccardResult(inter, len(sa) + len(sb) - inter)
+
+
+def run_eval_accuracy(config: "pipeline.RunConfig", ctx: Context | None = None) -> dict:
+    """Full pipeline, then the exhaustive comparison over the same signatures;
+    writes accuracy.json with the reference's layout (pipeline.cpp:563-583)."""
+    rep = pipeline.run_dedup(config, ctx=ctx)
+    manifest, _ = pipeline.build_manifest(config.inputs, config)
+    docs = []
+    for i in range(len(manifest.files)):
+        docs.extend(pipeline.surviving_documents(manifest, i, config))
+    fam = minhash.derive_family(config.seed, config.hash_count, config.shingle_len, config.unit)
+    oracle = standard_minhash_dupset(docs, fam, SimilarityThreshold(config.threshold), ctx)
+    n = manifest.total_surviving
+    acc = {"corpus_size": n,
+           "jaccard_vs_oracle": dupset_jaccard(rep.near_duplicates, oracle.doc_ids).value(),
+           "methods": [
+               {"method": "pipeline-lsh", "dupset_size": len(rep.near_duplicates),
+                "ratio": len(rep.near_duplicates) / n if n else 0.0,
+                "ratio_label": f"{len(rep.near_duplicates)} / {n}"},
+               {"method": "standard-minhash", "dupset_size": len(oracle.doc_ids),
+                "ratio": len(oracle.doc_ids) / n if n else 0.0,
+                "ratio_label": f"{len(oracle.doc_ids)} / {n}"}]}
+    with open(os.path.join(config.workspace, "accuracy.json"), "w") as f:
+        f.write(json.dumps(acc, indent=2) + "\n")
+    return acc

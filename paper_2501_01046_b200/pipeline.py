@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import NdDedupStats, NdParams, u8p, u64p
-from .corpus import CorpusManifest, build_manifest, surviving_documents
+from .corpus import CorpusManifest, build_manifest, surviving_documents  # noqa: F401
 from .dedup_graph import DedupReport, DuplicateGroup
 from .device import Context, default_context
 from .lsh import _ratio

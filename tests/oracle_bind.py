@@ -144,6 +144,8 @@ class Ref:
                                         C.c_uint64, C.c_uint64, C.c_uint32,
                                         C.POINTER(u64p), C.POINTER(u64p), C.POINTER(u32p),
                                         u64p]
+        L.ref_all_pairs_dupset.argtypes = [u32p, u64p, C.c_uint64, C.c_uint32, C.c_uint64,
+                                           C.c_uint64, C.c_uint, u64p, u64p]
         L.ref_union.argtypes = [u64p, u64p, C.c_uint64, C.POINTER(u64p), C.POINTER(u64p), u64p,
                                 u64p]
         L.ref_generate_synthetic.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
@@ -192,6 +194,16 @@ class Ref:
         for p in (lo, hi, m):
             self.lib.ref_free(p)
         return out
+
+    def all_pairs_dupset(self, sigs, num, den, workers=8, doc_ids=None):
+        sigs = np.ascontiguousarray(sigs, np.uint32)
+        n = sigs.shape[0]
+        out = np.zeros(n + 1, np.uint64)
+        k = C.c_uint64()
+        ids = None if doc_ids is None else _ptr(np.ascontiguousarray(doc_ids, np.uint64), u64p)
+        self._check(self.lib.ref_all_pairs_dupset(_ptr(sigs, u32p), ids, n, sigs.shape[1], num, den,
+                                                  workers, _ptr(out, u64p), C.byref(k)))
+        return out[: k.value]
 
     def union(self, lo, hi):
         lo = np.ascontiguousarray(lo, np.uint64)

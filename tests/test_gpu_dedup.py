@@ -308,3 +308,19 @@ def test_join_finds_pairs_whose_first_match_is_late(ctx, ref, thr):
                                   *thr)
     assert got == [DuplicatePair(int(a), int(c), int(d)) for a, c, d in zip(lo, hi, m)]
     assert got
+
+
+@pytest.mark.parametrize("n", [300, 6000])
+def test_all_pairs_dupset_vs_reference(ctx, ref, n):
+    # exhaustive oracle (oracle.cpp:53-108) on one cell of every document:
+    # n=300 takes the hash join, n=6000 the tiled all-pairs kernel
+    from paper_2501_01046_b200 import accuracy
+
+    data, offs = ref.generate_synthetic(n, n // 10, gmin=2, gmax=3, edit=(3, 100), len_min=300,
+                                        len_max=700, seed=n)
+    sig, _ = ref.signatures(data, offs, K=0, workers=8)
+    ids = np.arange(n, dtype=np.uint64) * 3 + 1
+    want = ref.all_pairs_dupset(sig, 4, 5, doc_ids=ids)
+    got = accuracy.all_pairs_dupset(sig, 128, SimilarityThreshold((4, 5)), ctx=ctx, doc_ids=ids)
+    assert got.doc_ids == want.tolist()
+    assert got.doc_ids
