@@ -43,7 +43,7 @@ typedef struct nd_params {
   uint32_t bands;           /* b */
   uint32_t rows;            /* r */
   uint32_t shingle_len;     /* L */
-  uint32_t unit;            /* 0 = byte (ShingleUnit::kByte); 1 = codepoint (unsupported) */
+  uint32_t unit;            /* 0 = byte (ShingleUnit::kByte); 1 = codepoint (kCodepoint) */
   uint32_t bucket_count;    /* K; 0 = choose_bucket_count(n, bucket_scale) */
   uint64_t threshold_num;   /* SimilarityThreshold (compare.hpp:28-37) */
   uint64_t threshold_den;
@@ -111,7 +111,9 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t hash_count,
 
 /* signature_of_document over a packed batch + band_bucket_ids
  * (minhash.hpp:71-78, lsh.hpp:38-40; caller pipeline.cpp:214-218).
- * bytes[offsets[i] .. offsets[i+1]) is document i (NFC UTF-8, byte units).
+ * bytes[offsets[i] .. offsets[i+1]) is document i (NFC UTF-8); its units are
+ * the bytes, or the decoded scalar values when the family was uploaded with
+ * unit 1 (text_units, text.cpp:115-122; decoded on the GPU).
  * sig_out: n*H u32 row-major; band_out: n*bands u32 (NULL to skip), ids mod K
  * (K == 0 -> raw u32 band row sums, K-independent).  Every document must
  * yield a full window (else ND_ERR_SHORT, nothing written).
@@ -128,6 +130,14 @@ int nd_signatures_h2d(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets
 int nd_signatures_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offsets,
                          uint64_t n, uint32_t bands, uint32_t rows, uint32_t bucket_count,
                          uint32_t* d_sig, uint32_t* d_band);
+
+/* text_units (text.hpp:32, text.cpp:101-122) over a packed batch, on the GPU:
+ * unit_offsets[n+1] (prefix sums of per-document unit counts; the counts are
+ * codepoint_count, text.cpp:88-99) and, when units_out is not NULL, the units
+ * (bytes widened, or scalar values with U+FFFD per ill-formed subpart).
+ * Call once with units_out = NULL to size the buffer.  Synchronous. */
+int nd_text_units(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                  uint32_t unit, uint64_t* unit_offsets, uint32_t* units_out);
 
 /* band_bucket_ids (lsh.hpp:38-40, lsh.cpp:42-60) over host signature rows
  * sigs[n*H] -> band ids[n*bands] (K == 0: raw u32 row sums). */

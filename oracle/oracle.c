@@ -166,6 +166,92 @@ int or_signature_bytes(const uint8_t* text, uint64_t len, const or_hash_fn* fns,
   return 0;
 }
 
+/* text.cpp:101-113 decode_codepoints: U8_NEXT walk (Unicode Table 3-7 ranges),
+ * one U+FFFD per maximal ill-formed subpart.  Returns the unit count; writes
+ * at most cap units. */
+uint64_t or_decode_codepoints(const uint8_t* s, uint64_t len, uint32_t* out, uint64_t cap) {
+  uint64_t i = 0, n = 0;
+  while (i < len) {
+    uint32_t b0 = s[i++], cp = 0xFFFD, c = 0, lo = 0x80, hi = 0xBF;
+    int need = -1, k;
+    if (b0 < 0x80) {
+      cp = b0;
+      need = 0;
+    } else if (b0 >= 0xC2 && b0 <= 0xDF) {
+      need = 1;
+      c = b0 & 0x1F;
+    } else if (b0 >= 0xE0 && b0 <= 0xEF) {
+      need = 2;
+      c = b0 & 0x0F;
+      if (b0 == 0xE0) lo = 0xA0;
+      if (b0 == 0xED) hi = 0x9F;
+    } else if (b0 >= 0xF0 && b0 <= 0xF4) {
+      need = 3;
+      c = b0 & 0x07;
+      if (b0 == 0xF0) lo = 0x90;
+      if (b0 == 0xF4) hi = 0x8F;
+    }
+    if (need > 0) {
+      for (k = 0; k < need; ++k) {
+        uint32_t b;
+        if (i >= len) break;
+        b = s[i];
+        if (b < lo || b > hi) break;
+        lo = 0x80;
+        hi = 0xBF;
+        c = (c << 6) | (b & 0x3F);
+        ++i;
+      }
+      cp = k == need ? c : 0xFFFD;
+    }
+    if (n < cap) out[n] = cp;
+    ++n;
+  }
+  return n;
+}
+
+/* minhash.cpp:133-162 over u32 units (text_units output); returns -1 if short */
+int or_signature_units(const uint32_t* u, uint64_t len, const or_hash_fn* fns, uint32_t H,
+                       uint32_t L, uint32_t* out) {
+  if (len < L) return -1;
+  for (uint32_t h = 0; h < H; ++h) {
+    const or_hash_fn* f = &fns[h];
+    uint32_t state = or_hash_window_direct(u, L, f);
+    uint32_t best = state;
+    for (uint64_t w = 1; w + L <= len; ++w) {
+      state = or_roll_next(state, u[w - 1], u[w + L - 1], f);
+      if (state < best) best = state;
+    }
+    out[h] = best;
+  }
+  return 0;
+}
+
+/* batch with a shingle unit (0 byte, 1 codepoint) */
+int or_signature_batch_unit(const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                            const or_hash_fn* fns, uint32_t H, uint32_t L, uint32_t unit,
+                            uint32_t* out) {
+  uint64_t i, j;
+  for (i = 0; i < n; ++i) {
+    const uint8_t* t = bytes + offsets[i];
+    uint64_t len = offsets[i + 1] - offsets[i];
+    uint32_t* units = (uint32_t*)malloc((len ? len : 1) * sizeof(uint32_t));
+    uint64_t m;
+    int rc;
+    if (!units) return -3;
+    if (unit == 1) {
+      m = or_decode_codepoints(t, len, units, len);
+    } else {
+      for (j = 0; j < len; ++j) units[j] = t[j];
+      m = len;
+    }
+    rc = or_signature_units(units, m, fns, H, L, out + i * H);
+    free(units);
+    if (rc != 0) return rc;
+  }
+  return 0;
+}
+
 int or_signature_batch(const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
                        const or_hash_fn* fns, uint32_t H, uint32_t L, uint32_t* out) {
   for (uint64_t i = 0; i < n; ++i) {

@@ -41,6 +41,15 @@ int or_signature_bytes(const uint8_t* text, uint64_t len, const or_hash_fn* fns,
 /* batch form over a packed buffer, rows written at out + i*H */
 int or_signature_batch(const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
                        const or_hash_fn* fns, uint32_t H, uint32_t L, uint32_t* out);
+/* text.cpp:101-113 decode_codepoints; returns the unit count (writes <= cap) */
+uint64_t or_decode_codepoints(const uint8_t* s, uint64_t len, uint32_t* out, uint64_t cap);
+/* signature_of_document over u32 units; returns -1 if short */
+int or_signature_units(const uint32_t* units, uint64_t len, const or_hash_fn* fns, uint32_t H,
+                       uint32_t L, uint32_t* out);
+/* batch form with a shingle unit (0 byte, 1 codepoint) */
+int or_signature_batch_unit(const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                            const or_hash_fn* fns, uint32_t H, uint32_t L, uint32_t unit,
+                            uint32_t* out);
 uint32_t or_choose_bucket_count(uint64_t n, uint64_t num, uint64_t den); /* lsh.cpp:26-40, 0 = error */
 void or_band_bucket_ids(const uint32_t* sig, uint32_t bands, uint32_t rows, uint32_t K,
                         uint32_t* out); /* lsh.cpp:42-60 */

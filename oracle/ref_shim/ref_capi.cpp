@@ -237,9 +237,10 @@ int ref_run_dedup(const char* input, const char* workspace, uint32_t H, uint32_t
                   uint32_t rows, uint32_t L, uint64_t thr_num, uint64_t thr_den,
                   uint64_t scale_num, uint64_t scale_den, uint64_t min_chars, uint64_t seed,
                   unsigned workers, uint64_t memory_budget, double* timings,
-                  uint64_t* candidate_pairs) {
+                  uint64_t* candidate_pairs, uint32_t unit) {
   return guarded([&] {
     RunConfig c;
+    c.unit = static_cast<ShingleUnit>(unit);
     c.inputs = {input};
     c.workspace = workspace;
     c.hash_count = H;

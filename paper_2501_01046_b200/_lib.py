@@ -81,6 +81,7 @@ SIGNATURES = {
                                     C.c_uint32, vp, vp]),
     "nd_signatures_device": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_uint32, C.c_uint32,
                                        C.c_uint32, vp, vp]),
+    "nd_text_units": (C.c_int, [vp, u8p, u64p, C.c_uint64, C.c_uint32, u64p, u32p]),
     "nd_band_keys": (C.c_int, [vp, u32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                C.c_uint32, u32p]),
     "nd_compare_cells": (C.c_int, [vp, u32p, C.c_uint64, C.c_uint32, u64p, u32p, C.c_uint64,

@@ -32,6 +32,14 @@
 // The "int" variant (ND_K1_KERNEL=int) keeps the all-integer Barrett
 // reduction (IMAD.WIDE + SHF + IMAD.HI) for comparison.
 //
+// Codepoint units ("wide" variant).  Scalar values reach 0x10FFFF, so
+// c_out*QLn needs 44 bits and the FP32 quotient estimate is no longer exact
+// enough; the units (decoded by k_utf8.cu) are u32 and each step is
+//   u = q*c + c_out*QLn + c_in          (2 IMAD.WIDE, u < p*(q + 2^21) < 2^44)
+//   k = umulhi(u >> 13, floor(2^45/p))  (k in {Q-1, Q}: the error is below
+//                                        u/2^45 + 2^13/p < 0.55)
+//   c' = min(r, r - p), r = u - k*p     (r in [0, 2p))
+//
 // Layout.  A warp owns one work item.  Its 32 lanes form Z groups of 32/Z
 // lanes; lane l of a group owns functions [l*F, l*F+F) of the padded family
 // (Hp = 32*F/Z; pad functions are copies of function 0 and never stored), and
@@ -82,6 +90,7 @@ struct FamPtrs {
   const float* qp;        // fl(q / p)
   const float* qlnp;      // fl(QLn / p)
   const float* c1e;       // -2^23 * qp + 2^-5 (exact)
+  const uint32_t* m45;    // floor(2^45 / p)
 };
 
 // ---------------------------------------------------------------------------
@@ -142,7 +151,7 @@ __global__ void k_bands_from_rows(const uint32_t* __restrict__ docs, uint32_t nd
 }
 
 // ---------------------------------------------------------------------------
-enum class Arith { kInt, kFq };
+enum class Arith { kInt, kFq, kWide };
 
 template <Arith A, int F>
 struct Consts;
@@ -172,6 +181,37 @@ struct Consts<Arith::kInt, F> {
       uint32_t k = __umulhi(t, m[f]);  // M = floor(2^40 / p): k in {Q-1, Q}
       uint32_t r = lo + k * negp[f];
       uint32_t c = min(r, r + negp[f]);
+      s[f] = c;
+      if (kMin) mn[f] = min(mn[f], c);
+    }
+  }
+};
+
+template <int F>
+struct Consts<Arith::kWide, F> {
+  uint32_t q[F], qln[F], m[F], negp[F];
+  __device__ void load(const FamPtrs& fp, int base) {
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      q[f] = fp.q[base + f];
+      qln[f] = fp.qln[base + f];
+      m[f] = fp.m45[base + f];
+      negp[f] = fp.negp[base + f];
+    }
+  }
+  // one rolling step for all F functions with units up to 0x10FFFF
+  template <bool kMin>
+  __device__ __forceinline__ void step(uint32_t cin, uint32_t cout, float /*cout_f*/,
+                                       uint32_t (&s)[F], uint32_t (&mn)[F]) const {
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      uint64_t u = static_cast<uint64_t>(cout) * qln[f] + cin;
+      u += static_cast<uint64_t>(q[f]) * s[f];
+      const uint32_t lo = static_cast<uint32_t>(u);
+      const uint32_t t = __funnelshift_r(lo, static_cast<uint32_t>(u >> 32), 13);
+      const uint32_t k = __umulhi(t, m[f]);
+      const uint32_t r = lo + k * negp[f];
+      const uint32_t c = min(r, r + negp[f]);
       s[f] = c;
       if (kMin) mn[f] = min(mn[f], c);
     }
@@ -220,9 +260,9 @@ struct Consts<Arith::kFq, F> {
   }
 };
 
-template <Arith A, int F, int Z>
+template <Arith A, int F, int Z, class T>
 __global__ void ND_K1_BOUNDS
-    k_signature(const uint8_t* __restrict__ text, const uint64_t* __restrict__ offsets,
+    k_signature(const T* __restrict__ text, const uint64_t* __restrict__ offsets,
                 const uint32_t* __restrict__ item_doc, const uint64_t* __restrict__ item_off,
                 uint64_t n_items, FamPtrs fam, uint32_t L, uint32_t H, uint32_t bands,
                 uint32_t rows, uint32_t K, uint32_t* __restrict__ sig,
@@ -260,7 +300,7 @@ __global__ void ND_K1_BOUNDS
   const uint64_t gs = ws + span * grp / Z;
   const uint64_t ge = ws + span * (grp + 1) / Z;
   const uint64_t e = ge + L - 1;  // one past the last character this slice reads
-  const uint8_t* base = text + off;
+  const T* base = text + off;
 
   Consts<A, F> k;
   k.load(fam, gl * F);
@@ -395,25 +435,35 @@ __global__ void ND_K1_BOUNDS
   }
 }
 
-template <Arith A, int F, int Z>
-void launch_k1(const DevFamily& fam, const uint8_t* d_bytes, const uint64_t* d_offsets,
+template <Arith A, int F, int Z, class T = uint8_t>
+void launch_k1(const DevFamily& fam, const void* d_text, const uint64_t* d_offsets,
                const uint32_t* item_doc, const uint64_t* item_off, uint64_t items, uint32_t bands,
                uint32_t rows, uint32_t K, uint32_t* d_sig, uint32_t* d_band, cudaStream_t s) {
-  FamPtrs p{fam.q, fam.qln, fam.m, fam.negp, fam.c3, fam.qp, fam.qlnp, fam.c1e};
+  FamPtrs p{fam.q, fam.qln, fam.m, fam.negp, fam.c3, fam.qp, fam.qlnp, fam.c1e, fam.m45};
   uint64_t blocks = (items + kWarps - 1) / kWarps;
-  k_signature<A, F, Z><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
-      d_bytes, d_offsets, item_doc, item_off, items, p, fam.L, fam.H, bands, rows, K, d_sig,
+  k_signature<A, F, Z, T><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
+      static_cast<const T*>(d_text), d_offsets, item_doc, item_off, items, p, fam.L, fam.H, bands, rows, K, d_sig,
       d_band);
   ND_CHECK_LAUNCH();
 }
 
-using Launcher = void (*)(const DevFamily&, const uint8_t*, const uint64_t*, const uint32_t*,
+using Launcher = void (*)(const DevFamily&, const void*, const uint64_t*, const uint32_t*,
                           const uint64_t*, uint64_t, uint32_t, uint32_t, uint32_t, uint32_t*,
                           uint32_t*, cudaStream_t);
 
 // (arith, Hp) -> instantiation; F = functions per lane, Z = window slices per
 // warp.  ND_K1_FZ="F,Z" overrides the default shape (tuning experiments).
-Launcher pick_launcher(bool int_arith, uint32_t Hp) {
+Launcher pick_launcher(bool int_arith, uint32_t Hp, bool codepoint) {
+  if (codepoint) {  // u32 units: wide arithmetic
+    switch (Hp) {
+      case 32: return launch_k1<Arith::kWide, 1, 1, uint32_t>;
+      case 64: return launch_k1<Arith::kWide, 2, 1, uint32_t>;
+      case 128: return launch_k1<Arith::kWide, 4, 1, uint32_t>;
+      case 256: return launch_k1<Arith::kWide, 8, 1, uint32_t>;
+      case 512: return launch_k1<Arith::kWide, 16, 1, uint32_t>;
+    }
+    return nullptr;
+  }
   if (int_arith) {
     switch (Hp) {
       case 32: return launch_k1<Arith::kInt, 1, 1>;
@@ -453,6 +503,19 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     fail(ND_ERR_CONFIG, "shingle length must be in [1, 64] on the GPU path");
   if (n > 0xFFFFFFFFull) fail(ND_ERR_CONFIG, "batch exceeds 2^32 documents");
   unsigned tb = 256;
+  const void* d_text = d_bytes;
+  if (fam.unit == 1) {
+    // codepoint units: decode, then plan and sign over the u32 unit arrays;
+    // unit counts are only known on the device, so the short check runs there
+    const uint32_t* units = nullptr;
+    const uint64_t* uoff = nullptr;
+    decode_codepoints_device(d_bytes, d_offsets, n, sc.units, sc.unit_off, sc.unit_cnt,
+                             sc.scan_tmp, s, &units, &uoff);
+    d_text = units;
+    d_offsets = uoff;
+    h_offsets = nullptr;
+    check_short = true;
+  }
   uint32_t hflags[4] = {0, 0, 0, 0};
   if (h_offsets) {  // host planning: only multi-item batches need the device plan
     for (uint64_t d = 0; d < n; ++d) {
@@ -502,9 +565,9 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     const char* v = getenv("ND_K1_KERNEL");
     return v && std::string(v) == "int";
   }();
-  Launcher go = pick_launcher(int_arith, fam.Hp);
+  Launcher go = pick_launcher(int_arith, fam.Hp, fam.unit == 1);
   if (!go) fail(ND_ERR_CONFIG, "hash count must be at most 512 on the GPU path");
-  go(fam, d_bytes, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, s);
+  go(fam, d_text, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, s);
   if (nmulti && d_band) {
     uint64_t total = static_cast<uint64_t>(nmulti) * bands;
     k_bands_from_rows<<<static_cast<unsigned>((total + tb - 1) / tb), tb, 0, s>>>(

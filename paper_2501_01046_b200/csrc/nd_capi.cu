@@ -279,19 +279,20 @@ int nd_ctx_set_stream(nd_ctx* ctx, void* stream) {
 int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L, uint32_t unit) {
   return guarded_impl(ctx, [&] {
     if (H == 0 || L == 0) fail(ND_ERR_CONFIG, "hash count and shingle length must be positive");
-    if (unit != 0)
-      fail(ND_ERR_CONFIG, "codepoint shingle units are not supported on the GPU path yet");
+    if (unit > 1) fail(ND_ERR_CONFIG, "unknown shingle unit");
     if (L > 64) fail(ND_ERR_CONFIG, "shingle length above 64 is not supported on the GPU path");
     uint32_t Hp = 32;
     while (Hp < H) Hp *= 2;
     if (Hp > 512) fail(ND_ERR_CONFIG, "hash count above 512 is not supported on the GPU path");
-    // 8 arrays of Hp entries: q, QLn, M, -p, c3 (u32) and q/p, QLn/p, c1e (f32)
-    std::vector<uint32_t> host(8 * Hp);
+    // 9 arrays of Hp entries: q, QLn, M, -p, c3 (u32), q/p, QLn/p, c1e (f32), M45 (u32)
+    std::vector<uint32_t> host(9 * Hp);
     for (uint32_t i = 0; i < Hp; ++i) {
       const nd_hash_fn& f = fns[i < H ? i : 0];  // pad with copies of fn 0 (never stored)
       uint64_t p = f.modulus;
       if (p < 257 || p >= (1u << 23) || f.base == 0 || f.base >= (1u << 16))
         fail(ND_ERR_CONFIG, "hash function outside the GPU arithmetic domain (p < 2^23, q < 2^16)");
+      if (unit == 1 && p <= 0x10FFFF)  // scalar values must already be residues (minhash.cpp:107-109)
+        fail(ND_ERR_CONFIG, "codepoint units need moduli above 0x10FFFF");
       uint64_t qL = static_cast<uint64_t>(f.base_power) * f.base % p;  // q^L = q^(L-1) * q
       uint32_t qln = static_cast<uint32_t>((p - qL) % p);
       float qp = static_cast<float>(static_cast<double>(f.base) / static_cast<double>(p));
@@ -305,8 +306,9 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L,
       std::memcpy(&host[5 * Hp + i], &qp, 4);
       std::memcpy(&host[6 * Hp + i], &qlnp, 4);
       std::memcpy(&host[7 * Hp + i], &c1e, 4);
+      host[8 * Hp + i] = static_cast<uint32_t>((1ull << 45) / p);
     }
-    uint32_t* d = ctx->fam_buf.as<uint32_t>(8 * Hp);
+    uint32_t* d = ctx->fam_buf.as<uint32_t>(9 * Hp);
     ND_CUDA(cudaMemcpy(d, host.data(), host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     ctx->fam.q = d;
     ctx->fam.qln = d + Hp;
@@ -316,6 +318,8 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L,
     ctx->fam.qp = reinterpret_cast<float*>(d + 5 * Hp);
     ctx->fam.qlnp = reinterpret_cast<float*>(d + 6 * Hp);
     ctx->fam.c1e = reinterpret_cast<float*>(d + 7 * Hp);
+    ctx->fam.m45 = d + 8 * Hp;
+    ctx->fam.unit = unit;
     ctx->fam.H = H;
     ctx->fam.Hp = Hp;
     ctx->fam.L = L;
@@ -329,6 +333,43 @@ int nd_signatures(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, ui
                   uint32_t* band_out) {
   return guarded_impl(ctx, [&] {
     signatures_host(ctx, bytes, offsets, n, bands, rows, K, sig_out, band_out);
+  });
+}
+
+int nd_text_units(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                  uint32_t unit, uint64_t* unit_offsets, uint32_t* units_out) {
+  return guarded_impl(ctx, [&] {
+    if (unit > 1) fail(ND_ERR_CONFIG, "unknown shingle unit");
+    if (!unit_offsets) fail(ND_ERR_CONFIG, "null unit_offsets");
+    for (uint64_t i = 0; i < n; ++i)
+      if (offsets[i + 1] < offsets[i]) fail(ND_ERR_CONFIG, "offsets must be non-decreasing");
+    const uint64_t nb = n ? offsets[n] - offsets[0] : 0;
+    if (unit == 0) {  // byte units: the counts are the lengths
+      for (uint64_t i = 0; i <= n; ++i) unit_offsets[i] = offsets[i] - offsets[0];
+      if (units_out)
+        for (uint64_t i = 0; i < nb; ++i) units_out[i] = bytes[offsets[0] + i];
+      return;
+    }
+    unit_offsets[0] = 0;
+    if (n == 0) return;
+    cudaStream_t s = ctx->stream;
+    uint8_t* dt = ctx->sig_in_text.as<uint8_t>(nb + 16);
+    uint64_t* doff = ctx->sig_in_off.as<uint64_t>(n + 1);
+    std::vector<uint64_t> rel(n + 1);
+    for (uint64_t i = 0; i <= n; ++i) rel[i] = offsets[i] - offsets[0];
+    ND_CUDA(cudaMemcpyAsync(dt, bytes + offsets[0], nb, cudaMemcpyHostToDevice, s));
+    ND_CUDA(cudaMemcpyAsync(doff, rel.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    const uint32_t* units = nullptr;
+    const uint64_t* uoff = nullptr;
+    SigScratch& sc = ctx->sig_scratch;
+    decode_codepoints_device(dt, doff, n, sc.units, sc.unit_off, sc.unit_cnt, sc.scan_tmp, s,
+                             &units, &uoff);
+    ND_CUDA(cudaMemcpyAsync(unit_offsets, uoff, (n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    ND_CUDA(cudaStreamSynchronize(s));
+    if (units_out && unit_offsets[n])
+      ND_CUDA(cudaMemcpyAsync(units_out, units, unit_offsets[n] * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, s));
+    ND_CUDA(cudaStreamSynchronize(s));
   });
 }
 

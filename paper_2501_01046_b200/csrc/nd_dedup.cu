@@ -51,8 +51,8 @@ void validate(const nd_params& p) {
 
 void ensure_family(nd_ctx* ctx, const nd_params& p) {
   const auto& fam = ctx->fam;
-  if (fam.q && fam.H == p.hash_count && fam.L == p.shingle_len && ctx->family_seed == p.seed &&
-      ctx->family_derived)
+  if (fam.q && fam.H == p.hash_count && fam.L == p.shingle_len && fam.unit == p.unit &&
+      ctx->family_seed == p.seed && ctx->family_derived)
     return;
   std::vector<nd_hash_fn> f = derive_family(p.seed, p.hash_count, p.shingle_len, p.unit);
   int rc = nd_family_upload(ctx, f.data(), p.hash_count, p.shingle_len, p.unit);

@@ -43,9 +43,11 @@ struct DevFamily {
   float* qp = nullptr;       // fl(q / p)
   float* qlnp = nullptr;     // fl(QLn / p)
   float* c1e = nullptr;      // -2^23 * qp + 2^-5
+  uint32_t* m45 = nullptr;   // floor(2^45 / p)  (codepoint units, "wide" variant)
   uint32_t H = 0;            // real hash count
   uint32_t Hp = 0;           // padded hash count
   uint32_t L = 0;
+  uint32_t unit = 0;         // 0 = byte, 1 = codepoint (ShingleUnit, text.hpp:23-26)
 };
 
 // Simple growable device scratch buffer.
@@ -98,11 +100,19 @@ struct PinnedBuf {
 // K1: signatures + band keys over device-resident packed text.
 // Returns ND_ERR_SHORT through the flag buffer when a document has no window.
 struct SigScratch {
-  DevBuf seg_count, item_off, item_doc, flags, multi_docs, scan_tmp;
+  DevBuf seg_count, item_off, item_doc, flags, multi_docs, scan_tmp, units, unit_off, unit_cnt;
   void release() {
-    for (DevBuf* b : {&seg_count, &item_off, &item_doc, &flags, &multi_docs, &scan_tmp}) b->release();
+    for (DevBuf* b : {&seg_count, &item_off, &item_doc, &flags, &multi_docs, &scan_tmp, &units,
+                      &unit_off, &unit_cnt})
+      b->release();
   }
 };
+// UTF-8 -> codepoint units (k_utf8.cu): units_out[unit_off_out[d] ..
+// unit_off_out[d+1]) are document d's units (decode_codepoints, text.cpp:101-113).
+void decode_codepoints_device(const uint8_t* d_text, const uint64_t* d_offsets, uint64_t n,
+                              DevBuf& units_buf, DevBuf& unit_off_buf, DevBuf& count_buf,
+                              DevBuf& scan_tmp, cudaStream_t s, const uint32_t** units_out,
+                              const uint64_t** unit_off_out);
 // h_offsets: optional host copy of d_offsets; when given, planning happens on
 // the host and the launch is fully asynchronous for single-item documents.
 void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint64_t* d_offsets,

@@ -27,12 +27,12 @@ from .device import Context, default_context
 
 __all__ = ["ShingleUnit", "HashFunctionParams", "HashFamily", "derive_family", "CleanDocument",
            "Signature", "ShortDocumentError", "signature_of_document", "signature_batch",
-           "pack_documents", "signatures_packed", "signatures_device"]
+           "pack_documents", "signatures_packed", "signatures_device", "text_units"]
 
 
 class ShingleUnit(enum.IntEnum):
     BYTE = 0       # ShingleUnit::kByte (text.hpp:23-26)
-    CODEPOINT = 1  # ShingleUnit::kCodepoint (not yet on the GPU path)
+    CODEPOINT = 1  # ShingleUnit::kCodepoint (decoded on the GPU, k_utf8.cu)
 
 
 @dataclass
@@ -121,16 +121,43 @@ def signatures_device(d_bytes: int, d_offsets: int, n: int, family: HashFamily, 
                                            C.c_void_p(d_band) if d_band else None))
 
 
+def text_units(data: np.ndarray, offsets: np.ndarray, unit: ShingleUnit,
+               ctx: Context | None = None, counts_only: bool = False):
+    """text_units (text.hpp:32, text.cpp:101-122) over a packed batch, decoded on
+    the GPU: returns (unit_offsets[n+1] u64, units u32 or None)."""
+    ctx = ctx or default_context()
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    n = len(offsets) - 1
+    uoff = np.zeros(n + 1, np.uint64)
+    dp = data.ctypes.data_as(u8p) if data.size else C.cast(C.c_char_p(b"\0"), u8p)
+    ctx.check(ctx.lib.nd_text_units(ctx.h, dp, offsets.ctypes.data_as(u64p), n, int(unit),
+                                    uoff.ctypes.data_as(u64p), None))
+    if counts_only:
+        return uoff, None
+    units = np.empty(int(uoff[-1]), np.uint32)
+    if units.size:
+        ctx.check(ctx.lib.nd_text_units(ctx.h, dp, offsets.ctypes.data_as(u64p), n, int(unit),
+                                        uoff.ctypes.data_as(u64p), units.ctypes.data_as(u32p)))
+    return uoff, units
+
+
+def _unit_counts(docs: Sequence[CleanDocument], unit: ShingleUnit, ctx) -> np.ndarray:
+    if unit == ShingleUnit.BYTE:
+        return np.fromiter((len(_as_bytes(d.text)) for d in docs), np.uint64, len(docs))
+    data, offsets = pack_documents(docs)
+    uoff, _ = text_units(data, offsets, unit, ctx=ctx, counts_only=True)
+    return np.diff(uoff)
+
+
 def signature_batch(docs: Sequence[CleanDocument], family: HashFamily,
                     on_short: Callable[[int], None] | None = None,
                     ctx: Context | None = None) -> list[Signature]:
     """minhash.cpp:164-177: order preserved; short documents are skipped and
     reported through on_short, never emitted with sentinel values."""
     keep = []
-    for d in docs:
-        units = len(_as_bytes(d.text)) if family.unit == ShingleUnit.BYTE else None
-        if units is None:
-            raise _lib.ConfigError(_lib.ND_ERR_CONFIG, "codepoint units are not supported on the GPU path")
+    counts = _unit_counts(docs, family.unit, ctx) if docs else []
+    for d, units in zip(docs, counts):
         if units < family.shingle_len:
             if on_short:
                 on_short(d.doc_id)
@@ -146,7 +173,7 @@ def signature_batch(docs: Sequence[CleanDocument], family: HashFamily,
 def signature_of_document(doc: CleanDocument, family: HashFamily,
                           ctx: Context | None = None) -> Signature:
     """minhash.cpp:133-162; raises ShortDocumentError without a full window."""
-    n = len(_as_bytes(doc.text))
+    n = int(_unit_counts([doc], family.unit, ctx)[0])
     if n < family.shingle_len:
         raise ShortDocumentError(_lib.ND_ERR_SHORT,
                                  f"document {doc.doc_id} has {n} units, needs {family.shingle_len}")

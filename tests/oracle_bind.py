@@ -62,6 +62,10 @@ class Oracle:
         L.or_roll_next.restype = C.c_uint32
         L.or_signature_batch.argtypes = [u8p, u64p, C.c_uint64, C.POINTER(HashFn), C.c_uint32,
                                          C.c_uint32, u32p]
+        L.or_signature_batch_unit.argtypes = [u8p, u64p, C.c_uint64, C.POINTER(HashFn),
+                                              C.c_uint32, C.c_uint32, C.c_uint32, u32p]
+        L.or_decode_codepoints.argtypes = [u8p, C.c_uint64, u32p, C.c_uint64]
+        L.or_decode_codepoints.restype = C.c_uint64
         L.or_choose_bucket_count.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
         L.or_choose_bucket_count.restype = C.c_uint32
         L.or_band_bucket_ids.argtypes = [u32p, C.c_uint32, C.c_uint32, C.c_uint32, u32p]
@@ -83,15 +87,28 @@ class Oracle:
             raise ValueError("derive_family failed")
         return fns
 
-    def signatures(self, data: np.ndarray, offsets: np.ndarray, fns, L: int = 5) -> np.ndarray:
+    def signatures(self, data: np.ndarray, offsets: np.ndarray, fns, L: int = 5,
+                   unit: int = 0) -> np.ndarray:
         n = len(offsets) - 1
         H = len(fns)
         out = np.zeros((n, H), dtype=np.uint32)
-        rc = self.lib.or_signature_batch(_ptr(data, u8p), _ptr(offsets, u64p), n, fns, H, L,
-                                         _ptr(out, u32p))
+        data = np.ascontiguousarray(data, np.uint8)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        if unit == 0:
+            rc = self.lib.or_signature_batch(_ptr(data, u8p), _ptr(offsets, u64p), n, fns, H, L,
+                                             _ptr(out, u32p))
+        else:
+            rc = self.lib.or_signature_batch_unit(_ptr(data, u8p), _ptr(offsets, u64p), n, fns, H,
+                                                  L, unit, _ptr(out, u32p))
         if rc != 0:
             raise ValueError("short document")
         return out
+
+    def decode_codepoints(self, b: bytes) -> list[int]:
+        a = np.frombuffer(b, np.uint8).copy() if b else np.zeros(1, np.uint8)
+        out = np.zeros(max(1, len(b)), np.uint32)
+        n = self.lib.or_decode_codepoints(_ptr(a, u8p), len(b), _ptr(out, u32p), len(out))
+        return out[:n].tolist()
 
     def band_ids(self, sigs: np.ndarray, bands: int, rows: int, K: int) -> np.ndarray:
         sigs = np.ascontiguousarray(sigs, dtype=np.uint32)
@@ -155,7 +172,7 @@ class Ref:
         L.ref_run_dedup.argtypes = [C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32,
                                     C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                     C.c_uint64, C.c_uint64, C.c_uint, C.c_uint64,
-                                    C.POINTER(C.c_double), u64p]
+                                    C.POINTER(C.c_double), u64p, C.c_uint32]
         self.lib = L
 
     def _check(self, rc):
@@ -168,13 +185,13 @@ class Ref:
         return fns
 
     def signatures(self, data, offsets, seed=5, H=128, L=5, bands=16, rows=8, K=0, workers=1,
-                   doc_ids=None):
+                   doc_ids=None, unit=0):
         n = len(offsets) - 1
         sig = np.zeros((n, H), np.uint32)
         band = np.zeros((n, bands), np.uint32)
         ids = None if doc_ids is None else _ptr(np.ascontiguousarray(doc_ids, np.uint64), u64p)
         self._check(self.lib.ref_signatures(_ptr(data, u8p), _ptr(offsets, u64p), ids, n, seed, H,
-                                            L, 0, bands, rows, K, workers, _ptr(sig, u32p),
+                                            L, unit, bands, rows, K, workers, _ptr(sig, u32p),
                                             _ptr(band, u32p)))
         return sig, band
 
@@ -234,10 +251,10 @@ class Ref:
         return data, offs
 
     def run_dedup(self, input_path, workspace, H=128, bands=16, rows=8, L=5, thr=(4, 5),
-                  scale=(2, 1), min_chars=200, seed=5, workers=1, memory_budget=0):
+                  scale=(2, 1), min_chars=200, seed=5, workers=1, memory_budget=0, unit=0):
         t = (C.c_double * 3)()
         cand = C.c_uint64()
         self._check(self.lib.ref_run_dedup(input_path.encode(), workspace.encode(), H, bands, rows,
                                            L, thr[0], thr[1], scale[0], scale[1], min_chars, seed,
-                                           workers, memory_budget, t, C.byref(cand)))
+                                           workers, memory_budget, t, C.byref(cand), unit))
         return list(t), cand.value

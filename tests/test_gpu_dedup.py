@@ -324,3 +324,37 @@ def test_all_pairs_dupset_vs_reference(ctx, ref, n):
     got = accuracy.all_pairs_dupset(sig, 128, SimilarityThreshold((4, 5)), ctx=ctx, doc_ids=ids)
     assert got.doc_ids == want.tolist()
     assert got.doc_ids
+
+
+def test_codepoint_unit_dedup_byte_identical(ctx, ref, tmp_path):
+    # --shingle-unit codepoint end to end: NFC-stable multi-byte text (Cyrillic,
+    # Greek, CJK, emoji, ASCII), planted near-duplicate pairs
+    import unicodedata
+
+    rng = np.random.default_rng(17)
+    alphabet = ([chr(c) for c in range(0x430, 0x450)] + [chr(c) for c in range(0x3B1, 0x3CA)]
+                + [chr(c) for c in range(0x4E00, 0x4E80)] + [chr(c) for c in range(0x1F600, 0x1F640)]
+                + list("abcdefghij    "))
+    docs = []
+    for _ in range(1200):
+        docs.append("".join(rng.choice(alphabet, size=int(rng.integers(250, 900)))))
+    for i in range(0, 300, 2):  # 150 near-duplicate pairs
+        t = list(docs[i])
+        for k in rng.choice(len(t), size=max(1, len(t) // 100), replace=False):
+            t[k] = alphabet[int(rng.integers(len(alphabet)))]
+        docs[i + 1] = "".join(t)
+    order = rng.permutation(len(docs))
+    corpus = str(tmp_path / "uni.jsonl")
+    with open(corpus, "w", encoding="utf-8") as f:
+        for i in order:
+            assert unicodedata.is_normalized("NFC", docs[i])
+            f.write(json.dumps({"text": docs[i]}, ensure_ascii=bool(i % 2)) + "\n")
+    ws_ref, ws_gpu = str(tmp_path / "r"), str(tmp_path / "g")
+    os.makedirs(ws_ref)
+    ref.run_dedup(corpus, ws_ref, workers=os.cpu_count(), unit=1)
+    cfg = pipeline.RunConfig(inputs=[corpus], workspace=ws_gpu, unit=pipeline.ShingleUnit.CODEPOINT)
+    rep = pipeline.run_dedup(cfg, ctx=ctx)
+    want = _files(ws_ref)
+    assert _files(ws_gpu) == want
+    assert json.loads(want["summary.json"])["duplicate_groups"] >= 140
+    assert rep.candidate_pairs == json.load(open(os.path.join(ws_ref, "compare_stage.json")))["candidate_pairs"]

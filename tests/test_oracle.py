@@ -166,3 +166,52 @@ def test_compare_and_union_match_reference(oracle, ref):
     lab = oracle.components(rlo.astype(np.uint32), rhi.astype(np.uint32), 120)
     got = sorted((int(lab[i]), i) for i in range(120) if lab[i] != 0xFFFFFFFF)
     assert got == list(zip(rep.tolist(), mem.tolist()))
+
+
+# ---- codepoint units (text.cpp:88-113) --------------------------------------
+def _rand_utf8(rng, n_units, ill_formed=False):
+    """Random text over 1..4-byte scalars (plus, optionally, ill-formed bytes)."""
+    pools = [(0x20, 0x7F), (0xA0, 0x800), (0x800, 0xD800), (0xE000, 0x10000), (0x10000, 0x110000)]
+    out = bytearray()
+    for _ in range(n_units):
+        k = rng.integers(0, len(pools) + (2 if ill_formed else 0))
+        if k >= len(pools):
+            out += bytes(rng.integers(0x80, 0x100, size=int(rng.integers(1, 4)), dtype=np.uint8))
+            continue
+        lo, hi = pools[k]
+        out += chr(int(rng.integers(lo, hi))).encode("utf-8")
+    return bytes(out)
+
+
+def test_decode_codepoints_maximal_subparts(oracle):
+    # Unicode 15 ch.3, Table 3-8 (U+FFFD for maximal subparts), which ICU's
+    # U8_NEXT (text.cpp:101-113) follows
+    b = bytes([0x61, 0xF1, 0x80, 0x80, 0xE1, 0x80, 0xC2, 0x62, 0x80, 0x63, 0x80, 0xBF, 0x64])
+    assert oracle.decode_codepoints(b) == [0x61, 0xFFFD, 0xFFFD, 0xFFFD, 0x62, 0xFFFD, 0x63,
+                                           0xFFFD, 0xFFFD, 0x64]
+    assert oracle.decode_codepoints("é€😀".encode()) == [0xE9, 0x20AC, 0x1F600]
+    assert oracle.decode_codepoints(b"\xed\xa0\x80") == [0xFFFD] * 3  # surrogate: ED A0 ill-formed
+    assert oracle.decode_codepoints(b"\xf0\x9f\x98") == [0xFFFD]  # truncated 4-byte sequence
+    assert oracle.decode_codepoints(b"\xc0\xaf") == [0xFFFD, 0xFFFD]  # overlong lead
+
+
+def test_decode_codepoints_matches_cpython(oracle):
+    # CPython's UTF-8 decoder implements the same maximal-subpart replacement
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        b = _rand_utf8(rng, int(rng.integers(0, 60)), ill_formed=True)
+        want = [ord(c) for c in b.decode("utf-8", errors="replace")]
+        assert oracle.decode_codepoints(b) == want, b
+
+
+def test_codepoint_signatures_oracle_vs_reference(oracle, ref):
+    rng = np.random.default_rng(9)
+    texts = [_rand_utf8(rng, int(n), ill_formed=bool(i % 3 == 0))
+             for i, n in enumerate(rng.integers(5, 400, size=60))]
+    offs = np.zeros(len(texts) + 1, np.uint64)
+    offs[1:] = np.cumsum([len(t) for t in texts])
+    data = np.frombuffer(b"".join(texts), np.uint8).copy()
+    for H, L in [(128, 5), (16, 3)]:
+        want, _ = ref.signatures(data, offs, seed=5, H=H, L=L, bands=0, rows=0, K=0, unit=1)
+        got = oracle.signatures(data, offs, oracle.derive_family(5, H, L), L, unit=1)
+        np.testing.assert_array_equal(got, want)
