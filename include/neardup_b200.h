@@ -191,6 +191,69 @@ int nd_dedup_fetch_groups(nd_ctx* ctx, uint64_t* members, uint64_t* group_start)
  * as written by pipeline.cpp:479-506) for the last dedup, into dir. */
 int nd_dedup_write_report(nd_ctx* ctx, const char* dir, uint64_t total_records);
 
+/* ---- staged workflow on disk: hash -> gather-compare -> union ---------------
+ * The reference persists every stage (pipeline.hpp:62-96): one .feds signature
+ * file per input file, one .pairs file per (worker, gather pass), then the
+ * report.  These entry points produce and consume the same bytes, so stages
+ * can be mixed with the reference's (e.g. its union stage on our pair files). */
+typedef struct nd_feds_header { /* SignatureFileHeader (sigstore.hpp:24-42) */
+  uint32_t hash_count, bands, rows, bucket_count, shingle_len, unit;
+  uint64_t family_seed, scale_num, scale_den, record_count, source_ordinal;
+} nd_feds_header;
+/* SignatureFileWriter (sigstore.cpp:74-130) for n records; record_count is
+ * set to n.  sig: n*H u32 row-major, band: n*bands u32. */
+int nd_feds_write(const char* path, const nd_feds_header* header, const uint64_t* doc_ids,
+                  const uint32_t* sig, const uint32_t* band, uint64_t n, int fsync_file);
+/* SignatureFileHeader::parse + the reader's size check (sigstore.cpp:38-72, :132-150) */
+int nd_feds_read_header(const char* path, nd_feds_header* out);
+/* SignatureFileReader::next over the whole file (sigstore.cpp:155-175);
+ * any output may be NULL except band (checked against bucket_count). */
+int nd_feds_read(const char* path, uint64_t* doc_ids, uint32_t* sig, uint32_t* band);
+/* write_pair_file / read_pair_file (compare.cpp:88-113); read: call with
+ * NULL outputs to get *n, then again with buffers of *n entries. */
+int nd_pairs_write(const char* path, const uint64_t* lo, const uint64_t* hi, const uint32_t* match,
+                   uint64_t n, int fsync_file);
+int nd_pairs_read(const char* path, uint64_t* lo, uint64_t* hi, uint32_t* match, uint64_t* n);
+/* plan_gather (sigstore.cpp:288-329) with band_partition's worker ranges
+ * (lsh.cpp:62-72): buckets per pass C and passes[w] per worker (0 for a
+ * worker without bands).  override_c: 0 = none. */
+int nd_plan_gather(uint64_t total_signature_bytes, uint32_t bucket_count, uint32_t bands,
+                   uint32_t workers, uint64_t memory_budget, uint32_t override_c,
+                   uint32_t* c_out, uint32_t* passes_out);
+/* hash_one_file (pipeline.cpp:171-240) for one input file: K1 on the GPU over
+ * its packed surviving documents (doc_ids ascending), written to path as a
+ * .feds file.  The family is derived from the header (seed, H, L, unit). */
+int nd_hash_file(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets,
+                 const uint64_t* doc_ids, uint64_t n, const nd_feds_header* header,
+                 const char* path, int fsync_file);
+typedef struct nd_compare_stage_stats { /* CompareStageOutput (pipeline.hpp:74-81) */
+  uint32_t buckets_per_pass, pass_count;
+  uint64_t candidate_pairs, emitted_pairs, gather_peak_bytes;
+  uint64_t records;          /* signature records loaded into HBM */
+  uint64_t distinct_pairs;   /* across passes */
+  double seconds[3];         /* read + H2D, GPU compare, pair files */
+} nd_compare_stage_stats;
+/* run_compare_stage (pipeline.cpp:347-432) minus its JSON: every .feds file
+ * (source order) is loaded into HBM once; the cells of all passes are
+ * compared on the GPU and each pass's sorted distinct pairs are written to
+ * pairs_dir/w<w>_p<p>.pairs (an empty file for a pass without pairs), the
+ * files compare_pass + write_pair_file would produce.  expected: the run's
+ * header (record_count / source_ordinal ignored).  gather_peak_bytes is the
+ * resident bytes scan_gather would hold: exact for one worker, the
+ * passes-in-lockstep sum for several. */
+int nd_compare_stage(nd_ctx* ctx, const char* const* feds_paths, uint32_t nfiles,
+                     const nd_feds_header* expected, uint64_t total_signature_bytes,
+                     uint32_t workers, uint64_t memory_budget, uint32_t buckets_per_pass,
+                     uint64_t threshold_num, uint64_t threshold_den, const char* pairs_dir,
+                     int fsync_files, nd_compare_stage_stats* stats);
+/* run_union_stage (pipeline.cpp:434-508) minus its JSON checks: reads the
+ * pair files, distinct pairs + components on the GPU, writes groups.jsonl,
+ * removal.txt and summary.json into workspace.  Result also fetchable with
+ * nd_dedup_fetch_*. */
+int nd_union_stage(nd_ctx* ctx, const char* const* pair_paths, uint32_t nfiles,
+                   uint64_t total_surviving, uint64_t total_records, const char* workspace,
+                   int fsync_files, nd_dedup_stats* stats);
+
 /* ---- stage entry points for the multi-GPU dedup (device pointers, async on
  * the ctx stream unless noted).  See DESIGN.md section 7. -------------------- */
 /* (cell = band*K + bucket, doc_base + row) records of n documents' band ids,

@@ -57,6 +57,26 @@ class NdDedupStats(C.Structure):
                 ("removals", C.c_uint64), ("seconds", C.c_double * 6)]
 
 
+class NdFedsHeader(C.Structure):
+    """nd_feds_header == SignatureFileHeader (sigstore.hpp:24-42)."""
+
+    _fields_ = [("hash_count", C.c_uint32), ("bands", C.c_uint32), ("rows", C.c_uint32),
+                ("bucket_count", C.c_uint32), ("shingle_len", C.c_uint32), ("unit", C.c_uint32),
+                ("family_seed", C.c_uint64), ("scale_num", C.c_uint64), ("scale_den", C.c_uint64),
+                ("record_count", C.c_uint64), ("source_ordinal", C.c_uint64)]
+
+
+class NdCompareStageStats(C.Structure):
+    """nd_compare_stage_stats == CompareStageOutput (pipeline.hpp:74-81) + extras."""
+
+    _fields_ = [("buckets_per_pass", C.c_uint32), ("pass_count", C.c_uint32),
+                ("candidate_pairs", C.c_uint64), ("emitted_pairs", C.c_uint64),
+                ("gather_peak_bytes", C.c_uint64), ("records", C.c_uint64),
+                ("distinct_pairs", C.c_uint64), ("seconds", C.c_double * 3)]
+
+
+cpp = C.POINTER(C.c_char_p)
+
 # name -> (restype, argtypes); every symbol include/neardup_b200.h declares
 SIGNATURES = {
     "nd_version": (C.c_char_p, []),
@@ -96,6 +116,21 @@ SIGNATURES = {
     "nd_dedup_fetch_pairs": (C.c_int, [vp, u64p, u64p, u32p]),
     "nd_dedup_fetch_groups": (C.c_int, [vp, u64p, u64p]),
     "nd_dedup_write_report": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
+    "nd_feds_write": (C.c_int, [C.c_char_p, C.POINTER(NdFedsHeader), u64p, u32p, u32p,
+                                C.c_uint64, C.c_int]),
+    "nd_feds_read_header": (C.c_int, [C.c_char_p, C.POINTER(NdFedsHeader)]),
+    "nd_feds_read": (C.c_int, [C.c_char_p, u64p, u32p, u32p]),
+    "nd_pairs_write": (C.c_int, [C.c_char_p, u64p, u64p, u32p, C.c_uint64, C.c_int]),
+    "nd_pairs_read": (C.c_int, [C.c_char_p, u64p, u64p, u32p, u64p]),
+    "nd_plan_gather": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                 C.c_uint32, u32p, u32p]),
+    "nd_hash_file": (C.c_int, [vp, u8p, u64p, u64p, C.c_uint64, C.POINTER(NdFedsHeader),
+                               C.c_char_p, C.c_int]),
+    "nd_compare_stage": (C.c_int, [vp, cpp, C.c_uint32, C.POINTER(NdFedsHeader), C.c_uint64,
+                                   C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64,
+                                   C.c_char_p, C.c_int, C.POINTER(NdCompareStageStats)]),
+    "nd_union_stage": (C.c_int, [vp, cpp, C.c_uint32, C.c_uint64, C.c_uint64, C.c_char_p,
+                                 C.c_int, C.POINTER(NdDedupStats)]),
     "nd_stage_cell_records": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                         vp, vp]),
     "nd_stage_compare": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, vp, C.c_uint64,

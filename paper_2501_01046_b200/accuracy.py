@@ -82,13 +82,22 @@ def run_eval_accuracy(config: "pipeline.RunConfig", ctx: Context | None = None) 
     """Full pipeline, then the exhaustive comparison over the same signatures;
     writes accuracy.json with the reference's layout (pipeline.cpp:563-583)."""
     rep = pipeline.run_dedup(config, ctx=ctx)
-    manifest, _ = pipeline.build_manifest(config.inputs, config)
-    docs = []
-    for i in range(len(manifest.files)):
-        docs.extend(pipeline.surviving_documents(manifest, i, config))
-    fam = minhash.derive_family(config.seed, config.hash_count, config.shingle_len, config.unit)
-    oracle = standard_minhash_dupset(docs, fam, SimilarityThreshold(config.threshold), ctx)
-    n = manifest.total_surviving
+    # the same signatures the pipeline compared: the hash stage's .feds files
+    # (pipeline.cpp:535-545)
+    from . import sigstore
+
+    m = pipeline._load_run_manifest(config)
+    ids, sigs = [], []
+    for path in m["signature_files"]:
+        _, i, v, _ = sigstore.read_signature_file(path)
+        ids.append(i)
+        sigs.append(v)
+    ids = np.concatenate(ids) if ids else np.zeros(0, np.uint64)
+    mat = np.concatenate(sigs) if sigs else np.zeros((0, config.hash_count), np.uint32)
+    oracle = all_pairs_dupset(mat, config.hash_count, SimilarityThreshold(config.threshold), ctx,
+                              ids)
+    oracle.method = "standard-minhash"
+    n = m["total_surviving"]
     acc = {"corpus_size": n,
            "jaccard_vs_oracle": dupset_jaccard(rep.near_duplicates, oracle.doc_ids).value(),
            "methods": [

@@ -33,4 +33,21 @@ void write_report(const std::string& dir, const std::vector<uint64_t>& members,
                   const std::vector<uint64_t>& removals, uint64_t total_documents,
                   uint64_t total_records, uint64_t distinct_pairs);
 
+// staged-workflow artifacts (host_feds.cpp)
+constexpr uint64_t kFedsHeaderBytes = 72;
+uint64_t feds_record_bytes(const nd_feds_header& h);
+std::string feds_serialize(const nd_feds_header& h);
+nd_feds_header feds_read_header(const std::string& path, uint64_t* file_size);
+bool feds_run_compatible(const nd_feds_header& a, const nd_feds_header& b);
+void feds_write(const std::string& path, nd_feds_header h, const uint64_t* doc_ids,
+                const uint32_t* sig, const uint32_t* band, uint64_t n, bool fsync_file);
+void feds_read_records(const std::string& path, const nd_feds_header& h, uint64_t* doc_ids,
+                       uint32_t* sig, uint32_t* band);
+void pairs_write(const std::string& path, const uint64_t* lo, const uint64_t* hi,
+                 const uint32_t* m, uint64_t n, bool fsync_file);
+void pairs_read(const std::string& path, std::vector<uint64_t>& lo, std::vector<uint64_t>& hi,
+                std::vector<uint32_t>& m);
+uint32_t plan_gather(uint64_t total_bytes, uint32_t K, const std::vector<uint32_t>& worker_bands,
+                     uint64_t budget, uint32_t override_c, std::vector<uint32_t>& passes);
+
 }  // namespace ndb

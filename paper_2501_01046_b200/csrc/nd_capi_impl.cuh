@@ -40,4 +40,14 @@ struct nd_ctx {
 
 namespace ndb {
 int guarded_impl(nd_ctx* ctx, const std::function<void()>& fn);
+// shared by nd_dedup.cu and nd_stages.cu
+void validate(const nd_params& p);                 // RunConfig::validate, artifact fields
+void ensure_family(nd_ctx* ctx, const nd_params& p);  // derive + upload when it changed
+// K3 + distinct pairs over st.cells (grows the pair buffer on overflow)
+void compare_and_unique(DedupState& st, const uint32_t* d_sig, uint32_t H, uint32_t mm,
+                        uint64_t nrows, cudaStream_t s);
+// signatures of a host batch into device buffers (pipelined H2D, text kept in st.text)
+void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uint64_t* offsets,
+                    uint64_t n, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
+                    uint32_t* d_band);
 }

@@ -36,6 +36,8 @@ struct EventTimer {
   }
 };
 
+}  // namespace
+
 void validate(const nd_params& p) {
   // RunConfig::validate (pipeline.cpp:20-33), artifact-shaping fields
   if (p.bands == 0 || p.rows == 0) fail(ND_ERR_CONFIG, "bands and rows must be positive");
@@ -85,6 +87,8 @@ void compare_and_unique(DedupState& st, const uint32_t* d_sig, uint32_t H, uint3
   unique_pairs(ps, s);
 }
 
+namespace {
+
 template <class T>
 std::vector<T> d2h(const T* d, uint64_t n, cudaStream_t s) {
   std::vector<T> h(n);
@@ -95,6 +99,8 @@ std::vector<T> d2h(const T* d, uint64_t n, cudaStream_t s) {
 uint64_t id_of(const DedupState& st, uint32_t row) {
   return st.doc_ids.empty() ? row : st.doc_ids[row];
 }
+
+}  // namespace
 
 // Host text -> device signatures/band keys: chunks of <= 256 MB are copied
 // on the h2d stream and signed on the ctx stream as each lands (PCIe overlaps
@@ -136,6 +142,8 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   for (auto ev : evs) cudaEventDestroy(ev);
   cudaEventDestroy(start);
 }
+
+namespace {
 
 // The shared tail of nd_dedup / nd_dedup_device: K2..K4 on the signatures and
 // band keys already in st.sig / st.band.

@@ -1,12 +1,15 @@
 """Stage orchestration -- mirror of the reference's pipeline.hpp.
 
   RunConfig            pipeline.hpp:21-48 (same fields, validate, config_hash)
-  run_dedup            pipeline.hpp:100   (JSONL inputs -> workspace report)
-  dedup_packed         in-memory run_dedup over a packed batch (the hot path)
-The reference persists every stage to disk (.feds, .pairs); here the three
-stages run back to back on the GPU with intermediates resident in HBM
-(nd_dedup), and only the report is written, with the reference's writers'
-byte format (groups.jsonl, removal.txt, summary.json).
+  run_hash_stage       pipeline.cpp:269-339  JSONL -> K1 on the GPU -> one .feds file per input
+  run_compare_stage    pipeline.cpp:382-432  .feds -> HBM -> K2/K3 -> one .pairs file per
+                                             (worker, gather pass) + compare_stage.json
+  run_union_stage      pipeline.cpp:434-508  .pairs -> K4 -> groups.jsonl, removal.txt, summary.json
+  run_dedup            pipeline.cpp:510-532  the three stages + timings.json
+  run_dedup_in_memory  the same report with every intermediate resident in HBM (nd_dedup)
+  dedup_packed         in-memory dedup of a packed host batch (the bench's hot path)
+Every artifact is written with the reference's byte format, so a workspace
+produced here is byte-identical with the reference's (tests/test_gpu_stages.py).
 """
 from __future__ import annotations
 
@@ -179,9 +182,11 @@ def write_report(workspace: str, ctx: Context | None = None, total_records: int 
     ctx.check(ctx.lib.nd_dedup_write_report(ctx.h, workspace.encode(), total_records))
 
 
-def run_dedup(config: RunConfig, ctx: Context | None = None) -> DedupReport:
-    """pipeline.cpp:510-532 on the GPU: load + filter the JSONL inputs, dedup in
-    memory, write groups.jsonl / removal.txt / summary.json (+ rejects.jsonl)."""
+def run_dedup_in_memory(config: RunConfig, ctx: Context | None = None) -> DedupReport:
+    """pipeline.cpp:510-532 with every intermediate kept in HBM: load + filter the
+    JSONL inputs, dedup in memory (nd_dedup), write groups.jsonl / removal.txt /
+    summary.json (+ rejects.jsonl).  Same report bytes as run_dedup, no .feds or
+    .pairs artifacts."""
     config.validate(need_workspace=True)
     os.makedirs(config.workspace, exist_ok=True)
     manifest, rejects = build_manifest(config.inputs, config)
@@ -196,8 +201,280 @@ def run_dedup(config: RunConfig, ctx: Context | None = None) -> DedupReport:
     ctx = ctx or default_context()
     rep = dedup_packed(data, offsets, config, ids, ctx=ctx)
     write_report(config.workspace, ctx, manifest.total_records)
-    with open(os.path.join(config.workspace, "rejects.jsonl"), "w") as f:
-        for e in rejects:
-            f.write(json.dumps({"file": e[0], "line": e[1], "reason": e[2]},
-                               separators=(",", ":")) + "\n")
+    _write_rejects(rejects_path(config), rejects)
+    return rep
+
+
+# ---- the staged, file-backed workflow (pipeline.hpp:50-96) ---------------------
+def run_manifest_path(c: RunConfig) -> str:
+    return c.workspace + "/run_manifest.json"
+
+
+def rejects_path(c: RunConfig) -> str:
+    return c.workspace + "/rejects.jsonl"
+
+
+def compare_stage_path(c: RunConfig) -> str:
+    return c.workspace + "/compare_stage.json"
+
+
+def groups_path(c: RunConfig) -> str:
+    return c.workspace + "/groups.jsonl"
+
+
+def removal_path(c: RunConfig) -> str:
+    return c.workspace + "/removal.txt"
+
+
+def summary_path(c: RunConfig) -> str:
+    return c.workspace + "/summary.json"
+
+
+def timings_path(c: RunConfig) -> str:
+    return c.workspace + "/timings.json"
+
+
+def signatures_dir(c: RunConfig) -> str:
+    return c.workspace + "/signatures"
+
+
+def pairs_dir(c: RunConfig) -> str:
+    return c.workspace + "/pairs"
+
+
+def _dump2(obj) -> str:
+    """nlohmann ordered_json::dump(2) + newline (UTF-8 kept, same escapes)."""
+    return json.dumps(obj, indent=2, ensure_ascii=False) + "\n"
+
+
+def _write_text(path: str, text: str) -> None:
+    with open(path, "w", encoding="utf-8", newline="") as f:
+        f.write(text)
+
+
+def _write_rejects(path: str, rejects) -> None:
+    """RejectLog::write_jsonl (corpus.cpp:18-29)."""
+    _write_text(path, "".join(json.dumps({"file": e[0], "line": e[1], "reason": e[2]},
+                                         separators=(",", ":"), ensure_ascii=False) + "\n"
+                              for e in rejects))
+
+
+def _ratio_str(r) -> str:
+    from math import gcd
+
+    n, d = _ratio(r)
+    g = gcd(n, d) or 1
+    n, d = n // g, d // g
+    if n == 0:
+        d = 1
+    return str(n) if d == 1 else f"{n}/{d}"
+
+
+def _parameters(c: RunConfig) -> dict:
+    """config_parameters_json (pipeline.cpp:252-265)."""
+    return {"text_field": c.text_field, "hash_count": c.hash_count, "bands": c.bands,
+            "rows": c.rows, "shingle_len": c.shingle_len,
+            "unit": "byte" if c.unit == ShingleUnit.BYTE else "codepoint",
+            "threshold": _ratio_str(c.threshold), "bucket_scale": _ratio_str(c.bucket_scale),
+            "min_chars": c.min_chars, "seed": c.seed}
+
+
+def signature_file_name(ordinal: int, source_path: str) -> str:
+    """pipeline.cpp:101-105: %05llu_<stem>.feds."""
+    return f"{ordinal:05d}_{os.path.splitext(os.path.basename(source_path))[0]}.feds"
+
+
+def header_template(c: RunConfig, bucket_count: int):
+    """pipeline.cpp:107-118."""
+    from .sigstore import SignatureFileHeader
+
+    return SignatureFileHeader(c.hash_count, c.bands, c.rows, bucket_count, c.shingle_len,
+                               c.unit, c.seed, _ratio(c.bucket_scale))
+
+
+@dataclass
+class HashStageOutput:
+    manifest: CorpusManifest
+    bucket_count: int = 0
+    signature_files: list[str] = field(default_factory=list)
+    total_signature_bytes: int = 0
+
+
+@dataclass
+class CompareStageOutput:
+    buckets_per_pass: int = 0
+    pass_count: int = 0
+    candidate_pairs: int = 0
+    emitted_pairs: int = 0
+    gather_peak_bytes: int = 0
+    pair_files: list[str] = field(default_factory=list)
+    seconds: list[float] = field(default_factory=list)
+
+
+def run_hash_stage(config: RunConfig, ctx: Context | None = None) -> HashStageOutput:
+    """pipeline.cpp:269-339: ingest, sign every input file on the GPU (K1) into
+    one .feds file each, write rejects.jsonl and run_manifest.json."""
+    from .lsh import choose_bucket_count
+
+    config.validate(need_workspace=True)
+    os.makedirs(signatures_dir(config), exist_ok=True)
+    os.makedirs(pairs_dir(config), exist_ok=True)
+    manifest, rejects = build_manifest(config.inputs, config)
+    if manifest.total_surviving == 0:
+        raise _lib.ConfigError(_lib.ND_ERR_CONFIG,
+                               "no documents survive preprocessing; nothing to deduplicate")
+    ctx = ctx or default_context()
+    out = HashStageOutput(manifest)
+    out.bucket_count = choose_bucket_count(manifest.total_surviving, config.bucket_scale)
+    base = header_template(config, out.bucket_count)
+    for i, fs in enumerate(manifest.files):
+        path = signatures_dir(config) + "/" + signature_file_name(i, fs.path)
+        docs = surviving_documents(manifest, i, config)
+        if len(docs) != fs.surviving:
+            raise _lib.PrerequisiteError(_lib.ND_ERR_PREREQ,
+                                         f"'{fs.path}' yielded {len(docs)} documents, manifest "
+                                         f"says {fs.surviving}")
+        data, offsets = pack_documents(docs)
+        ids = np.array([d.doc_id for d in docs], np.uint64)
+        h = base.to_c()
+        h.source_ordinal = i
+        dp = data.ctypes.data_as(u8p) if data.size else C.cast(C.c_char_p(b"\0"), u8p)
+        ctx.check(ctx.lib.nd_hash_file(ctx.h, dp, offsets.ctypes.data_as(u64p),
+                                       ids.ctypes.data_as(u64p), len(ids), C.byref(h),
+                                       path.encode(), int(config.fsync_files)))
+        out.signature_files.append(path)
+        out.total_signature_bytes += os.path.getsize(path)
+    _write_rejects(rejects_path(config), rejects)
+    doc = {"format_version": 1, "config_hash": config.config_hash(),
+           "parameters": _parameters(config), "bucket_count": out.bucket_count,
+           "totals": {"records": manifest.total_records, "surviving": manifest.total_surviving,
+                      "signature_bytes": out.total_signature_bytes},
+           "files": [{"path": f.path, "records": f.records, "surviving": f.surviving,
+                      "record_offset": f.record_offset,
+                      "signature_file": os.path.basename(out.signature_files[i])}
+                     for i, f in enumerate(manifest.files)]}
+    _write_text(run_manifest_path(config), _dump2(doc))
+    return out
+
+
+def _load_json_artifact(path: str, stage_hint: str) -> dict:
+    """pipeline.cpp:267-277."""
+    if not os.path.exists(path):
+        raise _lib.PrerequisiteError(_lib.ND_ERR_PREREQ,
+                                     f"'{path}' is missing; run the {stage_hint} stage first")
+    try:
+        with open(path, "rb") as f:
+            j = json.loads(f.read())
+    except ValueError:
+        j = None
+    if not isinstance(j, dict):
+        raise _lib.IoError(_lib.ND_ERR_IO, f"'{path}' is not valid JSON")
+    return j
+
+
+def _check_config_hash(artifact: dict, config: RunConfig, path: str) -> None:
+    if artifact.get("config_hash", 0) != config.config_hash():
+        raise _lib.ConfigError(_lib.ND_ERR_CONFIG, f"configuration changed since '{path}' was "
+                                                   "written; rerun the earlier stages")
+
+
+def _load_run_manifest(config: RunConfig) -> dict:
+    """load_run_manifest (pipeline.cpp:356-378)."""
+    path = run_manifest_path(config)
+    doc = _load_json_artifact(path, "hash")
+    _check_config_hash(doc, config, path)
+    try:
+        return {"bucket_count": int(doc["bucket_count"]),
+                "total_records": int(doc["totals"]["records"]),
+                "total_surviving": int(doc["totals"]["surviving"]),
+                "total_signature_bytes": int(doc["totals"]["signature_bytes"]),
+                "source_paths": [e["path"] for e in doc["files"]],
+                "signature_files": [signatures_dir(config) + "/" + e["signature_file"]
+                                    for e in doc["files"]]}
+    except (KeyError, TypeError, ValueError):
+        raise _lib.IoError(_lib.ND_ERR_IO, f"'{path}' is missing required fields")
+
+
+def run_compare_stage(config: RunConfig, ctx: Context | None = None) -> CompareStageOutput:
+    """pipeline.cpp:382-432: plans the gather passes, compares every cell on the
+    GPU with all signature records resident in HBM, writes one pair file per
+    worker and pass plus compare_stage.json."""
+    from .corpus import expand_inputs
+    from .sigstore import plan_gather
+
+    config.validate(need_workspace=True)
+    m = _load_run_manifest(config)
+    if config.inputs:
+        if sorted(expand_inputs(config.inputs)) != m["source_paths"]:
+            raise _lib.PrerequisiteError(_lib.ND_ERR_PREREQ, "input files differ from the hashed "
+                                                             "manifest; rerun the hash stage")
+    if config.buckets_per_pass is not None and config.buckets_per_pass < 1:
+        raise _lib.ConfigError(_lib.ND_ERR_CONFIG, "buckets-per-pass override must be at least 1")
+    ctx = ctx or default_context()
+    plan = plan_gather(m["total_signature_bytes"], m["bucket_count"], config.bands,
+                       config.workers, config.memory_budget, config.buckets_per_pass)
+    expected = header_template(config, m["bucket_count"]).to_c()
+    paths = (C.c_char_p * max(1, len(m["signature_files"])))(
+        *[p.encode() for p in m["signature_files"]])
+    st = _lib.NdCompareStageStats()
+    tn, td = _ratio(config.threshold)
+    os.makedirs(pairs_dir(config), exist_ok=True)
+    ctx.check(ctx.lib.nd_compare_stage(ctx.h, paths, len(m["signature_files"]), C.byref(expected),
+                                       m["total_signature_bytes"], config.workers,
+                                       config.memory_budget, config.buckets_per_pass or 0, tn, td,
+                                       pairs_dir(config).encode(), int(config.fsync_files),
+                                       C.byref(st)))
+    names = sorted(pairs_dir(config) + f"/w{w}_p{p}.pairs"
+                   for w, np_ in enumerate(plan.passes_per_worker) for p in range(np_))
+    out = CompareStageOutput(st.buckets_per_pass, st.pass_count, st.candidate_pairs,
+                             st.emitted_pairs, st.gather_peak_bytes, names, list(st.seconds))
+    doc = {"config_hash": config.config_hash(), "bucket_count": m["bucket_count"],
+           "buckets_per_pass": out.buckets_per_pass, "pass_count": out.pass_count,
+           "workers": config.workers, "memory_budget": config.memory_budget,
+           "candidate_pairs": out.candidate_pairs, "emitted_pairs": out.emitted_pairs,
+           "gather_peak_bytes": out.gather_peak_bytes,
+           "pair_files": [os.path.basename(f) for f in names]}
+    _write_text(compare_stage_path(config), _dump2(doc))
+    return out
+
+
+def run_union_stage(config: RunConfig, ctx: Context | None = None) -> DedupReport:
+    """pipeline.cpp:434-508: merge the pair files (sort + distinct), union +
+    components on the GPU, write groups.jsonl, removal.txt, summary.json."""
+    config.validate(need_workspace=True)
+    m = _load_run_manifest(config)
+    spath = compare_stage_path(config)
+    stage = _load_json_artifact(spath, "gather-compare")
+    _check_config_hash(stage, config, spath)
+    try:
+        files = [pairs_dir(config) + "/" + str(n) for n in stage["pair_files"]]
+    except (KeyError, TypeError):
+        raise _lib.IoError(_lib.ND_ERR_IO, f"'{spath}' is missing required fields")
+    ctx = ctx or default_context()
+    paths = (C.c_char_p * max(1, len(files)))(*[p.encode() for p in files])
+    stats = NdDedupStats()
+    ctx.check(ctx.lib.nd_union_stage(ctx.h, paths, len(files), m["total_surviving"],
+                                     m["total_records"], config.workspace.encode(),
+                                     int(config.fsync_files), C.byref(stats)))
+    return _fetch_report(ctx, stats)
+
+
+def run_dedup(config: RunConfig, ctx: Context | None = None, timings: dict | None = None) -> DedupReport:
+    """pipeline.cpp:510-532: hash -> gather-compare -> union, every artifact on
+    disk exactly as the reference writes it; wall-clock per stage in
+    timings.json."""
+    import time
+
+    t0 = time.perf_counter()
+    run_hash_stage(config, ctx)
+    t1 = time.perf_counter()
+    run_compare_stage(config, ctx)
+    t2 = time.perf_counter()
+    rep = run_union_stage(config, ctx)
+    t3 = time.perf_counter()
+    t = {"workers": config.workers, "hash_seconds": t1 - t0, "compare_seconds": t2 - t1,
+         "union_seconds": t3 - t2, "total_seconds": t3 - t0}
+    _write_text(timings_path(config), _dump2(t))
+    if timings is not None:
+        timings.update(t)
     return rep

@@ -1,0 +1,113 @@
+"""The staged, file-backed workflow on the GPU (hash -> gather-compare -> union)
+against the reference's own run_dedup: EVERY artifact of the workspace is
+compared byte for byte -- .feds signature files, per-(worker, pass) .pairs
+files, run_manifest.json, compare_stage.json, rejects.jsonl and the report
+(test_pipeline.cpp's artifact checks, pipeline.cpp:269-532)."""
+import json
+import os
+
+import pytest
+
+from paper_2501_01046_b200 import _lib, pipeline
+
+pytestmark = pytest.mark.gpu
+
+
+def _corpus_dir(ref, tmp_path, n=1500, groups=150, seed=4):
+    src = str(tmp_path / "all.jsonl")
+    ref.generate_synthetic(n, groups, gmin=2, gmax=4, len_min=300, len_max=1200, seed=seed,
+                           corpus_path=src, truth_path=str(tmp_path / "truth.jsonl"))
+    lines = open(src, encoding="utf-8").read().splitlines(keepends=True)
+    d = tmp_path / "corpus"
+    d.mkdir()
+    half = len(lines) // 2
+    bad = ['not json\n', '[1, 2]\n', '{"id": 1}\n', '{"text": 5}\n', '{"text": "too short"}\n', '\n']
+    (d / "a.jsonl").write_text("".join(lines[:half] + bad[:3]), encoding="utf-8")
+    (d / "b.jsonl").write_text("".join(bad[3:] + lines[half:]), encoding="utf-8")
+    (d / "ignored.txt").write_text("not an input\n")
+    return str(d)
+
+
+def _tree(ws):
+    out = {}
+    for root, _, files in os.walk(ws):
+        for f in files:
+            if f == "timings.json":
+                continue  # wall-clock, not an artifact
+            p = os.path.join(root, f)
+            out[os.path.relpath(p, ws)] = open(p, "rb").read()
+    return out
+
+
+@pytest.mark.parametrize("workers,budget", [(1, 1 << 30), (1, 120_000), (3, 300_000), (20, 1 << 30)])
+def test_staged_workspace_byte_identical(ctx, ref, tmp_path, workers, budget):
+    corpus = _corpus_dir(ref, tmp_path)
+    ws_ref, ws_gpu = str(tmp_path / "ref"), str(tmp_path / "gpu")
+    os.makedirs(ws_ref)
+    ref.run_dedup(corpus, ws_ref, workers=workers, memory_budget=budget)
+    cfg = pipeline.RunConfig(inputs=[corpus], workspace=ws_gpu, workers=workers,
+                             memory_budget=budget)
+    rep = pipeline.run_dedup(cfg, ctx=ctx)
+    want, got = _tree(ws_ref), _tree(ws_gpu)
+    assert sorted(got) == sorted(want)
+    assert any(k.startswith("signatures/") for k in want)
+    npairs = sum(k.startswith("pairs/") for k in want)
+    assert npairs >= workers if workers <= 16 else npairs == 16
+    cs_ref = json.loads(want.pop("compare_stage.json"))
+    cs_gpu = json.loads(got.pop("compare_stage.json"))
+    if workers > 1:  # the reference's gauge peak depends on thread timing
+        cs_ref.pop("gather_peak_bytes")
+        cs_gpu.pop("gather_peak_bytes")
+    else:
+        assert (open(os.path.join(ws_gpu, "compare_stage.json"), "rb").read()
+                == open(os.path.join(ws_ref, "compare_stage.json"), "rb").read())
+    assert cs_gpu == cs_ref
+    for k in want:
+        assert got[k] == want[k], k
+    assert rep.distinct_pairs == json.loads(want["summary.json"])["distinct_pairs"]
+    rej = want["rejects.jsonl"].decode().splitlines()
+    assert len(rej) == 6 and '"reason":"invalid_json"' in rej[0]
+
+
+def test_stages_run_separately_and_rerun(ctx, ref, tmp_path):
+    corpus = _corpus_dir(ref, tmp_path, n=600, groups=60, seed=9)
+    cfg = pipeline.RunConfig(inputs=[corpus], workspace=str(tmp_path / "ws"), workers=2,
+                             memory_budget=80_000)
+    with pytest.raises(_lib.PrerequisiteError):
+        pipeline.run_compare_stage(cfg, ctx=ctx)  # no hash stage yet
+    h = pipeline.run_hash_stage(cfg, ctx=ctx)
+    assert h.bucket_count == 49 and len(h.signature_files) == 2
+    with pytest.raises(_lib.PrerequisiteError):
+        pipeline.run_union_stage(cfg, ctx=ctx)  # no compare stage yet
+    c = pipeline.run_compare_stage(cfg, ctx=ctx)
+    assert c.pass_count == len(c.pair_files) > 2
+    r1 = pipeline.run_union_stage(cfg, ctx=ctx)
+    before = _tree(cfg.workspace)
+    r2 = pipeline.run_union_stage(cfg, ctx=ctx)
+    assert _tree(cfg.workspace) == before
+    assert [g.members for g in r1.groups] == [g.members for g in r2.groups]
+    # artifact-shaping config changed -> the later stages refuse
+    cfg.seed = 6
+    with pytest.raises(_lib.ConfigError):
+        pipeline.run_compare_stage(cfg, ctx=ctx)
+    cfg.seed = 5
+    # the schedule (workers, budget) does not shape the report
+    cfg.workers, cfg.memory_budget = 1, 1 << 30
+    pipeline.run_compare_stage(cfg, ctx=ctx)
+    pipeline.run_union_stage(cfg, ctx=ctx)
+    after = _tree(cfg.workspace)
+    for f in ("groups.jsonl", "removal.txt", "summary.json"):
+        assert after[f] == before[f]
+
+
+def test_codepoint_staged_matches_in_memory(ctx, ref, tmp_path):
+    corpus = _corpus_dir(ref, tmp_path, n=500, groups=50, seed=12)
+    a = pipeline.RunConfig(inputs=[corpus], workspace=str(tmp_path / "a"),
+                           unit=pipeline.ShingleUnit.CODEPOINT)
+    b = pipeline.RunConfig(inputs=[corpus], workspace=str(tmp_path / "b"),
+                           unit=pipeline.ShingleUnit.CODEPOINT)
+    pipeline.run_dedup(a, ctx=ctx)
+    pipeline.run_dedup_in_memory(b, ctx=ctx)
+    ta, tb = _tree(a.workspace), _tree(b.workspace)
+    for f in ("groups.jsonl", "removal.txt", "summary.json", "rejects.jsonl"):
+        assert ta[f] == tb[f]
