@@ -468,10 +468,13 @@ def run_dedup(config: RunConfig, ctx: Context | None = None, timings: dict | Non
     t0 = time.perf_counter()
     run_hash_stage(config, ctx)
     t1 = time.perf_counter()
-    run_compare_stage(config, ctx)
+    cmp = run_compare_stage(config, ctx)
     t2 = time.perf_counter()
     rep = run_union_stage(config, ctx)
     t3 = time.perf_counter()
+    rep.candidate_pairs = cmp.candidate_pairs
+    rep.stats["candidate_pairs"] = cmp.candidate_pairs
+    rep.stats["emitted_pairs"] = cmp.emitted_pairs
     t = {"workers": config.workers, "hash_seconds": t1 - t0, "compare_seconds": t2 - t1,
          "union_seconds": t3 - t2, "total_seconds": t3 - t0}
     _write_text(timings_path(config), _dump2(t))

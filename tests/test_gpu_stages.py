@@ -66,7 +66,7 @@ def test_staged_workspace_byte_identical(ctx, ref, tmp_path, workers, budget):
         assert got[k] == want[k], k
     assert rep.distinct_pairs == json.loads(want["summary.json"])["distinct_pairs"]
     rej = want["rejects.jsonl"].decode().splitlines()
-    assert len(rej) == 6 and '"reason":"invalid_json"' in rej[0]
+    assert len(rej) == 5 and '"reason":"invalid_json"' in rej[0]
 
 
 def test_stages_run_separately_and_rerun(ctx, ref, tmp_path):
