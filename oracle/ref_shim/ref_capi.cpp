@@ -14,6 +14,7 @@
 //   union_pairs/components/emit_report  dedup_graph.hpp:34-55
 //   generate_synthetic/write_synthetic  synthetic.hpp:57-63
 //   run_dedup                pipeline.hpp:100 (pipeline.cpp:510-532)
+//   run_eval_accuracy        pipeline.hpp:114 (pipeline.cpp:534-585)
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
@@ -268,6 +269,20 @@ int ref_run_dedup(const char* input, const char* workspace, uint32_t H, uint32_t
       timings[2] = std::chrono::duration<double>(t3 - t2).count();
     }
     if (candidate_pairs) *candidate_pairs = cmp.candidate_pairs;
+  });
+}
+
+// run_eval_accuracy over one input (file or directory) with the default
+// artifact-shaping parameters except workers / oracle override.
+int ref_eval_accuracy(const char* input, const char* workspace, unsigned workers,
+                      int oracle_override) {
+  return guarded([&] {
+    RunConfig c;
+    c.inputs = {input};
+    c.workspace = workspace;
+    c.workers = workers;
+    c.oracle_override = oracle_override != 0;
+    run_eval_accuracy(c);
   });
 }
 

@@ -173,7 +173,12 @@ class Ref:
                                     C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                     C.c_uint64, C.c_uint64, C.c_uint, C.c_uint64,
                                     C.POINTER(C.c_double), u64p, C.c_uint32]
+        L.ref_eval_accuracy.argtypes = [C.c_char_p, C.c_char_p, C.c_uint, C.c_int]
         self.lib = L
+
+    def eval_accuracy(self, input_path, workspace, workers=1, override=False):
+        self._check(self.lib.ref_eval_accuracy(input_path.encode(), workspace.encode(), workers,
+                                               int(override)))
 
     def _check(self, rc):
         if rc != 0:

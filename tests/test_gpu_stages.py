@@ -111,3 +111,18 @@ def test_codepoint_staged_matches_in_memory(ctx, ref, tmp_path):
     ta, tb = _tree(a.workspace), _tree(b.workspace)
     for f in ("groups.jsonl", "removal.txt", "summary.json", "rejects.jsonl"):
         assert ta[f] == tb[f]
+
+
+def test_eval_accuracy_byte_identical(ctx, ref, tmp_path):
+    # run_eval_accuracy (pipeline.cpp:534-585): pipeline LSH dupset vs the
+    # exhaustive all-pairs dupset over the same .feds signatures
+    from paper_2501_01046_b200 import accuracy
+
+    corpus = _corpus_dir(ref, tmp_path, n=1200, groups=200, seed=21)
+    ws_ref, ws_gpu = str(tmp_path / "r"), str(tmp_path / "g")
+    os.makedirs(ws_ref)
+    ref.eval_accuracy(corpus, ws_ref, workers=4)
+    acc = accuracy.run_eval_accuracy(pipeline.RunConfig(inputs=[corpus], workspace=ws_gpu), ctx=ctx)
+    want = open(os.path.join(ws_ref, "accuracy.json"), "rb").read()
+    assert open(os.path.join(ws_gpu, "accuracy.json"), "rb").read() == want
+    assert acc["corpus_size"] == 1200
