@@ -184,6 +184,9 @@ int nd_dedup_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offse
                     nd_dedup_stats* stats);
 /* distinct pairs (doc ids, sorted by (lo, hi)) of the last dedup */
 int nd_dedup_fetch_pairs(nd_ctx* ctx, uint64_t* lo, uint64_t* hi, uint32_t* match_count);
+/* signatures (n*H u32) and band ids (n*bands u32) the last dedup computed,
+ * rows in input order (either output may be NULL) */
+int nd_dedup_fetch_signatures(nd_ctx* ctx, uint32_t* sig, uint32_t* band);
 /* groups of the last dedup as doc ids: members in output order,
  * group_start[ngroups+1]; representative = members[group_start[g]] */
 int nd_dedup_fetch_groups(nd_ctx* ctx, uint64_t* members, uint64_t* group_start);

@@ -114,6 +114,7 @@ SIGNATURES = {
     "nd_dedup_device": (C.c_int, [vp, vp, vp, u64p, C.c_uint64, C.POINTER(NdParams),
                                   C.POINTER(NdDedupStats)]),
     "nd_dedup_fetch_pairs": (C.c_int, [vp, u64p, u64p, u32p]),
+    "nd_dedup_fetch_signatures": (C.c_int, [vp, u32p, u32p]),
     "nd_dedup_fetch_groups": (C.c_int, [vp, u64p, u64p]),
     "nd_dedup_write_report": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
     "nd_feds_write": (C.c_int, [C.c_char_p, C.POINTER(NdFedsHeader), u64p, u32p, u32p,

@@ -161,6 +161,7 @@ void dedup_tail(nd_ctx* ctx, DedupState& st, const nd_params& p, uint64_t n, nd_
   t.mark();  // 4
   ND_CUDA(cudaStreamSynchronize(s));
   st.documents = n;
+  st.bands = p.bands;
   st.valid = true;
   if (stats) {
     stats->documents = n;
@@ -258,6 +259,20 @@ int nd_dedup_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offse
                       st.sig_scratch, s, true, nullptr);
     t.mark();
     dedup_tail(ctx, st, p, n, stats, t);
+  });
+}
+
+int nd_dedup_fetch_signatures(nd_ctx* ctx, uint32_t* sig, uint32_t* band) {
+  return guarded_impl(ctx, [&] {
+    DedupState& st = ctx->dedup;
+    if (!st.valid || !ctx->fam.q) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");
+    cudaStream_t s = ctx->stream;
+    const uint64_t n = st.documents, H = ctx->fam.H;
+    if (sig && n)
+      ND_CUDA(cudaMemcpyAsync(sig, st.sig.ptr, n * H * 4, cudaMemcpyDeviceToHost, s));
+    if (band && n)
+      ND_CUDA(cudaMemcpyAsync(band, st.band.ptr, n * st.bands * 4, cudaMemcpyDeviceToHost, s));
+    ND_CUDA(cudaStreamSynchronize(s));
   });
 }
 

@@ -221,6 +221,7 @@ struct DedupState {
   std::vector<uint64_t> doc_ids;  // row -> doc id (empty = identity)
   uint64_t documents = 0;
   uint32_t K = 0;
+  uint32_t bands = 0;             // band keys per row in band
   bool valid = false;
   void release() {
     for (DevBuf* b : {&sig, &band, &text, &offs}) b->release();

@@ -215,3 +215,43 @@ def test_codepoint_signatures_oracle_vs_reference(oracle, ref):
         want, _ = ref.signatures(data, offs, seed=5, H=H, L=L, bands=0, rows=0, K=0, unit=1)
         got = oracle.signatures(data, offs, oracle.derive_family(5, H, L), L, unit=1)
         np.testing.assert_array_equal(got, want)
+
+
+def test_verify_drivers_match_single_thread_oracle(oracle):
+    # oracle/verify.c (full-scale parity driver) == or_compare_cell per cell
+    import ctypes as C
+
+    from oracle_bind import u32p, u64p
+
+    L = oracle.lib
+    L.ov_cells.argtypes = [u32p, C.c_uint64, C.c_uint32, C.c_uint32, u64p, u32p]
+    L.ov_compare_cells.argtypes = [u32p, C.c_uint32, u64p, u32p, C.c_uint64, C.c_uint64,
+                                   C.c_uint64, C.c_int, C.POINTER(u32p), C.POINTER(u32p),
+                                   C.POINTER(u32p), u64p]
+    L.ov_compare_cells.restype = C.c_int64
+    L.ov_free.argtypes = [C.c_void_p]
+    rng = np.random.default_rng(4)
+    n, H, B, K = 600, 64, 8, 12
+    sig = rng.integers(0, 6, size=(n, H), dtype=np.uint32)  # many near-duplicates
+    band = rng.integers(0, K, size=(n, B), dtype=np.uint32)
+    off = np.empty(B * K + 1, np.uint64)
+    rows = np.empty(n * B, np.uint32)
+    assert L.ov_cells(band.ctypes.data_as(u32p), n, B, K, off.ctypes.data_as(u64p),
+                      rows.ctypes.data_as(u32p)) == 0
+    want, cand = set(), 0
+    for c in range(B * K):
+        r = rows[int(off[c]):int(off[c + 1])]
+        assert (np.diff(r.astype(np.int64)) > 0).all()
+        assert (band[r, c // K] == c % K).all()
+        cand += len(r) * (len(r) - 1) // 2
+        lo, hi, m = oracle.compare_cell(sig, r, 1, 4)
+        want |= set(zip(lo.tolist(), hi.tolist(), m.tolist()))
+    lo_p, hi_p, m_p, cc = u32p(), u32p(), u32p(), C.c_uint64()
+    k = L.ov_compare_cells(sig.ctypes.data_as(u32p), H, off.ctypes.data_as(u64p),
+                           rows.ctypes.data_as(u32p), B * K, 1, 4, 3, C.byref(lo_p), C.byref(hi_p),
+                           C.byref(m_p), C.byref(cc))
+    got = set(zip(np.ctypeslib.as_array(lo_p, (k,)).tolist(), np.ctypeslib.as_array(hi_p, (k,)).tolist(),
+                  np.ctypeslib.as_array(m_p, (k,)).tolist()))
+    for p in (lo_p, hi_p, m_p):
+        L.ov_free(p)
+    assert cc.value == cand and got == want and len(want) > 100
