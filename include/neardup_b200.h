@@ -194,6 +194,37 @@ int nd_dedup_fetch_groups(nd_ctx* ctx, uint64_t* members, uint64_t* group_start)
  * as written by pipeline.cpp:479-506) for the last dedup, into dir. */
 int nd_dedup_write_report(nd_ctx* ctx, const char* dir, uint64_t total_records);
 
+/* ---- host document loader (corpus.cpp / text.cpp), multi-threaded C++ ------
+ * One JSONL file per call: lines split as for_each_raw_document
+ * (corpus.cpp:56-82), parsed by parse_jsonl_line's parser (nlohmann::json,
+ * corpus.cpp:31-54), NFC-normalised (text.cpp:70-86; UAX #15 tables from the
+ * UCD), code points counted and filtered by min_chars / can_shingle
+ * (corpus.cpp:93-141).  Reject reason codes: 1 invalid_json, 2 not_an_object,
+ * 3 missing_text_field, 4 text_field_not_string, 5 below_min_chars,
+ * 6 too_short_to_shingle.  Errors: nd_ingest_last_error(). */
+typedef struct nd_jsonl nd_jsonl;
+const char* nd_ingest_last_error(void);
+int nd_jsonl_load(const char* path, const char* text_field, uint64_t min_chars,
+                  uint32_t shingle_len, uint32_t unit, uint32_t threads, int keep_text,
+                  nd_jsonl** out);
+void nd_jsonl_counts(const nd_jsonl* f, uint64_t* records, uint64_t* surviving,
+                     uint64_t* text_bytes, uint64_t* rejects);
+/* rejects in line order: 1-based line numbers and reason codes */
+int nd_jsonl_rejects(const nd_jsonl* f, uint64_t* lines, uint32_t* reasons);
+/* the surviving documents, doc_id = record_offset + record ordinal
+ * (preprocess, corpus.cpp:93-101); bytes/offsets[n+1] need keep_text */
+int nd_jsonl_documents(const nd_jsonl* f, uint64_t record_offset, uint8_t* bytes,
+                       uint64_t* offsets, uint64_t* doc_ids, uint64_t* char_counts);
+void nd_jsonl_free(nd_jsonl* f);
+/* nfc_normalize (text.cpp:70-86): *out_len always set; copied when cap suffices */
+int nd_nfc_normalize(const uint8_t* in, uint64_t len, uint8_t* out, uint64_t cap,
+                     uint64_t* out_len);
+/* codepoint_count (text.cpp:88-99) */
+uint64_t nd_codepoint_count(const uint8_t* s, uint64_t len);
+/* parse_jsonl_line (corpus.cpp:31-54): *reason 0 = ok (text copied when cap suffices) */
+int nd_parse_jsonl_line(const char* line, uint64_t len, const char* text_field, uint32_t* reason,
+                        uint8_t* text_out, uint64_t cap, uint64_t* text_len);
+
 /* ---- staged workflow on disk: hash -> gather-compare -> union ---------------
  * The reference persists every stage (pipeline.hpp:62-96): one .feds signature
  * file per input file, one .pairs file per (worker, gather pass), then the

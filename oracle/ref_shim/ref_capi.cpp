@@ -15,7 +15,9 @@
 //   generate_synthetic/write_synthetic  synthetic.hpp:57-63
 //   run_dedup                pipeline.hpp:100 (pipeline.cpp:510-532)
 //   run_eval_accuracy        pipeline.hpp:114 (pipeline.cpp:534-585)
+#include <algorithm>
 #include <chrono>
+#include <filesystem>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -24,6 +26,7 @@
 #include <vector>
 
 #include "neardup/compare.hpp"
+#include "neardup/corpus.hpp"
 #include "neardup/dedup_graph.hpp"
 #include "neardup/lsh.hpp"
 #include "neardup/minhash.hpp"
@@ -283,6 +286,55 @@ int ref_eval_accuracy(const char* input, const char* workspace, unsigned workers
     c.workers = workers;
     c.oracle_override = oracle_override != 0;
     run_eval_accuracy(c);
+  });
+}
+
+// build_manifest + surviving_documents (corpus.cpp:109-163) over one input
+// (file or directory, expanded like the pipeline); rejects written with
+// RejectLog::write_jsonl; survivors returned packed (malloc'd).
+int ref_load_corpus(const char* input, const char* text_field, uint64_t min_chars, uint32_t L,
+                    uint32_t unit, const char* rejects_path, uint64_t* records,
+                    uint64_t* surviving, uint8_t** bytes, uint64_t** offsets, uint64_t** ids,
+                    uint64_t** chars) {
+  return guarded([&] {
+    std::vector<std::string> paths;
+    namespace fs = std::filesystem;
+    if (fs::is_directory(input)) {
+      for (const auto& e : fs::directory_iterator(input))
+        if (e.is_regular_file() && e.path().extension() == ".jsonl") paths.push_back(e.path().string());
+      std::sort(paths.begin(), paths.end());
+    } else {
+      paths.push_back(input);
+    }
+    IngestOptions o;
+    o.text_field = text_field;
+    o.min_chars = min_chars;
+    o.shingle_len = L;
+    o.unit = static_cast<ShingleUnit>(unit);
+    RejectLog rej;
+    CorpusManifest m = build_manifest(paths, o, &rej);
+    rej.write_jsonl(rejects_path);
+    std::string all;
+    std::vector<uint64_t> off{0}, id, ch;
+    for (size_t i = 0; i < m.files.size(); ++i)
+      for (const CleanDocument& d : surviving_documents(m, i, o)) {
+        all += d.text;
+        off.push_back(all.size());
+        id.push_back(d.doc_id);
+        ch.push_back(d.char_count);
+      }
+    *records = m.total_records;
+    *surviving = m.total_surviving;
+    *bytes = static_cast<uint8_t*>(std::malloc(all.size() + 1));
+    std::memcpy(*bytes, all.data(), all.size());
+    auto dup = [](const std::vector<uint64_t>& v) {
+      auto* p = static_cast<uint64_t*>(std::malloc(8 * (v.size() + 1)));
+      std::memcpy(p, v.data(), 8 * v.size());
+      return p;
+    };
+    *offsets = dup(off);
+    *ids = dup(id);
+    *chars = dup(ch);
   });
 }
 

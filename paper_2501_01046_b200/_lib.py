@@ -117,6 +117,17 @@ SIGNATURES = {
     "nd_dedup_fetch_signatures": (C.c_int, [vp, u32p, u32p]),
     "nd_dedup_fetch_groups": (C.c_int, [vp, u64p, u64p]),
     "nd_dedup_write_report": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
+    "nd_ingest_last_error": (C.c_char_p, []),
+    "nd_jsonl_load": (C.c_int, [C.c_char_p, C.c_char_p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                C.c_uint32, C.c_int, C.POINTER(vp)]),
+    "nd_jsonl_counts": (None, [vp, u64p, u64p, u64p, u64p]),
+    "nd_jsonl_rejects": (C.c_int, [vp, u64p, u32p]),
+    "nd_jsonl_documents": (C.c_int, [vp, C.c_uint64, u8p, u64p, u64p, u64p]),
+    "nd_jsonl_free": (None, [vp]),
+    "nd_nfc_normalize": (C.c_int, [u8p, C.c_uint64, u8p, C.c_uint64, u64p]),
+    "nd_codepoint_count": (C.c_uint64, [u8p, C.c_uint64]),
+    "nd_parse_jsonl_line": (C.c_int, [C.c_char_p, C.c_uint64, C.c_char_p, u32p, u8p, C.c_uint64,
+                                      u64p]),
     "nd_feds_write": (C.c_int, [C.c_char_p, C.POINTER(NdFedsHeader), u64p, u32p, u32p,
                                 C.c_uint64, C.c_int]),
     "nd_feds_read_header": (C.c_int, [C.c_char_p, C.POINTER(NdFedsHeader)]),
@@ -192,6 +203,7 @@ class ShortDocumentError(NdError):
 
 _CODE_TO_EXC = {ND_ERR_CONFIG: ConfigError, ND_ERR_IO: IoError, ND_ERR_PREREQ: PrerequisiteError,
                 ND_ERR_DEVICE: DeviceError, ND_ERR_SHORT: ShortDocumentError}
+ERRORS = _CODE_TO_EXC
 
 
 def check(rc: int, ctx=None) -> None:

@@ -37,6 +37,7 @@ def _json_inc() -> list[str]:
 def _headers_digest() -> str:
     h = hashlib.sha1()
     for f in sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp"))
+                    + glob.glob(os.path.join(CSRC, "*.inc"))
                     + glob.glob(os.path.join(ROOT, "include", "*.h"))):
         with open(f, "rb") as fh:
             h.update(fh.read())

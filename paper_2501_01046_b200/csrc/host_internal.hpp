@@ -5,6 +5,8 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <string_view>
+#include <utility>
 #include <vector>
 
 #include "neardup_b200.h"
@@ -49,5 +51,22 @@ void pairs_read(const std::string& path, std::vector<uint64_t>& lo, std::vector<
                 std::vector<uint32_t>& m);
 uint32_t plan_gather(uint64_t total_bytes, uint32_t K, const std::vector<uint32_t>& worker_bands,
                      uint64_t budget, uint32_t override_c, std::vector<uint32_t>& passes);
+
+// document loader (host_ingest.cpp)
+struct JsonlFile {
+  uint64_t records = 0;                                // valid JSONL records
+  std::vector<std::pair<uint64_t, uint8_t>> rejects;   // (1-based line, reason code)
+  std::vector<uint64_t> ordinal;                       // record ordinal of each survivor
+  std::vector<uint64_t> chars;                         // code points of each survivor
+  std::string bytes;                                   // survivors' NFC text (keep_text)
+  std::vector<uint64_t> offsets;                       // survivors + 1 (keep_text)
+};
+void load_jsonl(const std::string& path, const std::string& field, uint64_t min_chars,
+                uint32_t shingle_len, uint32_t unit, unsigned threads, bool keep_text,
+                JsonlFile& out);
+bool nfc_normalize_into(std::string_view in, std::string& out);
+std::string nfc_normalize(std::string_view in);
+uint64_t codepoint_count(std::string_view t);
+int parse_jsonl_line(std::string_view line, const std::string& field, std::string& text);
 
 }  // namespace ndb

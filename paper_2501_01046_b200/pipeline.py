@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import NdDedupStats, NdParams, u8p, u64p
-from .corpus import CorpusManifest, build_manifest, surviving_documents  # noqa: F401
+from .corpus import CorpusManifest, build_manifest, surviving_documents, surviving_packed  # noqa: F401
 from .dedup_graph import DedupReport, DuplicateGroup
 from .device import Context, default_context
 from .lsh import _ratio
@@ -193,11 +193,11 @@ def run_dedup_in_memory(config: RunConfig, ctx: Context | None = None) -> DedupR
     if manifest.total_surviving == 0:
         raise _lib.ConfigError(_lib.ND_ERR_CONFIG,
                                "no documents survive preprocessing; nothing to deduplicate")
-    docs = []
-    for i in range(len(manifest.files)):
-        docs.extend(surviving_documents(manifest, i, config))
-    data, offsets = pack_documents(docs)
-    ids = np.array([d.doc_id for d in docs], np.uint64)
+    parts = [surviving_packed(manifest, i, config) for i in range(len(manifest.files))]
+    data = np.concatenate([p[0] for p in parts])
+    offsets = np.zeros(manifest.total_surviving + 1, np.uint64)
+    np.cumsum(np.concatenate([np.diff(p[1]) for p in parts]), out=offsets[1:])
+    ids = np.concatenate([p[2] for p in parts])
     ctx = ctx or default_context()
     rep = dedup_packed(data, offsets, config, ids, ctx=ctx)
     write_report(config.workspace, ctx, manifest.total_records)
@@ -329,13 +329,11 @@ def run_hash_stage(config: RunConfig, ctx: Context | None = None) -> HashStageOu
     base = header_template(config, out.bucket_count)
     for i, fs in enumerate(manifest.files):
         path = signatures_dir(config) + "/" + signature_file_name(i, fs.path)
-        docs = surviving_documents(manifest, i, config)
-        if len(docs) != fs.surviving:
+        data, offsets, ids, _ = surviving_packed(manifest, i, config)
+        if len(ids) != fs.surviving:
             raise _lib.PrerequisiteError(_lib.ND_ERR_PREREQ,
-                                         f"'{fs.path}' yielded {len(docs)} documents, manifest "
+                                         f"'{fs.path}' yielded {len(ids)} documents, manifest "
                                          f"says {fs.surviving}")
-        data, offsets = pack_documents(docs)
-        ids = np.array([d.doc_id for d in docs], np.uint64)
         h = base.to_c()
         h.source_ordinal = i
         dp = data.ctypes.data_as(u8p) if data.size else C.cast(C.c_char_p(b"\0"), u8p)

@@ -174,7 +174,28 @@ class Ref:
                                     C.c_uint64, C.c_uint64, C.c_uint, C.c_uint64,
                                     C.POINTER(C.c_double), u64p, C.c_uint32]
         L.ref_eval_accuracy.argtypes = [C.c_char_p, C.c_char_p, C.c_uint, C.c_int]
+        L.ref_load_corpus.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                      C.c_char_p, u64p, u64p, C.POINTER(u8p), C.POINTER(u64p),
+                                      C.POINTER(u64p), C.POINTER(u64p)]
         self.lib = L
+
+    def load_corpus(self, input_path, rejects_path, text_field="text", min_chars=200, L=5,
+                    unit=0):
+        """-> (records, surviving, data u8, offsets u64, doc_ids u64, char_counts u64)."""
+        r, s = C.c_uint64(), C.c_uint64()
+        b, o, i, c = u8p(), u64p(), u64p(), u64p()
+        self._check(self.lib.ref_load_corpus(input_path.encode(), text_field.encode(), min_chars,
+                                             L, unit, rejects_path.encode(), C.byref(r),
+                                             C.byref(s), C.byref(b), C.byref(o), C.byref(i),
+                                             C.byref(c)))
+        n = s.value
+        offs = np.ctypeslib.as_array(o, (n + 1,)).copy()
+        data = np.ctypeslib.as_array(b, (int(offs[-1]) + 1,))[:int(offs[-1])].copy()
+        ids = np.ctypeslib.as_array(i, (n + 1,))[:n].copy()
+        ch = np.ctypeslib.as_array(c, (n + 1,))[:n].copy()
+        for p in (b, o, i, c):
+            self.lib.ref_free(p)
+        return r.value, n, data, offs, ids, ch
 
     def eval_accuracy(self, input_path, workspace, workers=1, override=False):
         self._check(self.lib.ref_eval_accuracy(input_path.encode(), workspace.encode(), workers,
