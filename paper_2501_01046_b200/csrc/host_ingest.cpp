@@ -225,15 +225,83 @@ uint64_t codepoint_count(std::string_view t) {
 }
 
 // parse_jsonl_line (corpus.cpp:31-54); reason codes: 0 ok, 1 invalid_json,
-// 2 not_an_object, 3 missing_text_field, 4 text_field_not_string
+// 2 not_an_object, 3 missing_text_field, 4 text_field_not_string.
+// nlohmann's SAX interface drives the same lexer and parser as the DOM parse
+// the reference does (so acceptance is identical) without building the DOM;
+// the DOM's object insertion keeps the LAST value of a repeated key, and so
+// does this handler.
+namespace {
+struct FieldSax {
+  const std::string* field;
+  std::string* text;
+  int depth = 0;
+  bool top_object = false, first = true, pending = false, found = false, is_string = false;
+  void value_event(bool str) {
+    if (first) {
+      first = false;
+      top_object = false;
+    }
+    if (depth == 1 && pending) {
+      found = true;
+      is_string = str;
+      pending = false;
+    }
+  }
+  bool null() { value_event(false); return true; }
+  bool boolean(bool) { value_event(false); return true; }
+  bool number_integer(nlohmann::json::number_integer_t) { value_event(false); return true; }
+  bool number_unsigned(nlohmann::json::number_unsigned_t) { value_event(false); return true; }
+  bool number_float(nlohmann::json::number_float_t, const std::string&) {
+    value_event(false);
+    return true;
+  }
+  bool string(std::string& v) {
+    const bool take = depth == 1 && pending;
+    value_event(true);
+    if (take) text->swap(v);
+    return true;
+  }
+  bool binary(nlohmann::json::binary_t&) { value_event(false); return true; }
+  bool start_object(std::size_t) {
+    if (first) {
+      first = false;
+      top_object = true;
+    } else {
+      value_event(false);
+    }
+    ++depth;
+    return true;
+  }
+  bool key(std::string& k) {
+    if (depth == 1) pending = k == *field;
+    return true;
+  }
+  bool end_object() { --depth; return true; }
+  bool start_array(std::size_t) {
+    if (first) {
+      first = false;
+      top_object = false;
+    } else {
+      value_event(false);
+    }
+    ++depth;
+    return true;
+  }
+  bool end_array() { --depth; return true; }
+  bool parse_error(std::size_t, const std::string&, const nlohmann::detail::exception&) {
+    return false;
+  }
+};
+}  // namespace
+
 int parse_jsonl_line(std::string_view line, const std::string& field, std::string& text) {
-  nlohmann::json j = nlohmann::json::parse(line, nullptr, /*allow_exceptions=*/false);
-  if (j.is_discarded()) return 1;
-  if (!j.is_object()) return 2;
-  auto it = j.find(field);
-  if (it == j.end()) return 3;
-  if (!it->is_string()) return 4;
-  text = it->get_ref<const std::string&>();
+  FieldSax h;
+  h.field = &field;
+  h.text = &text;
+  if (!nlohmann::json::sax_parse(line, &h, nlohmann::json::input_format_t::json, true)) return 1;
+  if (!h.top_object) return 2;
+  if (!h.found) return 3;
+  if (!h.is_string) return 4;
   return 0;
 }
 
