@@ -74,7 +74,12 @@ inline std::vector<Signature> signature_batch(Device& dev, std::span<const Clean
   std::vector<uint64_t> offsets{0};
   std::vector<uint64_t> ids;
   for (const CleanDocument& d : docs) {
-    if (d.text.size() < family.shingle_len) {
+    // units: bytes, or code points (nd_codepoint_count == text.cpp:88-99)
+    const uint64_t units = family.unit == ShingleUnit::kByte
+                               ? d.text.size()
+                               : nd_codepoint_count(reinterpret_cast<const uint8_t*>(d.text.data()),
+                                                    d.text.size());
+    if (units < family.shingle_len) {
       if (on_short) on_short(d.doc_id);
       continue;
     }
