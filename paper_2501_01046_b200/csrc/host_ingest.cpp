@@ -18,6 +18,11 @@
 // Lines are split into contiguous blocks, one per thread; ordinals and the
 // reject log are stitched back in line order, so the result is independent
 // of the thread count.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <cerrno>
 #include <cstdio>
@@ -294,7 +299,193 @@ struct FieldSax {
 };
 }  // namespace
 
+// Fast path for parse_jsonl_line: a recursive-descent scanner for a strict
+// SUBSET of the JSON nlohmann accepts -- objects, arrays, strings whose
+// escapes are the single-character ones, well-formed UTF-8 (Unicode Table
+// 3-7, the ranges nlohmann's lexer checks), integers of at most 18 digits,
+// true/false/null, whitespace ' ' '\t' '\n' '\r'.  Inside that subset
+// nlohmann accepts exactly the same lines and decodes the same text; anything
+// else (\u escapes, fractions/exponents, long numbers, a BOM, deep nesting,
+// every error) returns -1 and the line goes to nlohmann, whose verdict is
+// then final.  *ascii: the captured text is pure ASCII.
+namespace {
+struct Fast {
+  const unsigned char* p;
+  const unsigned char* e;
+  const std::string* field;
+  std::string* text;
+  bool top_object = false, found = false, is_string = false, ascii = true;
+  static bool ws(unsigned c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r'; }
+  void skip() {
+    while (p < e && ws(*p)) ++p;
+  }
+  // string body after the opening quote; out may be null (validate only)
+  bool str(std::string* out, bool* asc) {
+    const unsigned char* run = p;
+    for (;;) {
+      while (p < e && *p >= 0x20 && *p < 0x80 && *p != '"' && *p != '\\') ++p;
+      if (p >= e) return false;
+      const unsigned c = *p;
+      if (c == '"') {
+        if (out) out->append(reinterpret_cast<const char*>(run), p - run);
+        ++p;
+        return true;
+      }
+      if (c < 0x20) return false;
+      if (c == '\\') {
+        if (out) out->append(reinterpret_cast<const char*>(run), p - run);
+        if (p + 1 >= e) return false;
+        char d;
+        switch (p[1]) {
+          case '"': d = '"'; break;
+          case '\\': d = '\\'; break;
+          case '/': d = '/'; break;
+          case 'b': d = '\b'; break;
+          case 'f': d = '\f'; break;
+          case 'n': d = '\n'; break;
+          case 'r': d = '\r'; break;
+          case 't': d = '\t'; break;
+          default: return false;  // \u.. and invalid escapes: nlohmann decides
+        }
+        if (out) out->push_back(d);
+        p += 2;
+        run = p;
+        continue;
+      }
+      // c >= 0x80: one well-formed UTF-8 sequence
+      size_t i = static_cast<size_t>(p - run), len = static_cast<size_t>(e - run);
+      if (next_cp(run, i, len) < 0) return false;
+      if (asc) *asc = false;
+      p = run + i;
+    }
+  }
+  bool number() {
+    if (p < e && *p == '-') ++p;
+    if (p >= e || *p < '0' || *p > '9') return false;
+    const unsigned char* d0 = p;
+    if (*p == '0') {
+      ++p;
+    } else {
+      while (p < e && *p >= '0' && *p <= '9') ++p;
+    }
+    if (p - d0 > 18) return false;
+    if (p < e && ((*p >= '0' && *p <= '9') || *p == '.' || *p == 'e' || *p == 'E')) return false;
+    return true;
+  }
+  bool lit(const char* w, size_t n) {
+    if (static_cast<size_t>(e - p) < n || std::memcmp(p, w, n) != 0) return false;
+    p += n;
+    return true;
+  }
+  // capture: this value is the field's value at depth 1
+  bool value(int depth, bool capture) {
+    if (p >= e || depth > 64) return false;
+    const unsigned c = *p;
+    if (capture) {
+      found = true;
+      is_string = c == '"';
+    }
+    switch (c) {
+      case '"': {
+        ++p;
+        if (capture) {
+          text->clear();
+          ascii = true;
+          return str(text, &ascii);
+        }
+        return str(nullptr, nullptr);
+      }
+      case '{': {
+        ++p;
+        skip();
+        if (p < e && *p == '}') {
+          ++p;
+          return true;
+        }
+        for (;;) {
+          if (p >= e || *p != '"') return false;
+          ++p;
+          bool match = false;
+          if (depth == 0) {
+            key.clear();
+            if (!str(&key, nullptr)) return false;
+            match = key == *field;
+          } else if (!str(nullptr, nullptr)) {
+            return false;
+          }
+          skip();
+          if (p >= e || *p != ':') return false;
+          ++p;
+          skip();
+          if (!value(depth + 1, match)) return false;
+          skip();
+          if (p < e && *p == ',') {
+            ++p;
+            skip();
+            continue;
+          }
+          if (p < e && *p == '}') {
+            ++p;
+            return true;
+          }
+          return false;
+        }
+      }
+      case '[': {
+        ++p;
+        skip();
+        if (p < e && *p == ']') {
+          ++p;
+          return true;
+        }
+        for (;;) {
+          if (!value(depth + 1, false)) return false;
+          skip();
+          if (p < e && *p == ',') {
+            ++p;
+            skip();
+            continue;
+          }
+          if (p < e && *p == ']') {
+            ++p;
+            return true;
+          }
+          return false;
+        }
+      }
+      case 't': return lit("true", 4);
+      case 'f': return lit("false", 5);
+      case 'n': return lit("null", 4);
+      default: return number();
+    }
+  }
+  std::string key;
+};
+}  // namespace
+
+int parse_jsonl_line_fast(std::string_view line, const std::string& field, std::string& text,
+                          bool* ascii) {
+  Fast f;
+  f.p = reinterpret_cast<const unsigned char*>(line.data());
+  f.e = f.p + line.size();
+  f.field = &field;
+  f.text = &text;
+  if (line.size() >= 3 && f.p[0] == 0xEF && f.p[1] == 0xBB && f.p[2] == 0xBF) return -1;  // BOM
+  f.skip();
+  f.top_object = f.p < f.e && *f.p == '{';
+  if (!f.value(0, false)) return -1;
+  f.skip();
+  if (f.p != f.e) return -1;
+  if (!f.top_object) return 2;
+  if (!f.found) return 3;
+  if (!f.is_string) return 4;
+  if (ascii) *ascii = f.ascii;
+  return 0;
+}
+
 int parse_jsonl_line(std::string_view line, const std::string& field, std::string& text) {
+  const int r = parse_jsonl_line_fast(line, field, text, nullptr);
+  if (r >= 0) return r;
   FieldSax h;
   h.field = &field;
   h.text = &text;
@@ -310,61 +501,87 @@ void load_jsonl(const std::string& path, const std::string& field, uint64_t min_
                 uint32_t shingle_len, uint32_t unit, unsigned threads, bool keep_text,
                 JsonlFile& out) {
   if (shingle_len == 0) fail(ND_ERR_CONFIG, "shingle length must be positive");
-  FILE* f = std::fopen(path.c_str(), "rb");
-  if (!f) fail(ND_ERR_IO, "cannot open '" + path + "': " + std::strerror(errno));
-  std::string buf;
-  {
-    std::fseek(f, 0, SEEK_END);
-    const long sz = std::ftell(f);
-    std::fseek(f, 0, SEEK_SET);
-    buf.resize(sz > 0 ? static_cast<size_t>(sz) : 0);
-    const bool ok = buf.empty() || std::fread(buf.data(), 1, buf.size(), f) == buf.size();
-    std::fclose(f);
-    if (!ok) fail(ND_ERR_IO, "read failed for '" + path + "'");
+  const int fd = open(path.c_str(), O_RDONLY);
+  if (fd < 0) fail(ND_ERR_IO, "cannot open '" + path + "': " + std::strerror(errno));
+  struct stat sb;
+  if (fstat(fd, &sb) != 0) {
+    close(fd);
+    fail(ND_ERR_IO, "read failed for '" + path + "'");
   }
-  // line starts (std::getline semantics: a final line without '\n' counts)
-  std::vector<size_t> starts;
-  starts.push_back(0);
-  for (const char* p = buf.data(); (p = static_cast<const char*>(std::memchr(p, '\n', buf.data() + buf.size() - p)));) {
-    ++p;
-    starts.push_back(static_cast<size_t>(p - buf.data()));
+  const size_t size = static_cast<size_t>(sb.st_size);
+  const char* buf = nullptr;
+  void* map = MAP_FAILED;
+  if (size) {
+    map = mmap(nullptr, size, PROT_READ, MAP_PRIVATE, fd, 0);
+    if (map == MAP_FAILED) {
+      close(fd);
+      fail(ND_ERR_IO, "read failed for '" + path + "'");
+    }
+    madvise(map, size, MADV_SEQUENTIAL);
+    buf = static_cast<const char*>(map);
   }
-  if (starts.back() == buf.size()) starts.pop_back();  // no line after the final '\n'
-  const size_t nlines = starts.size();
-  starts.push_back(buf.size() + 1);  // sentinel: end of the last line (+1 for its '\n')
+  close(fd);
+  struct Unmap {
+    void* m;
+    size_t n;
+    ~Unmap() {
+      if (m != MAP_FAILED) munmap(m, n);
+    }
+  } unmap{map, size};
 
-  struct Block {
-    uint64_t records = 0;
-    std::vector<std::pair<uint64_t, uint8_t>> rejects;  // (line, reason)
-    std::string bytes;
-    std::vector<uint64_t> lens, ordinal, chars;         // ordinal: within the block
-  };
+  // T byte ranges, each starting at a line start (getline semantics: lines end
+  // at '\n'; a final line without '\n' counts, nothing after a final '\n')
   if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
-  threads = static_cast<unsigned>(std::min<size_t>(threads, std::max<size_t>(1, nlines / 256)));
-  std::vector<Block> blocks(threads);
+  threads = static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(threads, size / (1 << 16))));
+  std::vector<size_t> cut(threads + 1, size);
+  cut[0] = 0;
+  for (unsigned t = 1; t < threads; ++t) {
+    size_t c = std::max(cut[t - 1], size * t / threads);
+    const void* nl = c < size ? std::memchr(buf + c, '\n', size - c) : nullptr;
+    cut[t] = nl ? static_cast<size_t>(static_cast<const char*>(nl) - buf) + 1 : size;
+  }
+  out = JsonlFile{};
+  out.blocks.resize(threads);
   auto work = [&](unsigned t) {
-    Block& b = blocks[t];
-    const size_t l0 = nlines * t / threads, l1 = nlines * (t + 1) / threads;
+    JsonlFile::Block& b = out.blocks[t];
     std::string text, norm;
-    for (size_t l = l0; l < l1; ++l) {
-      size_t a = starts[l], e = starts[l + 1] - 1;  // [a, e) without '\n'
+    size_t a = cut[t];
+    const size_t end = cut[t + 1];
+    if (keep_text) b.bytes.reserve(end - a);  // decoded text is at most the line bytes, bar NFC growth
+    while (a < end) {
+      const void* nl = std::memchr(buf + a, '\n', end - a);
+      const size_t stop = nl ? static_cast<size_t>(static_cast<const char*>(nl) - buf) : end;
+      const uint64_t line_no = ++b.lines;  // local; made global after the join
+      size_t e = stop;
+      const size_t next = nl ? stop + 1 : end;
       if (e > a && buf[e - 1] == '\r') --e;
-      if (e == a) continue;
-      const int why = parse_jsonl_line(std::string_view(buf.data() + a, e - a), field, text);
+      if (e == a) {
+        a = next;
+        continue;
+      }
+      const std::string_view line(buf + a, e - a);
+      a = next;
+      bool ascii = false;
+      int why = parse_jsonl_line_fast(line, field, text, &ascii);
+      if (why < 0) {
+        ascii = false;
+        why = parse_jsonl_line(line, field, text);
+      }
       if (why) {
-        b.rejects.push_back({l + 1, static_cast<uint8_t>(why)});
+        b.rejects.push_back({line_no, static_cast<uint8_t>(why)});
         continue;
       }
       const uint64_t ord = b.records++;
-      const std::string& clean = nfc_normalize_into(text, norm) ? text : norm;
-      const uint64_t chars = codepoint_count(clean);
+      // ASCII text is NFC and has one code point per byte
+      const std::string& clean = ascii || nfc_normalize_into(text, norm) ? text : norm;
+      const uint64_t chars = ascii ? clean.size() : codepoint_count(clean);
       if (chars < min_chars) {
-        b.rejects.push_back({l + 1, 5});
+        b.rejects.push_back({line_no, 5});
         continue;
       }
       const uint64_t units = unit == 0 ? clean.size() : chars;
       if (units < shingle_len) {
-        b.rejects.push_back({l + 1, 6});
+        b.rejects.push_back({line_no, 6});
         continue;
       }
       b.ordinal.push_back(ord);
@@ -379,32 +596,46 @@ void load_jsonl(const std::string& path, const std::string& field, uint64_t min_
   for (unsigned t = 1; t < threads; ++t) th.emplace_back(work, t);
   work(0);
   for (auto& x : th) x.join();
+  // local line numbers and ordinals -> global
+  uint64_t lines = 0, records = 0;
+  for (auto& b : out.blocks) {
+    b.line_base = lines;
+    b.record_base = records;
+    b.doc_base = out.surviving;
+    b.byte_base = out.text_bytes;
+    for (auto& r : b.rejects) r.first += lines;
+    lines += b.lines;
+    records += b.records;
+    out.surviving += b.ordinal.size();
+    out.text_bytes += b.bytes.size();
+  }
+  out.records = records;
+  out.nrejects = 0;
+  for (auto& b : out.blocks) out.nrejects += b.rejects.size();
+}
 
-  out = JsonlFile{};
-  uint64_t base = 0, nbytes = 0, ndocs = 0;
-  for (auto& b : blocks) {
-    ndocs += b.ordinal.size();
-    nbytes += b.bytes.size();
-  }
-  out.ordinal.reserve(ndocs);
-  out.chars.reserve(ndocs);
-  if (keep_text) {
-    out.bytes.reserve(nbytes);
-    out.offsets.reserve(ndocs + 1);
-    out.offsets.push_back(0);
-  }
-  for (auto& b : blocks) {
-    for (auto& r : b.rejects) out.rejects.push_back(r);
+// survivors into caller buffers, one thread per block
+void jsonl_documents(const JsonlFile& f, uint64_t record_offset, uint8_t* bytes,
+                     uint64_t* offsets, uint64_t* doc_ids, uint64_t* char_counts) {
+  auto copy = [&](size_t t) {
+    const JsonlFile::Block& b = f.blocks[t];
+    uint64_t o = b.byte_base;
+    if (bytes && !b.bytes.empty()) std::memcpy(bytes + b.byte_base, b.bytes.data(), b.bytes.size());
     for (size_t k = 0; k < b.ordinal.size(); ++k) {
-      out.ordinal.push_back(base + b.ordinal[k]);
-      out.chars.push_back(b.chars[k]);
-      if (keep_text) out.offsets.push_back(out.offsets.back() + b.lens[k]);
+      const uint64_t i = b.doc_base + k;
+      if (doc_ids) doc_ids[i] = record_offset + b.record_base + b.ordinal[k];
+      if (char_counts) char_counts[i] = b.chars[k];
+      if (offsets) {
+        offsets[i] = o;
+        o += b.lens[k];
+      }
     }
-    if (keep_text) out.bytes += b.bytes;
-    base += b.records;
-    std::string().swap(b.bytes);
-  }
-  out.records = base;
+  };
+  std::vector<std::thread> th;
+  for (size_t t = 1; t < f.blocks.size(); ++t) th.emplace_back(copy, t);
+  if (!f.blocks.empty()) copy(0);
+  for (auto& x : th) x.join();
+  if (offsets) offsets[f.surviving] = f.text_bytes;
 }
 
 }  // namespace ndb

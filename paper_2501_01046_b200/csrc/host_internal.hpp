@@ -54,19 +54,27 @@ uint32_t plan_gather(uint64_t total_bytes, uint32_t K, const std::vector<uint32_
 
 // document loader (host_ingest.cpp)
 struct JsonlFile {
-  uint64_t records = 0;                                // valid JSONL records
-  std::vector<std::pair<uint64_t, uint8_t>> rejects;   // (1-based line, reason code)
-  std::vector<uint64_t> ordinal;                       // record ordinal of each survivor
-  std::vector<uint64_t> chars;                         // code points of each survivor
-  std::string bytes;                                   // survivors' NFC text (keep_text)
-  std::vector<uint64_t> offsets;                       // survivors + 1 (keep_text)
+  struct Block {                                      // one thread's contiguous lines
+    uint64_t lines = 0, records = 0;                  // local counts
+    uint64_t line_base = 0, record_base = 0, doc_base = 0, byte_base = 0;
+    std::vector<std::pair<uint64_t, uint8_t>> rejects;  // (1-based global line, reason)
+    std::vector<uint64_t> ordinal, chars, lens;       // per survivor (ordinal: local)
+    std::string bytes;                                // survivors' NFC text (keep_text)
+  };
+  std::vector<Block> blocks;
+  uint64_t records = 0, surviving = 0, text_bytes = 0, nrejects = 0;
 };
 void load_jsonl(const std::string& path, const std::string& field, uint64_t min_chars,
                 uint32_t shingle_len, uint32_t unit, unsigned threads, bool keep_text,
                 JsonlFile& out);
+void jsonl_documents(const JsonlFile& f, uint64_t record_offset, uint8_t* bytes,
+                     uint64_t* offsets, uint64_t* doc_ids, uint64_t* char_counts);
 bool nfc_normalize_into(std::string_view in, std::string& out);
 std::string nfc_normalize(std::string_view in);
 uint64_t codepoint_count(std::string_view t);
 int parse_jsonl_line(std::string_view line, const std::string& field, std::string& text);
+// strict-subset fast path; -1 = undecided (use parse_jsonl_line)
+int parse_jsonl_line_fast(std::string_view line, const std::string& field, std::string& text,
+                          bool* ascii);
 
 }  // namespace ndb

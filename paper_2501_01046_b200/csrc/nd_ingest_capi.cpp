@@ -52,33 +52,29 @@ int nd_jsonl_load(const char* path, const char* text_field, uint64_t min_chars,
 void nd_jsonl_counts(const nd_jsonl* h, uint64_t* records, uint64_t* surviving,
                      uint64_t* text_bytes, uint64_t* rejects) {
   if (records) *records = h->f.records;
-  if (surviving) *surviving = h->f.ordinal.size();
-  if (text_bytes) *text_bytes = h->f.bytes.size();
-  if (rejects) *rejects = h->f.rejects.size();
+  if (surviving) *surviving = h->f.surviving;
+  if (text_bytes) *text_bytes = h->f.text_bytes;
+  if (rejects) *rejects = h->f.nrejects;
 }
 
 int nd_jsonl_rejects(const nd_jsonl* h, uint64_t* lines, uint32_t* reasons) {
   return guarded([&] {
-    for (size_t i = 0; i < h->f.rejects.size(); ++i) {
-      if (lines) lines[i] = h->f.rejects[i].first;
-      if (reasons) reasons[i] = h->f.rejects[i].second;
-    }
+    size_t i = 0;
+    for (const auto& b : h->f.blocks)
+      for (const auto& r : b.rejects) {
+        if (lines) lines[i] = r.first;
+        if (reasons) reasons[i] = r.second;
+        ++i;
+      }
   });
 }
 
 int nd_jsonl_documents(const nd_jsonl* h, uint64_t record_offset, uint8_t* bytes,
                        uint64_t* offsets, uint64_t* doc_ids, uint64_t* char_counts) {
   return guarded([&] {
-    const auto& f = h->f;
     if ((bytes || offsets) && !h->keep_text)
       ndb::fail(ND_ERR_CONFIG, "loaded without keep_text; no document text kept");
-    if (bytes && !f.bytes.empty()) std::memcpy(bytes, f.bytes.data(), f.bytes.size());
-    for (size_t i = 0; i < f.ordinal.size(); ++i) {
-      if (doc_ids) doc_ids[i] = record_offset + f.ordinal[i];
-      if (char_counts) char_counts[i] = f.chars[i];
-    }
-    if (offsets)
-      for (size_t i = 0; i < f.offsets.size(); ++i) offsets[i] = f.offsets[i];
+    ndb::jsonl_documents(h->f, record_offset, bytes, offsets, doc_ids, char_counts);
   });
 }
 
