@@ -224,6 +224,10 @@ uint64_t nd_codepoint_count(const uint8_t* s, uint64_t len);
 /* parse_jsonl_line (corpus.cpp:31-54): *reason 0 = ok (text copied when cap suffices) */
 int nd_parse_jsonl_line(const char* line, uint64_t len, const char* text_field, uint32_t* reason,
                         uint8_t* text_out, uint64_t cap, uint64_t* text_len);
+/* same with the parser chosen: 0 fast scanner then nlohmann (the default),
+ * 1 nlohmann only, 2 fast scanner only (*reason 255 = undecided) */
+int nd_parse_jsonl_line_mode(const char* line, uint64_t len, const char* text_field, int mode,
+                             uint32_t* reason, uint8_t* text_out, uint64_t cap, uint64_t* text_len);
 
 /* ---- staged workflow on disk: hash -> gather-compare -> union ---------------
  * The reference persists every stage (pipeline.hpp:62-96): one .feds signature

@@ -128,6 +128,8 @@ SIGNATURES = {
     "nd_codepoint_count": (C.c_uint64, [u8p, C.c_uint64]),
     "nd_parse_jsonl_line": (C.c_int, [C.c_char_p, C.c_uint64, C.c_char_p, u32p, u8p, C.c_uint64,
                                       u64p]),
+    "nd_parse_jsonl_line_mode": (C.c_int, [C.c_char_p, C.c_uint64, C.c_char_p, C.c_int, u32p,
+                                           u8p, C.c_uint64, u64p]),
     "nd_feds_write": (C.c_int, [C.c_char_p, C.POINTER(NdFedsHeader), u64p, u32p, u32p,
                                 C.c_uint64, C.c_int]),
     "nd_feds_read_header": (C.c_int, [C.c_char_p, C.POINTER(NdFedsHeader)]),

@@ -486,6 +486,10 @@ int parse_jsonl_line_fast(std::string_view line, const std::string& field, std::
 int parse_jsonl_line(std::string_view line, const std::string& field, std::string& text) {
   const int r = parse_jsonl_line_fast(line, field, text, nullptr);
   if (r >= 0) return r;
+  return parse_jsonl_line_nlohmann(line, field, text);
+}
+
+int parse_jsonl_line_nlohmann(std::string_view line, const std::string& field, std::string& text) {
   FieldSax h;
   h.field = &field;
   h.text = &text;

@@ -73,6 +73,7 @@ bool nfc_normalize_into(std::string_view in, std::string& out);
 std::string nfc_normalize(std::string_view in);
 uint64_t codepoint_count(std::string_view t);
 int parse_jsonl_line(std::string_view line, const std::string& field, std::string& text);
+int parse_jsonl_line_nlohmann(std::string_view line, const std::string& field, std::string& text);
 // strict-subset fast path; -1 = undecided (use parse_jsonl_line)
 int parse_jsonl_line_fast(std::string_view line, const std::string& field, std::string& text,
                           bool* ascii);

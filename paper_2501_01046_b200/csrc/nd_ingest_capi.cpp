@@ -95,9 +95,26 @@ uint64_t nd_codepoint_count(const uint8_t* s, uint64_t len) {
 
 int nd_parse_jsonl_line(const char* line, uint64_t len, const char* field, uint32_t* reason,
                         uint8_t* text_out, uint64_t cap, uint64_t* text_len) {
+  return nd_parse_jsonl_line_mode(line, len, field, 0, reason, text_out, cap, text_len);
+}
+
+int nd_parse_jsonl_line_mode(const char* line, uint64_t len, const char* field, int mode,
+                             uint32_t* reason, uint8_t* text_out, uint64_t cap,
+                             uint64_t* text_len) {
   return guarded([&] {
     std::string t;
-    *reason = static_cast<uint32_t>(ndb::parse_jsonl_line(std::string_view(line, len), field, t));
+    const std::string f(field);
+    const std::string_view v(line, len);
+    int r;
+    if (mode == 2) {
+      r = ndb::parse_jsonl_line_fast(v, f, t, nullptr);
+      if (r < 0) r = 255;
+    } else if (mode == 1) {
+      r = ndb::parse_jsonl_line_nlohmann(v, f, t);
+    } else {
+      r = ndb::parse_jsonl_line(v, f, t);
+    }
+    *reason = static_cast<uint32_t>(r);
     *text_len = t.size();
     if (text_out && cap >= t.size() && !t.empty()) std::memcpy(text_out, t.data(), t.size());
   });

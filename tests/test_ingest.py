@@ -136,3 +136,63 @@ def test_loader_normalises_and_is_thread_invariant(tmp_path):
     assert got == want
     assert chars.tolist() == [len(w) for w in want]
     assert ids[0] == 7
+
+
+def _parse(line: bytes, mode: int, field=b"text"):
+    import ctypes as C
+
+    from paper_2501_01046_b200 import _lib
+
+    lib = _lib.load()
+    reason, n = C.c_uint32(), C.c_uint64()
+    out = (C.c_uint8 * (len(line) + 8))()
+    assert lib.nd_parse_jsonl_line_mode(line, len(line), field, mode, C.byref(reason), out,
+                                        len(out), C.byref(n)) == 0
+    return reason.value, bytes(out[:n.value]) if reason.value == 0 else None
+
+
+def test_fast_scanner_agrees_with_nlohmann():
+    # differential fuzz: the fast scanner either defers (255) or gives exactly
+    # nlohmann's verdict and text, on valid lines and on byte-level mutations
+    rng = np.random.default_rng(13)
+    atoms = [b'"x"', b'""', b'"a\\"b\\\\c\\/d\\n\\t"', b'"\\u00e9"', b'"\\ud83d\\ude00"', b'"\\ud800"',
+             b'"caf\xc3\xa9"', b'"\xe2\x82"', b'"\xff"', b'0', b'-0', b'12', b'-7', b'01', b'1.5',
+             b'1e3', b'123456789012345678', b'1234567890123456789', b'true', b'false', b'null',
+             b'tru', b'[]', b'{}', b'[1, 2]', b'{"a": [1, {"text": 2}]}', b'"\x7f"', b'"\x01"']
+
+    def value(d):
+        k = rng.integers(0, 10)
+        if d < 3 and k == 0:
+            return b"[" + b", ".join(value(d + 1) for _ in range(rng.integers(0, 3))) + b"]"
+        if d < 3 and k == 1:
+            return obj(d + 1)
+        return atoms[int(rng.integers(len(atoms)))]
+
+    def obj(d):
+        keys = [b'"text"', b'"id"', b'"t"', b'"text "', b'"te\\u0078t"']
+        items = [keys[int(rng.integers(len(keys)))] + b": " + value(d) for _ in range(rng.integers(0, 4))]
+        return b"{" + b", ".join(items) + b"}"
+
+    decided = 0
+    for _ in range(20000):
+        line = obj(0) if rng.random() < 0.85 else value(0)
+        if rng.random() < 0.5:  # mutate
+            b = bytearray(line)
+            for _ in range(int(rng.integers(1, 4))):
+                op, pos = rng.integers(0, 3), int(rng.integers(0, len(b) + 1))
+                if op == 0 and pos < len(b):
+                    del b[pos]
+                elif op == 1:
+                    b.insert(pos, int(rng.choice(list(b' {}[]",:\\\x00\x80\xc3ae0-'))))
+                elif pos < len(b):
+                    b[pos] = int(rng.integers(0, 256))
+            line = bytes(b)
+        if rng.random() < 0.1:
+            line = b" \t" + line + b" \r"
+        fast = _parse(line, 2)
+        ref = _parse(line, 1)
+        assert _parse(line, 0) == ref, line
+        if fast[0] != 255:
+            decided += 1
+            assert fast == ref, line
+    assert decided > 5000
