@@ -49,6 +49,7 @@
 // shared memory as (byte, float) pairs and read back as broadcast LDS.
 // Documents longer than kSeg windows are split into several work items that
 // meet through atomicMin; their band keys come from a follow-up pass.
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -63,10 +64,13 @@ namespace {
 #ifndef ND_K1_MINBLOCKS
 #define ND_K1_MINBLOCKS 0  // 0: no min-blocks hint (ptxas chose 96 registers)
 #endif
+// resident blocks per SM the register allocation must allow: the fq kernel
+// with 8 functions per lane fits 96 registers (5 blocks of 4 warps); the
+// persistent item loop would otherwise let ptxas take 128 (4 blocks)
 #if ND_K1_MINBLOCKS > 0
 #define ND_K1_BOUNDS __launch_bounds__(ND_K1_WARPS * 32, ND_K1_MINBLOCKS)
 #else
-#define ND_K1_BOUNDS __launch_bounds__(ND_K1_WARPS * 32)
+#define ND_K1_BOUNDS __launch_bounds__(ND_K1_WARPS * 32, k1_min_blocks(A, F))
 #endif
 #ifndef ND_K1_UNROLL4
 #define ND_K1_UNROLL4 1
@@ -152,6 +156,12 @@ __global__ void k_bands_from_rows(const uint32_t* __restrict__ docs, uint32_t nd
 
 // ---------------------------------------------------------------------------
 enum class Arith { kInt, kFq, kWide };
+// register caps (blocks of 4 warps per SM) that reproduce the allocation of
+// the one-item-per-warp kernel: fq F=4/8/16 -> 80/96/168 registers, int and
+// wide F<=4/8/16 -> 64/80/128
+__host__ __device__ constexpr int k1_min_blocks(Arith a, int f) {
+  return a == Arith::kFq ? (f <= 4 ? 6 : f <= 8 ? 5 : 3) : (f <= 4 ? 8 : f <= 8 ? 6 : 4);
+}
 
 template <Arith A, int F>
 struct Consts;
@@ -260,27 +270,21 @@ struct Consts<Arith::kFq, F> {
   }
 };
 
+// One work item (a document, or an 8192-window segment of a long one) for one
+// warp; `item` is warp-uniform.
 template <Arith A, int F, int Z, class T>
-__global__ void ND_K1_BOUNDS
-    k_signature(const T* __restrict__ text, const uint64_t* __restrict__ offsets,
-                const uint32_t* __restrict__ item_doc, const uint64_t* __restrict__ item_off,
-                uint64_t n_items, FamPtrs fam, uint32_t L, uint32_t H, uint32_t bands,
-                uint32_t rows, uint32_t K, uint32_t* __restrict__ sig,
-                uint32_t* __restrict__ band) {
+__device__ __forceinline__ void k1_item(
+    uint64_t item, const T* __restrict__ text, const uint64_t* __restrict__ offsets,
+    const uint32_t* __restrict__ item_doc, const uint64_t* __restrict__ item_off,
+    const FamPtrs& fam, uint32_t L, uint32_t H, uint32_t bands, uint32_t rows, uint32_t K,
+    uint32_t* __restrict__ sig, uint32_t* __restrict__ band, uint2 (*sbuf)[kLMax + chunk_for(Z)],
+    uint32_t (*sbuf256)[kLMax + chunk_for(Z)], uint32_t* srow) {
   constexpr int G = 32 / Z;  // lanes per group
-  constexpr int Hp = G * F;
   constexpr int kChunk = chunk_for(Z);
-  constexpr int kBuf = kChunk + kLMax;
-  __shared__ __align__(16) uint2 sbuf[kWarps][Z][kBuf];
-  __shared__ __align__(16) uint32_t sbuf256[kWarps][Z][kBuf];
-  __shared__ __align__(16) uint32_t srow[kWarps][Hp];
-  const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int grp = lane / G;
   const int gl = lane % G;
   const unsigned gmask = Z == 1 ? 0xFFFFFFFFu : (((1u << G) - 1u) << (grp * G));
-  const uint64_t item = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
-  if (item >= n_items) return;
 
   uint64_t doc = item;
   uint64_t ws = 0;
@@ -311,8 +315,8 @@ __global__ void ND_K1_BOUNDS
     mn[f] = 0xFFFFFFFFu;
   }
 
-  uint2* buf = sbuf[warp][grp];
-  uint32_t* buf256 = sbuf256[warp][grp];
+  uint2* buf = sbuf[grp];
+  uint32_t* buf256 = sbuf256[grp];
   uint64_t p_hi = ge > gs ? e : gs;  // positions [p_lo, p_hi) per chunk, descending
   bool first = true;
   while (p_hi > gs) {
@@ -424,7 +428,7 @@ __global__ void ND_K1_BOUNDS
       if (fbase + f < static_cast<int>(H)) out[fbase + f] = mn[f];
   }
   if (band == nullptr) return;
-  uint32_t* row = srow[warp];
+  uint32_t* row = srow;
 #pragma unroll
   for (int f = 0; f < F; ++f) row[fbase + f] = mn[f];
   __syncwarp(gmask);
@@ -435,21 +439,74 @@ __global__ void ND_K1_BOUNDS
   }
 }
 
+// next_item == nullptr: one item per warp (grid = items / kWarps).  Otherwise
+// persistent: a grid of resident blocks whose warps pull items from a global
+// counter, so a block is never held by one long item while its other warps
+// idle (lognormal lengths) and no block slot waits for a straggler.
+template <Arith A, int F, int Z, class T>
+__global__ void ND_K1_BOUNDS
+    k_signature(const T* __restrict__ text, const uint64_t* __restrict__ offsets,
+                const uint32_t* __restrict__ item_doc, const uint64_t* __restrict__ item_off,
+                uint64_t n_items, FamPtrs fam, uint32_t L, uint32_t H, uint32_t bands,
+                uint32_t rows, uint32_t K, uint32_t* __restrict__ sig,
+                uint32_t* __restrict__ band, unsigned long long* __restrict__ next_item) {
+  constexpr int G = 32 / Z;  // lanes per group
+  constexpr int Hp = G * F;
+  constexpr int kBuf = chunk_for(Z) + kLMax;
+  __shared__ __align__(16) uint2 sbuf[kWarps][Z][kBuf];
+  __shared__ __align__(16) uint32_t sbuf256[kWarps][Z][kBuf];
+  __shared__ __align__(16) uint32_t srow[kWarps][Hp];
+  const int warp = threadIdx.x >> 5;
+  if (next_item == nullptr) {
+    const uint64_t item = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
+    if (item < n_items)
+      k1_item<A, F, Z, T>(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K, sig,
+                          band, sbuf[warp], sbuf256[warp], srow[warp]);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(next_item, 1ull);
+    item = __shfl_sync(0xFFFFFFFFu, item, 0);
+    if (item >= n_items) break;
+    k1_item<A, F, Z, T>(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K, sig,
+                        band, sbuf[warp], sbuf256[warp], srow[warp]);
+    __syncwarp();
+  }
+}
+
 template <Arith A, int F, int Z, class T = uint8_t>
 void launch_k1(const DevFamily& fam, const void* d_text, const uint64_t* d_offsets,
                const uint32_t* item_doc, const uint64_t* item_off, uint64_t items, uint32_t bands,
-               uint32_t rows, uint32_t K, uint32_t* d_sig, uint32_t* d_band, cudaStream_t s) {
+               uint32_t rows, uint32_t K, uint32_t* d_sig, uint32_t* d_band,
+               unsigned long long* counter, cudaStream_t s) {
   FamPtrs p{fam.q, fam.qln, fam.m, fam.negp, fam.c3, fam.qp, fam.qlnp, fam.c1e, fam.m45};
   uint64_t blocks = (items + kWarps - 1) / kWarps;
+  if (counter) {  // persistent: resident blocks only
+    static int per_sm = -1;
+    if (per_sm < 0) {
+      ND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_signature<A, F, Z, T>,
+                                                            kWarps * 32, 0));
+      per_sm = std::max(per_sm, 1);
+    }
+    const uint64_t resident = static_cast<uint64_t>(per_sm) * sm_count();
+    if (blocks > resident) {
+      blocks = resident;
+      ND_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
+    } else {
+      counter = nullptr;  // one wave anyway
+    }
+  }
   k_signature<A, F, Z, T><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
-      static_cast<const T*>(d_text), d_offsets, item_doc, item_off, items, p, fam.L, fam.H, bands, rows, K, d_sig,
-      d_band);
+      static_cast<const T*>(d_text), d_offsets, item_doc, item_off, items, p, fam.L, fam.H, bands,
+      rows, K, d_sig, d_band, counter);
   ND_CHECK_LAUNCH();
 }
 
 using Launcher = void (*)(const DevFamily&, const void*, const uint64_t*, const uint32_t*,
                           const uint64_t*, uint64_t, uint32_t, uint32_t, uint32_t, uint32_t*,
-                          uint32_t*, cudaStream_t);
+                          uint32_t*, unsigned long long*, cudaStream_t);
 
 // (arith, Hp) -> instantiation; F = functions per lane, Z = window slices per
 // warp.  ND_K1_FZ="F,Z" overrides the default shape (tuning experiments).
@@ -567,7 +624,13 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   }();
   Launcher go = pick_launcher(int_arith, fam.Hp, fam.unit == 1);
   if (!go) fail(ND_ERR_CONFIG, "hash count must be at most 512 on the GPU path");
-  go(fam, d_text, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, s);
+  static const bool persistent = [] {
+    const char* v = getenv("ND_K1_PERSISTENT");
+    return !(v && std::string(v) == "0");
+  }();
+  unsigned long long* counter =
+      persistent ? sc.item_counter.as<unsigned long long>(1) : nullptr;
+  go(fam, d_text, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, counter, s);
   if (nmulti && d_band) {
     uint64_t total = static_cast<uint64_t>(nmulti) * bands;
     k_bands_from_rows<<<static_cast<unsigned>((total + tb - 1) / tb), tb, 0, s>>>(

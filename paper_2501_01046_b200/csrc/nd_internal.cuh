@@ -100,10 +100,11 @@ struct PinnedBuf {
 // K1: signatures + band keys over device-resident packed text.
 // Returns ND_ERR_SHORT through the flag buffer when a document has no window.
 struct SigScratch {
-  DevBuf seg_count, item_off, item_doc, flags, multi_docs, scan_tmp, units, unit_off, unit_cnt;
+  DevBuf seg_count, item_off, item_doc, flags, multi_docs, scan_tmp, units, unit_off, unit_cnt,
+      item_counter;
   void release() {
     for (DevBuf* b : {&seg_count, &item_off, &item_doc, &flags, &multi_docs, &scan_tmp, &units,
-                      &unit_off, &unit_cnt})
+                      &unit_off, &unit_cnt, &item_counter})
       b->release();
   }
 };
