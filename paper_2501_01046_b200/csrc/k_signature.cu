@@ -439,11 +439,165 @@ __device__ __forceinline__ void k1_item(
   }
 }
 
+// Dual-slice variant (fq arithmetic, byte units, all 32 lanes on one slice
+// set): lane l owns functions [l*F, l*F+F) and walks TWO slices of the
+// item's windows, A = the first ceil(span/2) windows and B = the last
+// ceil(span/2) (they overlap by at most one window, which the min absorbs),
+// stepping both in lockstep.  The two rolls of a function read the same
+// constant registers back to back (operand reuse) and are independent (ILP),
+// so a lane needs F*6 constant registers for 2F chains instead of 2F*6.
+template <int F>
+__device__ __forceinline__ void k1_item_dual(
+    uint64_t item, const uint8_t* __restrict__ text, const uint64_t* __restrict__ offsets,
+    const uint32_t* __restrict__ item_doc, const uint64_t* __restrict__ item_off,
+    const FamPtrs& fam, uint32_t L, uint32_t H, uint32_t bands, uint32_t rows, uint32_t K,
+    uint32_t* __restrict__ sig, uint32_t* __restrict__ band, uint2 (*sbuf)[kLMax + 128],
+    uint32_t (*sbuf256)[kLMax + 128], uint32_t* srow) {
+  constexpr int kChunk = 128;
+  const int lane = threadIdx.x & 31;
+  uint64_t doc = item;
+  uint64_t ws = 0;
+  bool multi = false;
+  if (item_doc) {
+    doc = item_doc[item];
+    const uint64_t seg = item - item_off[doc];
+    multi = item_off[doc + 1] - item_off[doc] > 1;
+    ws = seg * kSeg;
+  }
+  const uint64_t off = offsets[doc];
+  const uint64_t len = offsets[doc + 1] - off;
+  const uint64_t nwin = len - L + 1;
+  const uint64_t item_end = min(ws + kSeg, nwin);
+  const uint64_t S = (item_end - ws + 1) / 2;      // windows per slice
+  const uint8_t* baseA = text + off + ws;          // slice A starts at window ws
+  const uint8_t* baseB = text + off + item_end - S;  // slice B ends at the item's end
+  const uint64_t total = S + L - 1;                // positions per slice
+
+  Consts<Arith::kFq, F> k;
+  k.load(fam, lane * F);
+  uint32_t sa[F], sb[F], mn[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+    sa[f] = 0;
+    sb[f] = 0;
+    mn[f] = 0xFFFFFFFFu;
+  }
+  uint2* bufA = sbuf[0];
+  uint2* bufB = sbuf[1];
+  uint32_t* bufA256 = sbuf256[0];
+  uint32_t* bufB256 = sbuf256[1];
+  uint64_t p_hi = total;
+  bool first = true;
+  while (p_hi > 0) {
+    const uint64_t p_lo = p_hi > kChunk ? p_hi - kChunk : 0;
+    const int cnt = static_cast<int>(p_hi - p_lo);
+    for (int j = lane; j < cnt + static_cast<int>(L); j += 32) {
+      const uint64_t pos = p_lo + j;
+      const uint32_t ca = pos < total ? baseA[pos] : 0u;
+      const uint32_t cb = pos < total ? baseB[pos] : 0u;
+      bufA[j] = make_uint2(ca, __float_as_uint(static_cast<float>(ca)));
+      bufB[j] = make_uint2(cb, __float_as_uint(static_cast<float>(cb)));
+      bufA256[j] = ca << 8;
+      bufB256[j] = cb << 8;
+    }
+    __syncwarp();
+    int j = cnt - 1;
+    if (first) {  // L-1 warm-up positions: partial windows, not part of the minimum
+      for (int w = 0; w < static_cast<int>(L) - 1; ++w, --j) {
+        const uint2 oa = bufA[j + L], ob = bufB[j + L];
+        const uint32_t ca = bufA256[j], cb = bufB256[j];
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          sa[f] = k.roll(f, sa[f], ca, oa.x, __uint_as_float(oa.y));
+          sb[f] = k.roll(f, sb[f], cb, ob.x, __uint_as_float(ob.y));
+        }
+      }
+      first = false;
+    }
+    for (; j >= 1; j -= 2) {
+      const uint2 oa0 = bufA[j + L], oa1 = bufA[j - 1 + L];
+      const uint2 ob0 = bufB[j + L], ob1 = bufB[j - 1 + L];
+      const uint32_t ca0 = bufA256[j], ca1 = bufA256[j - 1];
+      const uint32_t cb0 = bufB256[j], cb1 = bufB256[j - 1];
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const uint32_t a0 = k.roll(f, sa[f], ca0, oa0.x, __uint_as_float(oa0.y));
+        const uint32_t b0 = k.roll(f, sb[f], cb0, ob0.x, __uint_as_float(ob0.y));
+        const uint32_t a1 = k.roll(f, a0, ca1, oa1.x, __uint_as_float(oa1.y));
+        const uint32_t b1 = k.roll(f, b0, cb1, ob1.x, __uint_as_float(ob1.y));
+        sa[f] = a1;
+        sb[f] = b1;
+        mn[f] = __vimin3_u32(mn[f], a0, a1);
+        mn[f] = __vimin3_u32(mn[f], b0, b1);
+      }
+    }
+    if (j == 0) {
+      const uint2 oa = bufA[L], ob = bufB[L];
+      const uint32_t ca = bufA256[0], cb = bufB256[0];
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        sa[f] = k.roll(f, sa[f], ca, oa.x, __uint_as_float(oa.y));
+        sb[f] = k.roll(f, sb[f], cb, ob.x, __uint_as_float(ob.y));
+        mn[f] = __vimin3_u32(mn[f], sa[f], sb[f]);
+      }
+    }
+    __syncwarp();
+    p_hi = p_lo;
+  }
+#pragma unroll
+  for (int f = 0; f < F; ++f) mn[f] >>= 8;  // scaled state -> canonical value
+  uint32_t* out = sig + doc * H;
+  const int fbase = lane * F;
+  if (multi) {
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+      if (fbase + f < static_cast<int>(H)) atomicMin(out + fbase + f, mn[f]);
+    return;
+  }
+  if ((H % 4) == 0 && (F % 4) == 0 && fbase + F <= static_cast<int>(H)) {
+#pragma unroll
+    for (int f = 0; f < F; f += 4)
+      *reinterpret_cast<uint4*>(out + fbase + f) = make_uint4(mn[f], mn[f + 1], mn[f + 2], mn[f + 3]);
+  } else {
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+      if (fbase + f < static_cast<int>(H)) out[fbase + f] = mn[f];
+  }
+  if (band == nullptr) return;
+#pragma unroll
+  for (int f = 0; f < F; ++f) srow[fbase + f] = mn[f];
+  __syncwarp();
+  for (uint32_t jb = lane; jb < bands; jb += 32) {
+    uint64_t sum = 0;
+    for (uint32_t r = 0; r < rows; ++r) sum += srow[jb * rows + r];
+    band[doc * bands + jb] = K ? static_cast<uint32_t>(sum % K) : static_cast<uint32_t>(sum);
+  }
+}
+
+template <Arith A, int F, int Z, class T, int SL>
+struct K1Item {
+  static __device__ __forceinline__ void run(
+      uint64_t item, const T* text, const uint64_t* offsets, const uint32_t* item_doc,
+      const uint64_t* item_off, const FamPtrs& fam, uint32_t L, uint32_t H, uint32_t bands,
+      uint32_t rows, uint32_t K, uint32_t* sig, uint32_t* band, uint2 (*sbuf)[kLMax + chunk_for(Z)],
+      uint32_t (*sbuf256)[kLMax + chunk_for(Z)], uint32_t* srow) {
+    if constexpr (SL == 2) {
+      static_assert(A == Arith::kFq && Z == 1 && chunk_for(Z) == 256, "dual-slice layout");
+      k1_item_dual<F>(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K, sig, band,
+                      reinterpret_cast<uint2(*)[kLMax + 128]>(sbuf),
+                      reinterpret_cast<uint32_t(*)[kLMax + 128]>(sbuf256), srow);
+    } else {
+      k1_item<A, F, Z, T>(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K, sig,
+                          band, sbuf, sbuf256, srow);
+    }
+  }
+};
+
 // next_item == nullptr: one item per warp (grid = items / kWarps).  Otherwise
 // persistent: a grid of resident blocks whose warps pull items from a global
 // counter, so a block is never held by one long item while its other warps
 // idle (lognormal lengths) and no block slot waits for a straggler.
-template <Arith A, int F, int Z, class T>
+template <Arith A, int F, int Z, class T, int SL>
 __global__ void ND_K1_BOUNDS
     k_signature(const T* __restrict__ text, const uint64_t* __restrict__ offsets,
                 const uint32_t* __restrict__ item_doc, const uint64_t* __restrict__ item_off,
@@ -453,15 +607,16 @@ __global__ void ND_K1_BOUNDS
   constexpr int G = 32 / Z;  // lanes per group
   constexpr int Hp = G * F;
   constexpr int kBuf = chunk_for(Z) + kLMax;
-  __shared__ __align__(16) uint2 sbuf[kWarps][Z][kBuf];
-  __shared__ __align__(16) uint32_t sbuf256[kWarps][Z][kBuf];
+  constexpr int kSlots = Z > SL ? Z : SL;  // staging buffers per warp
+  __shared__ __align__(16) uint2 sbuf[kWarps][kSlots][kBuf];
+  __shared__ __align__(16) uint32_t sbuf256[kWarps][kSlots][kBuf];
   __shared__ __align__(16) uint32_t srow[kWarps][Hp];
   const int warp = threadIdx.x >> 5;
   if (next_item == nullptr) {
     const uint64_t item = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
     if (item < n_items)
-      k1_item<A, F, Z, T>(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K, sig,
-                          band, sbuf[warp], sbuf256[warp], srow[warp]);
+      K1Item<A, F, Z, T, SL>::run(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows,
+                                  K, sig, band, sbuf[warp], sbuf256[warp], srow[warp]);
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -470,13 +625,13 @@ __global__ void ND_K1_BOUNDS
     if (lane == 0) item = atomicAdd(next_item, 1ull);
     item = __shfl_sync(0xFFFFFFFFu, item, 0);
     if (item >= n_items) break;
-    k1_item<A, F, Z, T>(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K, sig,
-                        band, sbuf[warp], sbuf256[warp], srow[warp]);
+    K1Item<A, F, Z, T, SL>::run(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K,
+                                sig, band, sbuf[warp], sbuf256[warp], srow[warp]);
     __syncwarp();
   }
 }
 
-template <Arith A, int F, int Z, class T = uint8_t>
+template <Arith A, int F, int Z, class T = uint8_t, int SL = 1>
 void launch_k1(const DevFamily& fam, const void* d_text, const uint64_t* d_offsets,
                const uint32_t* item_doc, const uint64_t* item_off, uint64_t items, uint32_t bands,
                uint32_t rows, uint32_t K, uint32_t* d_sig, uint32_t* d_band,
@@ -486,7 +641,7 @@ void launch_k1(const DevFamily& fam, const void* d_text, const uint64_t* d_offse
   if (counter) {  // persistent: resident blocks only
     static int per_sm = -1;
     if (per_sm < 0) {
-      ND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_signature<A, F, Z, T>,
+      ND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_signature<A, F, Z, T, SL>,
                                                             kWarps * 32, 0));
       per_sm = std::max(per_sm, 1);
     }
@@ -498,7 +653,7 @@ void launch_k1(const DevFamily& fam, const void* d_text, const uint64_t* d_offse
       counter = nullptr;  // one wave anyway
     }
   }
-  k_signature<A, F, Z, T><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
+  k_signature<A, F, Z, T, SL><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
       static_cast<const T*>(d_text), d_offsets, item_doc, item_off, items, p, fam.L, fam.H, bands,
       rows, K, d_sig, d_band, counter);
   ND_CHECK_LAUNCH();
@@ -530,6 +685,11 @@ Launcher pick_launcher(bool int_arith, uint32_t Hp, bool codepoint) {
       case 512: return launch_k1<Arith::kInt, 16, 1>;
     }
     return nullptr;
+  }
+  const char* dual = getenv("ND_K1_DUAL");
+  if (dual && std::string(dual) == "1") {
+    if (Hp == 128) return launch_k1<Arith::kFq, 4, 1, uint8_t, 2>;
+    if (Hp == 256) return launch_k1<Arith::kFq, 8, 1, uint8_t, 2>;
   }
   const char* fz = getenv("ND_K1_FZ");
   if (fz && Hp == 128) {
@@ -626,7 +786,7 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   if (!go) fail(ND_ERR_CONFIG, "hash count must be at most 512 on the GPU path");
   static const bool persistent = [] {
     const char* v = getenv("ND_K1_PERSISTENT");
-    return !(v && std::string(v) == "0");
+    return v && std::string(v) == "1";  // measured slower on C2 and C5
   }();
   unsigned long long* counter =
       persistent ? sc.item_counter.as<unsigned long long>(1) : nullptr;

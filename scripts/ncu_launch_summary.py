@@ -20,7 +20,8 @@ for r in rows[1:]:
     name = re.sub(r"ndb::", "", name)
     v = float(r[ix["Metric Value"]].replace(",", ""))
     unit = r[ix["Metric Unit"]]
-    scale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "byte": 1, "Kbyte": 1e3,
+    scale = {"ns": 1e-9, "us": 1e-6, "ms": 1e-3, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+             "second": 1.0, "s": 1.0, "byte": 1, "Kbyte": 1e3,
              "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1.0)
     d = launch.setdefault(lid, {"name": name})
     d[r[ix["Metric Name"]]] = v * scale
