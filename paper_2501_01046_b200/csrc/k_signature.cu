@@ -70,7 +70,7 @@ namespace {
 #if ND_K1_MINBLOCKS > 0
 #define ND_K1_BOUNDS __launch_bounds__(ND_K1_WARPS * 32, ND_K1_MINBLOCKS)
 #else
-#define ND_K1_BOUNDS __launch_bounds__(ND_K1_WARPS * 32, k1_min_blocks(A, F))
+#define ND_K1_BOUNDS __launch_bounds__(ND_K1_WARPS * 32, k1_min_blocks(A, F, SL))
 #endif
 #ifndef ND_K1_UNROLL4
 #define ND_K1_UNROLL4 1
@@ -159,8 +159,9 @@ enum class Arith { kInt, kFq, kWide };
 // register caps (blocks of 4 warps per SM) that reproduce the allocation of
 // the one-item-per-warp kernel: fq F=4/8/16 -> 80/96/168 registers, int and
 // wide F<=4/8/16 -> 64/80/128
-__host__ __device__ constexpr int k1_min_blocks(Arith a, int f) {
-  return a == Arith::kFq ? (f <= 4 ? 6 : f <= 8 ? 5 : 3) : (f <= 4 ? 8 : f <= 8 ? 6 : 4);
+__host__ __device__ constexpr int k1_min_blocks(Arith a, int f, int sl = 1) {
+  return sl == 2 ? (f <= 4 ? 6 : 4)
+                 : a == Arith::kFq ? (f <= 4 ? 6 : f <= 8 ? 5 : 3) : (f <= 4 ? 8 : f <= 8 ? 6 : 4);
 }
 
 template <Arith A, int F>
@@ -620,14 +621,18 @@ __global__ void ND_K1_BOUNDS
     return;
   }
   const int lane = threadIdx.x & 31;
-  for (;;) {
-    unsigned long long item = 0;
-    if (lane == 0) item = atomicAdd(next_item, 1ull);
-    item = __shfl_sync(0xFFFFFFFFu, item, 0);
-    if (item >= n_items) break;
+  unsigned long long item = 0;
+  if (lane == 0) item = atomicAdd(next_item, 1ull);
+  item = __shfl_sync(0xFFFFFFFFu, item, 0);
+  while (item < n_items) {
+    // claim the next item before working on this one: the atomic's round trip
+    // overlaps the item instead of idling the warp between items
+    unsigned long long next = 0;
+    if (lane == 0) next = atomicAdd(next_item, 1ull);
     K1Item<A, F, Z, T, SL>::run(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K,
                                 sig, band, sbuf[warp], sbuf256[warp], srow[warp]);
     __syncwarp();
+    item = __shfl_sync(0xFFFFFFFFu, next, 0);
   }
 }
 
@@ -687,10 +692,9 @@ Launcher pick_launcher(bool int_arith, uint32_t Hp, bool codepoint) {
     return nullptr;
   }
   const char* dual = getenv("ND_K1_DUAL");
-  if (dual && std::string(dual) == "1") {
-    if (Hp == 128) return launch_k1<Arith::kFq, 4, 1, uint8_t, 2>;
-    if (Hp == 256) return launch_k1<Arith::kFq, 8, 1, uint8_t, 2>;
-  }
+  const bool dual_on = !(dual && std::string(dual) == "0");
+  if (dual_on && Hp == 128) return launch_k1<Arith::kFq, 4, 1, uint8_t, 2>;
+  if (dual && std::string(dual) == "1" && Hp == 256) return launch_k1<Arith::kFq, 8, 1, uint8_t, 2>;
   const char* fz = getenv("ND_K1_FZ");
   if (fz && Hp == 128) {
     std::string v(fz);
@@ -786,7 +790,7 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   if (!go) fail(ND_ERR_CONFIG, "hash count must be at most 512 on the GPU path");
   static const bool persistent = [] {
     const char* v = getenv("ND_K1_PERSISTENT");
-    return v && std::string(v) == "1";  // measured slower on C2 and C5
+    return !(v && std::string(v) == "0");
   }();
   unsigned long long* counter =
       persistent ? sc.item_counter.as<unsigned long long>(1) : nullptr;
