@@ -694,7 +694,7 @@ Launcher pick_launcher(bool int_arith, uint32_t Hp, bool codepoint) {
   const char* dual = getenv("ND_K1_DUAL");
   const bool dual_on = !(dual && std::string(dual) == "0");
   if (dual_on && Hp == 128) return launch_k1<Arith::kFq, 4, 1, uint8_t, 2>;
-  if (dual && std::string(dual) == "1" && Hp == 256) return launch_k1<Arith::kFq, 8, 1, uint8_t, 2>;
+  if (dual_on && Hp == 256) return launch_k1<Arith::kFq, 8, 1, uint8_t, 2>;
   const char* fz = getenv("ND_K1_FZ");
   if (fz && Hp == 128) {
     std::string v(fz);
