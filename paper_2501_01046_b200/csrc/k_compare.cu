@@ -20,6 +20,8 @@
 // indices packed as lo << nb | hi so that sort + unique (compare.cpp:77-84)
 // is a single radix sort over 2*nb bits.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "nd_internal.cuh"
 
@@ -335,6 +337,157 @@ __global__ void __launch_bounds__(kJoinThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pigeonhole hash join (the default for cells of up to kJoinMax documents).
+//
+// With A = H - min_matches allowed mismatches, take NB = A + 1 disjoint blocks
+// of BW consecutive positions (NB * BW <= H).  An acceptable pair spoils at
+// most A blocks, so it agrees on EVERY position of at least one block: the
+// pairs worth counting are the pairs with an identical block k < NB.  Per
+// block, one hash table keyed by a 23-bit fingerprint of the block's BW values
+// chains the documents of the cell; each chained pair is checked by one
+// thread -- block k really identical (fingerprints may collide), no identical
+// block before k (so each pair is counted once per cell), then the exact
+// early-exit count (oracle.cpp:81-92).  With BW = 1 this is the per-position
+// join above; with BW = 4 a random pair shares a block with probability ~q^4
+// instead of ~q per position (q = chance two minima coincide, ~1/3000 here),
+// which removes almost all spurious candidates.
+template <int BW>
+__device__ __forceinline__ void load_block(const uint32_t* __restrict__ p, bool vec, uint32_t (&v)[BW]) {
+  if constexpr (BW % 4 == 0) {
+    if (vec) {
+#pragma unroll
+      for (int q = 0; q < BW / 4; ++q) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(p) + q);
+        v[4 * q] = x.x;
+        v[4 * q + 1] = x.y;
+        v[4 * q + 2] = x.z;
+        v[4 * q + 3] = x.w;
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < BW; ++t) v[t] = __ldg(p + t);
+}
+
+template <int BW>
+__device__ __forceinline__ uint32_t block_fp(const uint32_t (&v)[BW]) {
+  uint32_t h = 0x9E3779B9u;
+#pragma unroll
+  for (int t = 0; t < BW; ++t) {
+    h = (h ^ v[t]) * 0x85EBCA6Bu;
+    h ^= h >> 15;
+  }
+  return h & 0x7FFFFFu;
+}
+
+template <int BW>
+__device__ __forceinline__ bool same_block(const uint32_t* __restrict__ a,
+                                           const uint32_t* __restrict__ b, bool vec) {
+  uint32_t x[BW], y[BW];
+  load_block<BW>(a, vec, x);
+  load_block<BW>(b, vec, y);
+  bool eq = true;
+#pragma unroll
+  for (int t = 0; t < BW; ++t) eq &= x[t] == y[t];
+  return eq;
+}
+
+template <int BW>
+__device__ __forceinline__ void join_check_blocks(const uint32_t* __restrict__ sig, uint32_t H,
+                                                  uint32_t ra, uint32_t rb, uint32_t k, bool vec,
+                                                  uint32_t min_match, int nb,
+                                                  uint64_t* __restrict__ out_key,
+                                                  uint32_t* __restrict__ out_m,
+                                                  unsigned long long* __restrict__ count,
+                                                  uint64_t cap) {
+  const uint32_t* a = sig + static_cast<uint64_t>(ra) * H;
+  const uint32_t* b = sig + static_cast<uint64_t>(rb) * H;
+  if (!same_block<BW>(a + k * BW, b + k * BW, vec)) return;  // fingerprint collision
+  for (uint32_t j = 0; j < k; ++j)
+    if (same_block<BW>(a + j * BW, b + j * BW, vec)) return;  // counted at block j
+  bool alive;
+  const uint32_t m = full_matches(a, b, H, H - min_match, alive);
+  if (alive && m >= min_match) emit(ra, rb, m, nb, out_key, out_m, count, cap);
+}
+
+template <int DPT, int BW>
+__global__ void __launch_bounds__(kJoinThreads)
+    k_join_blocks(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
+                  const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
+                  uint32_t join_max, uint32_t tbits, uint32_t NB, uint32_t min_match, int nb,
+                  uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
+                  unsigned long long* __restrict__ count, uint64_t cap) {
+  extern __shared__ uint32_t jsm[];
+  const uint32_t n = cell_len[blockIdx.x];
+  if (n > join_max) return;  // big cells go to k_compare
+  const uint32_t T = 1u << tbits;
+  uint32_t* keys = jsm;                // T   (tag << 23 | fingerprint), tag 0 = empty
+  uint32_t* head = keys + T;           // T   (tag << 16 | doc)
+  uint32_t* next = head + T;           // join_max
+  uint32_t* rowsm = next + join_max;   // join_max
+  const uint64_t s = cell_start[blockIdx.x];
+  for (uint32_t i = threadIdx.x; i < n; i += kJoinThreads) rowsm[i] = rows[s + i];
+  for (uint32_t i = threadIdx.x; i < T; i += kJoinThreads) {
+    keys[i] = 0;
+    head[i] = 0;
+  }
+  __syncthreads();
+  const uint32_t mask = T - 1;
+  const bool vec = (H & 3) == 0;
+  // fingerprints of block 0, then block k+1 is loaded while block k is joined
+  uint32_t fp[DPT];
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const uint32_t d = threadIdx.x + j * kJoinThreads;
+    if (d < n) {
+      uint32_t v[BW];
+      load_block<BW>(sig + static_cast<uint64_t>(rowsm[d]) * H, vec, v);
+      fp[j] = block_fp<BW>(v);
+    }
+  }
+  for (uint32_t k = 0; k < NB; ++k) {
+    const uint32_t tag = k + 1;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const uint32_t d = threadIdx.x + j * kJoinThreads;
+      if (d >= n) break;
+      const uint32_t key = (tag << 23) | fp[j];
+      uint32_t h = (fp[j] * 0x9E3779B1u) >> (32 - tbits);
+      for (;;) {
+        const uint32_t cur = keys[h];
+        if (cur == key) break;
+        if ((cur >> 23) == tag) {  // another fingerprint of this block: probe on
+          h = (h + 1) & mask;
+          continue;
+        }
+        const uint32_t old = atomicCAS(&keys[h], cur, key);
+        if (old == cur || old == key) break;
+      }
+      const uint32_t prev = atomicExch(&head[h], (tag << 16) | d);
+      next[d] = (prev >> 16) == tag ? (prev & 0xFFFFu) : 0xFFFFFFFFu;
+    }
+    if (k + 1 < NB) {
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) {
+        const uint32_t d = threadIdx.x + j * kJoinThreads;
+        if (d < n) {
+          uint32_t v[BW];
+          load_block<BW>(sig + static_cast<uint64_t>(rowsm[d]) * H + (k + 1) * BW, vec, v);
+          fp[j] = block_fp<BW>(v);
+        }
+      }
+    }
+    __syncthreads();
+    for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads)
+      for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e])
+        join_check_blocks<BW>(sig, H, rowsm[d], rowsm[e], k, vec, min_match, nb, out_key, out_m,
+                              count, cap);
+    __syncthreads();
+  }
+}
+
 using CmpFn = void (*)(const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
                        const uint32_t*, const uint32_t*, const uint64_t*, uint32_t, int,
                        uint64_t*, uint32_t*, unsigned long long*, uint64_t);
@@ -356,26 +509,59 @@ void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32
   // cells of <= kJoinMax documents: hash join (one CTA per cell)
   const uint32_t P = H - min_match + 1;
   const uint32_t join_max = static_cast<uint32_t>(std::min<uint64_t>(cs.max_len, kJoinMax));
+  const char* jb = getenv("ND_JOIN_BLOCKS");  // read per call: tests switch it
+  const int join_mode = jb && std::string(jb) == "0" ? 1 : 2;  // 2 = blocks, 1 = per position
+  const uint32_t NB = H - min_match + 1;  // A + 1 blocks
+  int BW = 1;
+  for (int w : {8, 4, 2})
+    if (static_cast<uint64_t>(NB) * w <= H) {
+      BW = w;
+      break;
+    }
   if (join_max >= 2 && P <= 510) {
     uint32_t tbits = 4;
     while ((1u << tbits) < 2 * join_max) ++tbits;
     const size_t smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
-    using JoinFn = void (*)(const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
-                            const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, int,
-                            uint64_t*, uint32_t*, unsigned long long*, uint64_t);
-    JoinFn fn = join_max <= 2 * kJoinThreads   ? k_join<2>
-                : join_max <= 4 * kJoinThreads ? k_join<4>
-                : join_max <= 8 * kJoinThreads ? k_join<8>
-                                               : k_join<16>;
-    static_assert(16 * kJoinThreads >= kJoinMax, "k_join<16> must cover kJoinMax");
-    if (smem > 48 * 1024)
-      ND_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
     if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
-    fn<<<static_cast<unsigned>(cs.ncells), kJoinThreads, smem, s>>>(
-        d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len, join_max, tbits, P, min_match, nb,
-        out_key, out_m, count, cap);
-    ND_CHECK_LAUNCH();
+    const unsigned grid = static_cast<unsigned>(cs.ncells);
+    if (join_mode == 2 && BW > 1) {
+      using JoinBFn = void (*)(const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
+                               const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, int,
+                               uint64_t*, uint32_t*, unsigned long long*, uint64_t);
+      const int dpt = join_max <= 2 * kJoinThreads   ? 2
+                      : join_max <= 4 * kJoinThreads ? 4
+                      : join_max <= 8 * kJoinThreads ? 8
+                                                     : 16;
+      JoinBFn fn = nullptr;
+#define ND_JB(D, W) \
+  if (dpt == D && BW == W) fn = k_join_blocks<D, W>;
+      ND_JB(2, 2) ND_JB(2, 4) ND_JB(2, 8) ND_JB(4, 2) ND_JB(4, 4) ND_JB(4, 8)
+      ND_JB(8, 2) ND_JB(8, 4) ND_JB(8, 8) ND_JB(16, 2) ND_JB(16, 4) ND_JB(16, 8)
+#undef ND_JB
+      if (smem > 48 * 1024)
+        ND_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      fn<<<grid, kJoinThreads, smem, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
+                                          join_max, tbits, NB, min_match, nb, out_key, out_m,
+                                          count, cap);
+      ND_CHECK_LAUNCH();
+    } else {
+      using JoinFn = void (*)(const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
+                              const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, int,
+                              uint64_t*, uint32_t*, unsigned long long*, uint64_t);
+      JoinFn fn = join_max <= 2 * kJoinThreads   ? k_join<2>
+                  : join_max <= 4 * kJoinThreads ? k_join<4>
+                  : join_max <= 8 * kJoinThreads ? k_join<8>
+                                                 : k_join<16>;
+      static_assert(16 * kJoinThreads >= kJoinMax, "k_join<16> must cover kJoinMax");
+      if (smem > 48 * 1024)
+        ND_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      fn<<<grid, kJoinThreads, smem, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
+                                          join_max, tbits, P, min_match, nb, out_key, out_m, count,
+                                          cap);
+      ND_CHECK_LAUNCH();
+    }
   }
   if (cs.items == 0) return;  // no cell above kJoinMax
   CmpFn fn = nullptr;

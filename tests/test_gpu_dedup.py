@@ -358,3 +358,46 @@ def test_codepoint_unit_dedup_byte_identical(ctx, ref, tmp_path):
     assert _files(ws_gpu) == want
     assert json.loads(want["summary.json"])["duplicate_groups"] >= 140
     assert rep.candidate_pairs == json.load(open(os.path.join(ws_ref, "compare_stage.json")))["candidate_pairs"]
+
+
+@pytest.mark.parametrize("H,thr", [(128, (4, 5)), (256, (4, 5)), (128, (9, 10)), (64, (1, 2)),
+                                   (128, (0, 1)), (96, (3, 4))])
+def test_pigeonhole_join_adversarial(ctx, ref, monkeypatch, H, thr):
+    # pairs with close to A = H - min_matches mismatches spread one per block
+    # (as few identical blocks as possible), plus low-entropy values so that
+    # fingerprints and single positions collide a lot; both join modes and the
+    # reference's compare_bucket agree
+    rng = np.random.default_rng(H * 7 + thr[0])
+    n = 220
+    mm = _lib.load().nd_min_matches(H, thr[0], thr[1])
+    A = H - mm
+    NB = A + 1
+    bw = max(w for w in (1, 2, 4, 8) if NB * w <= H) if NB <= H else 1
+    base = rng.integers(0, 1 << 22, size=H).astype(np.uint32)
+    sig = np.empty((n, H), np.uint32)
+    for r in range(n):
+        row = base.copy()
+        kind = r % 3
+        if kind == 0:  # m mismatches, one per block, blocks chosen at random
+            m = int(np.clip(A + rng.integers(-2, 3), 0, H))
+            blocks = rng.permutation(max(NB, 1))[:m] if bw > 1 else rng.permutation(H)[:m]
+            for b in blocks:
+                p = int(b) * bw + int(rng.integers(0, bw)) if bw > 1 else int(b)
+                row[p] = (row[p] + 1 + rng.integers(0, 3)) % (1 << 22)
+            extra = max(0, m - len(blocks))
+            row[rng.choice(H, size=extra, replace=False)] ^= 1
+        elif kind == 1:  # low-entropy values: many equal positions between rows
+            row = rng.integers(0, 6, size=H).astype(np.uint32)
+        else:  # random row
+            row = rng.integers(0, 1 << 22, size=H).astype(np.uint32)
+        sig[r] = row
+    b = GatheredBucket(lsh.BucketKey(0, 0), list(range(n)), sig.reshape(-1))
+    t = SimilarityThreshold(thr)
+    lo, hi, m = ref.compare_cells(sig, np.array([0, n], np.uint64), np.arange(n, dtype=np.uint32),
+                                  *thr)
+    want = [DuplicatePair(int(a), int(c), int(d)) for a, c, d in zip(lo, hi, m)]
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ND_JOIN_BLOCKS", mode)
+        got = compare.compare_bucket(b, H, t, ctx=ctx)
+        assert got == want, (mode, len(got), len(want))
+    assert want
