@@ -419,6 +419,9 @@ __global__ void __launch_bounds__(kJoinThreads)
                   uint32_t join_max, uint32_t tbits, uint32_t NB, uint32_t min_match, int nb,
                   uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
                   unsigned long long* __restrict__ count, uint64_t cap) {
+  // one 16-byte load per document covers BPL blocks (BW <= 4); BW = 8 takes two
+  constexpr int BPL = BW >= 4 ? 1 : 4 / BW;
+  constexpr int VL = BW >= 4 ? BW : 4;
   extern __shared__ uint32_t jsm[];
   const uint32_t n = cell_len[blockIdx.x];
   if (n > join_max) return;  // big cells go to k_compare
@@ -436,55 +439,63 @@ __global__ void __launch_bounds__(kJoinThreads)
   __syncthreads();
   const uint32_t mask = T - 1;
   const bool vec = (H & 3) == 0;
-  // fingerprints of block 0, then block k+1 is loaded while block k is joined
-  uint32_t fp[DPT];
-#pragma unroll
-  for (int j = 0; j < DPT; ++j) {
-    const uint32_t d = threadIdx.x + j * kJoinThreads;
-    if (d < n) {
-      uint32_t v[BW];
-      load_block<BW>(sig + static_cast<uint64_t>(rowsm[d]) * H, vec, v);
-      fp[j] = block_fp<BW>(v);
-    }
-  }
-  for (uint32_t k = 0; k < NB; ++k) {
-    const uint32_t tag = k + 1;
+  for (uint32_t k0 = 0; k0 < NB; k0 += BPL) {
+    // fingerprints of blocks k0 .. k0+BPL-1 of this thread's documents
+    uint32_t fp[DPT][BPL];
+    const uint32_t p0 = k0 * BW;
+    const bool full = vec && p0 + VL <= H;
 #pragma unroll
     for (int j = 0; j < DPT; ++j) {
       const uint32_t d = threadIdx.x + j * kJoinThreads;
-      if (d >= n) break;
-      const uint32_t key = (tag << 23) | fp[j];
-      uint32_t h = (fp[j] * 0x9E3779B1u) >> (32 - tbits);
-      for (;;) {
-        const uint32_t cur = keys[h];
-        if (cur == key) break;
-        if ((cur >> 23) == tag) {  // another fingerprint of this block: probe on
-          h = (h + 1) & mask;
-          continue;
+      if (d < n) {
+        const uint32_t* r = sig + static_cast<uint64_t>(rowsm[d]) * H + p0;
+        uint32_t v[VL];
+        if (full) {
+          load_block<VL>(r, true, v);
+        } else {
+#pragma unroll
+          for (int t = 0; t < VL; ++t) v[t] = p0 + t < H ? __ldg(r + t) : 0u;
         }
-        const uint32_t old = atomicCAS(&keys[h], cur, key);
-        if (old == cur || old == key) break;
+#pragma unroll
+        for (int b = 0; b < BPL; ++b) {
+          uint32_t w[BW];
+#pragma unroll
+          for (int t = 0; t < BW; ++t) w[t] = v[b * BW + t];
+          fp[j][b] = block_fp<BW>(w);
+        }
       }
-      const uint32_t prev = atomicExch(&head[h], (tag << 16) | d);
-      next[d] = (prev >> 16) == tag ? (prev & 0xFFFFu) : 0xFFFFFFFFu;
     }
-    if (k + 1 < NB) {
+#pragma unroll
+    for (int b = 0; b < BPL; ++b) {
+      const uint32_t k = k0 + b;
+      if (k >= NB) continue;
+      const uint32_t tag = k + 1;
 #pragma unroll
       for (int j = 0; j < DPT; ++j) {
         const uint32_t d = threadIdx.x + j * kJoinThreads;
-        if (d < n) {
-          uint32_t v[BW];
-          load_block<BW>(sig + static_cast<uint64_t>(rowsm[d]) * H + (k + 1) * BW, vec, v);
-          fp[j] = block_fp<BW>(v);
+        if (d >= n) continue;  // (not break: keeps fp[][] in registers)
+        const uint32_t key = (tag << 23) | fp[j][b];
+        uint32_t h = (fp[j][b] * 0x9E3779B1u) >> (32 - tbits);
+        for (;;) {
+          const uint32_t cur = keys[h];
+          if (cur == key) break;
+          if ((cur >> 23) == tag) {  // another fingerprint of this block: probe on
+            h = (h + 1) & mask;
+            continue;
+          }
+          const uint32_t old = atomicCAS(&keys[h], cur, key);
+          if (old == cur || old == key) break;
         }
+        const uint32_t prev = atomicExch(&head[h], (tag << 16) | d);
+        next[d] = (prev >> 16) == tag ? (prev & 0xFFFFu) : 0xFFFFFFFFu;
       }
+      __syncthreads();
+      for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads)
+        for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e])
+          join_check_blocks<BW>(sig, H, rowsm[d], rowsm[e], k, vec, min_match, nb, out_key, out_m,
+                                count, cap);
+      __syncthreads();
     }
-    __syncthreads();
-    for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads)
-      for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e])
-        join_check_blocks<BW>(sig, H, rowsm[d], rowsm[e], k, vec, min_match, nb, out_key, out_m,
-                              count, cap);
-    __syncthreads();
   }
 }
 

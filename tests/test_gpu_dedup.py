@@ -388,6 +388,8 @@ def test_pigeonhole_join_adversarial(ctx, ref, monkeypatch, H, thr):
             row[rng.choice(H, size=extra, replace=False)] ^= 1
         elif kind == 1:  # low-entropy values: many equal positions between rows
             row = rng.integers(0, 6, size=H).astype(np.uint32)
+        elif r % 9 == 2:  # copies of the base: pairs with the kind-0 rows near the bound
+            pass
         else:  # random row
             row = rng.integers(0, 1 << 22, size=H).astype(np.uint32)
         sig[r] = row
