@@ -515,6 +515,33 @@ __device__ __forceinline__ void k1_item_dual(
       }
       first = false;
     }
+    for (; j >= 3; j -= 4) {  // 4 windows per slice per iteration: 32F window-function steps
+      const uint2 oa0 = bufA[j + L], oa1 = bufA[j - 1 + L], oa2 = bufA[j - 2 + L],
+                  oa3 = bufA[j - 3 + L];
+      const uint2 ob0 = bufB[j + L], ob1 = bufB[j - 1 + L], ob2 = bufB[j - 2 + L],
+                  ob3 = bufB[j - 3 + L];
+      const uint32_t ca0 = bufA256[j], ca1 = bufA256[j - 1], ca2 = bufA256[j - 2],
+                     ca3 = bufA256[j - 3];
+      const uint32_t cb0 = bufB256[j], cb1 = bufB256[j - 1], cb2 = bufB256[j - 2],
+                     cb3 = bufB256[j - 3];
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const uint32_t a0 = k.roll(f, sa[f], ca0, oa0.x, __uint_as_float(oa0.y));
+        const uint32_t b0 = k.roll(f, sb[f], cb0, ob0.x, __uint_as_float(ob0.y));
+        const uint32_t a1 = k.roll(f, a0, ca1, oa1.x, __uint_as_float(oa1.y));
+        const uint32_t b1 = k.roll(f, b0, cb1, ob1.x, __uint_as_float(ob1.y));
+        const uint32_t a2 = k.roll(f, a1, ca2, oa2.x, __uint_as_float(oa2.y));
+        const uint32_t b2 = k.roll(f, b1, cb2, ob2.x, __uint_as_float(ob2.y));
+        const uint32_t a3 = k.roll(f, a2, ca3, oa3.x, __uint_as_float(oa3.y));
+        const uint32_t b3 = k.roll(f, b2, cb3, ob3.x, __uint_as_float(ob3.y));
+        sa[f] = a3;
+        sb[f] = b3;
+        mn[f] = __vimin3_u32(mn[f], a0, a1);
+        mn[f] = __vimin3_u32(mn[f], b0, b1);
+        mn[f] = __vimin3_u32(mn[f], a2, a3);
+        mn[f] = __vimin3_u32(mn[f], b2, b3);
+      }
+    }
     for (; j >= 1; j -= 2) {
       const uint2 oa0 = bufA[j + L], oa1 = bufA[j - 1 + L];
       const uint2 ob0 = bufB[j + L], ob1 = bufB[j - 1 + L];
