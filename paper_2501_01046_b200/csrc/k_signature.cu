@@ -447,15 +447,21 @@ __device__ __forceinline__ void k1_item(
 // stepping both in lockstep.  The two rolls of a function read the same
 // constant registers back to back (operand reuse) and are independent (ILP),
 // so a lane needs F*6 constant registers for 2F chains instead of 2F*6.
-template <int F>
+template <int F, int Z>
 __device__ __forceinline__ void k1_item_dual(
     uint64_t item, const uint8_t* __restrict__ text, const uint64_t* __restrict__ offsets,
     const uint32_t* __restrict__ item_doc, const uint64_t* __restrict__ item_off,
     const FamPtrs& fam, uint32_t L, uint32_t H, uint32_t bands, uint32_t rows, uint32_t K,
     uint32_t* __restrict__ sig, uint32_t* __restrict__ band, uint2 (*sbuf)[kLMax + 128],
     uint32_t (*sbuf256)[kLMax + 128], uint32_t* srow) {
+  // Z groups of G lanes: group z takes the z-th of Z equal parts of the item's
+  // windows and walks it as two slices (A, B); lane gl owns functions gl*F..
   constexpr int kChunk = 128;
+  constexpr int G = 32 / Z;
   const int lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int gl = lane % G;
+  const unsigned gmask = Z == 1 ? 0xFFFFFFFFu : (((1u << G) - 1u) << (grp * G));
   uint64_t doc = item;
   uint64_t ws = 0;
   bool multi = false;
@@ -469,13 +475,16 @@ __device__ __forceinline__ void k1_item_dual(
   const uint64_t len = offsets[doc + 1] - off;
   const uint64_t nwin = len - L + 1;
   const uint64_t item_end = min(ws + kSeg, nwin);
-  const uint64_t S = (item_end - ws + 1) / 2;      // windows per slice
-  const uint8_t* baseA = text + off + ws;          // slice A starts at window ws
-  const uint8_t* baseB = text + off + item_end - S;  // slice B ends at the item's end
-  const uint64_t total = S + L - 1;                // positions per slice
+  const uint64_t span = item_end - ws;
+  const uint64_t gs = ws + span * grp / Z;         // this group's windows [gs, ge)
+  const uint64_t ge = ws + span * (grp + 1) / Z;
+  const uint64_t S = (ge - gs + 1) / 2;            // windows per slice
+  const uint8_t* baseA = text + off + gs;          // slice A starts at window gs
+  const uint8_t* baseB = text + off + ge - S;      // slice B ends at window ge
+  const uint64_t total = ge > gs ? S + L - 1 : 0;  // positions per slice
 
   Consts<Arith::kFq, F> k;
-  k.load(fam, lane * F);
+  k.load(fam, gl * F);
   uint32_t sa[F], sb[F], mn[F];
 #pragma unroll
   for (int f = 0; f < F; ++f) {
@@ -483,16 +492,16 @@ __device__ __forceinline__ void k1_item_dual(
     sb[f] = 0;
     mn[f] = 0xFFFFFFFFu;
   }
-  uint2* bufA = sbuf[0];
-  uint2* bufB = sbuf[1];
-  uint32_t* bufA256 = sbuf256[0];
-  uint32_t* bufB256 = sbuf256[1];
+  uint2* bufA = sbuf[2 * grp];
+  uint2* bufB = sbuf[2 * grp + 1];
+  uint32_t* bufA256 = sbuf256[2 * grp];
+  uint32_t* bufB256 = sbuf256[2 * grp + 1];
   uint64_t p_hi = total;
   bool first = true;
   while (p_hi > 0) {
     const uint64_t p_lo = p_hi > kChunk ? p_hi - kChunk : 0;
     const int cnt = static_cast<int>(p_hi - p_lo);
-    for (int j = lane; j < cnt + static_cast<int>(L); j += 32) {
+    for (int j = gl; j < cnt + static_cast<int>(L); j += G) {
       const uint64_t pos = p_lo + j;
       const uint32_t ca = pos < total ? baseA[pos] : 0u;
       const uint32_t cb = pos < total ? baseB[pos] : 0u;
@@ -501,7 +510,7 @@ __device__ __forceinline__ void k1_item_dual(
       bufA256[j] = ca << 8;
       bufB256[j] = cb << 8;
     }
-    __syncwarp();
+    __syncwarp(gmask);
     int j = cnt - 1;
     if (first) {  // L-1 warm-up positions: partial windows, not part of the minimum
       for (int w = 0; w < static_cast<int>(L) - 1; ++w, --j) {
@@ -569,13 +578,21 @@ __device__ __forceinline__ void k1_item_dual(
         mn[f] = __vimin3_u32(mn[f], sa[f], sb[f]);
       }
     }
-    __syncwarp();
+    __syncwarp(gmask);
     p_hi = p_lo;
+  }
+  if (Z > 1) {  // the groups' partial minima meet
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+#pragma unroll
+      for (int o = G; o < 32; o <<= 1) mn[f] = min(mn[f], __shfl_xor_sync(0xFFFFFFFFu, mn[f], o));
+    if (grp != 0) return;
   }
 #pragma unroll
   for (int f = 0; f < F; ++f) mn[f] >>= 8;  // scaled state -> canonical value
   uint32_t* out = sig + doc * H;
-  const int fbase = lane * F;
+  const int fbase = gl * F;
   if (multi) {
 #pragma unroll
     for (int f = 0; f < F; ++f)
@@ -594,12 +611,17 @@ __device__ __forceinline__ void k1_item_dual(
   if (band == nullptr) return;
 #pragma unroll
   for (int f = 0; f < F; ++f) srow[fbase + f] = mn[f];
-  __syncwarp();
-  for (uint32_t jb = lane; jb < bands; jb += 32) {
+  __syncwarp(gmask);
+  for (uint32_t jb = gl; jb < bands; jb += G) {
     uint64_t sum = 0;
     for (uint32_t r = 0; r < rows; ++r) sum += srow[jb * rows + r];
     band[doc * bands + jb] = K ? static_cast<uint32_t>(sum % K) : static_cast<uint32_t>(sum);
   }
+}
+
+// row length of a warp's staging buffers
+__host__ __device__ constexpr int k1_buf_rows(int Z, int SL) {
+  return (SL == 2 ? 128 : chunk_for(Z)) + kLMax;
 }
 
 template <Arith A, int F, int Z, class T, int SL>
@@ -607,16 +629,18 @@ struct K1Item {
   static __device__ __forceinline__ void run(
       uint64_t item, const T* text, const uint64_t* offsets, const uint32_t* item_doc,
       const uint64_t* item_off, const FamPtrs& fam, uint32_t L, uint32_t H, uint32_t bands,
-      uint32_t rows, uint32_t K, uint32_t* sig, uint32_t* band, uint2 (*sbuf)[kLMax + chunk_for(Z)],
-      uint32_t (*sbuf256)[kLMax + chunk_for(Z)], uint32_t* srow) {
+      uint32_t rows, uint32_t K, uint32_t* sig, uint32_t* band, uint2* sbuf, uint32_t* sbuf256,
+      uint32_t* srow) {
+    constexpr int R = k1_buf_rows(Z, SL);
     if constexpr (SL == 2) {
-      static_assert(A == Arith::kFq && Z == 1 && chunk_for(Z) == 256, "dual-slice layout");
-      k1_item_dual<F>(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K, sig, band,
-                      reinterpret_cast<uint2(*)[kLMax + 128]>(sbuf),
-                      reinterpret_cast<uint32_t(*)[kLMax + 128]>(sbuf256), srow);
+      static_assert(A == Arith::kFq && R == kLMax + 128, "dual-slice layout");
+      k1_item_dual<F, Z>(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K, sig,
+                         band, reinterpret_cast<uint2(*)[R]>(sbuf),
+                         reinterpret_cast<uint32_t(*)[R]>(sbuf256), srow);
     } else {
       k1_item<A, F, Z, T>(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K, sig,
-                          band, sbuf, sbuf256, srow);
+                          band, reinterpret_cast<uint2(*)[R]>(sbuf),
+                          reinterpret_cast<uint32_t(*)[R]>(sbuf256), srow);
     }
   }
 };
@@ -634,8 +658,8 @@ __global__ void ND_K1_BOUNDS
                 uint32_t* __restrict__ band, unsigned long long* __restrict__ next_item) {
   constexpr int G = 32 / Z;  // lanes per group
   constexpr int Hp = G * F;
-  constexpr int kBuf = chunk_for(Z) + kLMax;
-  constexpr int kSlots = Z > SL ? Z : SL;  // staging buffers per warp
+  constexpr int kBuf = k1_buf_rows(Z, SL);
+  constexpr int kSlots = Z * SL;  // staging buffers per warp
   __shared__ __align__(16) uint2 sbuf[kWarps][kSlots][kBuf];
   __shared__ __align__(16) uint32_t sbuf256[kWarps][kSlots][kBuf];
   __shared__ __align__(16) uint32_t srow[kWarps][Hp];
@@ -644,7 +668,7 @@ __global__ void ND_K1_BOUNDS
     const uint64_t item = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
     if (item < n_items)
       K1Item<A, F, Z, T, SL>::run(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows,
-                                  K, sig, band, sbuf[warp], sbuf256[warp], srow[warp]);
+                                  K, sig, band, &sbuf[warp][0][0], &sbuf256[warp][0][0], srow[warp]);
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -657,7 +681,7 @@ __global__ void ND_K1_BOUNDS
     unsigned long long next = 0;
     if (lane == 0) next = atomicAdd(next_item, 1ull);
     K1Item<A, F, Z, T, SL>::run(item, text, offsets, item_doc, item_off, fam, L, H, bands, rows, K,
-                                sig, band, sbuf[warp], sbuf256[warp], srow[warp]);
+                                sig, band, &sbuf[warp][0][0], &sbuf256[warp][0][0], srow[warp]);
     __syncwarp();
     item = __shfl_sync(0xFFFFFFFFu, next, 0);
   }
@@ -720,6 +744,9 @@ Launcher pick_launcher(bool int_arith, uint32_t Hp, bool codepoint) {
   }
   const char* dual = getenv("ND_K1_DUAL");
   const bool dual_on = !(dual && std::string(dual) == "0");
+  const char* dz = getenv("ND_K1_DUALZ");
+  if (dual_on && Hp == 128 && dz && std::string(dz) == "2")
+    return launch_k1<Arith::kFq, 8, 2, uint8_t, 2>;
   if (dual_on && Hp == 128) return launch_k1<Arith::kFq, 4, 1, uint8_t, 2>;
   if (dual_on && Hp == 256) return launch_k1<Arith::kFq, 8, 1, uint8_t, 2>;
   const char* fz = getenv("ND_K1_FZ");
