@@ -744,10 +744,12 @@ Launcher pick_launcher(bool int_arith, uint32_t Hp, bool codepoint) {
   }
   const char* dual = getenv("ND_K1_DUAL");
   const bool dual_on = !(dual && std::string(dual) == "0");
+  // H=128: 2 groups x 16 lanes x 8 functions x 2 slices (3.15 T HWE/s on C2;
+  // ND_K1_DUALZ=1: 32 lanes x 4 functions x 2 slices, 3.07 T)
   const char* dz = getenv("ND_K1_DUALZ");
-  if (dual_on && Hp == 128 && dz && std::string(dz) == "2")
-    return launch_k1<Arith::kFq, 8, 2, uint8_t, 2>;
-  if (dual_on && Hp == 128) return launch_k1<Arith::kFq, 4, 1, uint8_t, 2>;
+  if (dual_on && Hp == 128 && dz && std::string(dz) == "1")
+    return launch_k1<Arith::kFq, 4, 1, uint8_t, 2>;
+  if (dual_on && Hp == 128) return launch_k1<Arith::kFq, 8, 2, uint8_t, 2>;
   if (dual_on && Hp == 256) return launch_k1<Arith::kFq, 8, 1, uint8_t, 2>;
   const char* fz = getenv("ND_K1_FZ");
   if (fz && Hp == 128) {
