@@ -413,15 +413,16 @@ __device__ __forceinline__ void join_check_blocks(const uint32_t* __restrict__ s
 }
 
 template <int DPT, int BW>
-__global__ void __launch_bounds__(kJoinThreads)
+__global__ void __launch_bounds__(kJoinThreads, 4)
     k_join_blocks(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
                   const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
                   uint32_t join_max, uint32_t tbits, uint32_t NB, uint32_t min_match, int nb,
                   uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
                   unsigned long long* __restrict__ count, uint64_t cap) {
-  // one 16-byte load per document covers BPL blocks (BW <= 4); BW = 8 takes two
-  constexpr int BPL = BW >= 4 ? 1 : 4 / BW;
-  constexpr int VL = BW >= 4 ? BW : 4;
+  // one 32-byte sector per document (two 16-byte loads) covers BPL = 8 / BW
+  // blocks: a 16-byte load would still move a whole DRAM sector
+  constexpr int BPL = 8 / BW;
+  constexpr int VL = 8;
   extern __shared__ uint32_t jsm[];
   const uint32_t n = cell_len[blockIdx.x];
   if (n > join_max) return;  // big cells go to k_compare
