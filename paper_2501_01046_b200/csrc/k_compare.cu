@@ -413,7 +413,7 @@ __device__ __forceinline__ void join_check_blocks(const uint32_t* __restrict__ s
 }
 
 template <int DPT, int BW>
-__global__ void __launch_bounds__(kJoinThreads, 4)
+__global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
     k_join_blocks(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
                   const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
                   uint32_t join_max, uint32_t tbits, uint32_t NB, uint32_t min_match, int nb,
