@@ -118,7 +118,7 @@ void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets,
   ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
 
   // chunking: <= kChunkBytes of text and <= kChunkDocs documents per chunk
-  constexpr uint64_t kChunkBytes = 256ull << 20;
+  constexpr uint64_t kChunkBytes = 64ull << 20;  // small enough that fill + drain are short
   constexpr uint64_t kChunkDocs = 1ull << 20;
   std::vector<std::pair<uint64_t, uint64_t>> chunks;
   for (uint64_t d0 = 0; d0 < n;) {

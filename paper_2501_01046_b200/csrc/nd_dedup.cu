@@ -122,7 +122,7 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   ND_CUDA(cudaEventRecord(start, s));
   ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
   ND_CUDA(cudaMemcpyAsync(d_off, h_off, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->h2d));
-  constexpr uint64_t kChunk = 256ull << 20;
+  constexpr uint64_t kChunk = 64ull << 20;
   std::vector<cudaEvent_t> evs;
   for (uint64_t d0 = 0; d0 < n;) {
     uint64_t d1 = d0 + 1;
