@@ -59,6 +59,7 @@ nd_ctx::~nd_ctx() {
     if (slot[i].comp) cudaStreamDestroy(slot[i].comp);
   }
   pinned_off.release();
+  for (auto& r : ring) r.release();
   synth_buf.release();
   sig_scratch.release();
   dedup.release();

@@ -20,6 +20,7 @@ struct nd_ctx {
     cudaEvent_t h2d_done = nullptr, comp_done = nullptr, d2h_done = nullptr;
   } slot[2];
   ndb::PinnedBuf pinned_off;
+  ndb::DevBuf ring[3];          // text chunks streaming through h2d_signatures
   ndb::DevBuf synth_buf;
   ndb::DevBuf fam_buf, sig_in_text, sig_in_off;
   ndb::DevFamily fam;

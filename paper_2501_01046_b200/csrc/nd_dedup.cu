@@ -102,9 +102,9 @@ uint64_t id_of(const DedupState& st, uint32_t row) {
 
 }  // namespace
 
-// Host text -> device signatures/band keys: chunks of <= 256 MB are copied
-// on the h2d stream and signed on the ctx stream as each lands (PCIe overlaps
-// K1).  The text stays in st.text.
+// Host text -> device signatures/band keys: chunks of <= 64 MB are copied
+// on the h2d stream into a ring of chunk buffers and signed on the ctx stream
+// as each lands (PCIe overlaps K1; the paper's double buffering).
 void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uint64_t* offsets,
                     uint64_t n, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
                     uint32_t* d_band) {
@@ -112,34 +112,54 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   cudaStream_t s = ctx->stream;
   ctx->ensure_streams();
   const uint32_t H = ctx->fam.H;
-  const uint64_t total = offsets[n] - offsets[0];
-  uint8_t* d_text = st.text.as<uint8_t>(total + 16);
   uint64_t* d_off = st.offs.as<uint64_t>(n + 1);
   uint64_t* h_off = static_cast<uint64_t*>(ctx->pinned_off.get((n + 1) * sizeof(uint64_t)));
   for (uint64_t i = 0; i <= n; ++i) h_off[i] = offsets[i] - offsets[0];
-  cudaEvent_t start;
-  ND_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-  ND_CUDA(cudaEventRecord(start, s));
-  ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
-  ND_CUDA(cudaMemcpyAsync(d_off, h_off, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->h2d));
+  // chunks of <= 64 MB of text (a longer document is a chunk of its own)
   constexpr uint64_t kChunk = 64ull << 20;
-  std::vector<cudaEvent_t> evs;
+  std::vector<std::pair<uint64_t, uint64_t>> chunks;
+  uint64_t max_bytes = 0;
   for (uint64_t d0 = 0; d0 < n;) {
     uint64_t d1 = d0 + 1;
     while (d1 < n && h_off[d1 + 1] - h_off[d0] <= kChunk) ++d1;
-    ND_CUDA(cudaMemcpyAsync(d_text + h_off[d0], bytes + offsets[0] + h_off[d0], h_off[d1] - h_off[d0],
+    chunks.push_back({d0, d1});
+    max_bytes = std::max(max_bytes, h_off[d1] - h_off[d0]);
+    d0 = d1;
+  }
+  // the text streams through a ring of kRing chunk buffers: only signatures
+  // and band keys stay in HBM, so the batch is bounded by 4H+4b bytes per
+  // document, not by its text
+  constexpr int kRing = 3;
+  uint8_t* ring[kRing];
+  for (int r = 0; r < kRing; ++r) ring[r] = ctx->ring[r].as<uint8_t>(max_bytes + 16);
+  cudaEvent_t start, k1_done[kRing];
+  ND_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  for (auto& e : k1_done) ND_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  ND_CUDA(cudaEventRecord(start, s));
+  ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
+  ND_CUDA(cudaMemcpyAsync(d_off, h_off, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->h2d));
+  std::vector<cudaEvent_t> evs;
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    const auto [d0, d1] = chunks[c];
+    const int r = static_cast<int>(c % kRing);
+    if (c >= kRing) ND_CUDA(cudaStreamWaitEvent(ctx->h2d, k1_done[r], 0));  // slot free again
+    ND_CUDA(cudaMemcpyAsync(ring[r], bytes + offsets[0] + h_off[d0], h_off[d1] - h_off[d0],
                             cudaMemcpyHostToDevice, ctx->h2d));
     cudaEvent_t ev;
     ND_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     ND_CUDA(cudaEventRecord(ev, ctx->h2d));
     ND_CUDA(cudaStreamWaitEvent(s, ev, 0));
     evs.push_back(ev);
-    launch_signatures(ctx->fam, d_text, d_off + d0, d1 - d0, bands, rows, K, d_sig + d0 * H,
-                      d_band ? d_band + d0 * bands : nullptr, st.sig_scratch, s, false, h_off + d0);
-    d0 = d1;
+    // offsets stay batch-absolute: the kernel reads text + offset, so the
+    // text pointer is the slot shifted back by the chunk's first offset
+    launch_signatures(ctx->fam, ring[r] - h_off[d0], d_off + d0, d1 - d0, bands, rows, K,
+                      d_sig + d0 * H, d_band ? d_band + d0 * bands : nullptr, st.sig_scratch, s,
+                      false, h_off + d0);
+    ND_CUDA(cudaEventRecord(k1_done[r], s));
   }
   // events may be destroyed once enqueued work referencing them is recorded
   for (auto ev : evs) cudaEventDestroy(ev);
+  for (auto e : k1_done) cudaEventDestroy(e);
   cudaEventDestroy(start);
 }
 
