@@ -267,10 +267,16 @@ int nd_hash_file(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets,
 typedef struct nd_compare_stage_stats { /* CompareStageOutput (pipeline.hpp:74-81) */
   uint32_t buckets_per_pass, pass_count;
   uint64_t candidate_pairs, emitted_pairs, gather_peak_bytes;
-  uint64_t records;          /* signature records loaded into HBM */
-  uint64_t distinct_pairs;   /* across passes */
-  double seconds[3];         /* read + H2D, GPU compare, pair files */
+  uint64_t records;          /* signature records read */
+  uint64_t distinct_pairs;   /* summed over bucket intervals */
+  double seconds[3];         /* read, GPU compare (all intervals), pair files */
+  uint32_t intervals;        /* bucket intervals the cells went to the GPU in */
 } nd_compare_stage_stats;
+/* HBM the compare stage may fill with one bucket interval's signatures and
+ * cell records (0 = 70 % of the free device memory).  Corpora above it are
+ * compared in several intervals (out-of-core), each a union of whole gather
+ * passes, with identical output files. */
+int nd_set_hbm_budget(nd_ctx* ctx, uint64_t bytes);
 /* run_compare_stage (pipeline.cpp:347-432) minus its JSON: every .feds file
  * (source order) is loaded into HBM once; the cells of all passes are
  * compared on the GPU and each pass's sorted distinct pairs are written to

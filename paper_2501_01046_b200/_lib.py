@@ -72,7 +72,8 @@ class NdCompareStageStats(C.Structure):
     _fields_ = [("buckets_per_pass", C.c_uint32), ("pass_count", C.c_uint32),
                 ("candidate_pairs", C.c_uint64), ("emitted_pairs", C.c_uint64),
                 ("gather_peak_bytes", C.c_uint64), ("records", C.c_uint64),
-                ("distinct_pairs", C.c_uint64), ("seconds", C.c_double * 3)]
+                ("distinct_pairs", C.c_uint64), ("seconds", C.c_double * 3),
+                ("intervals", C.c_uint32)]
 
 
 cpp = C.POINTER(C.c_char_p)
@@ -143,6 +144,7 @@ SIGNATURES = {
     "nd_compare_stage": (C.c_int, [vp, cpp, C.c_uint32, C.POINTER(NdFedsHeader), C.c_uint64,
                                    C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64,
                                    C.c_char_p, C.c_int, C.POINTER(NdCompareStageStats)]),
+    "nd_set_hbm_budget": (C.c_int, [vp, C.c_uint64]),
     "nd_union_stage": (C.c_int, [vp, cpp, C.c_uint32, C.c_uint64, C.c_uint64, C.c_char_p,
                                  C.c_int, C.POINTER(NdDedupStats)]),
     "nd_stage_cell_records": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,

@@ -30,6 +30,7 @@ struct nd_ctx {
   ndb::DedupState api, api2;    // last nd_compare_cells / nd_union
   ndb::DedupState h2d_state;    // text staging of nd_signatures_h2d
   ndb::SortScratch stage_sort;  // nd_stage_cell_records
+  uint64_t hbm_budget = 0;      // compare-stage HBM budget (0 = 70 % of free memory)
   uint64_t family_seed = 0;
   bool family_derived = false;  // family came from derive_family(family_seed, ...)
   std::string err;

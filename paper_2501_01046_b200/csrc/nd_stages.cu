@@ -6,15 +6,19 @@
 //
 // The reference's compare stage re-scans every .feds file once per gather pass
 // (scan_gather, sigstore.cpp:228-286) so that each pass's cells fit a host-RAM
-// budget.  180 GB of HBM holds the signatures of every configuration here, so
-// the records are loaded once and ALL cells are compared in one K3 launch; the
-// pass structure only decides which file each accepted pair is written to.
+// budget.  Here the records are read once into host memory and the cells go to
+// the GPU in as few bucket intervals as the HBM budget allows (one, holding
+// every cell, for every configuration measured here; more when the signatures
+// exceed the budget -- out-of-core passes, each a union of whole gather passes);
+// each interval's cells are compared in one K3 launch, and the pass structure
+// only decides which file each accepted pair is written to.
 // A pass is (worker w = owner of band j, bucket interval [p*C, (p+1)*C)), and
 // acceptance depends on the two signatures only, so a distinct accepted pair
 // (lo, hi) belongs to exactly the passes {pass(j, bucket_j(lo)) : bucket_j(lo)
 // == bucket_j(hi)}; compare_pass's per-pass sort + unique (compare.cpp:77-84)
 // is a stable sort of those (pass, pair) tags by pass and a first-of-run skip.
 #include <algorithm>
+#include <cstring>
 #include <chrono>
 #include <cstdio>
 #include <string>
@@ -30,46 +34,35 @@ unsigned blocks_for(uint64_t n, unsigned tb) {
 }
 
 // number of bands in which the two rows of distinct pair i share a bucket
+// inside the current bucket interval [k0, k1)
 __global__ void k_pair_pass_count(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi,
                                   uint64_t np, const uint32_t* __restrict__ band, uint32_t bands,
-                                  uint32_t* __restrict__ cnt) {
+                                  uint32_t k0, uint32_t k1, uint32_t* __restrict__ cnt) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= np) return;
   const uint32_t* a = band + static_cast<uint64_t>(lo[i]) * bands;
   const uint32_t* b = band + static_cast<uint64_t>(hi[i]) * bands;
   uint32_t c = 0;
-  for (uint32_t j = 0; j < bands; ++j) c += a[j] == b[j];
+  for (uint32_t j = 0; j < bands; ++j) c += a[j] == b[j] && a[j] >= k0 && a[j] < k1;
   cnt[i] = c;
 }
 
 // (pass, pair) tags; pass(j, k) = band_base[j] + k / C
 __global__ void k_pair_pass_emit(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi,
                                  uint64_t np, const uint32_t* __restrict__ band, uint32_t bands,
-                                 const uint32_t* __restrict__ band_base, uint32_t C,
-                                 const uint64_t* __restrict__ off, uint32_t* __restrict__ pass,
-                                 uint32_t* __restrict__ pair) {
+                                 uint32_t k0, uint32_t k1, const uint32_t* __restrict__ band_base,
+                                 uint32_t C, const uint64_t* __restrict__ off,
+                                 uint32_t* __restrict__ pass, uint32_t* __restrict__ pair) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= np) return;
   const uint32_t* a = band + static_cast<uint64_t>(lo[i]) * bands;
   const uint32_t* b = band + static_cast<uint64_t>(hi[i]) * bands;
   uint64_t o = off[i];
   for (uint32_t j = 0; j < bands; ++j) {
-    if (a[j] != b[j]) continue;
+    if (a[j] != b[j] || a[j] < k0 || a[j] >= k1) continue;
     pass[o] = band_base[j] + a[j] / C;
     pair[o] = static_cast<uint32_t>(i);
     ++o;
-  }
-}
-
-// records per pass: what scan_gather charges to the gauge before dropping
-// singletons (sigstore.cpp:262-266)
-__global__ void k_pass_records(const uint32_t* __restrict__ band, uint64_t m, uint32_t bands,
-                               const uint32_t* __restrict__ band_base, uint32_t C,
-                               unsigned long long* __restrict__ hist) {
-  for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < m;
-       r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t j = static_cast<uint32_t>(r % bands);
-    atomicAdd(&hist[band_base[j] + band[r] / C], 1ull);
   }
 }
 
@@ -199,7 +192,7 @@ int nd_compare_stage(nd_ctx* ctx, const char* const* feds_paths, uint32_t nfiles
     for (uint32_t w = 0, j = 0; w < workers; ++w)
       for (uint32_t k = 0; k < wbands[w]; ++k) band_base[j++] = pass_base[w];
 
-    // ---- every record into host SoA buffers, then HBM
+    // ---- every record into host SoA buffers
     std::vector<nd_feds_header> hs(nfiles);
     uint64_t n = 0;
     for (uint32_t f = 0; f < nfiles; ++f) {
@@ -221,75 +214,154 @@ int nd_compare_stage(nd_ctx* ctx, const char* const* feds_paths, uint32_t nfiles
       if (ids[i] <= ids[i - 1])
         fail(ND_ERR_CONFIG, "signature files are not in ascending doc_id order; "
                             "pass them in manifest order");
-    cudaStream_t s = ctx->stream;
-    uint32_t* d_sig = st.sig.as<uint32_t>(n * H + 1);
-    uint32_t* d_band = st.band.as<uint32_t>(n * B + 1);
-    if (n) {
-      ND_CUDA(cudaMemcpyAsync(d_sig, hsig.data(), n * H * 4, cudaMemcpyHostToDevice, s));
-      ND_CUDA(cudaMemcpyAsync(d_band, hband.data(), n * B * 4, cudaMemcpyHostToDevice, s));
-    }
-    st.doc_ids = std::move(ids);
-    st.K = K;
-    ND_CUDA(cudaStreamSynchronize(s));
     const double t_load = since(t0);
     auto t1 = std::chrono::steady_clock::now();
 
-    // ---- all cells at once: K2 grouping, K3 compare, distinct pairs
+    // ---- records per bucket -> bucket intervals [k0, k1) that fit the HBM
+    // budget, aligned to the gather passes (multiples of C) so that every
+    // pass lies inside exactly one interval.  One interval = everything in
+    // HBM at once; more = out-of-core passes over the host-resident records.
+    std::vector<uint64_t> per_bucket(K, 0);
+    for (uint64_t i = 0; i < n * B; ++i) ++per_bucket[hband[i]];
+    const uint64_t row_bytes = 4ull * H + 4ull * B + 8;   // signature + band ids + doc map
+    const uint64_t rec_bytes = 8 * 4;                      // record + sort scratch + cell CSR
+    uint64_t budget = ctx->hbm_budget;
+    if (budget == 0) {
+      size_t fr = 0, tot = 0;
+      ND_CUDA(cudaMemGetInfo(&fr, &tot));
+      budget = static_cast<uint64_t>(fr) / 10 * 7;
+    }
+    std::vector<std::pair<uint32_t, uint32_t>> intervals;
+    {
+      const uint64_t whole = n * row_bytes + n * B * rec_bytes;
+      if (whole <= budget) {
+        intervals.push_back({0, K});
+      } else {
+        uint32_t k0 = 0;
+        uint64_t acc = 0;
+        for (uint32_t k = 0; k < K; k += C) {
+          const uint32_t k1 = std::min<uint64_t>(K, uint64_t(k) + C);
+          uint64_t recs = 0;
+          for (uint32_t b = k; b < k1; ++b) recs += per_bucket[b];
+          const uint64_t bytes = recs * (row_bytes + rec_bytes);  // a record may bring its row
+          if (k > k0 && acc + bytes > budget) {
+            intervals.push_back({k0, k});
+            k0 = k;
+            acc = 0;
+          }
+          acc += bytes;
+        }
+        intervals.push_back({k0, K});
+      }
+    }
+
+    cudaStream_t s = ctx->stream;
     const uint32_t mm = min_matches(H, thr_num, thr_den);
-    uint64_t tagged = 0;
-    std::vector<uint32_t> hpass, hpair, plo, phi, pm;
-    std::vector<unsigned long long> hist(std::max<uint32_t>(total_passes, 1), 0);
-    uint64_t distinct = 0, candidates = 0;
-    if (n) {
-      build_cells_from_bands(st.cells, d_band, n, B, K, kCmpRows, s);
-      compare_and_unique(st, d_sig, H, mm, n, s);
-      candidates = st.cells.candidate_pairs;
-      distinct = st.pairs.distinct;
+    uint64_t candidates = 0, distinct_total = 0;
+    // accepted (pass, lo doc, hi doc, match) in per-pass (lo, hi) order
+    std::vector<uint32_t> out_pass, out_m;
+    std::vector<uint64_t> out_lo, out_hi;
+    std::vector<uint32_t> sel;                  // rows of this interval
+    std::vector<uint32_t> rkeys, rvals;         // (cell, local row) records
+    for (auto [k0, k1] : intervals) {
+      // documents with a band bucket in [k0, k1), and their in-range records
+      const bool all = k0 == 0 && k1 == K;
+      sel.clear();
+      rkeys.clear();
+      rvals.clear();
+      for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t* bi = hband.data() + i * B;
+        bool any = all;
+        for (uint32_t j = 0; j < B && !any; ++j) any = bi[j] >= k0 && bi[j] < k1;
+        if (!any) continue;
+        const uint32_t local = static_cast<uint32_t>(sel.size());
+        sel.push_back(static_cast<uint32_t>(i));
+        if (!all)
+          for (uint32_t j = 0; j < B; ++j)
+            if (bi[j] >= k0 && bi[j] < k1) {
+              rkeys.push_back(j * K + bi[j]);
+              rvals.push_back(local);
+            }
+      }
+      const uint64_t m = sel.size();
+      if (m == 0) continue;
+      uint32_t* d_sig = st.sig.as<uint32_t>(m * H + 1);
+      uint32_t* d_band = st.band.as<uint32_t>(m * B + 1);
+      if (all) {
+        ND_CUDA(cudaMemcpyAsync(d_sig, hsig.data(), m * H * 4, cudaMemcpyHostToDevice, s));
+        ND_CUDA(cudaMemcpyAsync(d_band, hband.data(), m * B * 4, cudaMemcpyHostToDevice, s));
+        build_cells_from_bands(st.cells, d_band, m, B, K, kCmpRows, s);
+      } else {
+        std::vector<uint32_t> gs(m * H), gb(m * B);
+        for (uint64_t r = 0; r < m; ++r) {
+          std::memcpy(gs.data() + r * H, hsig.data() + uint64_t(sel[r]) * H, 4ull * H);
+          std::memcpy(gb.data() + r * B, hband.data() + uint64_t(sel[r]) * B, 4ull * B);
+        }
+        ND_CUDA(cudaMemcpyAsync(d_sig, gs.data(), m * H * 4, cudaMemcpyHostToDevice, s));
+        ND_CUDA(cudaMemcpyAsync(d_band, gb.data(), m * B * 4, cudaMemcpyHostToDevice, s));
+        const uint64_t nr = rkeys.size();
+        uint32_t* dk = st.cells.rec_keys.as<uint32_t>(nr + 1);
+        uint32_t* dv = st.cells.rec_vals.as<uint32_t>(nr + 1);
+        ND_CUDA(cudaMemcpyAsync(dk, rkeys.data(), nr * 4, cudaMemcpyHostToDevice, s));
+        ND_CUDA(cudaMemcpyAsync(dv, rvals.data(), nr * 4, cudaMemcpyHostToDevice, s));
+        build_cells_from_records(st.cells, dk, dv, nr, uint64_t(B) * K, kCmpRows, s);
+        ND_CUDA(cudaStreamSynchronize(s));  // gs / gb / rkeys / rvals leave scope
+      }
+      compare_and_unique(st, d_sig, H, mm, m, s);
+      candidates += st.cells.candidate_pairs;
+      const uint64_t distinct = st.pairs.distinct;
+      distinct_total += distinct;
+      if (distinct == 0) continue;
+      PairSet& ps = st.pairs;
       uint32_t* d_bb = st.cells.maxbuf.as<uint32_t>(B);
       ND_CUDA(cudaMemcpyAsync(d_bb, band_base.data(), B * 4, cudaMemcpyHostToDevice, s));
-      // records per pass (gather gauge)
-      auto* d_hist = st.cells.scan.as<unsigned long long>(hist.size());
-      ND_CUDA(cudaMemsetAsync(d_hist, 0, hist.size() * 8, s));
-      k_pass_records<<<std::min(blocks_for(n * B, 256), 148u * 16), 256, 0, s>>>(d_band, n * B, B,
-                                                                                d_bb, C, d_hist);
+      uint32_t* cnt = ps.flag.as<uint32_t>(distinct);
+      uint64_t* off = ps.idx.as<uint64_t>(distinct + 1);
+      k_pair_pass_count<<<blocks_for(distinct, 256), 256, 0, s>>>(ps.lo, ps.hi, distinct, d_band, B,
+                                                                 k0, k1, cnt);
       ND_CHECK_LAUNCH();
-      ND_CUDA(cudaMemcpyAsync(hist.data(), d_hist, hist.size() * 8, cudaMemcpyDeviceToHost, s));
-      if (distinct) {
-        PairSet& ps = st.pairs;
-        uint32_t* cnt = ps.flag.as<uint32_t>(distinct);
-        uint64_t* off = ps.idx.as<uint64_t>(distinct + 1);
-        k_pair_pass_count<<<blocks_for(distinct, 256), 256, 0, s>>>(ps.lo, ps.hi, distinct, d_band,
-                                                                   B, cnt);
-        ND_CHECK_LAUNCH();
-        scan_u32_to_u64(cnt, off, distinct, ps.scan, s);
-        ND_CUDA(cudaMemcpyAsync(&tagged, off + distinct, 8, cudaMemcpyDeviceToHost, s));
-        ND_CUDA(cudaStreamSynchronize(s));
-        uint32_t* d_pass = st.cells.rec_keys.as<uint32_t>(tagged);
-        uint32_t* d_pair = st.cells.rec_vals.as<uint32_t>(tagged);
-        k_pair_pass_emit<<<blocks_for(distinct, 256), 256, 0, s>>>(ps.lo, ps.hi, distinct, d_band,
-                                                                  B, d_bb, C, off, d_pass, d_pair);
-        ND_CHECK_LAUNCH();
-        // stable by pass: pairs stay in (lo, hi) order inside each pass
-        radix_sort_u32(d_pass, d_pair, tagged, bits_for(total_passes ? total_passes - 1 : 0),
-                       st.cells.sort, s);
-        hpass.resize(tagged);
-        hpair.resize(tagged);
-        plo.resize(distinct);
-        phi.resize(distinct);
-        pm.resize(distinct);
-        ND_CUDA(cudaMemcpyAsync(hpass.data(), d_pass, tagged * 4, cudaMemcpyDeviceToHost, s));
-        ND_CUDA(cudaMemcpyAsync(hpair.data(), d_pair, tagged * 4, cudaMemcpyDeviceToHost, s));
-        ND_CUDA(cudaMemcpyAsync(plo.data(), ps.lo, distinct * 4, cudaMemcpyDeviceToHost, s));
-        ND_CUDA(cudaMemcpyAsync(phi.data(), ps.hi, distinct * 4, cudaMemcpyDeviceToHost, s));
-        ND_CUDA(cudaMemcpyAsync(pm.data(), ps.mc, distinct * 4, cudaMemcpyDeviceToHost, s));
-      }
+      scan_u32_to_u64(cnt, off, distinct, ps.scan, s);
+      uint64_t tagged = 0;
+      ND_CUDA(cudaMemcpyAsync(&tagged, off + distinct, 8, cudaMemcpyDeviceToHost, s));
       ND_CUDA(cudaStreamSynchronize(s));
+      uint32_t* d_pass = st.cells.rec_keys.as<uint32_t>(tagged + 1);
+      uint32_t* d_pair = st.cells.rec_vals.as<uint32_t>(tagged + 1);
+      k_pair_pass_emit<<<blocks_for(distinct, 256), 256, 0, s>>>(ps.lo, ps.hi, distinct, d_band, B,
+                                                                k0, k1, d_bb, C, off, d_pass,
+                                                                d_pair);
+      ND_CHECK_LAUNCH();
+      // stable by pass: pairs stay in (lo, hi) order inside each pass
+      radix_sort_u32(d_pass, d_pair, tagged, bits_for(total_passes ? total_passes - 1 : 0),
+                     st.cells.sort, s);
+      std::vector<uint32_t> hpass(tagged), hpair(tagged), plo(distinct), phi(distinct), pm(distinct);
+      ND_CUDA(cudaMemcpyAsync(hpass.data(), d_pass, tagged * 4, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaMemcpyAsync(hpair.data(), d_pair, tagged * 4, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaMemcpyAsync(plo.data(), ps.lo, distinct * 4, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaMemcpyAsync(phi.data(), ps.hi, distinct * 4, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaMemcpyAsync(pm.data(), ps.mc, distinct * 4, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaStreamSynchronize(s));
+      for (uint64_t t = 0; t < tagged; ++t) {
+        const uint32_t i = hpair[t];
+        // the pair shares this pass through two bands: compare_pass's unique
+        if (t > 0 && hpass[t] == hpass[t - 1] && hpair[t - 1] == i) continue;
+        out_pass.push_back(hpass[t]);
+        out_lo.push_back(ids[sel[plo[i]]]);
+        out_hi.push_back(ids[sel[phi[i]]]);
+        out_m.push_back(pm[i]);
+      }
     }
+    // passes in increasing order across intervals (intervals ascend in bucket,
+    // passes of one worker ascend in bucket, workers interleave): group by pass
+    std::vector<uint64_t> order(out_pass.size());
+    for (uint64_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](uint64_t x, uint64_t y) { return out_pass[x] < out_pass[y]; });
     const double t_gpu = since(t1);
     auto t2 = std::chrono::steady_clock::now();
 
-    // ---- one pair file per (worker, pass), doc ids, first-of-run per pass
+    // ---- one pair file per (worker, pass)
     uint64_t emitted = 0, cursor = 0;
+    const uint64_t tagged = order.size();
     std::vector<uint64_t> lo, hi;
     std::vector<uint32_t> m;
     const std::string dir(pairs_dir);
@@ -299,14 +371,11 @@ int nd_compare_stage(nd_ctx* ctx, const char* const* feds_paths, uint32_t nfiles
         lo.clear();
         hi.clear();
         m.clear();
-        uint32_t prev = 0xFFFFFFFFu;
-        for (; cursor < tagged && hpass[cursor] == gp; ++cursor) {
-          const uint32_t i = hpair[cursor];
-          if (i == prev) continue;  // the pair shares this pass through two bands
-          prev = i;
-          lo.push_back(st.doc_ids[plo[i]]);
-          hi.push_back(st.doc_ids[phi[i]]);
-          m.push_back(pm[i]);
+        for (; cursor < tagged && out_pass[order[cursor]] == gp; ++cursor) {
+          const uint64_t x = order[cursor];
+          lo.push_back(out_lo[x]);
+          hi.push_back(out_hi[x]);
+          m.push_back(out_m[x]);
         }
         emitted += lo.size();
         pairs_write(dir + "/w" + std::to_string(w) + "_p" + std::to_string(pp) + ".pairs",
@@ -317,6 +386,9 @@ int nd_compare_stage(nd_ctx* ctx, const char* const* feds_paths, uint32_t nfiles
     // scan_gather's gauge: every record of a pass is resident at the end of
     // its scan; workers run their p-th passes side by side
     const uint64_t entry = 8 + 4ull * H;
+    std::vector<uint64_t> hist(std::max<uint32_t>(total_passes, 1), 0);
+    for (uint64_t i = 0; i < n; ++i)
+      for (uint32_t j = 0; j < B; ++j) ++hist[band_base[j] + hband[i * B + j] / C];
     uint64_t peak = 0;
     const uint32_t maxp = passes.empty() ? 0 : *std::max_element(passes.begin(), passes.end());
     for (uint32_t pp = 0; pp < maxp; ++pp) {
@@ -333,12 +405,17 @@ int nd_compare_stage(nd_ctx* ctx, const char* const* feds_paths, uint32_t nfiles
       stats->emitted_pairs = emitted;
       stats->gather_peak_bytes = peak;
       stats->records = n;
-      stats->distinct_pairs = distinct;
+      stats->distinct_pairs = distinct_total;
+      stats->intervals = static_cast<uint32_t>(intervals.size());
       stats->seconds[0] = t_load;
       stats->seconds[1] = t_gpu;
       stats->seconds[2] = since(t2);
     }
   });
+}
+
+int nd_set_hbm_budget(nd_ctx* ctx, uint64_t bytes) {
+  return guarded_impl(ctx, [&] { ctx->hbm_budget = bytes; });
 }
 
 int nd_union_stage(nd_ctx* ctx, const char* const* pair_paths, uint32_t nfiles,

@@ -49,6 +49,9 @@ class RunConfig:
     tile_size: int = 32
     fsync_files: bool = False
     oracle_override: bool = False
+    # schedule only (not artifact-shaping): HBM the compare stage may fill per
+    # bucket interval; 0 = 70 % of free device memory (nd_set_hbm_budget)
+    hbm_budget: int = 0
 
     def validate(self, need_workspace: bool = False) -> None:
         """pipeline.cpp:20-33."""
@@ -309,6 +312,7 @@ class CompareStageOutput:
     gather_peak_bytes: int = 0
     pair_files: list[str] = field(default_factory=list)
     seconds: list[float] = field(default_factory=list)
+    intervals: int = 1
 
 
 def run_hash_stage(config: RunConfig, ctx: Context | None = None) -> HashStageOutput:
@@ -417,6 +421,7 @@ def run_compare_stage(config: RunConfig, ctx: Context | None = None) -> CompareS
     st = _lib.NdCompareStageStats()
     tn, td = _ratio(config.threshold)
     os.makedirs(pairs_dir(config), exist_ok=True)
+    ctx.check(ctx.lib.nd_set_hbm_budget(ctx.h, config.hbm_budget))
     ctx.check(ctx.lib.nd_compare_stage(ctx.h, paths, len(m["signature_files"]), C.byref(expected),
                                        m["total_signature_bytes"], config.workers,
                                        config.memory_budget, config.buckets_per_pass or 0, tn, td,
@@ -425,7 +430,8 @@ def run_compare_stage(config: RunConfig, ctx: Context | None = None) -> CompareS
     names = sorted(pairs_dir(config) + f"/w{w}_p{p}.pairs"
                    for w, np_ in enumerate(plan.passes_per_worker) for p in range(np_))
     out = CompareStageOutput(st.buckets_per_pass, st.pass_count, st.candidate_pairs,
-                             st.emitted_pairs, st.gather_peak_bytes, names, list(st.seconds))
+                             st.emitted_pairs, st.gather_peak_bytes, names, list(st.seconds),
+                             st.intervals)
     doc = {"config_hash": config.config_hash(), "bucket_count": m["bucket_count"],
            "buckets_per_pass": out.buckets_per_pass, "pass_count": out.pass_count,
            "workers": config.workers, "memory_budget": config.memory_budget,

@@ -39,14 +39,22 @@ def _tree(ws):
     return out
 
 
-@pytest.mark.parametrize("workers,budget", [(1, 1 << 30), (1, 120_000), (3, 300_000), (20, 1 << 30)])
-def test_staged_workspace_byte_identical(ctx, ref, tmp_path, workers, budget):
+@pytest.mark.parametrize("workers,budget,hbm", [(1, 1 << 30, 0), (1, 120_000, 0), (3, 300_000, 0),
+                                                (20, 1 << 30, 0), (1, 120_000, 250_000),
+                                                (3, 300_000, 400_000)])
+def test_staged_workspace_byte_identical(ctx, ref, tmp_path, workers, budget, hbm):
+    # hbm > 0: a tiny HBM budget forces the out-of-core compare (several
+    # bucket intervals, each a union of whole gather passes)
     corpus = _corpus_dir(ref, tmp_path)
     ws_ref, ws_gpu = str(tmp_path / "ref"), str(tmp_path / "gpu")
     os.makedirs(ws_ref)
     ref.run_dedup(corpus, ws_ref, workers=workers, memory_budget=budget)
     cfg = pipeline.RunConfig(inputs=[corpus], workspace=ws_gpu, workers=workers,
-                             memory_budget=budget)
+                             memory_budget=budget, hbm_budget=hbm)
+    if hbm:
+        pipeline.run_hash_stage(cfg, ctx=ctx)
+        c = pipeline.run_compare_stage(cfg, ctx=ctx)
+        assert c.intervals > 2, c.intervals
     rep = pipeline.run_dedup(cfg, ctx=ctx)
     want, got = _tree(ws_ref), _tree(ws_gpu)
     assert sorted(got) == sorted(want)
