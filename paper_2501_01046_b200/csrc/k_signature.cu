@@ -440,33 +440,6 @@ __device__ __forceinline__ void k1_item(
   }
 }
 
-// Stages positions [lo, lo + count) of src into (byte, float) pairs and
-// 256*byte words, positions >= limit as 0: the G lanes of a group read the
-// span as 16-byte-aligned uint4 words (one LDG.128 per lane per 16 bytes; a
-// word may reach a few bytes outside the span, always inside the 16-byte
-// block of an in-span byte, hence inside the allocation) and scatter the
-// bytes to shared memory.
-__device__ __forceinline__ void stage_bytes16(const uint8_t* __restrict__ src, uint64_t lo,
-                                              uint64_t limit, int count, uint2* __restrict__ buf,
-                                              uint32_t* __restrict__ buf256, int gl, int G) {
-  const uint8_t* a = src + lo;
-  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15);
-  const int shift = static_cast<int>(reinterpret_cast<uintptr_t>(a) - a0);
-  const int words = (shift + count + 15) >> 4;
-  for (int w = gl; w < words; w += G) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(a0) + w);
-    const uint32_t part[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int j = 16 * w + q - shift;
-      if (j < 0 || j >= count) continue;
-      const uint32_t c = lo + j < limit ? (part[q >> 2] >> (8 * (q & 3))) & 0xFFu : 0u;
-      buf[j] = make_uint2(c, __float_as_uint(static_cast<float>(c)));
-      buf256[j] = c << 8;
-    }
-  }
-}
-
 // Dual-slice variant (fq arithmetic, byte units, all 32 lanes on one slice
 // set): lane l owns functions [l*F, l*F+F) and walks TWO slices of the
 // item's windows, A = the first ceil(span/2) windows and B = the last
@@ -528,8 +501,15 @@ __device__ __forceinline__ void k1_item_dual(
   while (p_hi > 0) {
     const uint64_t p_lo = p_hi > kChunk ? p_hi - kChunk : 0;
     const int cnt = static_cast<int>(p_hi - p_lo);
-    stage_bytes16(baseA, p_lo, total, cnt + static_cast<int>(L), bufA, bufA256, gl, G);
-    stage_bytes16(baseB, p_lo, total, cnt + static_cast<int>(L), bufB, bufB256, gl, G);
+    for (int j = gl; j < cnt + static_cast<int>(L); j += G) {
+      const uint64_t pos = p_lo + j;
+      const uint32_t ca = pos < total ? baseA[pos] : 0u;
+      const uint32_t cb = pos < total ? baseB[pos] : 0u;
+      bufA[j] = make_uint2(ca, __float_as_uint(static_cast<float>(ca)));
+      bufB[j] = make_uint2(cb, __float_as_uint(static_cast<float>(cb)));
+      bufA256[j] = ca << 8;
+      bufB256[j] = cb << 8;
+    }
     __syncwarp(gmask);
     int j = cnt - 1;
     if (first) {  // L-1 warm-up positions: partial windows, not part of the minimum
