@@ -117,6 +117,10 @@ class GpuStages:
 def _all_gather_var(dist, t, group, torch):
     """all_gather of a 1-D/2-D tensor whose first dimension differs per rank."""
     world = dist.get_world_size(group)
+    dev = t.device
+    if _host_collectives(dist, group, dev):  # gloo: collectives on host copies
+        out, sizes = _all_gather_var(dist, t.cpu(), group, torch)
+        return out.to(dev), sizes
     n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
@@ -127,6 +131,12 @@ def _all_gather_var(dist, t, group, torch):
     outs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(outs, pad, group=group)
     return torch.cat([o[:s] for o, s in zip(outs, sizes)]), sizes
+
+
+def _host_collectives(dist, group, device) -> bool:
+    """NCCL runs the collectives on device tensors; a gloo group (CPU protocol
+    tests, or several ranks sharing one GPU in the GPU tests) gets host copies."""
+    return device.type == "cuda" and dist.get_backend(group) == "gloo"
 
 
 def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists") -> ShardResult:
@@ -140,9 +150,11 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists") -> S
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = stages.device
+    host = _host_collectives(dist, group, dev)
+    cdev = torch.device("cpu") if host else dev  # where collective buffers live
     n_local = len(offsets) - 1
     # 1. global N, K, doc_base
-    cnt = torch.tensor([n_local], dtype=torch.int64, device=dev)
+    cnt = torch.tensor([n_local], dtype=torch.int64, device=cdev)
     counts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(counts, cnt, group=group)
     counts = [int(c.item()) for c in counts]
@@ -166,22 +178,23 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists") -> S
         torch.zeros(0, dtype=torch.int64, device=dev)
     edges = [0] + [int(x) for x in splits.tolist()] + [keys.shape[0]]
     send = [edges[i + 1] - edges[i] for i in range(world)]
-    send_t = torch.tensor(send, dtype=torch.int64, device=dev)
+    send_t = torch.tensor(send, dtype=torch.int64, device=cdev)
     recv_t = torch.empty_like(send_t)
     dist.all_to_all_single(recv_t, send_t, group=group)
     recv = [int(x) for x in recv_t.tolist()]
-    rkeys = torch.empty(sum(recv), dtype=keys.dtype, device=dev)
-    rvals = torch.empty(sum(recv), dtype=vals.dtype, device=dev)
-    dist.all_to_all_single(rkeys, keys, recv, send, group=group)
-    dist.all_to_all_single(rvals, vals, recv, send, group=group)
+    rkeys = torch.empty(sum(recv), dtype=keys.dtype, device=cdev)
+    rvals = torch.empty(sum(recv), dtype=vals.dtype, device=cdev)
+    dist.all_to_all_single(rkeys, keys.to(cdev), recv, send, group=group)
+    dist.all_to_all_single(rvals, vals.to(cdev), recv, send, group=group)
+    rkeys, rvals = rkeys.to(dev), rvals.to(dev)
     # 4. all signature rows on every rank
     sig_all, _ = _all_gather_var(dist, sig, group, torch)
     # 5. compare the owned cells
     thr = _ratio(config.threshold)
     lo, hi, m, cand_local = stages.compare(sig_all, rkeys, rvals, b * K, config.hash_count, thr)
-    emitted = torch.tensor([lo.shape[0]], dtype=torch.int64, device=dev)
+    emitted = torch.tensor([lo.shape[0]], dtype=torch.int64, device=cdev)
     # candidate pairs of the owned cells (sum n(n-1)/2, pipeline.cpp:406-411)
-    cand = torch.tensor([cand_local], dtype=torch.int64, device=dev)
+    cand = torch.tensor([cand_local], dtype=torch.int64, device=cdev)
     dist.all_reduce(cand, group=group)
     dist.all_reduce(emitted, group=group)
     # 6. edges everywhere, union stage

@@ -39,3 +39,54 @@ def test_sharded_nccl_world1_equals_single_gpu(ctx, ref):
     assert got, "planted corpus must produce groups"
     assert res.distinct_pairs == single.distinct_pairs
     assert res.candidate_pairs == single.candidate_pairs
+
+
+def _gpu_worker(rank, world, port, data, offs, out_path):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_01046_b200 import distributed, pipeline
+    from paper_2501_01046_b200.device import Context
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = len(offs) - 1
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    sub = offs[lo:hi + 1] - offs[lo]
+    shard = data[offs[lo]:offs[hi]]
+    ctx = Context(0)
+    res = distributed.dedup_sharded(shard, sub, pipeline.RunConfig(),
+                                    distributed.GpuStages(ctx, torch.device("cuda", 0)))
+    if rank == 0:
+        with open(out_path, "w") as f:
+            json.dump({"groups": [[g.representative, g.members] for g in res.report.groups],
+                       "distinct": res.distinct_pairs, "cand": res.candidate_pairs}, f)
+    dist.destroy_process_group()
+    ctx.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_cuda_stages_several_ranks(ctx, ref, tmp_path, world):
+    # the multi-rank protocol over the REAL device stages: `world` processes
+    # share the one GPU (gloo moves the collective buffers through the host;
+    # NCCL refuses two ranks on one device) -- owner split, all-to-all of cell
+    # records, all-gathers and the union all run on K1..K4
+    import torch.multiprocessing as mp
+
+    from paper_2501_01046_b200 import pipeline
+
+    data, offs = ref.generate_synthetic(2500, 200, gmin=2, gmax=4, edit=(2, 100), len_min=300,
+                                        len_max=900, seed=29)
+    out = str(tmp_path / "r.json")
+    mp.spawn(_gpu_worker, args=(world, _free_port(), data, offs, out), nprocs=world, join=True)
+    got = json.load(open(out))
+    single = pipeline.dedup_packed(data, offs, pipeline.RunConfig(), ctx=ctx)
+    assert got["groups"] == [[g.representative, g.members] for g in single.groups]
+    assert got["groups"]
+    assert got["distinct"] == single.distinct_pairs
+    assert got["cand"] == single.candidate_pairs
