@@ -261,12 +261,19 @@ def main():
         return
     import torch
 
+    # one rank per GPU over NCCL; ND_DIST_BACKEND=gloo lets several ranks
+    # share one GPU (harness check of the multi-rank path, not a measurement)
+    backend = os.environ.get("ND_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2501_01046_b200 import _lib, minhash
     from paper_2501_01046_b200.device import Context
 
@@ -301,7 +308,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

@@ -90,3 +90,24 @@ def test_sharded_cuda_stages_several_ranks(ctx, ref, tmp_path, world):
     assert got["groups"]
     assert got["distinct"] == single.distinct_pairs
     assert got["cand"] == single.candidate_pairs
+
+
+def test_bench_two_ranks_harness(tmp_path):
+    # bench.py's multi-rank path (barriers, max over ranks, sharded dedup,
+    # one JSON line on rank 0) with two ranks sharing the GPU through gloo
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ND_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--docs", "100000", "--no-cpu",
+           "--no-staged"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["dedup"]["documents"] == 200000 and d["gpu_launches"] > 0
