@@ -313,6 +313,22 @@ int nd_stage_compare(nd_ctx* ctx, const uint32_t* d_sig, uint64_t nrows, uint32_
                      const uint32_t* d_keys, const uint32_t* d_vals, uint64_t m,
                      uint64_t key_limit, uint64_t threshold_num, uint64_t threshold_den,
                      uint64_t* npairs_out, uint64_t* candidate_pairs_out);
+/* ---- compare over peer memory (replaces the all-gather of signature rows) ---
+ * Each rank exports its rows (copied into a ctx-owned allocation) as a CUDA
+ * IPC handle; after the handles are all-gathered, nd_peer_open maps the other
+ * ranks' rows (NVLink peer memory) and nd_stage_compare_peer runs
+ * nd_stage_compare with global row g read from the rank r where
+ * row_base[r] <= g < row_base[r+1].  Keep the exported rows alive (no
+ * nd_peer_close) until every rank has finished comparing. */
+#define ND_IPC_HANDLE_BYTES 64
+int nd_peer_export(nd_ctx* ctx, const uint32_t* d_sig, uint64_t rows, uint32_t hash_count,
+                   uint8_t* handle_out);
+int nd_peer_open(nd_ctx* ctx, const uint8_t* handles, const uint64_t* row_base, uint32_t world,
+                 uint32_t self);
+int nd_stage_compare_peer(nd_ctx* ctx, const uint32_t* d_keys, const uint32_t* d_vals,
+                          uint64_t m, uint64_t key_limit, uint64_t threshold_num,
+                          uint64_t threshold_den, uint64_t* npairs_out, uint64_t* candidate_pairs_out);
+int nd_peer_close(nd_ctx* ctx);
 /* copies the pairs of the last nd_stage_compare into device buffers */
 int nd_stage_pairs_copy(nd_ctx* ctx, uint32_t* d_lo, uint32_t* d_hi, uint32_t* d_match);
 /* union stage over gathered pairs (rows < nnodes, repeats allowed): distinct

@@ -151,6 +151,11 @@ SIGNATURES = {
                                         vp, vp]),
     "nd_stage_compare": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, vp, C.c_uint64,
                                    C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p]),
+    "nd_peer_export": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, u8p]),
+    "nd_peer_open": (C.c_int, [vp, u8p, u64p, C.c_uint32, C.c_uint32]),
+    "nd_stage_compare_peer": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64,
+                                        C.c_uint64, u64p, u64p]),
+    "nd_peer_close": (C.c_int, [vp]),
     "nd_stage_pairs_copy": (C.c_int, [vp, vp, vp, vp]),
     "nd_stage_union": (C.c_int, [vp, vp, vp, vp, C.c_uint64, C.c_uint64,
                                  C.POINTER(NdDedupStats)]),

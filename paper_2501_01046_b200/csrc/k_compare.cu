@@ -89,7 +89,7 @@ constexpr int kQueue = 1024;             // survivor slots per CTA (drained ever
 
 template <int Pf>
 __global__ void __launch_bounds__(kThreads)
-    k_compare(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
+    k_compare(const SigView sv, uint32_t H, const uint32_t* __restrict__ rows,
               const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
               const uint32_t* __restrict__ item_cell, const uint64_t* __restrict__ item_off,
               uint32_t min_match, int nb, uint64_t* __restrict__ out_key,
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kThreads)
     valid[r] = ri[r] < n;
     row[r] = valid[r] ? rows[s + ri[r]] : 0;
     if constexpr (Pf > 0) {
-      const uint32_t* my_sig = sig + static_cast<uint64_t>(row[r]) * H;
+      const uint32_t* my_sig = sv.row(row[r]);
 #pragma unroll
       for (int k = 0; k < Pf; ++k) pre[r][k] = valid[r] ? __ldg(my_sig + k) : 0xFFFFFFFFu;
     }
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kThreads)
       __syncthreads();
       for (uint32_t idx = threadIdx.x; idx < cmax * Pf; idx += kThreads) {
         const uint32_t c = idx / Pf, k = idx % Pf;
-        cols[c][k] = __ldg(sig + static_cast<uint64_t>(col_row[c]) * H + k);
+        cols[c][k] = __ldg(sv.row(col_row[c]) + k);
       }
     }
     __syncthreads();
@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(kThreads)
             queue[slot] = make_uint2(row[r], other);
           } else {  // queue full: count inline
             bool alive;
-            const uint32_t m = full_matches(sig + static_cast<uint64_t>(row[r]) * H,
-                                            sig + static_cast<uint64_t>(other) * H, H, allowed, alive);
+            const uint32_t m = full_matches(sv.row(row[r]),
+                                            sv.row(other), H, allowed, alive);
             if (alive && m >= min_match) emit(row[r], other, m, nb, out_key, out_m, count, cap);
           }
         }
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kThreads)
     for (uint32_t t = warp; t < lim; t += kWarpsPerBlock) {
       const uint2 pr = queue[t];
       uint32_t m;
-      if (warp_count(sig + static_cast<uint64_t>(pr.x) * H, sig + static_cast<uint64_t>(pr.y) * H, H,
+      if (warp_count(sv.row(pr.x), sv.row(pr.y), H,
                      allowed, min_match, m) && lane == 0)
         emit(pr.x, pr.y, m, nb, out_key, out_m, count, cap);
     }
@@ -211,14 +211,14 @@ __global__ void __launch_bounds__(kThreads)
 // early-exit count (oracle.cpp:81-92) and accepted pairs are emitted.
 constexpr int kJoinThreads = 256;
 
-__device__ __forceinline__ void join_check(const uint32_t* __restrict__ sig, uint32_t H,
+__device__ __forceinline__ void join_check(const SigView sv, uint32_t H,
                                            uint32_t ra, uint32_t rb, uint32_t k, uint32_t P,
                                            uint32_t min_match, int nb,
                                            uint64_t* __restrict__ out_key,
                                            uint32_t* __restrict__ out_m,
                                            unsigned long long* __restrict__ count, uint64_t cap) {
-  const uint32_t* a = sig + static_cast<uint64_t>(ra) * H;
-  const uint32_t* b = sig + static_cast<uint64_t>(rb) * H;
+  const uint32_t* a = sv.row(ra);
+  const uint32_t* b = sv.row(rb);
   const uint32_t allowed = H - min_match;
   uint32_t matches = 0, first = 0xFFFFFFFFu, pc;
   if (H >= 32 && (H & 3) == 0) {
@@ -265,7 +265,7 @@ __device__ __forceinline__ void join_check(const uint32_t* __restrict__ sig, uin
 // DPT = documents per thread (join_max <= DPT * kJoinThreads)
 template <int DPT>
 __global__ void __launch_bounds__(kJoinThreads)
-    k_join(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
+    k_join(const SigView sv, uint32_t H, const uint32_t* __restrict__ rows,
            const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
            uint32_t join_max, uint32_t tbits, uint32_t P, uint32_t min_match, int nb,
            uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kJoinThreads)
     for (int j = 0; j < DPT; ++j) {
       const uint32_t d = threadIdx.x + j * kJoinThreads;
       if (d < n) {
-        const uint32_t* r = sig + static_cast<uint64_t>(rowsm[d]) * H + k0;
+        const uint32_t* r = sv.row(rowsm[d]) + k0;
         if (vec && k0 + 4 <= H)
           val[j] = __ldg(reinterpret_cast<const uint4*>(r));
         else
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kJoinThreads)
       __syncthreads();
       for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads)
         for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e])
-          join_check(sig, H, rowsm[d], rowsm[e], k, P, min_match, nb, out_key, out_m, count, cap);
+          join_check(sv, H, rowsm[d], rowsm[e], k, P, min_match, nb, out_key, out_m, count, cap);
       __syncthreads();
     }
   }
@@ -395,15 +395,15 @@ __device__ __forceinline__ bool same_block(const uint32_t* __restrict__ a,
 }
 
 template <int BW>
-__device__ __forceinline__ void join_check_blocks(const uint32_t* __restrict__ sig, uint32_t H,
+__device__ __forceinline__ void join_check_blocks(const SigView sv, uint32_t H,
                                                   uint32_t ra, uint32_t rb, uint32_t k, bool vec,
                                                   uint32_t min_match, int nb,
                                                   uint64_t* __restrict__ out_key,
                                                   uint32_t* __restrict__ out_m,
                                                   unsigned long long* __restrict__ count,
                                                   uint64_t cap) {
-  const uint32_t* a = sig + static_cast<uint64_t>(ra) * H;
-  const uint32_t* b = sig + static_cast<uint64_t>(rb) * H;
+  const uint32_t* a = sv.row(ra);
+  const uint32_t* b = sv.row(rb);
   if (!same_block<BW>(a + k * BW, b + k * BW, vec)) return;  // fingerprint collision
   for (uint32_t j = 0; j < k; ++j)
     if (same_block<BW>(a + j * BW, b + j * BW, vec)) return;  // counted at block j
@@ -414,7 +414,7 @@ __device__ __forceinline__ void join_check_blocks(const uint32_t* __restrict__ s
 
 template <int DPT, int BW>
 __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
-    k_join_blocks(const uint32_t* __restrict__ sig, uint32_t H, const uint32_t* __restrict__ rows,
+    k_join_blocks(const SigView sv, uint32_t H, const uint32_t* __restrict__ rows,
                   const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
                   uint32_t join_max, uint32_t tbits, uint32_t NB, uint32_t min_match, int nb,
                   uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
     for (int j = 0; j < DPT; ++j) {
       const uint32_t d = threadIdx.x + j * kJoinThreads;
       if (d < n) {
-        const uint32_t* r = sig + static_cast<uint64_t>(rowsm[d]) * H + p0;
+        const uint32_t* r = sv.row(rowsm[d]) + p0;
         uint32_t v[VL];
         if (full) {
           load_block<VL>(r, true, v);
@@ -493,14 +493,14 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
       __syncthreads();
       for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads)
         for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e])
-          join_check_blocks<BW>(sig, H, rowsm[d], rowsm[e], k, vec, min_match, nb, out_key, out_m,
+          join_check_blocks<BW>(sv, H, rowsm[d], rowsm[e], k, vec, min_match, nb, out_key, out_m,
                                 count, cap);
       __syncthreads();
     }
   }
 }
 
-using CmpFn = void (*)(const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
+using CmpFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                        const uint32_t*, const uint32_t*, const uint64_t*, uint32_t, int,
                        uint64_t*, uint32_t*, unsigned long long*, uint64_t);
 
@@ -514,7 +514,7 @@ int compare_prefilter_width(uint32_t H, uint32_t min_match) {
   return 0;
 }
 
-void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32_t min_match,
+void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_match,
                     int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,
                     uint64_t cap, cudaStream_t s) {
   if (cs.ncells == 0 || min_match > H) return;
@@ -537,7 +537,7 @@ void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32
     if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
     const unsigned grid = static_cast<unsigned>(cs.ncells);
     if (join_mode == 2 && BW > 1) {
-      using JoinBFn = void (*)(const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
+      using JoinBFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                                const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, int,
                                uint64_t*, uint32_t*, unsigned long long*, uint64_t);
       const int dpt = join_max <= 2 * kJoinThreads   ? 2
@@ -558,7 +558,7 @@ void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32
                                           count, cap);
       ND_CHECK_LAUNCH();
     } else {
-      using JoinFn = void (*)(const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
+      using JoinFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                               const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, int,
                               uint64_t*, uint32_t*, unsigned long long*, uint64_t);
       JoinFn fn = join_max <= 2 * kJoinThreads   ? k_join<2>

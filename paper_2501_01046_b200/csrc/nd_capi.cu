@@ -59,6 +59,8 @@ nd_ctx::~nd_ctx() {
     if (slot[i].comp) cudaStreamDestroy(slot[i].comp);
   }
   pinned_off.release();
+  for (void* p : peer.opened) cudaIpcCloseMemHandle(p);
+  for (auto* b : {&peer.own, &peer.bases, &peer.row_base}) b->release();
   for (auto& r : ring) r.release();
   synth_buf.release();
   sig_scratch.release();

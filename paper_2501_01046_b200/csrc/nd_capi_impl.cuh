@@ -30,6 +30,13 @@ struct nd_ctx {
   ndb::DedupState api, api2;    // last nd_compare_cells / nd_union
   ndb::DedupState h2d_state;    // text staging of nd_signatures_h2d
   ndb::SortScratch stage_sort;  // nd_stage_cell_records
+  struct Peer {                 // signature rows of every rank in peer memory (nd_peer.cu)
+    ndb::DevBuf own, bases, row_base;
+    std::vector<void*> opened;  // IPC mappings of the other ranks' rows
+    ndb::SigView view;
+    uint32_t world = 0, H = 0;
+    uint64_t rows = 0;
+  } peer;
   uint64_t hbm_budget = 0;      // compare-stage HBM budget (0 = 70 % of free memory)
   uint64_t family_seed = 0;
   bool family_derived = false;  // family came from derive_family(family_seed, ...)
@@ -47,6 +54,8 @@ void validate(const nd_params& p);                 // RunConfig::validate, artif
 void ensure_family(nd_ctx* ctx, const nd_params& p);  // derive + upload when it changed
 // K3 + distinct pairs over st.cells (grows the pair buffer on overflow)
 void compare_and_unique(DedupState& st, const uint32_t* d_sig, uint32_t H, uint32_t mm,
+                        uint64_t nrows, cudaStream_t s);
+void compare_and_unique(DedupState& st, const SigView& d_sig, uint32_t H, uint32_t mm,
                         uint64_t nrows, cudaStream_t s);
 // signatures of a host batch into device buffers (pipelined H2D, text kept in st.text)
 void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uint64_t* offsets,

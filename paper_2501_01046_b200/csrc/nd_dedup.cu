@@ -67,6 +67,11 @@ void ensure_family(nd_ctx* ctx, const nd_params& p) {
 // re-runs once if the first pass overflowed it)
 void compare_and_unique(DedupState& st, const uint32_t* d_sig, uint32_t H, uint32_t mm,
                         uint64_t nrows, cudaStream_t s) {
+  compare_and_unique(st, SigView(d_sig, H), H, mm, nrows, s);
+}
+
+void compare_and_unique(DedupState& st, const SigView& d_sig, uint32_t H, uint32_t mm,
+                        uint64_t nrows, cudaStream_t s) {
   PairSet& ps = st.pairs;
   ps.nb = std::max(1, bits_for(nrows ? nrows - 1 : 0));
   if (2 * ps.nb > 64) fail(ND_ERR_CONFIG, "too many rows for packed pair keys");

@@ -183,7 +183,25 @@ struct PairSet {
   }
 };
 int compare_prefilter_width(uint32_t H, uint32_t min_match);
-void launch_compare(const CellSet& cs, const uint32_t* d_sig, uint32_t H, uint32_t min_match,
+// Signature rows as K3 reads them: one table (world == 1), or the rows of
+// `world` ranks in peer memory (global row g lives on the rank r with
+// row_base[r] <= g < row_base[r+1]; bases[] are IPC-mapped peer pointers).
+struct SigView {
+  const uint32_t* base0 = nullptr;
+  const uint32_t* const* bases = nullptr;  // device array [world]
+  const uint64_t* row_base = nullptr;      // device array [world + 1]
+  uint32_t world = 1;
+  uint32_t H = 0;
+  __host__ __device__ SigView() {}
+  __host__ __device__ SigView(const uint32_t* b, uint32_t h) : base0(b), H(h) {}
+  __device__ __forceinline__ const uint32_t* row(uint32_t g) const {
+    if (world <= 1) return base0 + static_cast<uint64_t>(g) * H;
+    uint32_t r = 0;
+    while (r + 1 < world && g >= row_base[r + 1]) ++r;
+    return bases[r] + (static_cast<uint64_t>(g) - row_base[r]) * H;
+  }
+};
+void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_match,
                     int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,
                     uint64_t cap, cudaStream_t s);
 uint64_t unique_pairs(PairSet& ps, cudaStream_t s);

@@ -11,7 +11,10 @@ contiguous ranges so that any number of GPUs is balanced (nd_cell_partition).
      split by owner range -> all-to-all (counts, then records).  Records
      arrive grouped by source rank = ascending rows, so a stable regroup keeps
      each cell's rows ascending, like the reference's file scan.
-  4. All-gather of the signature rows (every owner compares against any row).
+  4. Every owner must read any row: by default each rank exports its rows as
+     a CUDA IPC handle, the handles are all-gathered and K3 reads the other
+     ranks' rows in peer memory over NVLink (nd_peer.cu); ND_PEER_SIGS=0 (and
+     the CPU protocol tests) all-gather the rows instead.
   5. K2+K3 on the owned cells -> distinct pairs (global rows).
   6. All-gather of the pairs; K4 (distinct + components) on every rank
      (cheap, identical everywhere); rank 0 writes / returns the report.
@@ -24,6 +27,7 @@ NCCL over NVLink on GPUs, gloo on CPU for the protocol tests.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -100,6 +104,40 @@ class GpuStages:
             C.c_void_p(m.data_ptr())))
         self.ctx_sync()
         return lo[:k], hi[:k], m[:k], cand.value
+
+    # ---- compare over peer memory (nd_peer.cu): the other ranks' rows are read
+    # in place through CUDA IPC mappings instead of being all-gathered
+    peer_capable = True
+
+    def export_rows(self, sig) -> bytes:
+        h = (C.c_uint8 * 64)()
+        self.ctx.check(self.ctx.lib.nd_peer_export(self.ctx.h, C.c_void_p(sig.data_ptr()),
+                                                   sig.shape[0], sig.shape[1], h))
+        return bytes(h)
+
+    def open_peers(self, handles: bytes, row_base, world: int, rank: int) -> None:
+        hb = (C.c_uint8 * len(handles)).from_buffer_copy(handles)
+        rb = np.ascontiguousarray(row_base, np.uint64)
+        self.ctx.check(self.ctx.lib.nd_peer_open(self.ctx.h, hb, rb.ctypes.data_as(_lib.u64p),
+                                                 world, rank))
+
+    def compare_peer(self, keys, vals, key_limit, threshold):
+        t = self.torch
+        num, den = threshold
+        npairs, cand = C.c_uint64(), C.c_uint64()
+        self.ctx.check(self.ctx.lib.nd_stage_compare_peer(
+            self.ctx.h, C.c_void_p(keys.data_ptr()), C.c_void_p(vals.data_ptr()), keys.shape[0],
+            key_limit, num, den, C.byref(npairs), C.byref(cand)))
+        k = npairs.value
+        lo, hi, m = (self.tensor((max(k, 1),), t.int32) for _ in range(3))
+        self.ctx.check(self.ctx.lib.nd_stage_pairs_copy(
+            self.ctx.h, C.c_void_p(lo.data_ptr()), C.c_void_p(hi.data_ptr()),
+            C.c_void_p(m.data_ptr())))
+        self.ctx_sync()
+        return lo[:k], hi[:k], m[:k], cand.value
+
+    def close_peers(self) -> None:
+        self.ctx.check(self.ctx.lib.nd_peer_close(self.ctx.h))
 
     def union(self, lo, hi, m, nnodes):
         st = NdDedupStats()
@@ -187,11 +225,25 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists") -> S
     dist.all_to_all_single(rkeys, keys.to(cdev), recv, send, group=group)
     dist.all_to_all_single(rvals, vals.to(cdev), recv, send, group=group)
     rkeys, rvals = rkeys.to(dev), rvals.to(dev)
-    # 4. all signature rows on every rank
-    sig_all, _ = _all_gather_var(dist, sig, group, torch)
-    # 5. compare the owned cells
     thr = _ratio(config.threshold)
-    lo, hi, m, cand_local = stages.compare(sig_all, rkeys, rvals, b * K, config.hash_count, thr)
+    if getattr(stages, "peer_capable", False) and os.environ.get("ND_PEER_SIGS", "1") != "0":
+        # 4+5. compare the owned cells reading every rank's rows in peer memory:
+        # exchange IPC handles, map, compare, and keep the rows alive until
+        # every rank is done (barrier)
+        h = torch.tensor(list(stages.export_rows(sig)), dtype=torch.uint8, device=cdev)
+        hs = [torch.empty_like(h) for _ in range(world)]
+        dist.all_gather(hs, h, group=group)
+        handles = b"".join(bytes(x.cpu().tolist()) for x in hs)
+        row_base = [sum(counts[:r]) for r in range(world + 1)]
+        stages.open_peers(handles, row_base, world, rank)
+        lo, hi, m, cand_local = stages.compare_peer(rkeys, rvals, b * K, thr)
+        dist.barrier(group=group)
+        stages.close_peers()
+    else:
+        # 4. all signature rows on every rank
+        sig_all, _ = _all_gather_var(dist, sig, group, torch)
+        # 5. compare the owned cells
+        lo, hi, m, cand_local = stages.compare(sig_all, rkeys, rvals, b * K, config.hash_count, thr)
     emitted = torch.tensor([lo.shape[0]], dtype=torch.int64, device=cdev)
     # candidate pairs of the owned cells (sum n(n-1)/2, pipeline.cpp:406-411)
     cand = torch.tensor([cand_local], dtype=torch.int64, device=cdev)

@@ -70,14 +70,17 @@ def _gpu_worker(rank, world, port, data, offs, out_path):
     ctx.close()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_cuda_stages_several_ranks(ctx, ref, tmp_path, world):
+@pytest.mark.parametrize("world,peer", [(2, "1"), (3, "1"), (2, "0")])
+def test_sharded_cuda_stages_several_ranks(ctx, ref, tmp_path, monkeypatch, world, peer):
     # the multi-rank protocol over the REAL device stages: `world` processes
     # share the one GPU (gloo moves the collective buffers through the host;
     # NCCL refuses two ranks on one device) -- owner split, all-to-all of cell
-    # records, all-gathers and the union all run on K1..K4
+    # records, all-gathers and the union all run on K1..K4.  peer="1": K3 reads
+    # the other ranks' signature rows through CUDA IPC mappings (nd_peer.cu);
+    # "0": the rows are all-gathered
     import torch.multiprocessing as mp
 
+    monkeypatch.setenv("ND_PEER_SIGS", peer)
     from paper_2501_01046_b200 import pipeline
 
     data, offs = ref.generate_synthetic(2500, 200, gmin=2, gmax=4, edit=(2, 100), len_min=300,
