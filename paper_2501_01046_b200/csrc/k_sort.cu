@@ -8,7 +8,8 @@
 //
 // Per pass: k_upsweep (per-tile digit histogram) -> exclusive scan of the
 // digit-major [256 x tiles] histogram -> k_downsweep (warp-level stable
-// ranking with __match_any_sync, scatter).  HBM-bound: 2 reads + 1 write of
+// ranking with __match_any_sync, the tile staged in shared memory in digit
+// order, then each digit's run written contiguously).  HBM-bound: 2 reads + 1 write of
 // the records per pass.
 #include "nd_internal.cuh"
 
@@ -53,6 +54,9 @@ __global__ void __launch_bounds__(kSortThreads)
   constexpr int kWarpsPerBlock = kSortThreads / 32;
   __shared__ uint32_t whist[kWarpsPerBlock][kRadix];
   __shared__ uint64_t base_off[kRadix];
+  __shared__ uint32_t tile_cnt[kRadix], tile_start[kRadix];
+  __shared__ K sk[kSortTile];
+  __shared__ V sv[kSortTile];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < kWarpsPerBlock * kRadix; i += kSortThreads)
     (&whist[0][0])[i] = 0;
@@ -80,7 +84,7 @@ __global__ void __launch_bounds__(kSortThreads)
     __syncwarp();
   }
   __syncthreads();
-  // exclusive scan across warps, per digit
+  // exclusive scan across warps, per digit; tile digit totals
   for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
     uint32_t acc = 0;
 #pragma unroll
@@ -89,14 +93,49 @@ __global__ void __launch_bounds__(kSortThreads)
       whist[w][d] = acc;
       acc += c;
     }
+    tile_cnt[d] = acc;
   }
   __syncthreads();
+  // exclusive scan of the tile's digit totals (one warp, 8 digits per lane)
+  if (warp == 0) {
+    uint32_t c[kRadix / 32], sum = 0;
+#pragma unroll
+    for (int q = 0; q < kRadix / 32; ++q) {
+      c[q] = tile_cnt[lane * (kRadix / 32) + q];
+      sum += c[q];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int q = 0; q < kRadix / 32; ++q) {
+      tile_start[lane * (kRadix / 32) + q] = run;
+      run += c[q];
+    }
+  }
+  __syncthreads();
+  // stage the tile in digit order, then write each digit's run contiguously
+  // (consecutive threads -> consecutive addresses: coalesced stores)
 #pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
     if (dg[r] == 0xFFFFFFFFu) continue;
-    uint64_t dst = base_off[dg[r]] + whist[warp][dg[r]] + rk[r];
-    keys_out[dst] = k[r];
-    vals_out[dst] = v[r];
+    const uint32_t lp = tile_start[dg[r]] + whist[warp][dg[r]] + rk[r];
+    sk[lp] = k[r];
+    sv[lp] = v[r];
+  }
+  __syncthreads();
+  const uint64_t tbase = static_cast<uint64_t>(blockIdx.x) * kSortTile;
+  const uint32_t tn = n - tbase < kSortTile ? static_cast<uint32_t>(n - tbase) : kSortTile;
+  for (uint32_t i = threadIdx.x; i < tn; i += kSortThreads) {
+    const K key = sk[i];
+    const uint32_t d = digit_of(key, shift);
+    const uint64_t dst = base_off[d] + (i - tile_start[d]);
+    keys_out[dst] = key;
+    vals_out[dst] = sv[i];
   }
 }
 
