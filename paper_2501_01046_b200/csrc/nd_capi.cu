@@ -62,6 +62,9 @@ nd_ctx::~nd_ctx() {
   for (void* p : peer.opened) cudaIpcCloseMemHandle(p);
   for (auto* b : {&peer.own, &peer.bases, &peer.row_base}) b->release();
   for (auto& r : ring) r.release();
+  for (auto& r : ring_scratch) r.release();
+  for (auto& r : ring_stream)
+    if (r) cudaStreamDestroy(r);
   synth_buf.release();
   sig_scratch.release();
   dedup.release();
@@ -84,6 +87,11 @@ void nd_ctx::ensure_streams() {
     ND_CUDA(cudaEventCreateWithFlags(&slot[i].comp_done, cudaEventDisableTiming));
     ND_CUDA(cudaEventCreateWithFlags(&slot[i].d2h_done, cudaEventDisableTiming));
   }
+}
+
+void nd_ctx::ensure_ring_streams() {
+  for (auto& r : ring_stream)
+    if (!r) ND_CUDA(cudaStreamCreateWithFlags(&r, cudaStreamNonBlocking));
 }
 
 void nd_ctx::require_family() const {

@@ -21,6 +21,8 @@ struct nd_ctx {
   } slot[2];
   ndb::PinnedBuf pinned_off;
   ndb::DevBuf ring[3];          // text chunks streaming through h2d_signatures
+  cudaStream_t ring_stream[3] = {nullptr, nullptr, nullptr};
+  ndb::SigScratch ring_scratch[3];
   ndb::DevBuf synth_buf;
   ndb::DevBuf fam_buf, sig_in_text, sig_in_off;
   ndb::DevFamily fam;
@@ -44,6 +46,7 @@ struct nd_ctx {
 
   ~nd_ctx();
   void ensure_streams();
+  void ensure_ring_streams();
   void require_family() const;
 };
 

@@ -133,10 +133,13 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   }
   // the text streams through a ring of kRing chunk buffers: only signatures
   // and band keys stay in HBM, so the batch is bounded by 4H+4b bytes per
-  // document, not by its text
+  // document, not by its text.  Each slot has its own compute stream and K1
+  // scratch, so consecutive chunks' K1 launches overlap and one launch's tail
+  // (the longest documents of a lognormal chunk) does not idle the GPU.
   constexpr int kRing = 3;
   uint8_t* ring[kRing];
   for (int r = 0; r < kRing; ++r) ring[r] = ctx->ring[r].as<uint8_t>(max_bytes + 16);
+  ctx->ensure_ring_streams();
   cudaEvent_t start, k1_done[kRing];
   ND_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
   for (auto& e : k1_done) ND_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -147,21 +150,23 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   for (size_t c = 0; c < chunks.size(); ++c) {
     const auto [d0, d1] = chunks[c];
     const int r = static_cast<int>(c % kRing);
+    cudaStream_t cs = ctx->ring_stream[r];
     if (c >= kRing) ND_CUDA(cudaStreamWaitEvent(ctx->h2d, k1_done[r], 0));  // slot free again
     ND_CUDA(cudaMemcpyAsync(ring[r], bytes + offsets[0] + h_off[d0], h_off[d1] - h_off[d0],
                             cudaMemcpyHostToDevice, ctx->h2d));
     cudaEvent_t ev;
     ND_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     ND_CUDA(cudaEventRecord(ev, ctx->h2d));
-    ND_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    ND_CUDA(cudaStreamWaitEvent(cs, ev, 0));
     evs.push_back(ev);
     // offsets stay batch-absolute: the kernel reads text + offset, so the
     // text pointer is the slot shifted back by the chunk's first offset
     launch_signatures(ctx->fam, ring[r] - h_off[d0], d_off + d0, d1 - d0, bands, rows, K,
-                      d_sig + d0 * H, d_band ? d_band + d0 * bands : nullptr, st.sig_scratch, s,
-                      false, h_off + d0);
-    ND_CUDA(cudaEventRecord(k1_done[r], s));
+                      d_sig + d0 * H, d_band ? d_band + d0 * bands : nullptr,
+                      ctx->ring_scratch[r], cs, false, h_off + d0);
+    ND_CUDA(cudaEventRecord(k1_done[r], cs));
   }
+  for (int r = 0; r < kRing; ++r) ND_CUDA(cudaStreamWaitEvent(s, k1_done[r], 0));
   // events may be destroyed once enqueued work referencing them is recorded
   for (auto ev : evs) cudaEventDestroy(ev);
   for (auto e : k1_done) cudaEventDestroy(e);
