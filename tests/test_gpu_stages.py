@@ -134,3 +134,28 @@ def test_eval_accuracy_byte_identical(ctx, ref, tmp_path):
     want = open(os.path.join(ws_ref, "accuracy.json"), "rb").read()
     assert open(os.path.join(ws_gpu, "accuracy.json"), "rb").read() == want
     assert acc["corpus_size"] == 1200
+
+
+@pytest.mark.parametrize("H,bands,rows,thr,L", [(100, 20, 5, (4, 5), 5), (60, 12, 5, (3, 4), 4),
+                                                (512, 64, 8, (4, 5), 5), (32, 8, 4, (1, 2), 3),
+                                                (256, 16, 16, (9, 10), 7)])
+def test_unusual_shapes_workspace_byte_identical(ctx, ref, tmp_path, H, bands, rows, thr, L):
+    # hash counts that are not a K1 tile size (padded families), one- to
+    # 16-row bands, other shingle lengths and thresholds: every artifact equal
+    corpus = _corpus_dir(ref, tmp_path, n=900, groups=90, seed=H + L)
+    ws_ref, ws_gpu = str(tmp_path / "ref"), str(tmp_path / "gpu")
+    os.makedirs(ws_ref)
+    ref.run_dedup(corpus, ws_ref, H=H, bands=bands, rows=rows, L=L, thr=thr, workers=2,
+                  memory_budget=400_000)
+    cfg = pipeline.RunConfig(inputs=[corpus], workspace=ws_gpu, hash_count=H, bands=bands,
+                             rows=rows, shingle_len=L, threshold=thr, workers=2,
+                             memory_budget=400_000)
+    pipeline.run_dedup(cfg, ctx=ctx)
+    want, got = _tree(ws_ref), _tree(ws_gpu)
+    assert sorted(got) == sorted(want)
+    cs_ref, cs_gpu = (json.loads(x.pop("compare_stage.json")) for x in (want, got))
+    cs_ref.pop("gather_peak_bytes")
+    cs_gpu.pop("gather_peak_bytes")
+    assert cs_gpu == cs_ref
+    for k in want:
+        assert got[k] == want[k], k
