@@ -9,7 +9,7 @@ import threading
 import numpy as np
 
 from . import _lib
-from ._lib import check, u8p, u32p, u64p
+from ._lib import check
 
 
 def _p(a: np.ndarray, t):

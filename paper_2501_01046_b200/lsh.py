@@ -15,7 +15,7 @@ from fractions import Fraction
 import numpy as np
 
 from . import _lib
-from ._lib import check, u32p, u64p
+from ._lib import check, u32p
 from .device import Context, default_context
 
 

@@ -26,7 +26,7 @@ from .corpus import CorpusManifest, build_manifest, surviving_documents, survivi
 from .dedup_graph import DedupReport, DuplicateGroup
 from .device import Context, default_context
 from .lsh import _ratio
-from .minhash import ShingleUnit, pack_documents
+from .minhash import ShingleUnit, pack_documents  # noqa: F401  (re-exported: the reference API)
 
 
 @dataclass
