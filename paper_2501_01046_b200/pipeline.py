@@ -485,3 +485,35 @@ def run_dedup(config: RunConfig, ctx: Context | None = None, timings: dict | Non
     if timings is not None:
         timings.update(t)
     return rep
+
+
+@dataclass
+class BenchRow:
+    workers: int
+    timings: dict
+
+
+def run_bench(config: RunConfig, worker_counts, ctx: Context | None = None) -> list[BenchRow]:
+    """pipeline.cpp:587-613: one full run_dedup per worker count, each in its own
+    sub-workspace (bench_w<N>), and bench.json with the stage times.  On the GPU
+    the worker count only shapes the gather-pass plan (and so the pair files),
+    never the report."""
+    from dataclasses import replace
+
+    if not worker_counts:
+        raise _lib.ConfigError(_lib.ND_ERR_CONFIG, "bench needs at least one worker count")
+    rows = []
+    for w in worker_counts:
+        sub = replace(config, workers=w or 1,
+                      workspace=config.workspace + f"/bench_w{w or 1}")
+        os.makedirs(sub.workspace, exist_ok=True)
+        t = {}
+        run_dedup(sub, ctx, timings=t)
+        rows.append(BenchRow(sub.workers, t))
+    os.makedirs(config.workspace, exist_ok=True)
+    _write_text(config.workspace + "/bench.json",
+                _dump2([{"workers": r.workers, "hash_seconds": r.timings["hash_seconds"],
+                         "compare_seconds": r.timings["compare_seconds"],
+                         "union_seconds": r.timings["union_seconds"],
+                         "total_seconds": r.timings["total_seconds"]} for r in rows]))
+    return rows

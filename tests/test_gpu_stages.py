@@ -159,3 +159,18 @@ def test_unusual_shapes_workspace_byte_identical(ctx, ref, tmp_path, H, bands, r
     assert cs_gpu == cs_ref
     for k in want:
         assert got[k] == want[k], k
+
+
+def test_run_bench_layout(ctx, ref, tmp_path):
+    # run_bench (pipeline.cpp:587-613): sub-workspaces per worker count with
+    # identical reports, bench.json rows in the reference's key order
+    corpus = _corpus_dir(ref, tmp_path, n=400, groups=40, seed=31)
+    cfg = pipeline.RunConfig(inputs=[corpus], workspace=str(tmp_path / "b"))
+    rows = pipeline.run_bench(cfg, [1, 3], ctx=ctx)
+    assert [r.workers for r in rows] == [1, 3]
+    b = json.load(open(os.path.join(cfg.workspace, "bench.json")))
+    assert [list(r) for r in b] == [["workers", "hash_seconds", "compare_seconds",
+                                     "union_seconds", "total_seconds"]] * 2
+    t1, t3 = (_tree(os.path.join(cfg.workspace, f"bench_w{w}")) for w in (1, 3))
+    for f in ("groups.jsonl", "removal.txt", "summary.json"):
+        assert t1[f] == t3[f]
