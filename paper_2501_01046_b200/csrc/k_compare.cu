@@ -531,17 +531,12 @@ void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_
       break;
     }
   if (join_max >= 2 && P <= 510) {
-    // hash table size: the block join keeps the load factor <= 0.8 (its
-    // shared memory, not its probes, limits residency: at n ~ 2700 a 2x
-    // table allows 2 CTAs per SM, 1.25x allows 4); the per-position join <= 0.5
-    const bool blocks = join_mode == 2 && BW > 1;
-    const uint32_t want = blocks ? join_max + join_max / 4 : 2 * join_max;
     uint32_t tbits = 4;
-    while ((1u << tbits) < want) ++tbits;
+    while ((1u << tbits) < 2 * join_max) ++tbits;
     const size_t smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
     if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
     const unsigned grid = static_cast<unsigned>(cs.ncells);
-    if (blocks) {
+    if (join_mode == 2 && BW > 1) {
       using JoinBFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                                const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, int,
                                uint64_t*, uint32_t*, unsigned long long*, uint64_t);
