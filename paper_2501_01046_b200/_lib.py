@@ -85,6 +85,10 @@ SIGNATURES = {
     "nd_last_error_global": (C.c_char_p, []),
     "nd_derive_family": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                    C.POINTER(NdHashFn)]),
+    "nd_mod_pow": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, u64p]),
+    "nd_is_prime_u32": (C.c_int, [C.c_uint32]),
+    "nd_hash_window_direct": (C.c_int, [u32p, C.c_uint32, C.POINTER(NdHashFn), u32p]),
+    "nd_roll_next": (C.c_uint32, [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(NdHashFn)]),
     "nd_choose_bucket_count": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, u32p]),
     "nd_min_matches": (C.c_uint32, [C.c_uint32, C.c_uint64, C.c_uint64]),
     "nd_band_partition": (C.c_int, [C.c_uint32, C.c_uint32, u32p]),

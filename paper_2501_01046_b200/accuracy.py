@@ -2,6 +2,7 @@
 run_eval_accuracy (pipeline.cpp:534-585), SURVEY 8f rank 4.
 
   exact_window_jaccard     oracle.cpp:32-51   (host; set arithmetic on windows)
+  estimator_error_stats    oracle.cpp:143-162 (K1 signatures + exact Jaccard per pair)
   all_pairs_dupset         oracle.cpp:53-108  -> K3 over ONE cell holding every document
   standard_minhash_dupset  oracle.cpp:110-122 -> K1 + the above
   dupset_jaccard           oracle.cpp:124-141 (host merge of sorted id lists)
@@ -19,7 +20,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import compare, minhash, pipeline
+from . import _lib, compare, minhash, pipeline
 from .compare import GatheredBucket, GatherResult, SimilarityThreshold
 from .device import Context
 from .lsh import BucketKey
@@ -40,16 +41,59 @@ class NearDuplicateSet:
     doc_ids: list[int]
 
 
-def exact_window_jaccard(a: bytes, b: bytes, shingle_len: int) -> JaccardResult:
-    """|A ∩ B| / |A ∪ B| over distinct byte windows (oracle.cpp:32-51)."""
+def _units(t: bytes, unit) -> list:
+    if unit == minhash.ShingleUnit.BYTE:
+        return list(t)
+    # decode_codepoints (text.cpp:101-113): CPython's decoder replaces the same
+    # maximal ill-formed subparts with U+FFFD (pinned in tests/test_oracle.py)
+    return [ord(c) for c in t.decode("utf-8", errors="replace")]
+
+
+def exact_window_jaccard(a, b, shingle_len: int,
+                         unit=minhash.ShingleUnit.BYTE) -> JaccardResult:
+    """|A ∩ B| / |A ∪ B| over distinct unit windows (oracle.cpp:32-51)."""
     if shingle_len == 0:
-        raise ValueError("shingle length must be positive")
-    if len(a) < shingle_len or len(b) < shingle_len:
-        raise minhash.ShortDocumentError(6, f"document too short for a {shingle_len}-unit window")
-    sa = {a[i:i + shingle_len] for i in range(len(a) - shingle_len + 1)}
-    sb = {b[i:i + shingle_len] for i in range(len(b) - shingle_len + 1)}
+        raise _lib.ConfigError(_lib.ND_ERR_CONFIG, "shingle length must be positive")
+    ua = _units(a.encode() if isinstance(a, str) else bytes(a), unit)
+    ub = _units(b.encode() if isinstance(b, str) else bytes(b), unit)
+    if len(ua) < shingle_len or len(ub) < shingle_len:
+        raise minhash.ShortDocumentError(_lib.ND_ERR_SHORT,
+                                         f"document too short for a {shingle_len}-unit window")
+    sa = {tuple(ua[i:i + shingle_len]) for i in range(len(ua) - shingle_len + 1)}
+    sb = {tuple(ub[i:i + shingle_len]) for i in range(len(ub) - shingle_len + 1)}
     inter = len(sa & sb)
     return JaccardResult(inter, len(sa) + len(sb) - inter)
+
+
+@dataclass
+class PairErrorSample:
+    exact_jaccard: float = 0.0
+    estimated: float = 0.0  # signature match fraction
+    abs_error: float = 0.0
+
+
+@dataclass
+class EstimatorStats:
+    samples: list
+    mean_abs_error: float = 0.0
+
+
+def estimator_error_stats(pairs, family, ctx: Context | None = None) -> EstimatorStats:
+    """oracle.cpp:143-162: exact window Jaccard vs the signature estimate per
+    document pair (signatures on the GPU, one batch for all pairs)."""
+    docs = [d for pair in pairs for d in pair]
+    sigs = minhash.signature_batch(docs, family, ctx=ctx) if docs else []
+    if len(sigs) != len(docs):
+        raise minhash.ShortDocumentError(_lib.ND_ERR_SHORT, "a document has no full window")
+    stats = EstimatorStats([])
+    for i, (a, b) in enumerate(pairs):
+        exact = exact_window_jaccard(a.text, b.text, family.shingle_len, family.unit).value()
+        m = int((sigs[2 * i].values == sigs[2 * i + 1].values).sum())
+        est = m / family.hash_count
+        stats.samples.append(PairErrorSample(exact, est, abs(est - exact)))
+    if stats.samples:
+        stats.mean_abs_error = sum(x.abs_error for x in stats.samples) / len(stats.samples)
+    return stats
 
 
 def all_pairs_dupset(signatures, hash_count: int, threshold: SimilarityThreshold,

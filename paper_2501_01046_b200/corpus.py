@@ -76,6 +76,39 @@ def parse_jsonl_line(line: bytes | str, text_field: str):
     return True, bytes(out[:n.value]), None
 
 
+def for_each_raw_document(path: str, file_ordinal: int, text_field: str, rejects, fn) -> int:
+    """corpus.cpp:56-82: valid records in order (record ordinals count valid
+    records), malformed lines to `rejects` as (path, line, reason); returns the
+    record count.  The bulk loader is JsonlFile; this is the per-record API."""
+    try:
+        fh = open(path, "rb")
+    except OSError as e:
+        raise _lib.IoError(_lib.ND_ERR_IO, f"cannot open '{path}': {e.strerror}")
+    ordinal = 0
+    with fh:
+        for line_no, raw in enumerate(fh, start=1):
+            line = raw[:-1] if raw.endswith(b"\n") else raw
+            if line.endswith(b"\r"):
+                line = line[:-1]
+            if not line:
+                continue
+            ok, text, reason = parse_jsonl_line(line, text_field)
+            if not ok:
+                if rejects is not None:
+                    rejects.append((path, line_no, reason))
+                continue
+            fn(RawDocument(file_ordinal, ordinal, line_no, text))
+            ordinal += 1
+    return ordinal
+
+
+def load_jsonl_file(path: str, file_ordinal: int, text_field: str, rejects=None) -> list[RawDocument]:
+    """corpus.cpp:84-91."""
+    docs = []
+    for_each_raw_document(path, file_ordinal, text_field, rejects, docs.append)
+    return docs
+
+
 def nfc_normalize(text: bytes | str) -> bytes:
     lib = _lib.load()
     raw = _b(text)

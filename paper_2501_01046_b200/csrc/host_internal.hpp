@@ -24,6 +24,10 @@ uint64_t bounded_random(std::mt19937_64& rng, uint64_t bound);
 std::vector<nd_hash_fn> derive_family(uint64_t seed, uint32_t H, uint32_t L, uint32_t unit);
 uint32_t choose_bucket_count(uint64_t n, uint64_t num, uint64_t den);
 uint32_t min_matches(uint32_t H, uint64_t num, uint64_t den);
+uint64_t mod_pow_checked(uint64_t base, uint64_t exp, uint64_t mod);
+bool is_prime(uint32_t n);
+uint32_t hash_window_direct(const uint32_t* w, uint32_t len, const nd_hash_fn& f);
+uint32_t roll_next(uint32_t state, uint32_t outgoing, uint32_t incoming, const nd_hash_fn& f);
 
 // synthetic corpus (synth.cu)
 void synth_generate(const nd_synth_spec& spec, uint8_t* bytes, uint64_t* offsets,

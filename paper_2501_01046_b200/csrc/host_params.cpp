@@ -142,4 +142,40 @@ uint32_t min_matches(uint32_t H, uint64_t num, uint64_t den) {
   return m > H ? H + 1 : static_cast<uint32_t>(m);
 }
 
+// ---- public scalar primitives of minhash.hpp (host) ------------------------
+uint64_t mod_pow_checked(uint64_t base, uint64_t exp, uint64_t mod) {  // minhash.cpp:10-20
+  if (mod == 0) fail(ND_ERR_CONFIG, "mod_pow: zero modulus");
+  return mod_pow(base, exp, mod);
+}
+
+bool is_prime(uint32_t n) { return is_prime_u32(n); }  // minhash.cpp:22-50
+
+namespace {
+// minhash.cpp:61-67: x mod p for x < 2^48 through floor(2^64 / p)
+uint32_t barrett(uint64_t x, const nd_hash_fn& f) {
+  const uint64_t q = static_cast<uint64_t>((static_cast<u128>(x) * f.reduce_factor) >> 64);
+  uint64_t r = x - q * f.modulus;
+  while (r >= f.modulus) r -= f.modulus;
+  return static_cast<uint32_t>(r);
+}
+}  // namespace
+
+// minhash.cpp:111-119 (Horner from the last unit)
+uint32_t hash_window_direct(const uint32_t* w, uint32_t len, const nd_hash_fn& f) {
+  if (len == 0) fail(ND_ERR_CONFIG, "hash_window_direct: empty window");
+  uint64_t acc = 0;
+  for (uint32_t i = len; i-- > 0;) acc = barrett(acc * f.base + w[i], f);
+  return static_cast<uint32_t>(acc);
+}
+
+// minhash.cpp:121-131 (Eq. 5 update)
+uint32_t roll_next(uint32_t state, uint32_t outgoing, uint32_t incoming, const nd_hash_fn& f) {
+  const uint64_t dropped = static_cast<uint64_t>(state) + f.modulus - outgoing;
+  const uint64_t shifted = barrett(dropped * f.base_inverse, f);
+  const uint64_t appended = barrett(static_cast<uint64_t>(incoming) * f.base_power, f);
+  uint64_t sum = shifted + appended;
+  if (sum >= f.modulus) sum -= f.modulus;
+  return static_cast<uint32_t>(sum);
+}
+
 }  // namespace ndb

@@ -203,6 +203,21 @@ int nd_derive_family(uint64_t seed, uint32_t H, uint32_t L, uint32_t unit, nd_ha
   });
 }
 
+int nd_mod_pow(uint64_t base, uint64_t exp, uint64_t mod, uint64_t* out) {
+  return guarded_impl(nullptr, [&] { *out = mod_pow_checked(base, exp, mod); });
+}
+
+int nd_is_prime_u32(uint32_t n) { return is_prime(n) ? 1 : 0; }
+
+int nd_hash_window_direct(const uint32_t* window, uint32_t len, const nd_hash_fn* f,
+                          uint32_t* out) {
+  return guarded_impl(nullptr, [&] { *out = hash_window_direct(window, len, *f); });
+}
+
+uint32_t nd_roll_next(uint32_t state, uint32_t outgoing, uint32_t incoming, const nd_hash_fn* f) {
+  return roll_next(state, outgoing, incoming, *f);
+}
+
 int nd_choose_bucket_count(uint64_t n, uint64_t num, uint64_t den, uint32_t* out) {
   return guarded_impl(nullptr, [&] { *out = choose_bucket_count(n, num, den); });
 }

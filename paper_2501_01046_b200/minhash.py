@@ -26,6 +26,7 @@ from ._lib import ShortDocumentError, check, u8p, u32p, u64p
 from .device import Context, default_context
 
 __all__ = ["ShingleUnit", "HashFunctionParams", "HashFamily", "derive_family", "CleanDocument",
+           "mod_pow", "is_prime_u32", "hash_window_direct", "roll_next",
            "Signature", "ShortDocumentError", "signature_of_document", "signature_batch",
            "pack_documents", "signatures_packed", "signatures_device", "text_units"]
 
@@ -46,6 +47,32 @@ class HashFamily:
     def params(self) -> list[tuple[int, int, int, int, int]]:
         return [(f.modulus, f.base, f.base_inverse, f.base_power, f.reduce_factor)
                 for f in self.functions]
+
+
+def mod_pow(base: int, exp: int, mod: int) -> int:
+    """minhash.cpp:10-20 (ConfigError for a zero modulus)."""
+    out = C.c_uint64()
+    check(_lib.load().nd_mod_pow(base, exp, mod, C.byref(out)))
+    return out.value
+
+
+def is_prime_u32(n: int) -> bool:
+    """minhash.cpp:22-50: Miller-Rabin with bases {2, 3, 5, 7}."""
+    return bool(_lib.load().nd_is_prime_u32(n))
+
+
+def hash_window_direct(window, f: "HashFunctionParams") -> int:
+    """minhash.cpp:111-119: sum c_i q^i mod p by Horner from the last unit."""
+    w = np.ascontiguousarray(window, np.uint32)
+    out = C.c_uint32()
+    check(_lib.load().nd_hash_window_direct(w.ctypes.data_as(u32p), len(w), C.byref(f),
+                                            C.byref(out)))
+    return out.value
+
+
+def roll_next(state: int, outgoing: int, incoming: int, f: "HashFunctionParams") -> int:
+    """minhash.cpp:121-131: the Eq. 5 update."""
+    return int(_lib.load().nd_roll_next(state, outgoing, incoming, C.byref(f)))
 
 
 def derive_family(seed: int, hash_count: int, shingle_len: int,

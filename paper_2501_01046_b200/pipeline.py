@@ -237,6 +237,17 @@ def timings_path(c: RunConfig) -> str:
     return c.workspace + "/timings.json"
 
 
+def accuracy_path(c: RunConfig) -> str:
+    return c.workspace + "/accuracy.json"
+
+
+def run_eval_accuracy(config: RunConfig, ctx: Context | None = None) -> dict:
+    """pipeline.cpp:534-585 (implemented in accuracy.py)."""
+    from .accuracy import run_eval_accuracy as _run
+
+    return _run(config, ctx=ctx)
+
+
 def signatures_dir(c: RunConfig) -> str:
     return c.workspace + "/signatures"
 

@@ -145,3 +145,47 @@ def read_pair_file(path: str):
         check(lib.nd_pairs_read(path.encode(), lo.ctypes.data_as(u64p), hi.ctypes.data_as(u64p),
                                 m.ctypes.data_as(u32p), C.byref(n)))
     return lo, hi, m
+
+
+def scan_gather(paths, expected: SignatureFileHeader, bands, bucket_first: int, bucket_last: int):
+    """sigstore.cpp:228-286: one scan of the signature files keeping, per band in
+    `bands` (an lsh.BandRange), the documents whose bucket lies in
+    [bucket_first, bucket_last); cells of a single document are dropped.  Files
+    must come in source order (doc ids ascending).  Returns a compare.GatherResult
+    (buckets sorted by key, doc ids ascending).  Host reference-API form; the
+    compare stage itself groups every cell on the GPU (nd_compare_stage)."""
+    from .compare import GatheredBucket, GatherResult
+    from .lsh import BucketKey
+
+    if bucket_last > expected.bucket_count or bucket_first > bucket_last:
+        raise _lib.ConfigError(_lib.ND_ERR_CONFIG, "gather bucket interval out of range")
+    if bands.last > expected.bands or bands.first > bands.last:
+        raise _lib.ConfigError(_lib.ND_ERR_CONFIG, "gather band range out of range")
+    width, rng = bucket_last - bucket_first, bands.last - bands.first
+    if width == 0 or rng == 0:
+        return GatherResult([])
+    ids_l, sig_l, band_l = [], [], []
+    for p in paths:
+        h, ids, v, b = read_signature_file(p)
+        if not h.run_compatible(expected):
+            raise _lib.ConfigError(_lib.ND_ERR_CONFIG,
+                                   f"'{p}' was written with different parameters than this run")
+        ids_l.append(ids)
+        sig_l.append(v)
+        band_l.append(b)
+    H = expected.hash_count
+    ids = np.concatenate(ids_l) if ids_l else np.zeros(0, np.uint64)
+    sig = np.concatenate(sig_l) if sig_l else np.zeros((0, H), np.uint32)
+    band = np.concatenate(band_l) if band_l else np.zeros((0, expected.bands), np.uint32)
+    out = []
+    for j in range(bands.first, bands.last):
+        col = band[:, j]
+        for k in range(bucket_first, bucket_last):
+            rows = np.flatnonzero(col == k)
+            if len(rows) < 2:
+                continue
+            if (np.diff(ids[rows].astype(np.int64)) <= 0).any():
+                raise _lib.ConfigError(_lib.ND_ERR_CONFIG, "signature files are not in ascending "
+                                                           "doc_id order; pass them in manifest order")
+            out.append(GatheredBucket(BucketKey(j, k), ids[rows].tolist(), sig[rows].reshape(-1)))
+    return GatherResult(out)

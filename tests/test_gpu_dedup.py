@@ -403,3 +403,29 @@ def test_pigeonhole_join_adversarial(ctx, ref, monkeypatch, H, thr):
         got = compare.compare_bucket(b, H, t, ctx=ctx)
         assert got == want, (mode, len(got), len(want))
     assert want
+
+
+def test_estimator_error_stats(ctx, oracle):
+    # oracle.cpp:143-162: per pair exact window Jaccard vs signature estimate
+    from paper_2501_01046_b200 import accuracy
+
+    rng = np.random.default_rng(5)
+    base = bytes(rng.integers(97, 123, size=800, dtype=np.uint8))
+    edit = bytearray(base)
+    for i in rng.choice(800, size=20, replace=False):
+        edit[i] = 97 + (edit[i] - 96) % 26
+    other = bytes(rng.integers(97, 123, size=700, dtype=np.uint8))
+    D = minhash.CleanDocument
+    pairs = [(D(0, base), D(1, base)), (D(2, base), D(3, bytes(edit))), (D(4, base), D(5, other))]
+    fam = minhash.derive_family(5, 128, 5)
+    st = accuracy.estimator_error_stats(pairs, fam, ctx=ctx)
+    assert st.samples[0].exact_jaccard == 1.0 and st.samples[0].estimated == 1.0
+    assert 0.5 < st.samples[1].exact_jaccard < 0.95
+    sigs = oracle.signatures(np.frombuffer(base + bytes(edit), np.uint8).copy(),
+                             np.array([0, 800, 1600], np.uint64), oracle.derive_family(5, 128))
+    assert st.samples[1].estimated == (sigs[0] == sigs[1]).sum() / 128
+    assert st.samples[2].exact_jaccard < 0.05
+    assert abs(st.mean_abs_error - sum(s.abs_error for s in st.samples) / 3) < 1e-12
+    # codepoint windows
+    j = accuracy.exact_window_jaccard("ЖЖЖЖЖa", "ЖЖЖЖЖb", 5, minhash.ShingleUnit.CODEPOINT)
+    assert (j.intersection, j.union_size) == (1, 3)

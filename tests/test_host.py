@@ -127,3 +127,36 @@ def test_synthetic_mode1_is_deterministic_and_shaped():
     lens = np.diff(o)
     assert lens.min() >= 200 and lens.max() <= 200_000
     assert 1500 < np.median(lens) < 2600
+
+
+def test_scalar_minhash_primitives():
+    # test_minhash.cpp:16-74: modulus 97, base 10; mod_pow / Miller-Rabin
+    from paper_2501_01046_b200 import _lib, minhash
+
+    f = _lib.NdHashFn(modulus=97, base=10, base_inverse=68, base_power=pow(10, 2, 97),
+                      reduce_factor=(1 << 64) // 97)
+    assert minhash.hash_window_direct([1, 2, 3], f) == 30
+    assert minhash.roll_next(30, 1, 4, f) == 44
+    assert minhash.hash_window_direct([2, 3, 4], f) == 44
+    with pytest.raises(_lib.ConfigError):
+        minhash.hash_window_direct([], f)
+    assert minhash.mod_pow(3, 100, 97) == pow(3, 100, 97)
+    assert minhash.mod_pow(5, 0, 1) == 0
+    with pytest.raises(_lib.ConfigError):
+        minhash.mod_pow(3, 4, 0)
+    assert [p for p in range(60) if minhash.is_prime_u32(p)] == [
+        2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53, 59]
+    assert minhash.is_prime_u32(2147483647) and not minhash.is_prime_u32(25326001)
+
+
+def test_raw_document_iteration(tmp_path):
+    # for_each_raw_document / load_jsonl_file (corpus.cpp:56-91)
+    from paper_2501_01046_b200 import corpus
+
+    p = tmp_path / "x.jsonl"
+    p.write_bytes(b'{"text": "a"}\n\nnot json\r\n{"text": "b"}\r\n[1]\n{"text": "c"}')
+    rejects = []
+    docs = corpus.load_jsonl_file(str(p), 7, "text", rejects)
+    assert [(d.file_ordinal, d.record_ordinal, d.line, d.text) for d in docs] == [
+        (7, 0, 1, b"a"), (7, 1, 4, b"b"), (7, 2, 6, b"c")]
+    assert rejects == [(str(p), 3, "invalid_json"), (str(p), 5, "not_an_object")]

@@ -130,3 +130,31 @@ def test_reference_artifacts_rewrite_byte_identical(ref, oracle, tmp_path):
         lo, hi, m = sigstore.read_pair_file(src)
         sigstore.write_pair_file(out, lo, hi, m)
         assert open(out, "rb").read() == open(src, "rb").read()
+
+
+def test_scan_gather_cases(tmp_path):
+    # test_sigstore.cpp:147-212
+    from paper_2501_01046_b200.lsh import BandRange, BucketKey
+
+    h = _toy()
+    _write(tmp_path / "a.feds", h, RECS[:2] + [(2, [9, 10, 11, 12], [2, 3])])
+    _write(tmp_path / "b.feds", _toy(source_ordinal=1), [(3, [13, 14, 15, 16], [1, 3])])
+    paths = [str(tmp_path / "a.feds"), str(tmp_path / "b.feds")]
+    g = sigstore.scan_gather(paths, h, BandRange(0, 1), 1, 2)
+    assert len(g.buckets) == 1 and g.buckets[0].key == BucketKey(0, 1)
+    assert list(g.buckets[0].doc_ids) == [0, 1, 3]
+    assert list(g.buckets[0].signatures) == [1, 2, 3, 4, 5, 6, 7, 8, 13, 14, 15, 16]
+    g = sigstore.scan_gather(paths, h, BandRange(0, 2), 0, 5)
+    assert [b.key for b in g.buckets] == [BucketKey(0, 1), BucketKey(1, 3)]
+    assert list(g.buckets[1].doc_ids) == [0, 2, 3]
+    assert sigstore.scan_gather(paths, h, BandRange(0, 2), 4, 4).buckets == []
+    _write(tmp_path / "d.feds", h, [(5, [1, 2, 3, 4], [1, 3]), (3, [5, 6, 7, 8], [1, 3])])
+    with pytest.raises(_lib.ConfigError):
+        sigstore.scan_gather([str(tmp_path / "d.feds")], h, BandRange(0, 2), 0, 5)
+    _write(tmp_path / "o.feds", _toy(family_seed=99), [(0, [1, 2, 3, 4], [1, 3])])
+    with pytest.raises(_lib.ConfigError):
+        sigstore.scan_gather([str(tmp_path / "o.feds")], h, BandRange(0, 2), 0, 5)
+    with pytest.raises(_lib.ConfigError):
+        sigstore.scan_gather([], h, BandRange(0, 2), 0, 6)
+    with pytest.raises(_lib.ConfigError):
+        sigstore.scan_gather([], h, BandRange(0, 3), 0, 5)
