@@ -63,7 +63,6 @@ const char* nd_last_error_global(void);
 /* derive_family (minhash.hpp:42, minhash.cpp:71-105); out holds H entries */
 int nd_derive_family(uint64_t seed, uint32_t hash_count, uint32_t shingle_len, uint32_t unit,
                      nd_hash_fn* out);
-/* choose_bucket_count (lsh.hpp:33, lsh.cpp:26-40) */
 /* scalar primitives of minhash.hpp (host; minhash.cpp:10-50, :111-131):
  * mod_pow (ND_ERR_CONFIG for a zero modulus), Miller-Rabin is_prime_u32,
  * hash_window_direct (Horner, ND_ERR_CONFIG for an empty window) and the
@@ -73,6 +72,7 @@ int nd_is_prime_u32(uint32_t n);
 int nd_hash_window_direct(const uint32_t* window, uint32_t len, const nd_hash_fn* fn,
                           uint32_t* out);
 uint32_t nd_roll_next(uint32_t state, uint32_t outgoing, uint32_t incoming, const nd_hash_fn* fn);
+/* choose_bucket_count (lsh.hpp:33, lsh.cpp:26-40) */
 int nd_choose_bucket_count(uint64_t doc_count, uint64_t scale_num, uint64_t scale_den,
                            uint32_t* bucket_count_out);
 /* SimilarityThreshold::min_matches (compare.hpp:35, compare.cpp:17-22) */
