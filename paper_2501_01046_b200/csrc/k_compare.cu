@@ -404,9 +404,12 @@ __device__ __forceinline__ void join_check_blocks(const SigView sv, uint32_t H,
                                                   uint64_t cap) {
   const uint32_t* a = sv.row(ra);
   const uint32_t* b = sv.row(rb);
-  if (!same_block<BW>(a + k * BW, b + k * BW, vec)) return;  // fingerprint collision
+  // earlier blocks first: a near-duplicate pair is rediscovered in almost
+  // every block, and its block 0 is almost always identical -- one load pair
+  // rejects the rediscovery
   for (uint32_t j = 0; j < k; ++j)
     if (same_block<BW>(a + j * BW, b + j * BW, vec)) return;  // counted at block j
+  if (!same_block<BW>(a + k * BW, b + k * BW, vec)) return;  // fingerprint collision
   bool alive;
   const uint32_t m = full_matches(a, b, H, H - min_match, alive);
   if (alive && m >= min_match) emit(ra, rb, m, nb, out_key, out_m, count, cap);
