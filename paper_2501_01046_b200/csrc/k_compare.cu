@@ -423,9 +423,7 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
                   uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
                   unsigned long long* __restrict__ count, uint64_t cap) {
   // one 32-byte sector per document (two 16-byte loads) covers BPL = 8 / BW
-  // blocks: a 16-byte load would still move a whole DRAM sector.  The BPL
-  // blocks of a load phase share one table round (distinct tags, one pair of
-  // barriers), so the cell is joined in NB / BPL rounds.
+  // blocks: a 16-byte load would still move a whole DRAM sector
   constexpr int BPL = 8 / BW;
   constexpr int VL = 8;
   extern __shared__ uint32_t jsm[];
@@ -434,8 +432,8 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
   const uint32_t T = 1u << tbits;
   uint32_t* keys = jsm;                // T   (tag << 23 | fingerprint), tag 0 = empty
   uint32_t* head = keys + T;           // T   (tag << 16 | doc)
-  uint32_t* next = head + T;           // BPL * join_max (chain links per block of the round)
-  uint32_t* rowsm = next + BPL * join_max;  // join_max
+  uint32_t* next = head + T;           // join_max
+  uint32_t* rowsm = next + join_max;   // join_max
   const uint64_t s = cell_start[blockIdx.x];
   for (uint32_t i = threadIdx.x; i < n; i += kJoinThreads) rowsm[i] = rows[s + i];
   for (uint32_t i = threadIdx.x; i < T; i += kJoinThreads) {
@@ -471,8 +469,6 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
         }
       }
     }
-    // insert every block of the round; a slot whose tag is > k0 belongs to
-    // this round (tags only grow), anything older is free
 #pragma unroll
     for (int b = 0; b < BPL; ++b) {
       const uint32_t k = k0 + b;
@@ -483,11 +479,11 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
         const uint32_t d = threadIdx.x + j * kJoinThreads;
         if (d >= n) continue;  // (not break: keeps fp[][] in registers)
         const uint32_t key = (tag << 23) | fp[j][b];
-        uint32_t h = (fp[j][b] * 0x9E3779B1u + tag * 0x632BE5ABu) >> (32 - tbits);
+        uint32_t h = (fp[j][b] * 0x9E3779B1u) >> (32 - tbits);
         for (;;) {
           const uint32_t cur = keys[h];
           if (cur == key) break;
-          if ((cur >> 23) > k0) {  // taken in this round: probe on
+          if ((cur >> 23) == tag) {  // another fingerprint of this block: probe on
             h = (h + 1) & mask;
             continue;
           }
@@ -495,21 +491,15 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
           if (old == cur || old == key) break;
         }
         const uint32_t prev = atomicExch(&head[h], (tag << 16) | d);
-        next[b * join_max + d] = (prev >> 16) == tag ? (prev & 0xFFFFu) : 0xFFFFFFFFu;
+        next[d] = (prev >> 16) == tag ? (prev & 0xFFFFu) : 0xFFFFFFFFu;
       }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int b = 0; b < BPL; ++b) {
-      const uint32_t k = k0 + b;
-      if (k >= NB) continue;
-      const uint32_t* nx = next + b * join_max;
+      __syncthreads();
       for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads)
-        for (uint32_t e = nx[d]; e != 0xFFFFFFFFu; e = nx[e])
+        for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e])
           join_check_blocks<BW>(sv, H, rowsm[d], rowsm[e], k, vec, min_match, nb, out_key, out_m,
                                 count, cap);
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -544,26 +534,12 @@ void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_
       break;
     }
   if (join_max >= 2 && P <= 510) {
-    // per-position join: one block per round, load factor <= 0.5; block join:
-    // BPL = 8 / BW blocks share a round, load factor <= 0.8
-    auto table_bits = [](uint64_t want) {
-      uint32_t t = 4;
-      while ((1ull << t) < want) ++t;
-      return t;
-    };
-    bool blocks = join_mode == 2 && BW > 1;
-    uint32_t bpl = blocks ? 8 / BW : 1;
-    uint32_t tbits = table_bits(blocks ? (5ull * bpl * join_max + 3) / 4 : 2ull * join_max);
-    size_t smem = (2u * (1u << tbits) + (bpl + 1u) * join_max) * sizeof(uint32_t);
-    if (blocks && smem > 200 * 1024) {  // very large cells at BW <= 2: per-position join
-      blocks = false;
-      bpl = 1;
-      tbits = table_bits(2ull * join_max);
-      smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
-    }
+    uint32_t tbits = 4;
+    while ((1u << tbits) < 2 * join_max) ++tbits;
+    const size_t smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
     if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
     const unsigned grid = static_cast<unsigned>(cs.ncells);
-    if (blocks) {
+    if (join_mode == 2 && BW > 1) {
       using JoinBFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                                const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, int,
                                uint64_t*, uint32_t*, unsigned long long*, uint64_t);
