@@ -2,12 +2,43 @@
 // neardup::b200 (include/neardup_b200.hpp) on the same inputs, in the
 // reference's types.  Built by oracle/Makefile against the reference sources
 // in place; run by tests/test_gpu_facade.py on the GPU box.
+#include <unistd.h>
+
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
 #include <map>
+#include <sstream>
 #include <vector>
 
+#include "neardup/pipeline.hpp"
 #include "neardup/synthetic.hpp"
 #include "neardup_b200.hpp"
+
+namespace {
+std::string slurp(const std::filesystem::path& p) {
+  std::ifstream f(p, std::ios::binary);
+  std::ostringstream ss;
+  ss << f.rdbuf();
+  return ss.str();
+}
+
+// every file of two workspaces, byte for byte (timings.json excepted)
+bool same_workspace(const std::string& a, const std::string& b) {
+  namespace fs = std::filesystem;
+  std::map<std::string, std::string> fa, fb;
+  for (auto* pr : {&a, &b})
+    for (const auto& e : fs::recursive_directory_iterator(*pr))
+      if (e.is_regular_file() && e.path().filename() != "timings.json")
+        (pr == &a ? fa : fb)[fs::relative(e.path(), *pr).string()] = slurp(e.path());
+  if (fa.size() != fb.size()) return std::printf("FAIL workspace file sets %zu vs %zu\n", fa.size(), fb.size()), false;
+  for (const auto& [k, v] : fa) {
+    auto it = fb.find(k);
+    if (it == fb.end() || it->second != v) return std::printf("FAIL workspace file %s\n", k.c_str()), false;
+  }
+  return true;
+}
+}  // namespace
 
 using namespace neardup;
 
@@ -67,6 +98,24 @@ int main() {
   uint64_t cand = 0;
   DedupReport rep = b200::dedup_in_memory(dev, clean, cfg, &cand);
   (void)rep;
+
+  // the staged workflow: reference run_dedup vs b200::run_dedup, whole workspaces
+  namespace fs = std::filesystem;
+  const fs::path tmp = fs::temp_directory_path() / ("nd_facade_" + std::to_string(::getpid()));
+  fs::create_directories(tmp / "in");
+  write_synthetic(corpus, (tmp / "in" / "corpus.jsonl").string(), (tmp / "truth.jsonl").string());
+  RunConfig rc;
+  rc.inputs = {(tmp / "in").string()};
+  rc.memory_budget = 300000;  // several gather passes
+  rc.workspace = (tmp / "ws_ref").string();
+  fs::create_directories(rc.workspace);
+  DedupReport want = run_dedup(rc);
+  rc.workspace = (tmp / "ws_gpu").string();
+  DedupReport got = b200::run_dedup(dev, rc);
+  if (want.groups.size() != got.groups.size() || want.removals != got.removals)
+    return std::puts("FAIL staged report"), 1;
+  if (!same_workspace((tmp / "ws_ref").string(), (tmp / "ws_gpu").string())) return 1;
+  fs::remove_all(tmp);
   std::printf("FACADE OK signatures=%zu pairs=%zu groups=%zu\n", gpu.size(), pg.size(), gg.size());
   return 0;
 }
