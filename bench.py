@@ -165,6 +165,34 @@ def cpu_reference_rate(data, offs, sample_docs: int, workers: int):
     return n / dt, n, dt
 
 
+def cpu_reference_dedup_rate(data, offs, docs: int, workers: int):
+    """The reference's own run_dedup (all three stages, oracle/_ref) on the
+    first `docs` documents written as JSONL, on the host cores: the CPU
+    counterpart of the `dedup` and `staged` lines."""
+    import shutil
+    import tempfile
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import Ref
+
+    ref = Ref()
+    tmp = tempfile.mkdtemp(prefix="nd_refdedup_")
+    try:
+        src = os.path.join(tmp, "c.jsonl")
+        raw = np.asarray(data[:int(offs[docs])]).tobytes()
+        o = offs[:docs + 1].astype(np.int64)
+        with open(src, "wb") as f:
+            f.write(b"".join(b'{"text":"' + raw[o[i]:o[i + 1]] + b'"}\n' for i in range(docs)))
+        ws = os.path.join(tmp, "ws")
+        os.makedirs(ws)
+        t = time.perf_counter()
+        ref.run_dedup(src, ws, workers=workers, memory_budget=64 << 30)
+        dt = time.perf_counter() - t
+        return docs / dt, dt
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+
+
 def calibrate_cpu_sample(data, offs, workers: int, target_s: float):
     rate, _, _ = cpu_reference_rate(data, offs, max(256, 64 * workers), workers)
     return int(min(len(offs) - 1, max(512, rate * target_s)))
@@ -464,6 +492,16 @@ def main():
         except Exception as e:  # the baseline is reported, not required
             cpu = {"value": None, "unit": "docs/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
+        if dedup is not None:
+            try:
+                n = min(50_000, docs)
+                rate, dt = cpu_reference_dedup_rate(data, offs, n, os.cpu_count() or 1)
+                dedup["cpu_baseline"] = {
+                    "value": rate, "unit": "docs/s", "cores": os.cpu_count(), "kind": "reference",
+                    "sample": f"reference run_dedup (JSONL -> report, all stages) on the first {n} "
+                              f"docs of the shard ({dt:.1f} s)"}
+            except Exception as e:
+                dedup["cpu_baseline"] = {"value": None, "sample": f"unavailable: {e}"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "docs/s", "n_gpus": world,
