@@ -8,6 +8,8 @@ the multi-threaded C++ loader of libneardup_b200 (csrc/host_ingest.cpp):
   preprocess             corpus.cpp:93-101 (NFC, code point count, min_chars)
   can_shingle            corpus.cpp:103-107
   build_manifest         corpus.cpp:109-141 (sorted paths, record offsets, reject log)
+  build_manifest_cached  the same scan keeping the packed text of the files that
+                         fit a host-memory cap (no second parse for those)
   surviving_documents    corpus.cpp:143-163
   surviving_packed       the same documents as one packed batch (text + offsets +
                          doc ids), the input the GPU stages take
@@ -201,6 +203,29 @@ def expand_inputs(inputs) -> list[str]:
 
 def build_manifest(inputs, config):
     """-> (CorpusManifest, rejects [(path, line, reason)] in file and line order)."""
+    manifest, rejects, _ = build_manifest_cached(inputs, config, 0)
+    return manifest, rejects
+
+
+def _host_memory_bytes() -> int:
+    try:
+        return os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        return 0
+
+
+def default_text_cache_bytes() -> int:
+    """How much preprocessed text the stages keep between the manifest scan and
+    hashing: a quarter of the free host memory, at most 32 GiB."""
+    return min(_host_memory_bytes() // 4, 32 << 30)
+
+
+def build_manifest_cached(inputs, config, keep_text_bytes: int):
+    """build_manifest that keeps the parsed, NFC-normalised text of the first
+    files whose texts fit in `keep_text_bytes`, so the stages pack them without
+    the reference's second parse of every file (corpus.cpp:143-163 re-reads
+    what corpus.cpp:109-141 already read).  -> (manifest, rejects,
+    {file index: packed (text, offsets, doc ids, char counts)})."""
     paths = sorted(expand_inputs(inputs))
     if not paths:
         raise _lib.ConfigError(_lib.ND_ERR_CONFIG, "no input files given")
@@ -210,16 +235,21 @@ def build_manifest(inputs, config):
     manifest = CorpusManifest()
     rejects = []
     offset = 0
-    for p in paths:
-        f = JsonlFile(p, config, keep_text=False)
+    cache = {}
+    for i, p in enumerate(paths):
+        keep = keep_text_bytes > 0 and len(cache) == i
+        f = JsonlFile(p, config, keep_text=keep)
         st = FileStats(p, f.records, f.surviving, offset)
         rejects.extend((p, line, why) for line, why in f.rejects())
+        if keep and f.text_bytes <= keep_text_bytes:
+            cache[i] = f.packed(offset)
+            keep_text_bytes -= f.text_bytes
         f.close()
         manifest.total_records += st.records
         manifest.total_surviving += st.surviving
         offset += st.records
         manifest.files.append(st)
-    return manifest, rejects
+    return manifest, rejects, cache
 
 
 def surviving_packed(manifest: CorpusManifest, index: int, config):

@@ -22,7 +22,8 @@ import numpy as np
 
 from . import _lib
 from ._lib import NdDedupStats, NdParams, u8p, u64p
-from .corpus import CorpusManifest, build_manifest, surviving_documents, surviving_packed  # noqa: F401
+from .corpus import (CorpusManifest, build_manifest, build_manifest_cached,  # noqa: F401
+                     default_text_cache_bytes, surviving_documents, surviving_packed)
 from .dedup_graph import DedupReport, DuplicateGroup
 from .device import Context, default_context
 from .lsh import _ratio
@@ -192,11 +193,13 @@ def run_dedup_in_memory(config: RunConfig, ctx: Context | None = None) -> DedupR
     .pairs artifacts."""
     config.validate(need_workspace=True)
     os.makedirs(config.workspace, exist_ok=True)
-    manifest, rejects = build_manifest(config.inputs, config)
+    manifest, rejects, cache = build_manifest_cached(config.inputs, config,
+                                                     default_text_cache_bytes())
     if manifest.total_surviving == 0:
         raise _lib.ConfigError(_lib.ND_ERR_CONFIG,
                                "no documents survive preprocessing; nothing to deduplicate")
-    parts = [surviving_packed(manifest, i, config) for i in range(len(manifest.files))]
+    parts = [cache.pop(i, None) or surviving_packed(manifest, i, config)
+             for i in range(len(manifest.files))]
     data = np.concatenate([p[0] for p in parts])
     offsets = np.zeros(manifest.total_surviving + 1, np.uint64)
     np.cumsum(np.concatenate([np.diff(p[1]) for p in parts]), out=offsets[1:])
@@ -334,7 +337,8 @@ def run_hash_stage(config: RunConfig, ctx: Context | None = None) -> HashStageOu
     config.validate(need_workspace=True)
     os.makedirs(signatures_dir(config), exist_ok=True)
     os.makedirs(pairs_dir(config), exist_ok=True)
-    manifest, rejects = build_manifest(config.inputs, config)
+    manifest, rejects, cache = build_manifest_cached(config.inputs, config,
+                                                     default_text_cache_bytes())
     if manifest.total_surviving == 0:
         raise _lib.ConfigError(_lib.ND_ERR_CONFIG,
                                "no documents survive preprocessing; nothing to deduplicate")
@@ -344,7 +348,9 @@ def run_hash_stage(config: RunConfig, ctx: Context | None = None) -> HashStageOu
     base = header_template(config, out.bucket_count)
     for i, fs in enumerate(manifest.files):
         path = signatures_dir(config) + "/" + signature_file_name(i, fs.path)
-        data, offsets, ids, _ = surviving_packed(manifest, i, config)
+        packed = cache.pop(i, None)
+        data, offsets, ids, _ = packed if packed is not None else surviving_packed(manifest, i,
+                                                                                  config)
         if len(ids) != fs.surviving:
             raise _lib.PrerequisiteError(_lib.ND_ERR_PREREQ,
                                          f"'{fs.path}' yielded {len(ids)} documents, manifest "

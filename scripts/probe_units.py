@@ -1,4 +1,4 @@
-"""K1 throughput, byte vs codepoint units, on the C2 shard (device-resident).
+"""K1 throughput, byte vs codepoint units (fq-cp and wide K1 variants), on the C2 shard (device-resident).
     python scripts/probe_units.py [docs]"""
 import ctypes as C
 import sys
@@ -28,7 +28,11 @@ ctx.check(lib.nd_synth_text_device(ctx.h, C.byref(spec), C.c_void_p(d_offs.data_
 d_sig = torch.empty((n, 128), dtype=torch.int32, device="cuda")
 d_band = torch.empty((n, 16), dtype=torch.int32, device="cuda")
 hwe = float((np.diff(offs).astype(np.float64) - 4).sum() * 128)
-for unit in (minhash.ShingleUnit.BYTE, minhash.ShingleUnit.CODEPOINT):
+import os  # noqa: E402
+
+for unit, cp in ((minhash.ShingleUnit.BYTE, ""), (minhash.ShingleUnit.CODEPOINT, "fq"),
+                 (minhash.ShingleUnit.CODEPOINT, "wide")):
+    os.environ["ND_K1_CP"] = cp
     fam = minhash.derive_family(5, 128, 5, unit)
     for it in range(4):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -38,4 +42,4 @@ for unit in (minhash.ShingleUnit.BYTE, minhash.ShingleUnit.CODEPOINT):
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    print(f"{unit.name:9s} {ms:8.2f} ms  {n / ms / 1e3:6.2f} M docs/s  {hwe / ms / 1e9:.3f} T HWE/s")
+    print(f"{unit.name:9s} {cp:4s} {ms:8.2f} ms  {n / ms / 1e3:6.2f} M docs/s  {hwe / ms / 1e9:.3f} T HWE/s")
