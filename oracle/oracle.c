@@ -47,6 +47,15 @@ uint64_t or_bounded_random(or_mt64* g, uint64_t bound) {
   }
 }
 
+/* n successive bounded_random(rng, bound) draws of mt19937_64(seed): the
+ * random streams the reference's acceptance criteria draw their inputs from
+ * (acceptance_main.cpp:123-124, :534-545) */
+void or_bounded_stream(uint64_t seed, uint64_t bound, uint64_t n, uint32_t* out) {
+  or_mt64 g;
+  or_mt64_seed(&g, seed);
+  for (uint64_t i = 0; i < n; ++i) out[i] = (uint32_t)or_bounded_random(&g, bound);
+}
+
 /* minhash.cpp:10-20 */
 uint64_t or_mod_pow(uint64_t base, uint64_t exp, uint64_t mod) {
   uint64_t result = 1 % mod;

@@ -30,6 +30,7 @@ typedef struct {
 void or_mt64_seed(or_mt64* g, uint64_t seed);
 uint64_t or_mt64_next(or_mt64* g);
 uint64_t or_bounded_random(or_mt64* g, uint64_t bound);               /* util.cpp:70-79 */
+void or_bounded_stream(uint64_t seed, uint64_t bound, uint64_t n, uint32_t* out);
 uint64_t or_mod_pow(uint64_t base, uint64_t exp, uint64_t mod);       /* minhash.cpp:10-20 */
 int or_is_prime_u32(uint32_t n);                                      /* minhash.cpp:22-50 */
 int or_derive_family(uint64_t seed, uint32_t H, uint32_t L, or_hash_fn* out); /* minhash.cpp:71-105 */

@@ -79,7 +79,14 @@ class Oracle:
         L.or_is_prime_u32.argtypes = [C.c_uint32]
         L.or_mod_pow.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
         L.or_mod_pow.restype = C.c_uint64
+        L.or_bounded_stream.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, u32p]
         self.lib = L
+
+    def bounded_stream(self, seed: int, bound: int, n: int) -> np.ndarray:
+        """n draws bounded_random(mt19937_64(seed), bound) (util.cpp:70-79)."""
+        out = np.empty(n, np.uint32)
+        self.lib.or_bounded_stream(seed, bound, n, _ptr(out, u32p))
+        return out
 
     def derive_family(self, seed: int, H: int, L: int = 5):
         fns = (HashFn * H)()
