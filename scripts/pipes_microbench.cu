@@ -51,6 +51,34 @@ __global__ void k_ffma(unsigned* out, float a, float b) {
   if (s == 1234.5f) out[0] = 1;
 }
 
+__global__ void k_dfma(unsigned* out, double a, double b) {
+  double x[8];
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[i]) : "d"(a), "d"(b));
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 1234.5) out[0] = 1;
+}
+
+// 1 DFMA : 1 IMAD.WIDE -- do the FP64 and the integer multiplier overlap?
+__global__ void k_dfma_wide(unsigned* out, double a, double b) {
+  double x[4];
+  unsigned long long y[4];
+  for (int i = 0; i < 4; ++i) { x[i] = threadIdx.x + i; y[i] = threadIdx.x * 3 + i; }
+  const unsigned m = (unsigned)(a * 1000.0);
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[i]) : "d"(a), "d"(b));
+      asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(y[i]) : "r"((unsigned)y[i]), "r"(m));
+    }
+  double s = 0;
+  for (int i = 0; i < 4; ++i) s += x[i] + (double)y[i];
+  if (s == 1234.5) out[0] = 1;
+}
+
 __global__ void k_ffma3(unsigned* out, float a, float b) {  // 3 distinct register sources
   float x[8], y[8];
   for (int i = 0; i < 8; ++i) { x[i] = threadIdx.x + i; y[i] = i * a; }
@@ -151,6 +179,71 @@ __global__ void k_roll_uni(unsigned* out, const RollC* rc, unsigned seed) {
   if (r == 0x12345) out[0] = r;
 }
 
+// FP64 quotient (codepoint-sized units, c < 2^21): u = q*s + c_out*QLn + c_in
+// is exact in FP64; floor(u * up(1/p)) is exactly Q = floor(u/p) (the
+// rounding error u*2^-52/p is below the 1/p gap to the next integer), read as
+// the low word of fma_rd(u, up(1/p), 1.5*2^52).
+//  hybrid: 3 DFMA + 1 DADD (state -> double) + 3 IMAD (r = u - Q*p mod 2^32)
+//  pure:   5 FP64 ops, the state stays a double
+__global__ void k_roll_f64h(unsigned* out, const RollC* rc, unsigned seed) {
+  double qd[8], qlnd[8], ipd[8];
+  unsigned qi[8], qlni[8], negpi[8];
+  for (int f = 0; f < 8; ++f) {
+    const unsigned p = 2097143u + 2 * ((threadIdx.x * 8 + f) & 63), q = 257 + 2 * f;
+    qd[f] = q; qlnd[f] = (p - 7) % p; ipd[f] = __drcp_ru((double)p);
+    qi[f] = q; qlni[f] = (p - 7) % p; negpi[f] = 0u - p;
+  }
+  unsigned s[8], mn[8];
+  for (int f = 0; f < 8; ++f) { s[f] = 0; mn[f] = ~0u; }
+  unsigned ch = seed + threadIdx.x;
+  for (int it = 0; it < ITERS; ++it) {
+    ch = ch * 1664525u + 1013904223u;
+    const unsigned cin = ch >> 11, cout = (ch * 747796405u) >> 11;
+    const double cind = cin, coutd = cout;
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      const double t = __fma_rn(coutd, qlnd[f], cind);
+      const double sd = __hiloint2double(0x43300000, s[f]) - 4503599627370496.0;
+      const double u = __fma_rn(qd[f], sd, t);
+      const unsigned k = __double2loint(__fma_rd(u, ipd[f], 6755399441055744.0));
+      unsigned x = s[f] * qi[f] + cin;
+      x = cout * qlni[f] + x;
+      x = k * negpi[f] + x;
+      s[f] = x;
+      mn[f] = min(mn[f], x);
+    }
+  }
+  unsigned r = 0;
+  for (int f = 0; f < 8; ++f) r ^= mn[f];
+  if (r == 0x12345) out[0] = r;
+}
+
+__global__ void k_roll_f64p(unsigned* out, const RollC* rc, unsigned seed) {
+  double qd[8], qlnd[8], ipd[8], negpd[8];
+  for (int f = 0; f < 8; ++f) {
+    const unsigned p = 2097143u + 2 * ((threadIdx.x * 8 + f) & 63), q = 257 + 2 * f;
+    qd[f] = q; qlnd[f] = (p - 7) % p; ipd[f] = __drcp_ru((double)p); negpd[f] = -(double)p;
+  }
+  double s[8], mn[8];
+  for (int f = 0; f < 8; ++f) { s[f] = 0; mn[f] = 1e300; }
+  unsigned ch = seed + threadIdx.x;
+  for (int it = 0; it < ITERS; ++it) {
+    ch = ch * 1664525u + 1013904223u;
+    const double cind = ch >> 11, coutd = (ch * 747796405u) >> 11;
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      const double t = __fma_rn(coutd, qlnd[f], cind);
+      const double u = __fma_rn(qd[f], s[f], t);
+      const double kd = __fma_rd(u, ipd[f], 6755399441055744.0) - 6755399441055744.0;
+      s[f] = __fma_rn(kd, negpd[f], u);
+      mn[f] = fmin(mn[f], s[f]);
+    }
+  }
+  double r = 0;
+  for (int f = 0; f < 8; ++f) r += mn[f];
+  if (r == 1234.5) out[0] = 1;
+}
+
 // constants as immediates (what a family-specialised JIT kernel would see)
 __global__ void k_roll_imm(unsigned* out, const RollC* rc, unsigned seed) {
   unsigned s[8], mn[8];
@@ -234,9 +327,13 @@ int main() {
   run("FFMA(imm)", k_ffma, 1.0001f, 0.5f, 1, sms, clk);
   run("FFMA(3reg)", k_ffma3, 1.0001f, 0.5f, 1, sms, clk);
   run("ALU", k_alu, 3u, 7u, 1, sms, clk);
+  run("DFMA", k_dfma, 1.0001, 0.5, 1, sms, clk);
+  run("DFMA+WIDE", k_dfma_wide, 1.0001, 0.5, 1, sms, clk);
   run("mix 1:1:1", k_mix, 3u, 7u, 3, sms, clk);
   run_roll("roll(reg)", k_roll_reg, sms, clk);
   run_roll("roll(uniform)", k_roll_uni, sms, clk);
   run_roll("roll(imm)", k_roll_imm, sms, clk);
+  run_roll("roll f64 hybrid", k_roll_f64h, sms, clk);
+  run_roll("roll f64 pure", k_roll_f64p, sms, clk);
   return 0;
 }
