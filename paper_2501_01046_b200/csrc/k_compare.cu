@@ -394,22 +394,59 @@ __device__ __forceinline__ bool same_block(const uint32_t* __restrict__ a,
   return eq;
 }
 
+// Pairs of one cell already handled at an earlier block (open addressing over
+// (d << 12 | e) + 1, d < e < kJoinMax).  A near-duplicate pair shares almost
+// every block, so it is rediscovered in almost every block's chains; the set
+// answers those rediscoveries from shared memory instead of re-reading two
+// blocks of both rows from HBM.  Entries only go from empty to full, and a
+// pair is inserted in an earlier phase (barrier-separated) than any lookup
+// that must see it.
+constexpr int kPsetProbes = 64;  // an entry lies within this many slots of its home
+static_assert(kJoinMax <= 4096, "pair keys pack two 12-bit document indices");
+
+__device__ __forceinline__ bool pset_has(const uint32_t* pset, uint32_t smask, uint32_t key) {
+  uint32_t h = (key * 0x9E3779B1u) & smask;
+  for (int probe = 0; probe < kPsetProbes; ++probe, h = (h + 1) & smask) {
+    const uint32_t c = pset[h];
+    if (c == key) return true;
+    if (c == 0) return false;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void pset_add(uint32_t* pset, uint32_t smask, uint32_t key,
+                                         int* full) {
+  uint32_t h = (key * 0x9E3779B1u) & smask;
+  for (int probe = 0; probe < kPsetProbes; ++probe, h = (h + 1) & smask) {
+    const uint32_t old = atomicCAS(&pset[h], 0u, key);
+    if (old == 0 || old == key) return;
+  }
+  *full = 1;  // not recorded: later blocks fall back to the HBM check
+}
+
 template <int BW>
 __device__ __forceinline__ void join_check_blocks(const SigView sv, uint32_t H,
-                                                  uint32_t ra, uint32_t rb, uint32_t k, bool vec,
+                                                  uint32_t d, uint32_t e, const uint32_t* rowsm,
+                                                  uint32_t k, bool vec, uint32_t* pset,
+                                                  uint32_t smask, int* full, bool exact_set,
                                                   uint32_t min_match, int nb,
                                                   uint64_t* __restrict__ out_key,
                                                   uint32_t* __restrict__ out_m,
                                                   unsigned long long* __restrict__ count,
                                                   uint64_t cap) {
+  const uint32_t key = ((min(d, e) << 12) | max(d, e)) + 1u;
+  if (smask && pset_has(pset, smask, key)) return;  // identical at an earlier block: counted there
+  const uint32_t ra = rowsm[d], rb = rowsm[e];
   const uint32_t* a = sv.row(ra);
   const uint32_t* b = sv.row(rb);
-  // earlier blocks first: a near-duplicate pair is rediscovered in almost
-  // every block, and its block 0 is almost always identical -- one load pair
-  // rejects the rediscovery
-  for (uint32_t j = 0; j < k; ++j)
-    if (same_block<BW>(a + j * BW, b + j * BW, vec)) return;  // counted at block j
+  // with a complete set, absence proves no earlier block is identical (each
+  // identical block j < k put the pair into block j's chains and the set);
+  // after an overflow, check the earlier blocks in HBM
+  if (!exact_set)
+    for (uint32_t j = 0; j < k; ++j)
+      if (same_block<BW>(a + j * BW, b + j * BW, vec)) return;
   if (!same_block<BW>(a + k * BW, b + k * BW, vec)) return;  // fingerprint collision
+  if (smask) pset_add(pset, smask, key, full);
   bool alive;
   const uint32_t m = full_matches(a, b, H, H - min_match, alive);
   if (alive && m >= min_match) emit(ra, rb, m, nb, out_key, out_m, count, cap);
@@ -419,27 +456,33 @@ template <int DPT, int BW>
 __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
     k_join_blocks(const SigView sv, uint32_t H, const uint32_t* __restrict__ rows,
                   const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
-                  uint32_t join_max, uint32_t tbits, uint32_t NB, uint32_t min_match, int nb,
-                  uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
-                  unsigned long long* __restrict__ count, uint64_t cap) {
+                  uint32_t join_max, uint32_t tbits, uint32_t sbits, uint32_t NB,
+                  uint32_t min_match, int nb, uint64_t* __restrict__ out_key,
+                  uint32_t* __restrict__ out_m, unsigned long long* __restrict__ count,
+                  uint64_t cap) {
   // one 32-byte sector per document (two 16-byte loads) covers BPL = 8 / BW
   // blocks: a 16-byte load would still move a whole DRAM sector
   constexpr int BPL = 8 / BW;
   constexpr int VL = 8;
   extern __shared__ uint32_t jsm[];
+  __shared__ int pset_full;
   const uint32_t n = cell_len[blockIdx.x];
   if (n > join_max) return;  // big cells go to k_compare
   const uint32_t T = 1u << tbits;
+  const uint32_t S = 1u << sbits;
   uint32_t* keys = jsm;                // T   (tag << 23 | fingerprint), tag 0 = empty
   uint32_t* head = keys + T;           // T   (tag << 16 | doc)
-  uint32_t* next = head + T;           // join_max
-  uint32_t* rowsm = next + join_max;   // join_max
+  uint32_t* pset = head + T;           // S   handled pairs (pset_has / pset_add)
+  uint32_t* rowsm = pset + S;          // join_max
+  uint16_t* next = reinterpret_cast<uint16_t*>(rowsm + join_max);  // join_max (0xFFFF = end)
   const uint64_t s = cell_start[blockIdx.x];
   for (uint32_t i = threadIdx.x; i < n; i += kJoinThreads) rowsm[i] = rows[s + i];
   for (uint32_t i = threadIdx.x; i < T; i += kJoinThreads) {
     keys[i] = 0;
     head[i] = 0;
   }
+  for (uint32_t i = threadIdx.x; i < S; i += kJoinThreads) pset[i] = 0;
+  if (threadIdx.x == 0) pset_full = 0;
   __syncthreads();
   const uint32_t mask = T - 1;
   const bool vec = (H & 3) == 0;
@@ -491,13 +534,14 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
           if (old == cur || old == key) break;
         }
         const uint32_t prev = atomicExch(&head[h], (tag << 16) | d);
-        next[d] = (prev >> 16) == tag ? (prev & 0xFFFFu) : 0xFFFFFFFFu;
+        next[d] = (prev >> 16) == tag ? static_cast<uint16_t>(prev) : uint16_t{0xFFFF};
       }
       __syncthreads();
+      const bool exact_set = S > 1 && *static_cast<volatile int*>(&pset_full) == 0;
       for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads)
-        for (uint32_t e = next[d]; e != 0xFFFFFFFFu; e = next[e])
-          join_check_blocks<BW>(sv, H, rowsm[d], rowsm[e], k, vec, min_match, nb, out_key, out_m,
-                                count, cap);
+        for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e])
+          join_check_blocks<BW>(sv, H, d, e, rowsm, k, vec, pset, S - 1, &pset_full, exact_set,
+                                min_match, nb, out_key, out_m, count, cap);
       __syncthreads();
     }
   }
@@ -534,15 +578,26 @@ void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_
       break;
     }
   if (join_max >= 2 && P <= 510) {
+    // table slots >= n / load; the default load 1/2 (ND_JOIN_LOAD = percent)
+    const char* jl = getenv("ND_JOIN_LOAD");
+    const uint32_t load_pct = jl ? static_cast<uint32_t>(std::max(10, std::min(95, atoi(jl)))) : 50;
     uint32_t tbits = 4;
-    while ((1u << tbits) < 2 * join_max) ++tbits;
+    while ((1ull << tbits) * load_pct < 100ull * join_max) ++tbits;
+    // handled-pair set of the block join: 2^sbits >= join_max / 2 slots
+    // (overflow only costs the HBM checks of earlier blocks)
+    uint32_t sbits = 8;
+    while ((1u << sbits) < join_max / 2) ++sbits;
+    const char* ps = getenv("ND_JOIN_PSET");  // 0: no set (HBM checks of earlier blocks)
+    if (ps && ps[0] == '0') sbits = 0;
     const size_t smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
+    const size_t smem_b = (2u * (1u << tbits) + (sbits ? 1u << sbits : 1u)) * sizeof(uint32_t) +
+                          join_max * (sizeof(uint32_t) + sizeof(uint16_t));
     if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
     const unsigned grid = static_cast<unsigned>(cs.ncells);
     if (join_mode == 2 && BW > 1) {
       using JoinBFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
-                               const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, int,
-                               uint64_t*, uint32_t*, unsigned long long*, uint64_t);
+                               const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
+                               int, uint64_t*, uint32_t*, unsigned long long*, uint64_t);
       const int dpt = join_max <= 2 * kJoinThreads   ? 2
                       : join_max <= 4 * kJoinThreads ? 4
                       : join_max <= 8 * kJoinThreads ? 8
@@ -553,12 +608,12 @@ void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_
       ND_JB(2, 2) ND_JB(2, 4) ND_JB(2, 8) ND_JB(4, 2) ND_JB(4, 4) ND_JB(4, 8)
       ND_JB(8, 2) ND_JB(8, 4) ND_JB(8, 8) ND_JB(16, 2) ND_JB(16, 4) ND_JB(16, 8)
 #undef ND_JB
-      if (smem > 48 * 1024)
+      if (smem_b > 48 * 1024)
         ND_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-      fn<<<grid, kJoinThreads, smem, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
-                                          join_max, tbits, NB, min_match, nb, out_key, out_m,
-                                          count, cap);
+                                     static_cast<int>(smem_b)));
+      fn<<<grid, kJoinThreads, smem_b, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
+                                            join_max, tbits, sbits, NB, min_match, nb, out_key,
+                                            out_m, count, cap);
       ND_CHECK_LAUNCH();
     } else {
       using JoinFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,

@@ -1,5 +1,6 @@
 """One in-memory dedup of the bench workload (C2: 1M docs, device-resident text),
-for kernel-level profiling: python scripts/dedup_once.py [docs] [H]"""
+for kernel-level profiling: python scripts/dedup_once.py [docs] [H] [K]
+(K: bucket count override; e.g. 1M docs at K=365 gives C3's ~2740-document cells)"""
 import ctypes as C
 import sys
 
@@ -12,6 +13,7 @@ from paper_2501_01046_b200.device import Context  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 H = int(sys.argv[2]) if len(sys.argv) > 2 else 128
+K = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 lib = _lib.load()
 spec = _lib.NdSynthSpec(doc_count=n, group_count=n // 20, group_size_min=2, group_size_max=2,
                         edit_num=1, edit_den=100, len_min=1600, len_max=2400, seed=1, mode=1)
@@ -23,7 +25,7 @@ d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
 d_text = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
 ctx.check(lib.nd_synth_text_device(ctx.h, C.byref(spec), C.c_void_p(d_offs.data_ptr()),
                                    C.c_void_p(d_text.data_ptr())))
-params = pipeline.RunConfig(hash_count=H, bands=H // 8, rows=8).to_params()
+params = pipeline.RunConfig(hash_count=H, bands=H // 8, rows=8).to_params(K)
 st = _lib.NdDedupStats()
 for _ in range(2):
     ctx.check(lib.nd_dedup_device(ctx.h, C.c_void_p(d_text.data_ptr()), C.c_void_p(d_offs.data_ptr()),

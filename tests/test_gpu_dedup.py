@@ -405,6 +405,30 @@ def test_pigeonhole_join_adversarial(ctx, ref, monkeypatch, H, thr):
     assert want
 
 
+@pytest.mark.parametrize("n,H", [(700, 128), (2600, 128), (900, 256)])
+def test_block_join_handled_pair_set_overflow(ctx, ref, monkeypatch, n, H):
+    # one big cluster: every pair is a near-duplicate rediscovered in almost
+    # every block, far more pairs than the handled-pair set holds (2^k >=
+    # n/2 slots), so the join falls back to checking earlier blocks in HBM;
+    # with the set, without it (ND_JOIN_PSET=0) and the reference agree
+    rng = np.random.default_rng(n + H)
+    base = rng.integers(0, 1 << 22, size=H).astype(np.uint32)
+    sig = np.tile(base, (n, 1))
+    hit = rng.random((n, H)) < rng.choice([0.02, 0.08, 0.25], size=n)[:, None]
+    sig[hit] = rng.integers(0, 1 << 22, size=int(hit.sum())).astype(np.uint32)
+    sig[n // 2:] = rng.integers(0, 1 << 22, size=(n - n // 2, H)).astype(np.uint32)
+    idx = np.arange(n // 2, n - 1, 7)
+    sig[idx] = sig[idx + 1]  # exact pairs in the random half
+    b = GatheredBucket(lsh.BucketKey(0, 0), list(range(n)), sig.reshape(-1))
+    lo, hi, m = ref.compare_cells(sig, np.array([0, n], np.uint64), np.arange(n, dtype=np.uint32),
+                                  4, 5)
+    want = [DuplicatePair(int(a), int(c), int(d)) for a, c, d in zip(lo, hi, m)]
+    assert len(want) > n
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ND_JOIN_PSET", mode)
+        assert compare.compare_bucket(b, H, SimilarityThreshold((4, 5)), ctx=ctx) == want, mode
+
+
 def test_estimator_error_stats(ctx, oracle):
     # oracle.cpp:143-162: per pair exact window Jaccard vs signature estimate
     from paper_2501_01046_b200 import accuracy
