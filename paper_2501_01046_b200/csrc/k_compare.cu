@@ -452,8 +452,10 @@ __device__ __forceinline__ void join_check_blocks(const SigView sv, uint32_t H,
   if (alive && m >= min_match) emit(ra, rb, m, nb, out_key, out_m, count, cap);
 }
 
-template <int DPT, int BW>
-__global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
+// TPB threads per CTA: 256, or 512 for big cells (twice the warps per SM at
+// the same 2 CTAs per SM that their shared memory allows)
+template <int DPT, int BW, int TPB>
+__global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
     k_join_blocks(const SigView sv, uint32_t H, const uint32_t* __restrict__ rows,
                   const uint64_t* __restrict__ cell_start, const uint32_t* __restrict__ cell_len,
                   uint32_t join_max, uint32_t tbits, uint32_t sbits, uint32_t NB,
@@ -476,12 +478,12 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
   uint32_t* rowsm = pset + S;          // join_max
   uint16_t* next = reinterpret_cast<uint16_t*>(rowsm + join_max);  // join_max (0xFFFF = end)
   const uint64_t s = cell_start[blockIdx.x];
-  for (uint32_t i = threadIdx.x; i < n; i += kJoinThreads) rowsm[i] = rows[s + i];
-  for (uint32_t i = threadIdx.x; i < T; i += kJoinThreads) {
+  for (uint32_t i = threadIdx.x; i < n; i += TPB) rowsm[i] = rows[s + i];
+  for (uint32_t i = threadIdx.x; i < T; i += TPB) {
     keys[i] = 0;
     head[i] = 0;
   }
-  for (uint32_t i = threadIdx.x; i < S; i += kJoinThreads) pset[i] = 0;
+  for (uint32_t i = threadIdx.x; i < S; i += TPB) pset[i] = 0;
   if (threadIdx.x == 0) pset_full = 0;
   __syncthreads();
   const uint32_t mask = T - 1;
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
     const bool full = vec && p0 + VL <= H;
 #pragma unroll
     for (int j = 0; j < DPT; ++j) {
-      const uint32_t d = threadIdx.x + j * kJoinThreads;
+      const uint32_t d = threadIdx.x + j * TPB;
       if (d < n) {
         const uint32_t* r = sv.row(rowsm[d]) + p0;
         uint32_t v[VL];
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
       const uint32_t tag = k + 1;
 #pragma unroll
       for (int j = 0; j < DPT; ++j) {
-        const uint32_t d = threadIdx.x + j * kJoinThreads;
+        const uint32_t d = threadIdx.x + j * TPB;
         if (d >= n) continue;  // (not break: keeps fp[][] in registers)
         const uint32_t key = (tag << 23) | fp[j][b];
         uint32_t h = (fp[j][b] * 0x9E3779B1u) >> (32 - tbits);
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(kJoinThreads, DPT <= 4 ? 8 : 4)
       }
       __syncthreads();
       const bool exact_set = S > 1 && *static_cast<volatile int*>(&pset_full) == 0;
-      for (uint32_t d = threadIdx.x; d < n; d += kJoinThreads)
+      for (uint32_t d = threadIdx.x; d < n; d += TPB)
         for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e])
           join_check_blocks<BW>(sv, H, d, e, rowsm, k, vec, pset, S - 1, &pset_full, exact_set,
                                 min_match, nb, out_key, out_m, count, cap);
@@ -598,22 +600,24 @@ void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_
       using JoinBFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                                const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
                                int, uint64_t*, uint32_t*, unsigned long long*, uint64_t);
-      const int dpt = join_max <= 2 * kJoinThreads   ? 2
-                      : join_max <= 4 * kJoinThreads ? 4
-                      : join_max <= 8 * kJoinThreads ? 8
-                                                     : 16;
+      // 512 threads per CTA for cells above 1024 documents: -33 % K3 time on
+      // C3-sized cells; smaller cells are faster with 256
+      const int tpb = join_max > 1024 ? 512 : 256;
+      static_assert(8 * 512 >= kJoinMax, "k_join_blocks<8, *, 512> must cover kJoinMax");
+      const int dpt = join_max <= 2u * tpb ? 2 : join_max <= 4u * tpb ? 4 : join_max <= 8u * tpb ? 8 : 16;
       JoinBFn fn = nullptr;
-#define ND_JB(D, W) \
-  if (dpt == D && BW == W) fn = k_join_blocks<D, W>;
-      ND_JB(2, 2) ND_JB(2, 4) ND_JB(2, 8) ND_JB(4, 2) ND_JB(4, 4) ND_JB(4, 8)
-      ND_JB(8, 2) ND_JB(8, 4) ND_JB(8, 8) ND_JB(16, 2) ND_JB(16, 4) ND_JB(16, 8)
+#define ND_JB(D, W, P) \
+  if (dpt == D && BW == W && tpb == P) fn = k_join_blocks<D, W, P>;
+      ND_JB(2, 2, 256) ND_JB(2, 4, 256) ND_JB(2, 8, 256) ND_JB(4, 2, 256) ND_JB(4, 4, 256)
+      ND_JB(4, 8, 256) ND_JB(4, 2, 512) ND_JB(4, 4, 512) ND_JB(4, 8, 512) ND_JB(8, 2, 512)
+      ND_JB(8, 4, 512) ND_JB(8, 8, 512)
 #undef ND_JB
       if (smem_b > 48 * 1024)
         ND_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem_b)));
-      fn<<<grid, kJoinThreads, smem_b, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
-                                            join_max, tbits, sbits, NB, min_match, nb, out_key,
-                                            out_m, count, cap);
+      fn<<<grid, tpb, smem_b, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
+                                   join_max, tbits, sbits, NB, min_match, nb, out_key, out_m,
+                                   count, cap);
       ND_CHECK_LAUNCH();
     } else {
       using JoinFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
