@@ -401,7 +401,7 @@ __device__ __forceinline__ bool same_block(const uint32_t* __restrict__ a,
 // blocks of both rows from HBM.  Entries only go from empty to full, and a
 // pair is inserted in an earlier phase (barrier-separated) than any lookup
 // that must see it.
-constexpr int kPsetProbes = 64;  // an entry lies within this many slots of its home
+constexpr int kPsetProbes = 16;  // an entry lies within this many slots of its home
 static_assert(kJoinMax <= 4096, "pair keys pack two 12-bit document indices");
 
 __device__ __forceinline__ bool pset_has(const uint32_t* pset, uint32_t smask, uint32_t key) {
@@ -435,18 +435,19 @@ __device__ __forceinline__ void join_check_blocks(const SigView sv, uint32_t H,
                                                   unsigned long long* __restrict__ count,
                                                   uint64_t cap) {
   const uint32_t key = ((min(d, e) << 12) | max(d, e)) + 1u;
-  if (smask && pset_has(pset, smask, key)) return;  // identical at an earlier block: counted there
+  // after an overflow the set is dropped (misses would probe long runs)
+  if (exact_set && pset_has(pset, smask, key)) return;  // identical at an earlier block
   const uint32_t ra = rowsm[d], rb = rowsm[e];
   const uint32_t* a = sv.row(ra);
   const uint32_t* b = sv.row(rb);
   // with a complete set, absence proves no earlier block is identical (each
   // identical block j < k put the pair into block j's chains and the set);
-  // after an overflow, check the earlier blocks in HBM
+  // without one (overflow, or ND_JOIN_PSET=0), check the earlier blocks in HBM
   if (!exact_set)
     for (uint32_t j = 0; j < k; ++j)
       if (same_block<BW>(a + j * BW, b + j * BW, vec)) return;
   if (!same_block<BW>(a + k * BW, b + k * BW, vec)) return;  // fingerprint collision
-  if (smask) pset_add(pset, smask, key, full);
+  if (exact_set) pset_add(pset, smask, key, full);
   bool alive;
   const uint32_t m = full_matches(a, b, H, H - min_match, alive);
   if (alive && m >= min_match) emit(ra, rb, m, nb, out_key, out_m, count, cap);
@@ -587,8 +588,10 @@ void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_
     while ((1ull << tbits) * load_pct < 100ull * join_max) ++tbits;
     // handled-pair set of the block join: 2^sbits >= join_max / 2 slots
     // (overflow only costs the HBM checks of earlier blocks)
+    const char* sd = getenv("ND_JOIN_PSET_DIV");  // tuning: slots >= join_max / div
+    const uint32_t sdiv = sd ? std::max(1, atoi(sd)) : 2;
     uint32_t sbits = 8;
-    while ((1u << sbits) < join_max / 2) ++sbits;
+    while ((1u << sbits) < join_max / sdiv) ++sbits;
     const char* ps = getenv("ND_JOIN_PSET");  // 0: no set (HBM checks of earlier blocks)
     if (ps && ps[0] == '0') sbits = 0;
     const size_t smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
