@@ -463,10 +463,11 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
                   uint32_t min_match, int nb, uint64_t* __restrict__ out_key,
                   uint32_t* __restrict__ out_m, unsigned long long* __restrict__ count,
                   uint64_t cap) {
-  // one 32-byte sector per document (two 16-byte loads) covers BPL = 8 / BW
-  // blocks: a 16-byte load would still move a whole DRAM sector
-  constexpr int BPL = 8 / BW;
-  constexpr int VL = 8;
+  // VL values per document and group of BPL = VL / BW blocks: one 32-byte
+  // sector (a 16-byte load would still move a whole sector), or 64 bytes
+  // for the big-cell variant
+  constexpr int VL = (TPB == 512 && BW >= 4) ? 16 : 8;
+  constexpr int BPL = VL / BW;
   extern __shared__ uint32_t jsm[];
   __shared__ int pset_full;
   const uint32_t n = cell_len[blockIdx.x];
