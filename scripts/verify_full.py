@@ -13,6 +13,7 @@ duplicate group of a paper-scale run checked against the CPU side.
   4. components by the oracle's union-find (or_components) vs the GPU's groups.
 
     python scripts/verify_full.py c3 [--docs N] [--out profiles/r1_c3_full_parity.json]
+    python scripts/verify_full.py c4 --rows 0:16000000 --skip-pairs   (split runs)
 """
 import argparse
 import ctypes as C
@@ -46,6 +47,10 @@ def main():
     ap.add_argument("--chunk", type=int, default=500_000)
     ap.add_argument("--threads", type=int, default=os.cpu_count())
     ap.add_argument("--out", default=None)
+    # split runs (one gpurun call is capped at an hour): verify signature rows
+    # [a, b) only, and/or skip the pair + group stages
+    ap.add_argument("--rows", default=None, help="a:b")
+    ap.add_argument("--skip-pairs", action="store_true")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     docs = a.docs or cfg["docs"]
@@ -95,8 +100,10 @@ def main():
     t = time.time()
     bad_sig = bad_band = 0
     first_bad = None
-    for c0 in range(0, docs, a.chunk):
-        c1 = min(docs, c0 + a.chunk)
+    r0, r1 = (int(x) for x in a.rows.split(":")) if a.rows else (0, docs)
+    r1 = min(r1, docs)
+    for c0 in range(r0, r1, a.chunk):
+        c1 = min(r1, c0 + a.chunk)
         b0, b1 = int(offs[c0]), int(offs[c1])
         text = d_text[b0:b1].cpu().numpy()
         co = (offs[c0:c1 + 1] - offs[c0]).astype(np.uint64)
@@ -108,14 +115,23 @@ def main():
         bad_band += len(db)
         if first_bad is None and (len(ds) or len(db)):
             first_bad = int(c0 + (ds[0] if len(ds) else db[0]))
-        if (c0 // a.chunk) % 10 == 0:
+        if ((c0 - r0) // a.chunk) % 10 == 0:
             log(stage="signatures", done=c1, bad_sig=bad_sig, bad_band=bad_band,
                 seconds=time.time() - t)
-    res.update(signatures_checked=docs, signature_rows_differing=bad_sig,
+    res.update(signatures_checked=r1 - r0, signature_rows=[r0, r1],
+               signature_rows_differing=bad_sig,
                band_rows_differing=bad_band, first_bad_doc=first_bad,
                reference_signature_seconds=time.time() - t)
     log(stage="signatures_done", bad_sig=bad_sig, bad_band=bad_band,
         seconds=res["reference_signature_seconds"])
+
+    if a.skip_pairs:
+        res["bit_exact_rows"] = bool(bad_sig == 0 and bad_band == 0)
+        log(stage="done", **res)
+        if a.out:
+            with open(a.out, "w") as f:
+                json.dump(res, f, indent=1)
+        return
 
     # ---- 3. cells + every candidate pair by the C oracle ----------------------
     o = Oracle()
