@@ -403,9 +403,22 @@ def main():
                 d1.record(stream)
                 barrier()
                 dms = max_over_ranks(d0.elapsed_time(d1) / reps)
+                # one more run with the collectives timed on the device
+                tm = {}
+                distributed.dedup_sharded(data, offs, cfg, stages, fetch="arrays", timings=tm)
+                xms = max_over_ranks(tm["exchange_ms"])
+                ems = max_over_ranks(tm["edges_ms"])
+                xbytes = max_over_ranks(float(tm["exchange_sent_bytes"]))
                 dedup = {"value": world * docs / (dms / 1e3), "unit": "docs/s", "ms_per_run": dms,
                          "distinct_pairs": res.distinct_pairs, "candidate_pairs": res.candidate_pairs,
                          "emitted_pairs": res.emitted_pairs, "documents": res.documents,
+                         "all_to_all": {"ms": xms, "max_bytes_sent_per_rank": xbytes,
+                                        "bus_gb_s": xbytes / (xms / 1e3) / 1e9 if xms else None,
+                                        "note": "cell-record exchange (keys + rows), device time "
+                                                "max over ranks; bus GB/s = bytes a rank sends "
+                                                "to its peers / time (NVLink 5: 900 GB/s per "
+                                                "direction)"},
+                         "edges_all_gather": {"ms": ems, "bytes": tm["edges_bytes"]},
                          "note": f"sharded dedup over {world} GPUs (NCCL all-to-all of cell "
                                  "records, all-gather of signatures and edges), pinned host "
                                  "shards -> groups on rank 0"}

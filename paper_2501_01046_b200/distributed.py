@@ -171,14 +171,24 @@ def _all_gather_var(dist, t, group, torch):
     return torch.cat([o[:s] for o, s in zip(outs, sizes)]), sizes
 
 
+def _events(torch, dev, timings):
+    if timings is None or dev.type != "cuda":
+        return None
+    return [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+
 def _host_collectives(dist, group, device) -> bool:
     """NCCL runs the collectives on device tensors; a gloo group (CPU protocol
     tests, or several ranks sharing one GPU in the GPU tests) gets host copies."""
     return device.type == "cuda" and dist.get_backend(group) == "gloo"
 
 
-def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists") -> ShardResult:
-    """Distributed in-memory dedup of this rank's shard (see module doc)."""
+def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists",
+                  timings: dict | None = None) -> ShardResult:
+    """Distributed in-memory dedup of this rank's shard (see module doc).
+    `timings` (optional) receives this rank's device times of the cell-record
+    all-to-all and the edge all-gather (CUDA events on the current stream,
+    which waits for the collective) and the bytes it sent / received."""
     import torch
     import torch.distributed as dist
 
@@ -222,9 +232,15 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists") -> S
     recv = [int(x) for x in recv_t.tolist()]
     rkeys = torch.empty(sum(recv), dtype=keys.dtype, device=cdev)
     rvals = torch.empty(sum(recv), dtype=vals.dtype, device=cdev)
+    ev = _events(torch, dev, timings)
+    if ev:
+        ev[0].record()
     dist.all_to_all_single(rkeys, keys.to(cdev), recv, send, group=group)
     dist.all_to_all_single(rvals, vals.to(cdev), recv, send, group=group)
+    if ev:
+        ev[1].record()
     rkeys, rvals = rkeys.to(dev), rvals.to(dev)
+    rec_bytes = keys.element_size() + vals.element_size()
     thr = _ratio(config.threshold)
     if getattr(stages, "peer_capable", False) and os.environ.get("ND_PEER_SIGS", "1") != "0":
         # 4+5. compare the owned cells reading every rank's rows in peer memory:
@@ -251,7 +267,18 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists") -> S
     dist.all_reduce(emitted, group=group)
     # 6. edges everywhere, union stage
     trip = torch.stack([lo, hi, m], dim=1) if lo.numel() else torch.zeros((0, 3), dtype=lo.dtype, device=dev)
+    if ev:
+        ev[2].record()
     all_trip, _ = _all_gather_var(dist, trip, group, torch)
+    if ev:
+        ev[3].record()
+        torch.cuda.synchronize(dev)
+        timings.update(
+            exchange_ms=ev[0].elapsed_time(ev[1]),
+            exchange_sent_bytes=(sum(send) - send[rank]) * rec_bytes,
+            exchange_recv_bytes=(sum(recv) - recv[rank]) * rec_bytes,
+            edges_ms=ev[2].elapsed_time(ev[3]),
+            edges_bytes=int(all_trip.numel()) * all_trip.element_size())
     st = stages.union(all_trip[:, 0].contiguous(), all_trip[:, 1].contiguous(),
                       all_trip[:, 2].contiguous(), N)
     rep = stages.report(st, fetch) if (rank == 0 and fetch) else None
