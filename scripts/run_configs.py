@@ -36,6 +36,10 @@ CONFIGS = {
                sigma=900, group_frac=0.10, gmin=2, gmax=5),
     "c4": dict(docs=30_000_000, H=256, bands=32, rows=8, len_min=2200, len_max=100_000,
                sigma=900, group_frac=0.10, gmin=2, gmax=5),
+    # the bench.py workload (BASELINE configs[1]): 1M docs, uniform 1600-2400 B, 10% in
+    # near-duplicate pairs -- same generator spec as bench.py
+    "c2": dict(docs=1_000_000, H=128, bands=16, rows=8, len_min=1600, len_max=2400,
+               sigma=0, group_frac=0.10, gmin=2, gmax=2, law=0, seed=1, K=2000),
     # long-document skew: 2M docs, lognormal median 2 KB up to 200 KB, 30% in clusters of 2-20
     "c5": dict(docs=2_000_000, H=128, bands=16, rows=8, len_min=2000, len_max=200_000,
                sigma=1200, group_frac=0.30, gmin=2, gmax=20),
@@ -46,8 +50,9 @@ def spec_for(cfg, docs):
     mean_group = (cfg["gmin"] + cfg["gmax"]) / 2
     return _lib.NdSynthSpec(doc_count=docs, group_count=int(docs * cfg["group_frac"] / mean_group),
                             group_size_min=cfg["gmin"], group_size_max=cfg["gmax"], edit_num=1,
-                            edit_den=100, len_min=cfg["len_min"], len_max=cfg["len_max"], seed=3,
-                            mode=1, len_law=1, sigma_milli=cfg["sigma"])
+                            edit_den=100, len_min=cfg["len_min"], len_max=cfg["len_max"],
+                            seed=cfg.get("seed", 3), mode=1, len_law=cfg.get("law", 1),
+                            sigma_milli=cfg["sigma"])
 
 
 def main():
@@ -78,7 +83,7 @@ def main():
     torch.cuda.synchronize()
     t_gen = time.time() - t0
     rc = pipeline.RunConfig(hash_count=cfg["H"], bands=cfg["bands"], rows=cfg["rows"])
-    params = rc.to_params()
+    params = rc.to_params(cfg.get("K", 0))
     stats = _lib.NdDedupStats()
     runs = []
     for it in range(2):  # warm-up + timed

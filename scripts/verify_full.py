@@ -69,7 +69,7 @@ def main():
     d_text = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
     ctx.check(lib.nd_synth_text_device(ctx.h, C.byref(spec), C.c_void_p(d_offs.data_ptr()),
                                        C.c_void_p(d_text.data_ptr())))
-    params = pipeline.RunConfig(hash_count=H, bands=B, rows=cfg["rows"]).to_params()
+    params = pipeline.RunConfig(hash_count=H, bands=B, rows=cfg["rows"]).to_params(cfg.get("K", 0))
     stats = _lib.NdDedupStats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
