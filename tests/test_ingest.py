@@ -114,6 +114,16 @@ def test_loader_matches_reference(ref, tmp_path, unit, L, min_chars):
     np.testing.assert_array_equal(ids, r_ids)
     np.testing.assert_array_equal(chars, r_ch)
     np.testing.assert_array_equal(lens, np.diff(r_offs))
+    # the stages' single-parse variant: cached files pack identically, the cap
+    # keeps a prefix of the files and the manifest does not change
+    for cap in (1 << 40, len(parts[0][0]), 0):
+        m2, rej2, cache = corpus.build_manifest_cached([str(d)], cfg, cap)
+        assert (m2, rej2) == (m, rejects)
+        assert sorted(cache) == list(range(len(cache)))
+        assert len(cache) == (2 if cap == 1 << 40 else 1 if cap else 0)
+        for i, packed in cache.items():
+            for a, b in zip(packed, parts[i]):
+                np.testing.assert_array_equal(a, b)
 
 
 def test_loader_normalises_and_is_thread_invariant(tmp_path):
