@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
                   uint32_t join_max, uint32_t tbits, uint32_t sbits, uint32_t NB,
                   uint32_t min_match, int nb, uint64_t* __restrict__ out_key,
                   uint32_t* __restrict__ out_m, unsigned long long* __restrict__ count,
-                  uint64_t cap) {
+                  uint64_t cap, bool two_barriers) {
   // VL values per document and group of BPL = VL / BW blocks: one 32-byte
   // sector (a 16-byte load would still move a whole sector), or 64 bytes
   // for the big-cell variant
@@ -478,7 +478,11 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
   uint32_t* head = keys + T;           // T   (tag << 16 | doc)
   uint32_t* pset = head + T;           // S   handled pairs (pset_has / pset_add)
   uint32_t* rowsm = pset + S;          // join_max
-  uint16_t* next = reinterpret_cast<uint16_t*>(rowsm + join_max);  // join_max (0xFFFF = end)
+  // chain links, double-buffered by block parity: the walk of block k reads
+  // next[k & 1] while faster threads already insert block k + 1 into the
+  // other half, so one barrier per block suffices (an insert of block k + 2
+  // waits behind block k + 1's barrier, which every walker of k has passed)
+  uint16_t* next2 = reinterpret_cast<uint16_t*>(rowsm + join_max);  // 2 x join_max (0xFFFF = end)
   const uint64_t s = cell_start[blockIdx.x];
   for (uint32_t i = threadIdx.x; i < n; i += TPB) rowsm[i] = rows[s + i];
   for (uint32_t i = threadIdx.x; i < T; i += TPB) {
@@ -521,6 +525,7 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
       const uint32_t k = k0 + b;
       if (k >= NB) continue;
       const uint32_t tag = k + 1;
+      uint16_t* next = next2 + (k & 1) * join_max;
 #pragma unroll
       for (int j = 0; j < DPT; ++j) {
         const uint32_t d = threadIdx.x + j * TPB;
@@ -546,7 +551,7 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
         for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e])
           join_check_blocks<BW>(sv, H, d, e, rowsm, k, vec, pset, S - 1, &pset_full, exact_set,
                                 min_match, nb, out_key, out_m, count, cap);
-      __syncthreads();
+      if (two_barriers) __syncthreads();
     }
   }
 }
@@ -597,13 +602,15 @@ void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_
     if (ps && ps[0] == '0') sbits = 0;
     const size_t smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
     const size_t smem_b = (2u * (1u << tbits) + (sbits ? 1u << sbits : 1u)) * sizeof(uint32_t) +
-                          join_max * (sizeof(uint32_t) + sizeof(uint16_t));
+                          join_max * (sizeof(uint32_t) + 2 * sizeof(uint16_t));
+    const char* tb = getenv("ND_JOIN_TWO_BARRIERS");  // 1: the barrier after each walk too
+    const bool two_barriers = tb && tb[0] == '1';
     if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
     const unsigned grid = static_cast<unsigned>(cs.ncells);
     if (join_mode == 2 && BW > 1) {
       using JoinBFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                                const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
-                               int, uint64_t*, uint32_t*, unsigned long long*, uint64_t);
+                               int, uint64_t*, uint32_t*, unsigned long long*, uint64_t, bool);
       // 512 threads per CTA for cells above 1024 documents: -33 % K3 time on
       // C3-sized cells; smaller cells are faster with 256
       const int tpb = join_max > 1024 ? 512 : 256;
@@ -621,7 +628,7 @@ void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_
                                      static_cast<int>(smem_b)));
       fn<<<grid, tpb, smem_b, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
                                    join_max, tbits, sbits, NB, min_match, nb, out_key, out_m,
-                                   count, cap);
+                                   count, cap, two_barriers);
       ND_CHECK_LAUNCH();
     } else {
       using JoinFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
