@@ -427,6 +427,12 @@ def test_block_join_handled_pair_set_overflow(ctx, ref, monkeypatch, n, H):
     for mode in ("1", "0"):
         monkeypatch.setenv("ND_JOIN_PSET", mode)
         assert compare.compare_bucket(b, H, SimilarityThreshold((4, 5)), ctx=ctx) == want, mode
+    # one barrier per block (double-buffered chain links, the default) and
+    # the second barrier after each walk agree on the heaviest walks
+    monkeypatch.setenv("ND_JOIN_PSET", "1")
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ND_JOIN_TWO_BARRIERS", mode)
+        assert compare.compare_bucket(b, H, SimilarityThreshold((4, 5)), ctx=ctx) == want, mode
 
 
 def test_estimator_error_stats(ctx, oracle):
