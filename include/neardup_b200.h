@@ -114,7 +114,14 @@ void nd_ctx_destroy(nd_ctx* ctx);
 const char* nd_last_error(const nd_ctx* ctx);
 /* stream all device work of this ctx is ordered on (cudaStream_t; NULL = own) */
 int nd_ctx_set_stream(nd_ctx* ctx, void* cuda_stream);
-/* Uploads the family (derive_family's output) for signature kernels. */
+/* Uploads the family (derive_family's output, or a hand-built one) for the
+ * signature kernels.  ND_ERR_CONFIG unless every function meets the
+ * reference's own preconditions: modulus above the largest unit
+ * (minhash.cpp:107-109), modulus < 2^31, base_inverse / base_power /
+ * reduce_factor as derive_family computes them (minhash.cpp:99-101).
+ * derive_family's domain (2^21 <= p < 2^23, q < 2^16) runs the FP32-quotient
+ * kernel; any other accepted family runs the reference's 64-bit Barrett
+ * reduction (exact, slower). */
 int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t hash_count,
                      uint32_t shingle_len, uint32_t unit);
 

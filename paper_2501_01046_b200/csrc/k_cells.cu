@@ -67,6 +67,13 @@ __global__ void k_cells_compact(const uint64_t* __restrict__ run_start, const ui
   atomicMax(max_len, static_cast<unsigned long long>(len));
 }
 
+__global__ void k_all_pairs_tiles(const uint32_t* __restrict__ cell_len, uint64_t cells,
+                                  uint32_t tile_rows, uint32_t* __restrict__ cell_tiles) {
+  uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (c >= cells) return;
+  cell_tiles[c] = (cell_len[c] + tile_rows - 1) / tile_rows;
+}
+
 __global__ void k_item_cells(const uint64_t* __restrict__ item_off, uint64_t cells,
                              uint32_t* __restrict__ item_cell) {
   uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -92,6 +99,7 @@ void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint6
     cs.join_enabled = !(j && j[0] == '0');
   }
   cs.records = m;
+  cs.tile_rows = tile_rows;
   cs.ncells = 0;
   cs.items = 0;
   cs.candidate_pairs = 0;
@@ -147,6 +155,34 @@ void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint6
   if (cs.items)
     k_item_cells<<<blocks_for(cells, tb), tb, 0, s>>>(cs.item_off, cells, cs.item_cell);
   ND_CHECK_LAUNCH();
+}
+
+// The hash joins cannot take this compare (launch_compare: P > kJoinMaxP):
+// give every cell all-pairs tiles, so that no cell of <= kJoinMax documents
+// is left without a kernel (every cell is compared, compare.cpp:24-67).
+void cells_all_pairs_tiles(CellSet& cs, cudaStream_t s) {
+  if (!cs.join_enabled || cs.ncells == 0) {
+    cs.join_enabled = false;
+    return;
+  }
+  const unsigned tb = 256;
+  const uint64_t cells = cs.ncells;
+  uint32_t* ctiles = cs.ctiles.as<uint32_t>(cells);
+  k_all_pairs_tiles<<<blocks_for(cells, tb), tb, 0, s>>>(cs.cell_len, cells, cs.tile_rows, ctiles);
+  ND_CHECK_LAUNCH();
+  cs.item_off = cs.ioff.as<uint64_t>(cells + 1);
+  scan_u32_to_u64(ctiles, cs.item_off, cells, cs.scan, s);
+  uint64_t items = 0;
+  ND_CUDA(cudaMemcpyAsync(&items, cs.item_off + cells, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  ND_CUDA(cudaStreamSynchronize(s));
+  cs.items = items;
+  cs.join_enabled = false;
+  cs.max_len = 0;
+  cs.item_cell = cs.icell.as<uint32_t>(cs.items + 1);
+  if (cs.items) {
+    k_item_cells<<<blocks_for(cells, tb), tb, 0, s>>>(cs.item_off, cells, cs.item_cell);
+    ND_CHECK_LAUNCH();
+  }
 }
 
 void make_records(const uint32_t* band, uint64_t n, uint32_t bands, uint32_t K, uint32_t doc_base,

@@ -248,11 +248,13 @@ __device__ __forceinline__ void join_check(const SigView sv, uint32_t H,
     }
   }
   if (pc - matches > allowed) return;     // accepting count already unreachable
-  // check each pair once per cell: at its FIRST matching position
+  // check each pair once per cell: at its FIRST matching position (this also
+  // rejects fingerprint collisions: a pair chained at k without a[k] == b[k])
   if (k < pc) {
     if (first != k) return;
   } else {
     if (first != 0xFFFFFFFFu) return;     // matched inside the prefix already
+    if (__ldg(a + k) != __ldg(b + k)) return;  // fingerprint collision
     for (uint32_t h = pc; h < k; ++h)
       if (__ldg(a + h) == __ldg(b + h)) return;
   }
@@ -312,7 +314,10 @@ __global__ void __launch_bounds__(kJoinThreads)
         const uint32_t d = threadIdx.x + j * kJoinThreads;
         if (d >= n) break;
         const uint32_t v = dk == 0 ? val[j].x : dk == 1 ? val[j].y : dk == 2 ? val[j].z : val[j].w;
-        const uint32_t key = (tag << 23) | v;
+        // keyed by a 23-bit fingerprint of the value (values are arbitrary
+        // u32, compare.cpp:24-67); join_check re-verifies a[k] == b[k]
+        const uint32_t fpv = (v * 0x9E3779B1u) ^ ((v * 0x85EBCA6Bu) >> 9);
+        const uint32_t key = (tag << 23) | (fpv & 0x7FFFFFu);
         uint32_t h = (v * 0x9E3779B1u) >> (32 - tbits);
         for (;;) {
           const uint32_t cur = keys[h];
@@ -570,12 +575,16 @@ int compare_prefilter_width(uint32_t H, uint32_t min_match) {
   return 0;
 }
 
-void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_match,
+void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_match,
                     int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,
                     uint64_t cap, cudaStream_t s) {
   if (cs.ncells == 0 || min_match > H) return;
   // cells of <= kJoinMax documents: hash join (one CTA per cell)
   const uint32_t P = H - min_match + 1;
+  // the joins tag table entries with 9-bit block numbers; beyond kJoinMaxP
+  // blocks every cell goes to the all-pairs kernel instead (K2 tiled the
+  // join's cells with zero all-pairs tiles, so re-tile them first)
+  if (P > kJoinMaxP && cs.join_enabled) cells_all_pairs_tiles(cs, s);
   const uint32_t join_max = static_cast<uint32_t>(std::min<uint64_t>(cs.max_len, kJoinMax));
   const char* jb = getenv("ND_JOIN_BLOCKS");  // read per call: tests switch it
   const int join_mode = jb && std::string(jb) == "0" ? 1 : 2;  // 2 = blocks, 1 = per position
@@ -586,7 +595,7 @@ void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_
       BW = w;
       break;
     }
-  if (join_max >= 2 && P <= 510) {
+  if (cs.join_enabled && join_max >= 2 && P <= kJoinMaxP) {
     // table slots >= n / load; the default load 1/2 (ND_JOIN_LOAD = percent)
     const char* jl = getenv("ND_JOIN_LOAD");
     const uint32_t load_pct = jl ? static_cast<uint32_t>(std::max(10, std::min(95, atoi(jl)))) : 50;

@@ -95,6 +95,8 @@ struct FamPtrs {
   const float* qlnp;      // fl(QLn / p)
   const float* c1e;       // -2^23 * qp + 2^-5 (exact)
   const uint32_t* m45;    // floor(2^45 / p)
+  const uint32_t* p;      // modulus (exact variant)
+  const unsigned long long* rf;  // floor(2^64 / p) (exact variant)
 };
 
 // ---------------------------------------------------------------------------
@@ -155,7 +157,7 @@ __global__ void k_bands_from_rows(const uint32_t* __restrict__ docs, uint32_t nd
 }
 
 // ---------------------------------------------------------------------------
-enum class Arith { kInt, kFq, kWide };
+enum class Arith { kInt, kFq, kWide, kExact };
 // register caps (blocks of 4 warps per SM) that reproduce the allocation of
 // the one-item-per-warp kernel: fq F=4/8/16 -> 80/96/168 registers, int and
 // wide F<=4/8/16 -> 64/80/128
@@ -223,6 +225,41 @@ struct Consts<Arith::kWide, F> {
       const uint32_t k = __umulhi(t, m[f]);
       const uint32_t r = lo + k * negp[f];
       const uint32_t c = min(r, r + negp[f]);
+      s[f] = c;
+      if (kMin) mn[f] = min(mn[f], c);
+    }
+  }
+};
+
+// Families outside the fast arithmetics' proven domain (hand-built
+// HashFunctionParams, see nd_family_upload): the reference's own Barrett
+// reduction with reduce_factor = floor(2^64/p) (minhash.cpp:61-67) over a
+// 64-bit u = q*c + c_out*QLn + c_in < 2^63 (p < 2^31).  k = umulhi64(u, rf)
+// is Q or Q-1 (u/2^64 < 1), so r = u - k*p lies in [0, 2p) < 2^32 and one
+// unsigned min canonicalises it.  Not a throughput path.
+template <int F>
+struct Consts<Arith::kExact, F> {
+  uint32_t q[F], qln[F], p[F];
+  unsigned long long rf[F];
+  __device__ void load(const FamPtrs& fp, int base) {
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      q[f] = fp.q[base + f];
+      qln[f] = fp.qln[base + f];
+      p[f] = fp.p[base + f];
+      rf[f] = fp.rf[base + f];
+    }
+  }
+  template <bool kMin>
+  __device__ __forceinline__ void step(uint32_t cin, uint32_t cout, float /*cout_f*/,
+                                       uint32_t (&s)[F], uint32_t (&mn)[F]) const {
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      const unsigned long long u = static_cast<unsigned long long>(cout) * qln[f] + cin +
+                                   static_cast<unsigned long long>(q[f]) * s[f];
+      const unsigned long long k = __umul64hi(u, rf[f]);
+      const uint32_t r = static_cast<uint32_t>(u) - static_cast<uint32_t>(k) * p[f];
+      const uint32_t c = min(r, r - p[f]);
       s[f] = c;
       if (kMin) mn[f] = min(mn[f], c);
     }
@@ -692,7 +729,8 @@ void launch_k1(const DevFamily& fam, const void* d_text, const uint64_t* d_offse
                const uint32_t* item_doc, const uint64_t* item_off, uint64_t items, uint32_t bands,
                uint32_t rows, uint32_t K, uint32_t* d_sig, uint32_t* d_band,
                unsigned long long* counter, cudaStream_t s) {
-  FamPtrs p{fam.q, fam.qln, fam.m, fam.negp, fam.c3, fam.qp, fam.qlnp, fam.c1e, fam.m45};
+  FamPtrs p{fam.q,   fam.qln,  fam.m,   fam.negp, fam.c3, fam.qp,
+            fam.qlnp, fam.c1e, fam.m45, fam.p,    fam.rf};
   uint64_t blocks = (items + kWarps - 1) / kWarps;
   if (counter) {  // persistent: resident blocks only
     static int per_sm = -1;
@@ -721,7 +759,17 @@ using Launcher = void (*)(const DevFamily&, const void*, const uint64_t*, const 
 
 // (arith, Hp) -> instantiation; F = functions per lane, Z = window slices per
 // warp.  ND_K1_FZ="F,Z" overrides the default shape (tuning experiments).
-Launcher pick_launcher(bool int_arith, uint32_t Hp, bool codepoint) {
+Launcher pick_launcher(bool int_arith, uint32_t Hp, bool codepoint, bool exact) {
+  if (exact) {  // families outside the fast domains (nd_family_upload)
+    switch (Hp) {
+      case 32: return codepoint ? launch_k1<Arith::kExact, 1, 1, uint32_t> : launch_k1<Arith::kExact, 1, 1>;
+      case 64: return codepoint ? launch_k1<Arith::kExact, 2, 1, uint32_t> : launch_k1<Arith::kExact, 2, 1>;
+      case 128: return codepoint ? launch_k1<Arith::kExact, 4, 1, uint32_t> : launch_k1<Arith::kExact, 4, 1>;
+      case 256: return codepoint ? launch_k1<Arith::kExact, 8, 1, uint32_t> : launch_k1<Arith::kExact, 8, 1>;
+      case 512: return codepoint ? launch_k1<Arith::kExact, 16, 1, uint32_t> : launch_k1<Arith::kExact, 16, 1>;
+    }
+    return nullptr;
+  }
   if (codepoint) {  // u32 units: wide arithmetic
     switch (Hp) {
       case 32: return launch_k1<Arith::kWide, 1, 1, uint32_t>;
@@ -842,7 +890,7 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     const char* v = getenv("ND_K1_KERNEL");
     return v && std::string(v) == "int";
   }();
-  Launcher go = pick_launcher(int_arith, fam.Hp, fam.unit == 1);
+  Launcher go = pick_launcher(int_arith, fam.Hp, fam.unit == 1, fam.exact);
   if (!go) fail(ND_ERR_CONFIG, "hash count must be at most 512 on the GPU path");
   static const bool persistent = [] {
     const char* v = getenv("ND_K1_PERSISTENT");

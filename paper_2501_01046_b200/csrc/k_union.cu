@@ -78,6 +78,9 @@ __global__ void k_mark(const uint32_t* __restrict__ lo, const uint32_t* __restri
                        uint32_t* __restrict__ in_edge) {
   uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= e) return;
+  // a self-loop record (possible in a hand-written .pairs file) makes no
+  // group by itself: components() keeps groups of 2+ (dedup_graph.cpp:70)
+  if (lo[i] == hi[i]) return;
   in_edge[lo[i]] = 1u;
   in_edge[hi[i]] = 1u;
 }

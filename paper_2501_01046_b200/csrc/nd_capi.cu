@@ -3,6 +3,7 @@
 // exception -> status mapping (reference taxonomy util.hpp:13-26).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -310,15 +311,58 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L,
     uint32_t Hp = 32;
     while (Hp < H) Hp *= 2;
     if (Hp > 512) fail(ND_ERR_CONFIG, "hash count above 512 is not supported on the GPU path");
-    // 9 arrays of Hp entries: q, QLn, M, -p, c3 (u32), q/p, QLn/p, c1e (f32), M45 (u32)
-    std::vector<uint32_t> host(9 * Hp);
+    // Validate every function against the reference's own preconditions.
+    // roll_next (minhash.cpp:121-131) is the exact window hash only when the
+    // units are residues (minhash.cpp:107-109: "units < 2^21 <= modulus") and
+    // base_inverse / base_power / reduce_factor are the constants derive_family
+    // computes (minhash.cpp:99-101); a hand-built HashFunctionParams (a public
+    // struct) that breaks them makes the reference compute something other
+    // than the window hash, which no exact GPU evaluation can reproduce.
+    bool fast = true;
+    for (uint32_t i = 0; i < H; ++i) {
+      const nd_hash_fn& f = fns[i];
+      const uint64_t p = f.modulus;
+      const uint64_t max_unit = unit == 1 ? 0x10FFFF : 0xFF;
+      if (p <= max_unit)
+        fail(ND_ERR_CONFIG, std::string("hash function ") + std::to_string(i) + ": modulus " +
+                                std::to_string(p) + " does not exceed the largest " +
+                                (unit == 1 ? "code point" : "byte") +
+                                " unit (units must be residues, minhash.cpp:107-109)");
+      if (p >= (1ull << 31))
+        fail(ND_ERR_CONFIG, "hash function " + std::to_string(i) +
+                                ": modulus must be below 2^31 on the GPU path");
+      const uint64_t q = f.base % p;
+      if (q * (f.base_inverse % p) % p != 1)
+        fail(ND_ERR_CONFIG, "hash function " + std::to_string(i) +
+                                ": base_inverse is not the inverse of base mod modulus");
+      uint64_t qpow = 1;
+      for (uint32_t e = 1; e < L; ++e) qpow = qpow * q % p;
+      if (f.base_power != qpow)
+        fail(ND_ERR_CONFIG, "hash function " + std::to_string(i) +
+                                ": base_power is not base^(L-1) mod modulus");
+      if (f.reduce_factor !=
+          static_cast<uint64_t>((static_cast<unsigned __int128>(1) << 64) / p))
+        fail(ND_ERR_CONFIG, "hash function " + std::to_string(i) +
+                                ": reduce_factor is not floor(2^64 / modulus)");
+      const uint64_t p_lo = unit == 1 ? 0x110000ull : (1ull << 21);
+      if (p < p_lo || p >= (1ull << 23) || f.base == 0 || f.base >= (1u << 16)) fast = false;
+    }
+    const char* fe = getenv("ND_K1_EXACT");  // 1: exact arithmetic for every family (tests)
+    if (fe && fe[0] == '1') fast = false;
+    // 9 arrays of Hp entries: q, QLn, M, -p, c3 (u32), q/p, QLn/p, c1e (f32), M45 (u32),
+    // then p (u32) and reduce_factor (u64, 8-byte aligned: Hp is even)
+    std::vector<uint32_t> host(12 * Hp);
     for (uint32_t i = 0; i < Hp; ++i) {
       const nd_hash_fn& f = fns[i < H ? i : 0];  // pad with copies of fn 0 (never stored)
       uint64_t p = f.modulus;
-      if (p < 257 || p >= (1u << 23) || f.base == 0 || f.base >= (1u << 16))
-        fail(ND_ERR_CONFIG, "hash function outside the GPU arithmetic domain (p < 2^23, q < 2^16)");
-      if (unit == 1 && p <= 0x10FFFF)  // scalar values must already be residues (minhash.cpp:107-109)
-        fail(ND_ERR_CONFIG, "codepoint units need moduli above 0x10FFFF");
+      host[9 * Hp + i] = static_cast<uint32_t>(p);
+      std::memcpy(&host[10 * Hp + 2 * i], &f.reduce_factor, 8);
+      if (!fast) {  // exact variant: q (reduced) and QLn only
+        const uint64_t q = f.base % p;
+        host[i] = static_cast<uint32_t>(q);
+        host[Hp + i] = static_cast<uint32_t>((p - static_cast<uint64_t>(f.base_power) * q % p) % p);
+        continue;
+      }
       uint64_t qL = static_cast<uint64_t>(f.base_power) * f.base % p;  // q^L = q^(L-1) * q
       uint32_t qln = static_cast<uint32_t>((p - qL) % p);
       float qp = static_cast<float>(static_cast<double>(f.base) / static_cast<double>(p));
@@ -334,7 +378,7 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L,
       std::memcpy(&host[7 * Hp + i], &c1e, 4);
       host[8 * Hp + i] = static_cast<uint32_t>((1ull << 45) / p);
     }
-    uint32_t* d = ctx->fam_buf.as<uint32_t>(9 * Hp);
+    uint32_t* d = ctx->fam_buf.as<uint32_t>(12 * Hp);
     ND_CUDA(cudaMemcpy(d, host.data(), host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     ctx->fam.q = d;
     ctx->fam.qln = d + Hp;
@@ -345,6 +389,9 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L,
     ctx->fam.qlnp = reinterpret_cast<float*>(d + 6 * Hp);
     ctx->fam.c1e = reinterpret_cast<float*>(d + 7 * Hp);
     ctx->fam.m45 = d + 8 * Hp;
+    ctx->fam.p = d + 9 * Hp;
+    ctx->fam.rf = reinterpret_cast<unsigned long long*>(d + 10 * Hp);
+    ctx->fam.exact = !fast;
     ctx->fam.unit = unit;
     ctx->fam.H = H;
     ctx->fam.Hp = Hp;

@@ -44,10 +44,17 @@ struct DevFamily {
   float* qlnp = nullptr;     // fl(QLn / p)
   float* c1e = nullptr;      // -2^23 * qp + 2^-5
   uint32_t* m45 = nullptr;   // floor(2^45 / p)  (codepoint units, "wide" variant)
+  uint32_t* p = nullptr;     // modulus           ("exact" variant)
+  unsigned long long* rf = nullptr;  // floor(2^64 / p) = reduce_factor (minhash.hpp:24)
   uint32_t H = 0;            // real hash count
   uint32_t Hp = 0;           // padded hash count
   uint32_t L = 0;
   uint32_t unit = 0;         // 0 = byte, 1 = codepoint (ShingleUnit, text.hpp:23-26)
+  // true when some function lies outside the domain the fast arithmetics are
+  // proven for (byte fq: 2^21 <= p < 2^23, q < 2^16; codepoint wide:
+  // 0x10FFFF < p < 2^23, q < 2^16): K1 then runs the 64-bit Barrett
+  // reduction of the reference itself (minhash.cpp:61-67), exact for p < 2^31
+  bool exact = false;
 };
 
 // Simple growable device scratch buffer.
@@ -139,6 +146,7 @@ int bits_for(uint64_t maxval);  // number of bits needed to hold maxval
 // K2 output: non-singleton LSH cells as CSR over sorted rows (k_cells.cu).
 constexpr uint32_t kCmpRows = 128;  // rows per compare work item (128 threads x kR)
 constexpr uint32_t kJoinMax = 4096;  // largest cell the hash join (k_join) takes
+constexpr uint32_t kJoinMaxP = 510;  // largest H - min_matches + 1 the joins' 9-bit tags take
 struct CellSet {
   DevBuf rec_keys, rec_vals, flag, run_idx, run_start, cstart, clen, ckey, cpairs, ctiles, pair_off,
       ioff, icell, scan, maxbuf;
@@ -146,6 +154,7 @@ struct CellSet {
   uint64_t max_len = 0;         // largest non-singleton cell
   SortScratch sort;
   uint64_t records = 0, ncells = 0, items = 0, candidate_pairs = 0;
+  uint32_t tile_rows = kCmpRows;
   const uint32_t* sorted_rows = nullptr;  // rows of all records, grouped by cell
   uint64_t* cell_start = nullptr;         // per non-singleton cell
   uint32_t* cell_len = nullptr;
@@ -162,6 +171,8 @@ struct CellSet {
 // records: keys = cell ids (< key_limit), vals = rows; both are permuted.
 void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint64_t m,
                               uint64_t key_limit, uint32_t tile_rows, cudaStream_t s);
+// re-tiles every cell for the all-pairs kernel (joins not applicable)
+void cells_all_pairs_tiles(CellSet& cs, cudaStream_t s);
 void make_records(const uint32_t* band, uint64_t n, uint32_t bands, uint32_t K, uint32_t doc_base,
                   uint32_t* keys, uint32_t* vals, cudaStream_t s);
 void build_cells_from_bands(CellSet& cs, const uint32_t* band, uint64_t n, uint32_t bands,
@@ -201,7 +212,7 @@ struct SigView {
     return bases[r] + (static_cast<uint64_t>(g) - row_base[r]) * H;
   }
 };
-void launch_compare(const CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_match,
+void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_match,
                     int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,
                     uint64_t cap, cudaStream_t s);
 uint64_t unique_pairs(PairSet& ps, cudaStream_t s);

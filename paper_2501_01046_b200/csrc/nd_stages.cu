@@ -427,16 +427,18 @@ int nd_union_stage(nd_ctx* ctx, const char* const* pair_paths, uint32_t nfiles,
     std::vector<uint32_t> m;
     for (uint32_t f = 0; f < nfiles; ++f) pairs_read(pair_paths[f], lo, hi, m);
     const uint64_t np = lo.size();
-    // node ids: doc ids themselves when they fit, else a dense renumbering
-    // (union_pairs renumbers densely too, dedup_graph.cpp:48-54)
+    // node ids: doc ids themselves when they are dense enough (the union
+    // arrays are sized by the largest id), else a dense renumbering of the
+    // ids that occur in pairs (union_pairs renumbers densely, dedup_graph.cpp:48-54)
     uint64_t maxid = 0;
     for (uint64_t i = 0; i < np; ++i) maxid = std::max(maxid, std::max(lo[i], hi[i]));
+    const bool direct = maxid < 0x7FFFFFFFull && maxid < 16 * np + (1ull << 20);
     DedupState& st = ctx->dedup;
     st.valid = false;
     st.doc_ids.clear();
     std::vector<uint32_t> l32(np), h32(np);
     uint64_t nnodes = np ? maxid + 1 : 1;
-    if (maxid < 0x7FFFFFFFull) {
+    if (direct) {
       for (uint64_t i = 0; i < np; ++i) {
         l32[i] = static_cast<uint32_t>(lo[i]);
         h32[i] = static_cast<uint32_t>(hi[i]);
