@@ -30,8 +30,8 @@ extern "C" {
 
 /* HashFunctionParams (minhash.hpp:17-25), byte-identical layout (24 bytes). */
 typedef struct nd_hash_fn {
-  uint32_t modulus;      /* prime p in [2^21, 2^23) */
-  uint32_t base;         /* prime q in (256, 2^16) */
+  uint32_t modulus;      /* prime p (derive_family: [2^21, 2^23); GPU path: < 2^31) */
+  uint32_t base;         /* prime q (derive_family: (256, 2^16)) */
   uint32_t base_inverse; /* q^-1 mod p */
   uint32_t base_power;   /* q^(L-1) mod p */
   uint64_t reduce_factor;/* floor(2^64 / p) */
@@ -190,7 +190,9 @@ typedef struct nd_dedup_stats {
   uint64_t duplicate_groups;
   uint64_t near_duplicates;
   uint64_t removals;
-  double seconds[6];         /* device time: sig, cells, compare, pairs, cc, d2h */
+  double seconds[6];         /* device time: sig (K1), cells (K2), compare (K3),
+                                distinct pairs (K4a sort + unique), cc (K4), d2h */
+  uint64_t cell_records;     /* sum of n over the non-singleton cells (K3's rows) */
 } nd_dedup_stats;
 int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const uint64_t* doc_ids,
              uint64_t n, const nd_params* params, nd_dedup_stats* stats);

@@ -155,6 +155,80 @@ int ref_compare_cells(const uint32_t* sigs, const uint64_t* doc_ids, uint32_t H,
   });
 }
 
+// Kernel-only CPU baseline of the compare step: cells are
+// gathered into GatheredBuckets (scan_gather's copies, timed apart), then
+// compare_bucket (compare.cpp:24-67) runs over every cell with the
+// reference's own parallel_for_index (util.cpp:81-122) -- parallel over cells,
+// not capped at one worker per band like run_compare_stage
+// (pipeline.cpp:387-420) -- and the accepted pairs are sorted + uniqued
+// (compare_pass, compare.cpp:77-84).  Times in seconds; counts out.
+int ref_compare_cells_timed(const uint32_t* sigs, uint32_t H, const uint64_t* cell_offsets,
+                            const uint32_t* cell_rows, uint64_t ncells, uint64_t thr_num,
+                            uint64_t thr_den, unsigned workers, double* gather_s,
+                            double* compare_s, double* unique_s, uint64_t* emitted,
+                            uint64_t* distinct, uint64_t** lo_out, uint64_t** hi_out) {
+  return guarded([&] {
+    using clk = std::chrono::steady_clock;
+    auto t0 = clk::now();
+    std::vector<GatheredBucket> cells(ncells);
+    parallel_for_index(ncells, workers, [&](uint64_t c) {
+      GatheredBucket& b = cells[c];
+      b.key = {0, static_cast<uint32_t>(c)};
+      for (uint64_t k = cell_offsets[c]; k < cell_offsets[c + 1]; ++k) {
+        const uint32_t r = cell_rows[k];
+        b.doc_ids.push_back(r);
+        b.signatures.insert(b.signatures.end(), sigs + static_cast<uint64_t>(r) * H,
+                            sigs + static_cast<uint64_t>(r + 1) * H);
+      }
+    });
+    auto t1 = clk::now();
+    const SimilarityThreshold thr{Ratio(thr_num, thr_den)};
+    std::vector<std::vector<DuplicatePair>> out(ncells);
+    parallel_for_index(ncells, workers,
+                       [&](uint64_t c) { out[c] = compare_bucket(cells[c], H, thr); });
+    auto t2 = clk::now();
+    std::vector<DuplicatePair> all;
+    for (auto& v : out) all.insert(all.end(), v.begin(), v.end());
+    *emitted = all.size();
+    std::sort(all.begin(), all.end(), [](const DuplicatePair& a, const DuplicatePair& b) {
+      return a.lo != b.lo ? a.lo < b.lo : a.hi < b.hi;
+    });
+    all.erase(std::unique(all.begin(), all.end(),
+                          [](const DuplicatePair& a, const DuplicatePair& b) {
+                            return a.lo == b.lo && a.hi == b.hi;
+                          }),
+              all.end());
+    auto t3 = clk::now();
+    *distinct = all.size();
+    *gather_s = std::chrono::duration<double>(t1 - t0).count();
+    *compare_s = std::chrono::duration<double>(t2 - t1).count();
+    *unique_s = std::chrono::duration<double>(t3 - t2).count();
+    *lo_out = static_cast<uint64_t*>(std::malloc(8 * (all.size() + 1)));
+    *hi_out = static_cast<uint64_t*>(std::malloc(8 * (all.size() + 1)));
+    for (size_t i = 0; i < all.size(); ++i) {
+      (*lo_out)[i] = all[i].lo;
+      (*hi_out)[i] = all[i].hi;
+    }
+  });
+}
+
+// union_pairs + components (dedup_graph.cpp:48-81) timed inside the library
+int ref_union_timed(const uint64_t* lo, const uint64_t* hi, uint64_t npairs, double* seconds,
+                    uint64_t* ngroups, uint64_t* nmembers) {
+  return guarded([&] {
+    std::vector<DuplicatePair> pairs(npairs);
+    for (uint64_t i = 0; i < npairs; ++i) pairs[i] = {lo[i], hi[i], 0};
+    auto t0 = std::chrono::steady_clock::now();
+    UnionFind uf = union_pairs(pairs);
+    std::vector<DuplicateGroup> groups = components(uf);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    uint64_t m = 0;
+    for (const auto& g : groups) m += g.members.size();
+    *ngroups = groups.size();
+    *nmembers = m;
+  });
+}
+
 // all_pairs_dupset (oracle.cpp:53-108): docs with any partner above the
 // threshold; out receives the sorted doc ids, *nout their count.
 int ref_all_pairs_dupset(const uint32_t* sigs, const uint64_t* doc_ids, uint64_t n, uint32_t H,

@@ -54,7 +54,8 @@ class NdDedupStats(C.Structure):
                 ("nonsingleton_cells", C.c_uint64), ("candidate_pairs", C.c_uint64),
                 ("emitted_pairs", C.c_uint64), ("distinct_pairs", C.c_uint64),
                 ("duplicate_groups", C.c_uint64), ("near_duplicates", C.c_uint64),
-                ("removals", C.c_uint64), ("seconds", C.c_double * 6)]
+                ("removals", C.c_uint64), ("seconds", C.c_double * 6),
+                ("cell_records", C.c_uint64)]
 
 
 class NdFedsHeader(C.Structure):

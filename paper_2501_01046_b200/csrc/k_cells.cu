@@ -53,6 +53,7 @@ __global__ void k_cells_compact(const uint64_t* __restrict__ run_start, const ui
                                 uint32_t* __restrict__ cell_key, uint64_t* __restrict__ cell_pairs,
                                 uint32_t* __restrict__ cell_tiles, uint32_t join_max,
                                 unsigned long long* __restrict__ max_len) {
+  // max_len[0]: largest cell; max_len[1]: sum of n over the kept cells
   uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (r >= runs || !keep[r]) return;
   uint64_t c = keep_idx[r];
@@ -65,6 +66,7 @@ __global__ void k_cells_compact(const uint64_t* __restrict__ run_start, const ui
   // cells the hash join takes (k_join) need no all-pairs tiles
   cell_tiles[c] = len > join_max ? static_cast<uint32_t>((len + tile_rows - 1) / tile_rows) : 0u;
   atomicMax(max_len, static_cast<unsigned long long>(len));
+  atomicAdd(max_len + 1, static_cast<unsigned long long>(len));
 }
 
 __global__ void k_all_pairs_tiles(const uint32_t* __restrict__ cell_len, uint64_t cells,
@@ -101,6 +103,7 @@ void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint6
   cs.records = m;
   cs.tile_rows = tile_rows;
   cs.ncells = 0;
+  cs.cell_records = 0;
   cs.items = 0;
   cs.candidate_pairs = 0;
   if (m == 0) return;
@@ -132,8 +135,8 @@ void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint6
   cs.cell_key = cs.ckey.as<uint32_t>(cells);
   uint64_t* cpairs = cs.cpairs.as<uint64_t>(cells + 1);
   uint32_t* ctiles = cs.ctiles.as<uint32_t>(cells);
-  unsigned long long* dmax = reinterpret_cast<unsigned long long*>(cs.maxbuf.as<uint64_t>(1));
-  ND_CUDA(cudaMemsetAsync(dmax, 0, sizeof(uint64_t), s));
+  unsigned long long* dmax = reinterpret_cast<unsigned long long*>(cs.maxbuf.as<uint64_t>(2));
+  ND_CUDA(cudaMemsetAsync(dmax, 0, 2 * sizeof(uint64_t), s));
   k_cells_compact<<<blocks_for(runs, tb), tb, 0, s>>>(run_start, keep, keep_idx, runs, keys,
                                                       tile_rows, cs.cell_start, cs.cell_len,
                                                       cs.cell_key, cpairs, ctiles,
@@ -143,14 +146,15 @@ void build_cells_from_records(CellSet& cs, uint32_t* keys, uint32_t* vals, uint6
   scan_u64(cpairs, pair_off, cells, cs.scan, s);
   cs.item_off = cs.ioff.as<uint64_t>(cells + 1);
   scan_u32_to_u64(ctiles, cs.item_off, cells, cs.scan, s);
-  uint64_t tail[3];
+  uint64_t tail[4];
   ND_CUDA(cudaMemcpyAsync(&tail[0], pair_off + cells, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   ND_CUDA(cudaMemcpyAsync(&tail[1], cs.item_off + cells, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-  ND_CUDA(cudaMemcpyAsync(&tail[2], dmax, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  ND_CUDA(cudaMemcpyAsync(&tail[2], dmax, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   ND_CUDA(cudaStreamSynchronize(s));
   cs.candidate_pairs = tail[0];
   cs.items = tail[1];
   cs.max_len = cs.join_enabled ? tail[2] : 0;
+  cs.cell_records = tail[3];
   cs.item_cell = cs.icell.as<uint32_t>(cs.items + 1);
   if (cs.items)
     k_item_cells<<<blocks_for(cells, tb), tb, 0, s>>>(cs.item_off, cells, cs.item_cell);

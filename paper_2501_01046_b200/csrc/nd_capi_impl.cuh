@@ -58,6 +58,8 @@ void ensure_family(nd_ctx* ctx, const nd_params& p);  // derive + upload when it
 // K3 + distinct pairs over st.cells (grows the pair buffer on overflow)
 void compare_and_unique(DedupState& st, const uint32_t* d_sig, uint32_t H, uint32_t mm,
                         uint64_t nrows, cudaStream_t s);
+void compare_pairs(DedupState& st, const SigView& d_sig, uint32_t H, uint32_t mm, uint64_t nrows,
+                   cudaStream_t s);
 void compare_and_unique(DedupState& st, const SigView& d_sig, uint32_t H, uint32_t mm,
                         uint64_t nrows, cudaStream_t s);
 // signatures of a host batch into device buffers (pipelined H2D, text kept in st.text)

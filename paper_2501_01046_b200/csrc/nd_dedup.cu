@@ -72,6 +72,13 @@ void compare_and_unique(DedupState& st, const uint32_t* d_sig, uint32_t H, uint3
 
 void compare_and_unique(DedupState& st, const SigView& d_sig, uint32_t H, uint32_t mm,
                         uint64_t nrows, cudaStream_t s) {
+  compare_pairs(st, d_sig, H, mm, nrows, s);
+  unique_pairs(st.pairs, s);
+}
+
+// K3 only: accepted pairs (with repeats across bands) into st.pairs
+void compare_pairs(DedupState& st, const SigView& d_sig, uint32_t H, uint32_t mm, uint64_t nrows,
+                   cudaStream_t s) {
   PairSet& ps = st.pairs;
   ps.nb = std::max(1, bits_for(nrows ? nrows - 1 : 0));
   if (2 * ps.nb > 64) fail(ND_ERR_CONFIG, "too many rows for packed pair keys");
@@ -89,7 +96,6 @@ void compare_and_unique(DedupState& st, const SigView& d_sig, uint32_t H, uint32
     if (got <= ps.cap) break;
     ps.cap = got + got / 4;
   }
-  unique_pairs(ps, s);
 }
 
 namespace {
@@ -185,10 +191,12 @@ void dedup_tail(nd_ctx* ctx, DedupState& st, const nd_params& p, uint64_t n, nd_
   build_cells_from_bands(st.cells, st.band.as<uint32_t>(n * p.bands), n, p.bands, st.K, kCmpRows,
                          s);
   t.mark();  // 2
-  compare_and_unique(st, st.sig.as<uint32_t>(n * H), H, mm, n, s);
+  compare_pairs(st, SigView(st.sig.as<uint32_t>(n * H), H), H, mm, n, s);
   t.mark();  // 3
-  components(st.groups, st.pairs.lo, st.pairs.hi, st.pairs.distinct, n, s);
+  unique_pairs(st.pairs, s);
   t.mark();  // 4
+  components(st.groups, st.pairs.lo, st.pairs.hi, st.pairs.distinct, n, s);
+  t.mark();  // 5
   ND_CUDA(cudaStreamSynchronize(s));
   st.documents = n;
   st.bands = p.bands;
@@ -206,9 +214,10 @@ void dedup_tail(nd_ctx* ctx, DedupState& st, const nd_params& p, uint64_t n, nd_
     stats->seconds[0] = t.seconds(0, 1);
     stats->seconds[1] = t.seconds(1, 2);
     stats->seconds[2] = t.seconds(2, 3);
-    stats->seconds[3] = 0;  // distinct pairs are folded into [2]
-    stats->seconds[4] = t.seconds(3, 4);
+    stats->seconds[3] = t.seconds(3, 4);
+    stats->seconds[4] = t.seconds(4, 5);
     stats->seconds[5] = 0;
+    stats->cell_records = st.cells.cell_records;
   }
 }
 

@@ -154,6 +154,7 @@ struct CellSet {
   uint64_t max_len = 0;         // largest non-singleton cell
   SortScratch sort;
   uint64_t records = 0, ncells = 0, items = 0, candidate_pairs = 0;
+  uint64_t cell_records = 0;    // sum of n over non-singleton cells
   uint32_t tile_rows = kCmpRows;
   const uint32_t* sorted_rows = nullptr;  // rows of all records, grouped by cell
   uint64_t* cell_start = nullptr;         // per non-singleton cell

@@ -172,6 +172,11 @@ class Ref:
                                            C.c_uint64, C.c_uint, u64p, u64p]
         L.ref_union.argtypes = [u64p, u64p, C.c_uint64, C.POINTER(u64p), C.POINTER(u64p), u64p,
                                 u64p]
+        dp = C.POINTER(C.c_double)
+        L.ref_compare_cells_timed.argtypes = [u32p, C.c_uint32, u64p, u32p, C.c_uint64,
+                                              C.c_uint64, C.c_uint64, C.c_uint, dp, dp, dp, u64p,
+                                              u64p, C.POINTER(u64p), C.POINTER(u64p)]
+        L.ref_union_timed.argtypes = [u64p, u64p, C.c_uint64, dp, u64p, u64p]
         L.ref_generate_synthetic.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
                                              C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
                                              C.c_uint64, C.c_uint32, C.c_char_p, C.c_char_p,
@@ -244,6 +249,35 @@ class Ref:
         for p in (lo, hi, m):
             self.lib.ref_free(p)
         return out
+
+    def compare_cells_timed(self, sigs, cell_offsets, cell_rows, num, den, workers):
+        """compare_bucket over every cell, parallel over cells (kernel-only CPU
+        baseline): returns dict of seconds + counts and the distinct (lo, hi) rows."""
+        sigs = np.ascontiguousarray(sigs, np.uint32)
+        co = np.ascontiguousarray(cell_offsets, np.uint64)
+        cr = np.ascontiguousarray(cell_rows, np.uint32)
+        g, c, u = C.c_double(), C.c_double(), C.c_double()
+        em, di = C.c_uint64(), C.c_uint64()
+        lo, hi = u64p(), u64p()
+        self._check(self.lib.ref_compare_cells_timed(
+            _ptr(sigs, u32p), sigs.shape[1], _ptr(co, u64p), _ptr(cr, u32p), len(co) - 1, num, den,
+            workers, C.byref(g), C.byref(c), C.byref(u), C.byref(em), C.byref(di), C.byref(lo),
+            C.byref(hi)))
+        k = di.value
+        plo = np.ctypeslib.as_array(lo, (k + 1,))[:k].copy()
+        phi = np.ctypeslib.as_array(hi, (k + 1,))[:k].copy()
+        self.lib.ref_free(lo)
+        self.lib.ref_free(hi)
+        return ({"gather_s": g.value, "compare_s": c.value, "unique_s": u.value,
+                 "emitted": em.value, "distinct": k}, plo, phi)
+
+    def union_timed(self, lo, hi):
+        lo = np.ascontiguousarray(lo, np.uint64)
+        hi = np.ascontiguousarray(hi, np.uint64)
+        t, g, m = C.c_double(), C.c_uint64(), C.c_uint64()
+        self._check(self.lib.ref_union_timed(_ptr(lo, u64p), _ptr(hi, u64p), len(lo), C.byref(t),
+                                             C.byref(g), C.byref(m)))
+        return {"seconds": t.value, "groups": g.value, "members": m.value}
 
     def all_pairs_dupset(self, sigs, num, den, workers=8, doc_ids=None):
         sigs = np.ascontiguousarray(sigs, np.uint32)
