@@ -29,7 +29,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 sys.path.insert(0, os.path.join(ROOT, "scripts"))
-from oracle_bind import Oracle, Ref, u32p, u64p  # noqa: E402
+from oracle_bind import Ref, u32p, u64p  # noqa: E402
 from run_configs import CONFIGS, spec_for  # noqa: E402
 
 from paper_2501_01046_b200 import _lib, pipeline  # noqa: E402
@@ -133,58 +133,15 @@ def main():
                 json.dump(res, f, indent=1)
         return
 
-    # ---- 3. cells + every candidate pair by the C oracle ----------------------
-    o = Oracle()
-    L = o.lib
-    L.ov_cells.argtypes = [u32p, C.c_uint64, C.c_uint32, C.c_uint32, u64p, u32p]
-    L.ov_compare_cells.argtypes = [u32p, C.c_uint32, u64p, u32p, C.c_uint64, C.c_uint64,
-                                   C.c_uint64, C.c_int, C.POINTER(u32p), C.POINTER(u32p),
-                                   C.POINTER(u32p), u64p]
-    L.ov_compare_cells.restype = C.c_int64
-    L.ov_free.argtypes = [C.c_void_p]
-    t = time.time()
-    cells = B * K
-    coff = np.empty(cells + 1, np.uint64)
-    rows = np.empty(docs * B, np.uint32)
-    assert L.ov_cells(band.ctypes.data_as(u32p), docs, B, K, coff.ctypes.data_as(u64p),
-                      rows.ctypes.data_as(u32p)) == 0
-    lo_p, hi_p, m_p, cand = u32p(), u32p(), u32p(), C.c_uint64()
-    k = L.ov_compare_cells(sig.ctypes.data_as(u32p), H, coff.ctypes.data_as(u64p),
-                           rows.ctypes.data_as(u32p), cells, 4, 5, a.threads, C.byref(lo_p),
-                           C.byref(hi_p), C.byref(m_p), C.byref(cand))
-    assert k >= 0
-    olo = np.ctypeslib.as_array(lo_p, (max(k, 1),))[:k].astype(np.uint64)
-    ohi = np.ctypeslib.as_array(hi_p, (max(k, 1),))[:k].astype(np.uint64)
-    om = np.ctypeslib.as_array(m_p, (max(k, 1),))[:k].copy()
-    for p in (lo_p, hi_p, m_p):
-        L.ov_free(p)
-    key = (olo << np.uint64(32)) | ohi
-    order = np.argsort(key, kind="stable")
-    key, om = key[order], om[order]
-    first = np.r_[True, key[1:] != key[:-1]]
-    key, om = key[first], om[first]
-    gkey = (plo << np.uint64(32)) | phi
-    res.update(candidate_pairs_oracle=int(cand.value), emitted_pairs_oracle=int(k),
-               distinct_pairs_oracle=int(len(key)),
-               pairs_identical=bool(np.array_equal(key, gkey) and np.array_equal(om, pm)),
-               oracle_compare_seconds=time.time() - t)
-    log(stage="pairs", **{x: res[x] for x in ("candidate_pairs_oracle", "distinct_pairs_oracle",
-                                               "pairs_identical", "oracle_compare_seconds")})
+    # ---- 3./4. every candidate pair + groups (tests/scale_check.py) ------------
+    import scale_check as sc
 
-    # ---- 4. components ----------------------------------------------------------
+    pr = sc.check_pairs(sig, band, K, 4, 5, (plo, phi, pm), threads=a.threads)
+    key = pr.pop("_keys")
+    res.update(pr)
+    log(stage="pairs", **pr)
     t = time.time()
-    lab = np.empty(docs, np.uint32)
-    lo32 = (key >> np.uint64(32)).astype(np.uint32)
-    hi32 = (key & np.uint64(0xFFFFFFFF)).astype(np.uint32)
-    L.or_components(lo32.ctypes.data_as(u32p), hi32.ctypes.data_as(u32p), len(key), docs,
-                    lab.ctypes.data_as(u32p))
-    glab = np.full(docs, 0xFFFFFFFF, np.uint32)
-    sizes = np.diff(gst).astype(np.int64)
-    reps = gmem[gst[:-1].astype(np.int64)]
-    glab[gmem.astype(np.int64)] = np.repeat(reps, sizes).astype(np.uint32)
-    res.update(groups_oracle=int(len(np.unique(lab[lab != 0xFFFFFFFF]))),
-               groups_identical=bool(np.array_equal(lab, glab)),
-               oracle_union_seconds=time.time() - t)
+    res.update(sc.check_groups(key, docs, (gmem, gst)), oracle_union_seconds=time.time() - t)
     res["bit_exact"] = bool(bad_sig == 0 and bad_band == 0 and res["pairs_identical"]
                             and res["groups_identical"]
                             and res["candidate_pairs_oracle"] == res["candidate_pairs_gpu"])
