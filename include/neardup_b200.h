@@ -193,6 +193,7 @@ typedef struct nd_dedup_stats {
   double seconds[6];         /* device time: sig (K1), cells (K2), compare (K3),
                                 distinct pairs (K4a sort + unique), cc (K4), d2h */
   uint64_t cell_records;     /* sum of n over the non-singleton cells (K3's rows) */
+  uint32_t intervals;        /* bucket intervals (1 = everything resident in HBM) */
 } nd_dedup_stats;
 int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const uint64_t* doc_ids,
              uint64_t n, const nd_params* params, nd_dedup_stats* stats);
@@ -211,6 +212,11 @@ int nd_dedup_fetch_groups(nd_ctx* ctx, uint64_t* members, uint64_t* group_start)
 /* Reference-identical report bytes (groups.jsonl, removal.txt, summary.json
  * as written by pipeline.cpp:479-506) for the last dedup, into dir. */
 int nd_dedup_write_report(nd_ctx* ctx, const char* dir, uint64_t total_records);
+/* Same; fsync_files != 0 fsyncs each file before closing it, as the
+ * reference's write_file_bytes does under --fsync (util.cpp:132-140,
+ * pipeline.cpp:487-506). */
+int nd_dedup_write_report_ex(nd_ctx* ctx, const char* dir, uint64_t total_records,
+                             int fsync_files);
 
 /* ---- host document loader (corpus.cpp / text.cpp), multi-threaded C++ ------
  * One JSONL file per call: lines split as for_each_raw_document

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <filesystem>
 #include <fstream>
 #include <sstream>
@@ -36,6 +37,7 @@
 #include "neardup/pipeline.hpp"
 #include "neardup/util.hpp"
 #include "neardup_b200.h"
+#include <unistd.h>
 
 #include <nlohmann/json.hpp>
 
@@ -223,11 +225,15 @@ namespace detail {
 namespace fs = std::filesystem;
 using ojson = nlohmann::ordered_json;
 
-inline void write_text(const std::string& path, const std::string& bytes) {
-  std::ofstream f(path, std::ios::binary);
+// write_file_bytes (util.cpp:132-140): write, flush, optional fsync, close
+inline void write_text(const std::string& path, const std::string& bytes, bool fsync_file = false) {
+  FILE* f = std::fopen(path.c_str(), "wb");
   if (!f) throw IoError("cannot create '" + path + "'");
-  f << bytes;
-  if (!f) throw IoError("write failed for '" + path + "'");
+  bool ok = bytes.empty() || std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size();
+  if (ok && std::fflush(f) != 0) ok = false;
+  if (ok && fsync_file && ::fsync(fileno(f)) != 0) ok = false;
+  if (std::fclose(f) != 0) ok = false;
+  if (!ok) throw IoError("write failed for '" + path + "'");
 }
 inline std::string read_text(const std::string& path) {
   std::ifstream f(path, std::ios::binary);
@@ -403,7 +409,8 @@ inline HashStageOutput run_hash_stage(Device& dev, const RunConfig& config) {
     files.push_back(e);
   }
   doc["files"] = files;
-  detail::write_text(config.workspace + "/run_manifest.json", doc.dump(2) + "\n");
+  detail::write_text(config.workspace + "/run_manifest.json", doc.dump(2) + "\n",
+                     config.fsync_files);  // pipeline.cpp:335
   return out;
 }
 
@@ -473,7 +480,8 @@ inline CompareStageOutput run_compare_stage(Device& dev, const RunConfig& config
   detail::ojson files = detail::ojson::array();
   for (const auto& f : out.pair_files) files.push_back(fs::path(f).filename().string());
   doc["pair_files"] = files;
-  detail::write_text(config.workspace + "/compare_stage.json", doc.dump(2) + "\n");
+  detail::write_text(config.workspace + "/compare_stage.json", doc.dump(2) + "\n",
+                     config.fsync_files);  // pipeline.cpp:444
   return out;
 }
 

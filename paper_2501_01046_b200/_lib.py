@@ -55,7 +55,7 @@ class NdDedupStats(C.Structure):
                 ("emitted_pairs", C.c_uint64), ("distinct_pairs", C.c_uint64),
                 ("duplicate_groups", C.c_uint64), ("near_duplicates", C.c_uint64),
                 ("removals", C.c_uint64), ("seconds", C.c_double * 6),
-                ("cell_records", C.c_uint64)]
+                ("cell_records", C.c_uint64), ("intervals", C.c_uint32)]
 
 
 class NdFedsHeader(C.Structure):
@@ -123,6 +123,7 @@ SIGNATURES = {
     "nd_dedup_fetch_signatures": (C.c_int, [vp, u32p, u32p]),
     "nd_dedup_fetch_groups": (C.c_int, [vp, u64p, u64p]),
     "nd_dedup_write_report": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
+    "nd_dedup_write_report_ex": (C.c_int, [vp, C.c_char_p, C.c_uint64, C.c_int]),
     "nd_ingest_last_error": (C.c_char_p, []),
     "nd_jsonl_load": (C.c_int, [C.c_char_p, C.c_char_p, C.c_uint64, C.c_uint32, C.c_uint32,
                                 C.c_uint32, C.c_int, C.POINTER(vp)]),

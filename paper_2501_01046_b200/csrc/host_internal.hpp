@@ -37,7 +37,7 @@ void synth_generate(const nd_synth_spec& spec, uint8_t* bytes, uint64_t* offsets
 void write_report(const std::string& dir, const std::vector<uint64_t>& members,
                   const std::vector<uint64_t>& group_start, const std::vector<uint64_t>& near,
                   const std::vector<uint64_t>& removals, uint64_t total_documents,
-                  uint64_t total_records, uint64_t distinct_pairs);
+                  uint64_t total_records, uint64_t distinct_pairs, bool fsync_files = false);
 
 // staged-workflow artifacts (host_feds.cpp)
 constexpr uint64_t kFedsHeaderBytes = 72;

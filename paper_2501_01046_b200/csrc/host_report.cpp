@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unistd.h>
 #include <vector>
 
 #include <nlohmann/json.hpp>
@@ -15,10 +16,13 @@
 namespace ndb {
 namespace {
 
-void write_file(const std::string& path, const std::string& bytes) {
+// write_file_bytes (util.cpp:132-140): write, flush, optional fsync, close
+void write_file(const std::string& path, const std::string& bytes, bool fsync_file) {
   FILE* f = std::fopen(path.c_str(), "wb");
   if (!f) fail(ND_ERR_IO, "cannot create '" + path + "': " + std::strerror(errno));
   bool ok = bytes.empty() || std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size();
+  if (ok && std::fflush(f) != 0) ok = false;
+  if (ok && fsync_file && fsync(fileno(f)) != 0) ok = false;
   if (std::fclose(f) != 0) ok = false;
   if (!ok) fail(ND_ERR_IO, "write failed for '" + path + "'");
 }
@@ -28,7 +32,7 @@ void write_file(const std::string& path, const std::string& bytes) {
 void write_report(const std::string& dir, const std::vector<uint64_t>& members,
                   const std::vector<uint64_t>& group_start, const std::vector<uint64_t>& near,
                   const std::vector<uint64_t>& removals, uint64_t total_documents,
-                  uint64_t total_records, uint64_t distinct_pairs) {
+                  uint64_t total_records, uint64_t distinct_pairs, bool fsync_files) {
   using ordered_json = nlohmann::ordered_json;
   const uint64_t groups = group_start.empty() ? 0 : group_start.size() - 1;
   std::string lines;
@@ -40,14 +44,14 @@ void write_report(const std::string& dir, const std::vector<uint64_t>& members,
     lines += j.dump();
     lines += '\n';
   }
-  write_file(dir + "/groups.jsonl", lines);
+  write_file(dir + "/groups.jsonl", lines, fsync_files);  // pipeline.cpp:487
 
   std::string rem;
   for (uint64_t d : removals) {
     rem += std::to_string(d);
     rem += '\n';
   }
-  write_file(dir + "/removal.txt", rem);
+  write_file(dir + "/removal.txt", rem, fsync_files);  // pipeline.cpp:494
 
   double ratio = total_documents > 0 ? static_cast<double>(near.size()) /
                                            static_cast<double>(total_documents)
@@ -61,7 +65,7 @@ void write_report(const std::string& dir, const std::vector<uint64_t>& members,
   summary["distinct_pairs"] = distinct_pairs;
   summary["ratio"] = ratio;
   summary["ratio_label"] = std::to_string(near.size()) + " / " + std::to_string(total_documents);
-  write_file(dir + "/summary.json", summary.dump(2) + "\n");
+  write_file(dir + "/summary.json", summary.dump(2) + "\n", fsync_files);  // pipeline.cpp:506
 }
 
 }  // namespace ndb

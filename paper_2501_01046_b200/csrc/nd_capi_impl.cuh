@@ -52,6 +52,10 @@ struct nd_ctx {
 
 namespace ndb {
 int guarded_impl(nd_ctx* ctx, const std::function<void()>& fn);
+// nd_signatures' host pipeline (chunks in, signature rows + band ids out)
+void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                     uint32_t bands, uint32_t rows, uint32_t K, uint32_t* sig_out,
+                     uint32_t* band_out);
 // shared by nd_dedup.cu and nd_stages.cu
 void validate(const nd_params& p);                 // RunConfig::validate, artifact fields
 void ensure_family(nd_ctx* ctx, const nd_params& p);  // derive + upload when it changed

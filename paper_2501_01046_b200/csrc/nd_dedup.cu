@@ -8,6 +8,7 @@
 // comparison (K3), distinct pairs + components (K4).  Only the report leaves
 // the device.
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -218,6 +219,168 @@ void dedup_tail(nd_ctx* ctx, DedupState& st, const nd_params& p, uint64_t n, nd_
     stats->seconds[4] = t.seconds(4, 5);
     stats->seconds[5] = 0;
     stats->cell_records = st.cells.cell_records;
+    stats->intervals = 1;
+  }
+}
+
+uint64_t hbm_budget_of(nd_ctx* ctx) {
+  if (ctx->hbm_budget) return ctx->hbm_budget;
+  size_t fr = 0, tot = 0;
+  ND_CUDA(cudaMemGetInfo(&fr, &tot));
+  return static_cast<uint64_t>(fr) / 10 * 7;
+}
+
+// Device bytes of the in-memory dedup per document: signature + band ids +
+// doc map, and per (document, band) record: key + row, their sort
+// alternates and the cell CSR (the same estimate as the staged compare's
+// interval plan, nd_stages.cu).
+constexpr uint64_t kRecBytes = 8 * 4;
+uint64_t row_bytes_of(const nd_params& p) { return 4ull * p.hash_count + 4ull * p.bands + 8; }
+
+// Out-of-core in-memory dedup (plan_gather's idea, sigstore.cpp:288-329,
+// applied to HBM instead of host RAM): when the signatures and cell records of
+// the batch would not fit the HBM budget, K1 streams them back to host memory
+// (nd_signatures' pipeline), the buckets are cut into intervals [k0, k1) whose
+// documents + records fit, and each interval runs K2 + K3 on just the
+// documents with a band bucket inside it and their in-range records.  Cells
+// are (band, bucket), so every cell lies in exactly one interval: the
+// candidate count is the sum over intervals, and the union of the intervals'
+// accepted pairs, sorted + uniqued once more, is the single-pass pair set
+// (a pair can be accepted in two intervals through two bands).
+void dedup_out_of_core(nd_ctx* ctx, DedupState& st, const nd_params& p, const uint8_t* bytes,
+                       const uint64_t* offsets, uint64_t n, uint64_t budget, nd_dedup_stats* stats) {
+  using clk = std::chrono::steady_clock;
+  auto sec = [](clk::time_point a) { return std::chrono::duration<double>(clk::now() - a).count(); };
+  cudaStream_t s = ctx->stream;
+  const uint32_t H = p.hash_count, B = p.bands, K = st.K;
+  auto t0 = clk::now();
+  st.host_sig.resize(n * H);
+  st.host_band.resize(n * B);
+  signatures_host(ctx, bytes, offsets, n, B, p.rows, K, st.host_sig.data(), st.host_band.data());
+  const double t_sig = sec(t0);
+  auto t1 = clk::now();
+  const uint32_t* hband = st.host_band.data();
+  std::vector<uint64_t> per_bucket(K, 0);
+  for (uint64_t i = 0; i < n * B; ++i) ++per_bucket[hband[i]];
+  const uint64_t row_bytes = row_bytes_of(p);
+  std::vector<std::pair<uint32_t, uint32_t>> intervals;
+  {
+    uint32_t k0 = 0;
+    uint64_t acc = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+      const uint64_t bytes_k = per_bucket[k] * (row_bytes + kRecBytes);  // a record may bring its row
+      if (k > k0 && acc + bytes_k > budget) {
+        intervals.push_back({k0, k});
+        k0 = k;
+        acc = 0;
+      }
+      acc += bytes_k;
+    }
+    intervals.push_back({k0, K});
+  }
+  const uint32_t mm = min_matches(H, p.threshold_num, p.threshold_den);
+  uint64_t candidates = 0, emitted = 0, cell_records = 0, ncells = 0;
+  std::vector<uint32_t> all_lo, all_hi, all_m, sel, rkeys, rvals, gs, hl, hh, hm;
+  double t_cells = 0, t_cmp = 0;
+  for (auto [k0, k1] : intervals) {
+    auto ta = clk::now();
+    sel.clear();
+    rkeys.clear();
+    rvals.clear();
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint32_t* bi = hband + i * B;
+      bool any = false;
+      for (uint32_t j = 0; j < B && !any; ++j) any = bi[j] >= k0 && bi[j] < k1;
+      if (!any) continue;
+      const uint32_t local = static_cast<uint32_t>(sel.size());
+      sel.push_back(static_cast<uint32_t>(i));
+      for (uint32_t j = 0; j < B; ++j)
+        if (bi[j] >= k0 && bi[j] < k1) {
+          rkeys.push_back(j * K + bi[j]);
+          rvals.push_back(local);
+        }
+    }
+    const uint64_t m = sel.size();
+    if (m == 0) continue;
+    gs.resize(m * H);
+    for (uint64_t r = 0; r < m; ++r)
+      std::memcpy(gs.data() + r * H, st.host_sig.data() + uint64_t(sel[r]) * H, 4ull * H);
+    uint32_t* d_sig = st.sig.as<uint32_t>(m * H + 1);
+    ND_CUDA(cudaMemcpyAsync(d_sig, gs.data(), m * H * 4, cudaMemcpyHostToDevice, s));
+    const uint64_t nr = rkeys.size();
+    uint32_t* dk = st.cells.rec_keys.as<uint32_t>(nr + 1);
+    uint32_t* dv = st.cells.rec_vals.as<uint32_t>(nr + 1);
+    ND_CUDA(cudaMemcpyAsync(dk, rkeys.data(), nr * 4, cudaMemcpyHostToDevice, s));
+    ND_CUDA(cudaMemcpyAsync(dv, rvals.data(), nr * 4, cudaMemcpyHostToDevice, s));
+    build_cells_from_records(st.cells, dk, dv, nr, uint64_t(B) * K, kCmpRows, s);
+    ND_CUDA(cudaStreamSynchronize(s));
+    auto tb = clk::now();
+    t_cells += std::chrono::duration<double>(tb - ta).count();
+    candidates += st.cells.candidate_pairs;
+    cell_records += st.cells.cell_records;
+    ncells += st.cells.ncells;
+    compare_and_unique(st, SigView(d_sig, H), H, mm, m, s);
+    emitted += st.pairs.count;
+    const uint64_t d = st.pairs.distinct;
+    hl.resize(d);
+    hh.resize(d);
+    hm.resize(d);
+    if (d) {
+      ND_CUDA(cudaMemcpyAsync(hl.data(), st.pairs.lo, d * 4, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaMemcpyAsync(hh.data(), st.pairs.hi, d * 4, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaMemcpyAsync(hm.data(), st.pairs.mc, d * 4, cudaMemcpyDeviceToHost, s));
+    }
+    ND_CUDA(cudaStreamSynchronize(s));
+    for (uint64_t i = 0; i < d; ++i) {  // interval-local rows -> batch rows
+      all_lo.push_back(sel[hl[i]]);
+      all_hi.push_back(sel[hh[i]]);
+      all_m.push_back(hm[i]);
+    }
+    t_cmp += sec(tb);
+  }
+  // the intervals' pairs -> one distinct set -> components over all rows
+  auto t2 = clk::now();
+  const uint64_t np = all_lo.size();
+  uint32_t* d_lo = st.cells.rec_keys.as<uint32_t>(np + 1);
+  uint32_t* d_hi = st.cells.rec_vals.as<uint32_t>(np + 1);
+  uint32_t* d_m = st.cells.run_idx.as<uint32_t>(np + 1);
+  if (np) {
+    ND_CUDA(cudaMemcpyAsync(d_lo, all_lo.data(), np * 4, cudaMemcpyHostToDevice, s));
+    ND_CUDA(cudaMemcpyAsync(d_hi, all_hi.data(), np * 4, cudaMemcpyHostToDevice, s));
+    ND_CUDA(cudaMemcpyAsync(d_m, all_m.data(), np * 4, cudaMemcpyHostToDevice, s));
+  }
+  st.pairs.nb = std::max(1, bits_for(n - 1));
+  pack_pairs(st.pairs, d_lo, d_hi, d_m, np, s);
+  unique_pairs(st.pairs, s);
+  ND_CUDA(cudaStreamSynchronize(s));
+  const double t_uni = sec(t2);
+  auto t3 = clk::now();
+  components(st.groups, st.pairs.lo, st.pairs.hi, st.pairs.distinct, n, s);
+  ND_CUDA(cudaStreamSynchronize(s));
+  st.sig.release();  // the rows live in host memory
+  st.sig_on_host = true;
+  st.documents = n;
+  st.bands = B;
+  st.intervals = static_cast<uint32_t>(intervals.size());
+  st.valid = true;
+  if (stats) {
+    *stats = nd_dedup_stats{};
+    stats->documents = n;
+    stats->bucket_count = K;
+    stats->nonsingleton_cells = ncells;
+    stats->candidate_pairs = candidates;
+    stats->emitted_pairs = emitted;
+    stats->distinct_pairs = st.pairs.distinct;
+    stats->duplicate_groups = st.groups.groups;
+    stats->near_duplicates = st.groups.members;
+    stats->removals = st.groups.removals;
+    stats->seconds[0] = t_sig;
+    stats->seconds[1] = t_cells;
+    stats->seconds[2] = t_cmp;
+    stats->seconds[3] = t_uni;
+    stats->seconds[4] = sec(t3);
+    stats->cell_records = cell_records;
+    stats->intervals = st.intervals;
   }
 }
 
@@ -254,6 +417,15 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
       if (offsets[i + 1] < offsets[i] || offsets[i + 1] - offsets[i] < p.shingle_len)
         fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has fewer units than the shingle length");
     st.K = bucket_count_for(p, n);
+    st.sig_on_host = false;
+    st.host_sig.clear();
+    st.host_band.clear();
+    st.intervals = 1;
+    const uint64_t budget = hbm_budget_of(ctx);
+    if (n * row_bytes_of(p) + n * p.bands * kRecBytes > budget) {
+      dedup_out_of_core(ctx, st, p, bytes, offsets, n, budget, stats);
+      return;
+    }
     cudaStream_t s = ctx->stream;
     EventTimer t(s);
     t.mark();  // 0
@@ -290,6 +462,10 @@ int nd_dedup_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offse
     set_doc_ids(st, doc_ids, n);
     if (n == 0) fail(ND_ERR_CONFIG, "no documents survive preprocessing; nothing to deduplicate");
     st.K = bucket_count_for(p, n);
+    st.sig_on_host = false;
+    st.host_sig.clear();
+    st.host_band.clear();
+    st.intervals = 1;
     cudaStream_t s = ctx->stream;
     EventTimer t(s);
     t.mark();
@@ -307,6 +483,11 @@ int nd_dedup_fetch_signatures(nd_ctx* ctx, uint32_t* sig, uint32_t* band) {
     if (!st.valid || !ctx->fam.q) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");
     cudaStream_t s = ctx->stream;
     const uint64_t n = st.documents, H = ctx->fam.H;
+    if (st.sig_on_host) {  // out-of-core run: rows in host memory
+      if (sig && n) std::memcpy(sig, st.host_sig.data(), n * H * 4);
+      if (band && n) std::memcpy(band, st.host_band.data(), n * st.bands * 4);
+      return;
+    }
     if (sig && n)
       ND_CUDA(cudaMemcpyAsync(sig, st.sig.ptr, n * H * 4, cudaMemcpyDeviceToHost, s));
     if (band && n)
@@ -351,6 +532,11 @@ int nd_dedup_fetch_groups(nd_ctx* ctx, uint64_t* members, uint64_t* group_start)
 }
 
 int nd_dedup_write_report(nd_ctx* ctx, const char* dir, uint64_t total_records) {
+  return nd_dedup_write_report_ex(ctx, dir, total_records, 0);
+}
+
+int nd_dedup_write_report_ex(nd_ctx* ctx, const char* dir, uint64_t total_records,
+                             int fsync_files) {
   return guarded_impl(ctx, [&] {
     DedupState& st = ctx->dedup;
     if (!st.valid) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");
@@ -366,7 +552,8 @@ int nd_dedup_write_report(nd_ctx* ctx, const char* dir, uint64_t total_records) 
     for (size_t i = 0; i < near.size(); ++i) nearv[i] = id_of(st, near[i]);
     for (size_t i = 0; i < rem.size(); ++i) remv[i] = id_of(st, rem[i]);
     write_report(dir, members, gs, nearv, remv, st.documents,
-                 total_records ? total_records : st.documents, st.pairs.distinct);
+                 total_records ? total_records : st.documents, st.pairs.distinct,
+                 fsync_files != 0);
   });
 }
 

@@ -250,6 +250,10 @@ struct DedupState {
   GroupSet groups;
   SigScratch sig_scratch;
   std::vector<uint64_t> doc_ids;  // row -> doc id (empty = identity)
+  // out-of-core dedup: signature rows + band ids stay in host memory
+  std::vector<uint32_t> host_sig, host_band;
+  bool sig_on_host = false;
+  uint32_t intervals = 1;         // bucket intervals of the last dedup
   uint64_t documents = 0;
   uint32_t K = 0;
   uint32_t bands = 0;             // band keys per row in band

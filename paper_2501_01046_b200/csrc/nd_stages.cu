@@ -421,7 +421,6 @@ int nd_set_hbm_budget(nd_ctx* ctx, uint64_t bytes) {
 int nd_union_stage(nd_ctx* ctx, const char* const* pair_paths, uint32_t nfiles,
                    uint64_t total_surviving, uint64_t total_records, const char* workspace,
                    int fsync_files, nd_dedup_stats* stats) {
-  (void)fsync_files;
   return guarded_impl(ctx, [&] {
     std::vector<uint64_t> lo, hi;
     std::vector<uint32_t> m;
@@ -485,7 +484,7 @@ int nd_union_stage(nd_ctx* ctx, const char* const* pair_paths, uint32_t nfiles,
       stats->near_duplicates = st.groups.members;
       stats->removals = st.groups.removals;
     }
-    const int rc = nd_dedup_write_report(ctx, workspace, total_records);
+    const int rc = nd_dedup_write_report_ex(ctx, workspace, total_records, fsync_files);
     if (rc != ND_OK) fail(rc, ctx->err);
   });
 }

@@ -157,6 +157,9 @@ def dedup_packed(data: np.ndarray, offsets: np.ndarray, config: RunConfig | None
     stats = NdDedupStats()
     params = config.to_params(bucket_count)
     dp = data.ctypes.data_as(u8p) if data.size else C.cast(C.c_char_p(b"\0"), u8p)
+    # HBM budget of the in-memory dedup (0 = 70% of free device memory):
+    # above it, bucket intervals run out of core over host-resident rows
+    ctx.check(ctx.lib.nd_set_hbm_budget(ctx.h, config.hbm_budget))
     ctx.check(ctx.lib.nd_dedup(ctx.h, dp, offsets.ctypes.data_as(u64p),
                                ids.ctypes.data_as(u64p) if ids is not None else None, n,
                                C.byref(params), C.byref(stats)))
@@ -264,9 +267,13 @@ def _dump2(obj) -> str:
     return json.dumps(obj, indent=2, ensure_ascii=False) + "\n"
 
 
-def _write_text(path: str, text: str) -> None:
+def _write_text(path: str, text: str, fsync: bool = False) -> None:
+    """write_file_bytes (util.cpp:132-140): write, flush, optional fsync."""
     with open(path, "w", encoding="utf-8", newline="") as f:
         f.write(text)
+        if fsync:
+            f.flush()
+            os.fsync(f.fileno())
 
 
 def _write_rejects(path: str, rejects) -> None:
@@ -372,7 +379,7 @@ def run_hash_stage(config: RunConfig, ctx: Context | None = None) -> HashStageOu
                       "record_offset": f.record_offset,
                       "signature_file": os.path.basename(out.signature_files[i])}
                      for i, f in enumerate(manifest.files)]}
-    _write_text(run_manifest_path(config), _dump2(doc))
+    _write_text(run_manifest_path(config), _dump2(doc), config.fsync_files)  # pipeline.cpp:335
     return out
 
 
@@ -455,7 +462,7 @@ def run_compare_stage(config: RunConfig, ctx: Context | None = None) -> CompareS
            "candidate_pairs": out.candidate_pairs, "emitted_pairs": out.emitted_pairs,
            "gather_peak_bytes": out.gather_peak_bytes,
            "pair_files": [os.path.basename(f) for f in names]}
-    _write_text(compare_stage_path(config), _dump2(doc))
+    _write_text(compare_stage_path(config), _dump2(doc), config.fsync_files)  # pipeline.cpp:444
     return out
 
 

@@ -459,3 +459,49 @@ def test_estimator_error_stats(ctx, oracle):
     # codepoint windows
     j = accuracy.exact_window_jaccard("ЖЖЖЖЖa", "ЖЖЖЖЖb", 5, minhash.ShingleUnit.CODEPOINT)
     assert (j.intersection, j.union_size) == (1, 3)
+
+
+@pytest.mark.parametrize("budget", [3_000_000, 400_000])
+def test_out_of_core_dedup_byte_identical(ctx, ref, tmp_path, budget):
+    # a small HBM budget cuts the buckets into intervals (plan_gather's idea,
+    # sigstore.cpp:288-329): pairs, groups and the report must equal the
+    # single-pass dedup's and the reference's
+    data, offs = ref.generate_synthetic(6000, 500, gmin=2, gmax=4, edit=(3, 100), len_min=300,
+                                        len_max=900, seed=19)
+    one = pipeline.dedup_packed(data, offs, pipeline.RunConfig(), ctx=ctx)
+    assert one.stats["intervals"] == 1
+    p1 = pipeline.dedup_pairs(one.distinct_pairs, ctx=ctx)
+    d1 = str(tmp_path / "one")
+    os.makedirs(d1)
+    pipeline.write_report(d1, ctx=ctx)
+    sig1 = minhash.signatures_packed(data, offs, minhash.derive_family(5, 128, 5), 16, 8,
+                                     one.stats["bucket_count"], ctx=ctx)
+    ooc = pipeline.dedup_packed(data, offs, pipeline.RunConfig(hbm_budget=budget), ctx=ctx)
+    assert ooc.stats["intervals"] >= 2, ooc.stats
+    assert ooc.candidate_pairs == one.candidate_pairs
+    assert ooc.stats["emitted_pairs"] >= one.stats["emitted_pairs"]
+    assert pipeline.dedup_pairs(ooc.distinct_pairs, ctx=ctx) == p1
+    d2 = str(tmp_path / "ooc")
+    os.makedirs(d2)
+    pipeline.write_report(d2, ctx=ctx)
+    assert _files(d2) == _files(d1)
+    assert [(g.representative, g.members) for g in ooc.groups] == \
+        [(g.representative, g.members) for g in one.groups]
+    # rows fetched from host memory equal K1's
+    import ctypes as C
+    n = len(offs) - 1
+    sig = np.empty((n, 128), np.uint32)
+    band = np.empty((n, 16), np.uint32)
+    ctx.check(ctx.lib.nd_dedup_fetch_signatures(ctx.h, sig.ctypes.data_as(_lib.u32p),
+                                                band.ctypes.data_as(_lib.u32p)))
+    assert np.array_equal(sig, sig1[0]) and np.array_equal(band, sig1[1])
+    # and the reference's run_dedup on the same documents
+    corpus = str(tmp_path / "c.jsonl")
+    with open(corpus, "w") as f:
+        for i in range(n):
+            f.write(json.dumps({"text": bytes(data[offs[i]:offs[i + 1]]).decode()}) + "\n")
+    ws_ref = str(tmp_path / "r")
+    os.makedirs(ws_ref)
+    _, cand = ref.run_dedup(corpus, ws_ref, workers=os.cpu_count())
+    assert cand == ooc.candidate_pairs
+    assert _files(ws_ref)["groups.jsonl"] == _files(d2)["groups.jsonl"]

@@ -174,3 +174,21 @@ def test_run_bench_layout(ctx, ref, tmp_path):
     t1, t3 = (_tree(os.path.join(cfg.workspace, f"bench_w{w}")) for w in (1, 3))
     for f in ("groups.jsonl", "removal.txt", "summary.json"):
         assert t1[f] == t3[f]
+
+
+def test_fsync_files_workspace_byte_identical(ctx, ref, tmp_path, monkeypatch):
+    # --fsync (RunConfig::fsync_files): every artifact the reference writes
+    # through write_file_bytes(..., fsync) (pipeline.cpp:335,444,487,494,506;
+    # SignatureFileWriter sigstore.cpp:117) is fsynced -- Python side files
+    # counted here, C++ writers exercised -- and the bytes do not change
+    corpus = _corpus_dir(ref, tmp_path)
+    ws_ref, ws_gpu = str(tmp_path / "ref"), str(tmp_path / "gpu")
+    os.makedirs(ws_ref)
+    ref.run_dedup(corpus, ws_ref)
+    synced = []
+    real = os.fsync
+    monkeypatch.setattr(os, "fsync", lambda fd: (synced.append(fd), real(fd))[1])
+    cfg = pipeline.RunConfig(inputs=[corpus], workspace=ws_gpu, fsync_files=True)
+    pipeline.run_dedup(cfg, ctx=ctx)
+    assert len(synced) == 2  # run_manifest.json, compare_stage.json
+    assert _tree(ws_gpu) == _tree(ws_ref)
