@@ -78,6 +78,9 @@ namespace {
 #ifndef ND_K1_ASM_ORDER
 #define ND_K1_ASM_ORDER 0
 #endif
+#ifndef ND_K1_I2F
+#define ND_K1_I2F 1  // float operand = I2FP(256c) instead of the 2^23-biased word
+#endif
 constexpr int kWarps = ND_K1_WARPS;  // warps per block
 constexpr int kLMax = 64;           // max shingle length
 // positions staged per chunk and group: (char, float) pairs, 8 B each
@@ -266,6 +269,39 @@ struct Consts<Arith::kExact, F> {
   }
 };
 
+#if ND_K1_I2F
+// fq arithmetic with the float operand converted exactly (I2FP.F32.U32 of
+// C = 256c < 2^31, <= 23 significant bits) instead of the 2^23-biased word:
+// no -2^23 q/p constant, 5 constants per function.
+//   R  = fma(float(C), fl(q/p)/256, fma(c_out, fl(QLn/p), 2^-5))
+//      in [u/p + 2^-5 - 0.009, u/p + 2^-5 + 0.009]  => floor(R - 1/2) in {Q-1, Q}
+//   256r = C*q + Kb*(-256p) + c_out*256QLn + 256c_in   (Kb = 0x4B000000 + k)
+template <int F>
+struct Consts<Arith::kFq, F> {
+  uint32_t q[F], qln256[F], negp256[F];
+  float qp256[F], qlnp[F];
+  __device__ void load(const FamPtrs& fp, int base) {
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      q[f] = fp.q[base + f];
+      qln256[f] = fp.qln[base + f] << 8;
+      negp256[f] = fp.negp[base + f] << 8;
+      qp256[f] = fp.qp[base + f] * 0.00390625f;
+      qlnp[f] = fp.qlnp[base + f];
+    }
+  }
+  __device__ __forceinline__ uint32_t roll(int f, uint32_t C, uint32_t cin256, uint32_t cout,
+                                           float cout_f) const {
+    const float t1 = __fmaf_rn(cout_f, qlnp[f], 0.03125f);
+    const float R = __fmaf_rn(__uint2float_rn(C), qp256[f], t1);
+    const uint32_t kb = __float_as_uint(__fadd_rd(R, 8388607.5f));
+    uint32_t x = cout * qln256[f] + cin256;
+    x = C * q[f] + x;
+    x = kb * negp256[f] + x;
+    return min(x, x + negp256[f]);
+  }
+};
+#else
 template <int F>
 struct Consts<Arith::kFq, F> {
   // integer constants pre-scaled by 256 (see step): the state is C = 256*c
@@ -307,6 +343,7 @@ struct Consts<Arith::kFq, F> {
     return min(x, x + negp256[f]);
   }
 };
+#endif
 
 // One work item (a document, or an 8192-window segment of a long one) for one
 // warp; `item` is warp-uniform.
