@@ -124,6 +124,11 @@ int nd_ctx_set_stream(nd_ctx* ctx, void* cuda_stream);
  * reduction (exact, slower). */
 int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t hash_count,
                      uint32_t shingle_len, uint32_t unit);
+/* Which signature kernel the uploaded family runs: "k1j" (family-specialised,
+ * compiled by NVRTC at upload), "k1" (per-lane register constants), "k1w"
+ * (codepoint units) or "k1x" (exact 64-bit Barrett); when K1j was eligible but
+ * could not be compiled the reason follows after ": ". */
+const char* nd_k1_kernel(nd_ctx* ctx);
 
 /* signature_of_document over a packed batch + band_bucket_ids
  * (minhash.hpp:71-78, lsh.hpp:38-40; caller pipeline.cpp:214-218).

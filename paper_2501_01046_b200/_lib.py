@@ -101,6 +101,7 @@ SIGNATURES = {
     "nd_last_error": (C.c_char_p, [vp]),
     "nd_ctx_set_stream": (C.c_int, [vp, vp]),
     "nd_family_upload": (C.c_int, [vp, C.POINTER(NdHashFn), C.c_uint32, C.c_uint32, C.c_uint32]),
+    "nd_k1_kernel": (C.c_char_p, [vp]),
     "nd_signatures": (C.c_int, [vp, u8p, u64p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                 u32p, u32p]),
     "nd_signatures_h2d": (C.c_int, [vp, u8p, u64p, C.c_uint64, C.c_uint32, C.c_uint32,

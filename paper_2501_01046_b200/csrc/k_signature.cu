@@ -140,6 +140,25 @@ __global__ void k_fill_multi(const uint32_t* __restrict__ multi_docs, uint32_t n
   }
 }
 
+// K1j work order: items by descending window count (stable), so the 32
+// items a warp takes have nearly equal lengths
+__global__ void k_item_len_keys(const uint64_t* __restrict__ offsets,
+                                const uint32_t* __restrict__ item_doc,
+                                const uint64_t* __restrict__ item_off, uint64_t n_items, uint32_t L,
+                                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n_items) return;
+  uint64_t doc = i, ws = 0;
+  if (item_doc) {
+    doc = item_doc[i];
+    ws = (i - item_off[doc]) * kSeg;
+  }
+  const uint64_t nwin = offsets[doc + 1] - offsets[doc] - L + 1;
+  const uint64_t w = min(nwin - ws, static_cast<uint64_t>(kSeg));
+  keys[i] = 16383u - static_cast<uint32_t>(w);  // kSeg < 2^14
+  vals[i] = static_cast<uint32_t>(i);
+}
+
 __global__ void k_iota_docs(uint32_t* __restrict__ v, uint64_t n) {
   uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i < n) v[i] = static_cast<uint32_t>(i);
@@ -935,7 +954,24 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   }();
   unsigned long long* counter =
       persistent ? sc.item_counter.as<unsigned long long>(1) : nullptr;
-  go(fam, d_text, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, counter, s);
+  if (fam.jit && fam.unit == 0) {
+    // K1j: items sorted by length, then the family-specialised kernel
+    uint32_t* keys = sc.order_keys.as<uint32_t>(items);
+    uint32_t* order = sc.order_vals.as<uint32_t>(items);
+    k_item_len_keys<<<static_cast<unsigned>((items + tb - 1) / tb), tb, 0, s>>>(
+        d_offsets, item_doc, item_off, items, fam.L, keys, order);
+    ND_CHECK_LAUNCH();
+    radix_sort_u32(keys, order, items, 14, sc.sort, s);
+    k1_jit_launch(fam.jit, static_cast<const uint8_t*>(d_text), d_offsets, order, item_doc,
+                  item_off, static_cast<uint32_t>(items), d_band ? bands : 0, rows, K, d_sig,
+                  d_band, sc.item_counter.as<unsigned long long>(k1_jit_passes(fam.jit)), s);
+    // band keys of every document from its finished row (keys is free again)
+    if (d_band) launch_band_keys(d_sig, n, fam.H, bands, rows, K, d_band, keys, s);
+    return;
+  } else {
+    go(fam, d_text, d_offsets, item_doc, item_off, items, bands, rows, K, d_sig, d_band, counter,
+       s);
+  }
   if (nmulti && d_band) {
     uint64_t total = static_cast<uint64_t>(nmulti) * bands;
     k_bands_from_rows<<<static_cast<unsigned>((total + tb - 1) / tb), tb, 0, s>>>(

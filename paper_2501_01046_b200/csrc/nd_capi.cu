@@ -394,11 +394,32 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L,
     ctx->fam.exact = !fast;
     ctx->fam.unit = unit;
     ctx->fam.H = H;
+    ctx->fam.L = L;
+    // K1j: compile (or find) the kernel specialised for this family; when
+    // NVRTC is unavailable the register-constant K1 runs (same bits)
+    ctx->fam.jit = nullptr;
+    ctx->k1_note.clear();
+    if (k1_jit_eligible(ctx->fam)) {
+      try {
+        ctx->fam.jit = k1_jit_prepare(fns, H, L);
+      } catch (const NdError& e) {
+        ctx->k1_note = e.what();
+      }
+    }
+    ctx->fam.H = H;
     ctx->fam.Hp = Hp;
     ctx->fam.L = L;
     ctx->family_host.assign(fns, fns + H);
     ctx->family_derived = false;
   });
+}
+
+const char* nd_k1_kernel(nd_ctx* ctx) {
+  static thread_local std::string out;
+  if (!ctx || !ctx->fam.q) return "";
+  out = ctx->fam.exact ? "k1x" : ctx->fam.jit ? "k1j" : ctx->fam.unit == 1 ? "k1w" : "k1";
+  if (!ctx->k1_note.empty()) out += ": " + ctx->k1_note;
+  return out.c_str();
 }
 
 int nd_signatures(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,

@@ -43,6 +43,7 @@ struct nd_ctx {
   uint64_t family_seed = 0;
   bool family_derived = false;  // family came from derive_family(family_seed, ...)
   std::string err;
+  std::string k1_note;          // why K1j is not used for the uploaded family (if it is not)
 
   ~nd_ctx();
   void ensure_streams();

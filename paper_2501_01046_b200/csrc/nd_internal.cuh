@@ -50,6 +50,7 @@ struct DevFamily {
   uint32_t Hp = 0;           // padded hash count
   uint32_t L = 0;
   uint32_t unit = 0;         // 0 = byte, 1 = codepoint (ShingleUnit, text.hpp:23-26)
+  void* jit = nullptr;        // K1j kernel specialised for this family (k1_jit.cpp), or null
   // true when some function lies outside the domain the fast arithmetics are
   // proven for (byte fq: 2^21 <= p < 2^23, q < 2^16; codepoint wide:
   // 0x10FFFF < p < 2^23, q < 2^16): K1 then runs the 64-bit Barrett
@@ -106,15 +107,34 @@ struct PinnedBuf {
 // ---- kernels / launchers (k_*.cu) -----------------------------------------
 // K1: signatures + band keys over device-resident packed text.
 // Returns ND_ERR_SHORT through the flag buffer when a document has no window.
-struct SigScratch {
-  DevBuf seg_count, item_off, item_doc, flags, multi_docs, scan_tmp, units, unit_off, unit_cnt,
-      item_counter;
+// Scratch for radix_sort_* (k_sort.cu).
+struct SortScratch {
+  DevBuf keys_alt, vals_alt, hist, offs, scan;
   void release() {
-    for (DevBuf* b : {&seg_count, &item_off, &item_doc, &flags, &multi_docs, &scan_tmp, &units,
-                      &unit_off, &unit_cnt, &item_counter})
-      b->release();
+    for (DevBuf* b : {&keys_alt, &vals_alt, &hist, &offs, &scan}) b->release();
   }
 };
+struct SigScratch {
+  DevBuf seg_count, item_off, item_doc, flags, multi_docs, scan_tmp, units, unit_off, unit_cnt,
+      item_counter, order_keys, order_vals;
+  SortScratch sort;  // K1j: items ordered by length
+  void release() {
+    for (DevBuf* b : {&seg_count, &item_off, &item_doc, &flags, &multi_docs, &scan_tmp, &units,
+                      &unit_off, &unit_cnt, &item_counter, &order_keys, &order_vals})
+      b->release();
+    sort.release();
+  }
+};
+// K1j: family-specialised signature kernel (k1_jit.cpp)
+bool k1_jit_eligible(const DevFamily& fam);
+void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L);
+double k1_jit_compile_seconds(const void* handle);
+uint32_t k1_jit_passes(const void* handle);
+std::string k1_jit_source(const nd_hash_fn* fns, uint32_t H, uint32_t L);
+void k1_jit_launch(const void* handle, const uint8_t* d_text, const uint64_t* d_offsets,
+                   const uint32_t* order, const uint32_t* item_doc, const uint64_t* item_off,
+                   uint32_t n_items, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
+                   uint32_t* d_band, unsigned long long* counter, cudaStream_t s);
 // UTF-8 -> codepoint units (k_utf8.cu): units_out[unit_off_out[d] ..
 // unit_off_out[d+1]) are document d's units (decode_codepoints, text.cpp:101-113).
 void decode_codepoints_device(const uint8_t* d_text, const uint64_t* d_offsets, uint64_t n,
@@ -128,13 +148,6 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
                        uint32_t* d_band, SigScratch& scratch, cudaStream_t stream,
                        bool check_short, const uint64_t* h_offsets);
 
-// Scratch for radix_sort_* (k_sort.cu).
-struct SortScratch {
-  DevBuf keys_alt, vals_alt, hist, offs, scan;
-  void release() {
-    for (DevBuf* b : {&keys_alt, &vals_alt, &hist, &offs, &scan}) b->release();
-  }
-};
 // Stable LSD radix sort of (key, value) pairs by the low key_bits bits.
 void radix_sort_u32(uint32_t* keys, uint32_t* vals, uint64_t n, int key_bits, SortScratch& sc,
                     cudaStream_t s);

@@ -62,11 +62,14 @@ for _ in range(10):
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(s); run(); e1.record(s); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
 h = int(np.frombuffer(sig.cpu().numpy().tobytes(), np.uint64).sum() % (1 << 61))
-print(json.dumps({"ms": min(ts), "ms_med": sorted(ts)[5], "hwe_T": hwe / min(ts) / 1e9, "sum": h}))
+print(json.dumps({"ms": min(ts), "ms_med": sorted(ts)[5], "hwe_T": hwe / min(ts) / 1e9, "sum": h,
+                  "kernel": ctx.lib.nd_k1_kernel(ctx.h).decode()}))
 """
 
 
-def run(reps):
+def run(reps, envs=None):
+    """envs: {"name": {"VAR": "value"}} variants by environment (in-tree library)
+    instead of the built library variants."""
     import numpy as np
 
     import bench
@@ -74,21 +77,26 @@ def run(reps):
     data, offs = bench.c2_corpus(bench.DOCS, 1)
     np.save("/tmp/k1v_data.npy", data)
     np.save("/tmp/k1v_offs.npy", offs)
-    libs = sorted(glob.glob(os.path.join(OUT, "lib_*.so")))
-    res = {os.path.basename(l)[4:-3]: [] for l in libs}
+    if envs:
+        cases = {k: v for k, v in envs.items()}
+    else:
+        cases = {os.path.basename(l)[4:-3]: {"ND_LIB_PATH": l}
+                 for l in sorted(glob.glob(os.path.join(OUT, "lib_*.so")))}
+    res = {k: [] for k in cases}
     for _ in range(reps):
-        for l in libs:
-            env = dict(os.environ, ND_LIB_PATH=l, ROOT=ROOT)
+        for name, extra in cases.items():
+            env = dict(os.environ, ROOT=ROOT, **extra)
             r = subprocess.run([sys.executable, "-c", PROBE], env=env, capture_output=True, text=True)
             line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-300:]
-            res[os.path.basename(l)[4:-3]].append(json.loads(line) if line.startswith("{") else line)
+            res[name].append(json.loads(line) if line.startswith("{") else line)
     for k, v in res.items():
         good = [x for x in v if isinstance(x, dict)]
         sums = {x["sum"] for x in good}
         print(json.dumps({"variant": k, "best_ms": min(x["ms"] for x in good) if good else None,
                           "T_hwe_s": max(x["hwe_T"] for x in good) if good else None,
                           "all_ms": [x["ms"] if isinstance(x, dict) else x for x in v],
-                          "checksums_agree": len(sums) == 1, "sum": sorted(sums)}))
+                          "checksums_agree": len(sums) == 1, "sum": sorted(sums),
+                          "kernel": good[0].get("kernel") if good else None}))
 
 
 if __name__ == "__main__":
@@ -96,4 +104,10 @@ if __name__ == "__main__":
         build(sys.argv[2:])
     else:
         reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 3
-        run(reps)
+        envs = None
+        if "--env" in sys.argv:  # --env name:VAR=val,VAR=val name2:...
+            envs = {}
+            for spec in sys.argv[sys.argv.index("--env") + 1:]:
+                name, _, kv = spec.partition(":")
+                envs[name] = dict(x.split("=", 1) for x in kv.split(",") if x)
+        run(reps, envs)
