@@ -238,15 +238,14 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
          "          i64 q = p - 3;\n"
          "          u32 cur = wp[0];\n";
     for (int k = 1; k <= R; ++k) {
-      // word k is needed iff it holds a byte q + i + L (i = 0..3); bytes at
-      // positions >= e read as 0 (the first word's c_out can be position e),
-      // and a word with no position below e is not loaded at all
-      const bool needed = k >= static_cast<int>(L) / 4;
-      s << "          u32 r" << k << " = 0u;\n";
-      if (needed)
-        s << "          { const i64 nv = e - (q + " << 4 * k << ");\n"
-          << "            if (nv > 0) r" << k << " = wp[" << k
-          << "] & (nv >= 4 ? 0xffffffffu : ((1u << (8 * (u32)nv)) - 1u)); }\n";
+      // the ring holds words q+4 .. q+4R (each shifts up one slot per word,
+      // so every slot is loaded, not only those the first word reads); bytes
+      // at positions >= e read as 0 (the first word's c_out can be position
+      // e), and a word with no position below e is not loaded at all
+      s << "          u32 r" << k << " = 0u;\n"
+        << "          { const i64 nv = e - (q + " << 4 * k << ");\n"
+        << "            if (nv > 0) r" << k << " = wp[" << k
+        << "] & (nv >= 4 ? 0xffffffffu : ((1u << (8 * (u32)nv)) - 1u)); }\n";
     }
     if (js.prefetch >= 2)
       s << "          u32 nx1 = (q - 4 >= wlo) ? wp[-1] : 0u;\n";

@@ -101,6 +101,25 @@ void nd_ctx::require_family() const {
 
 namespace ndb {
 
+// Text per chunk of the host pipelines (nd_signatures, nd_dedup).  64 MB
+// keeps the pipeline fill and drain short for the register-constant K1.
+// K1j runs pass-major over the chunk's items and needs ~1e5 items per launch
+// to occupy the GPU, so its chunks ramp up 64, 128, 256, 512 MB: the first
+// copy still lands quickly, later launches are large.
+uint64_t h2d_chunk_bytes(const DevFamily& fam, size_t chunk_index) {
+  static const uint64_t first_mb = [] {
+    const char* v = getenv("ND_H2D_FIRST_MB");  // tuning
+    return v ? std::max(1, atoi(v)) : 64;
+  }();
+  static const uint64_t max_mb = [] {
+    const char* v = getenv("ND_H2D_MAX_MB");  // tuning
+    return v ? std::max(1, atoi(v)) : 512;
+  }();
+  constexpr uint64_t kSmall = 64ull << 20;
+  if (!fam.jit) return kSmall;
+  return std::min<uint64_t>(max_mb << 20, (first_mb << 20) << std::min<size_t>(chunk_index, 6));
+}
+
 // Host-pipelined signatures: chunks of documents are copied in (h2d stream),
 // signed on alternating compute streams, and copied out (d2h stream), so the
 // PCIe transfers of chunk c+1 / c-1 overlap the kernel of chunk c (the
@@ -129,13 +148,13 @@ void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets,
   ND_CUDA(cudaEventRecord(start, ctx->stream));
   ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
 
-  // chunking: <= kChunkBytes of text and <= kChunkDocs documents per chunk
-  constexpr uint64_t kChunkBytes = 64ull << 20;  // small enough that fill + drain are short
+  // chunking: <= chunk_bytes(c) of text and <= kChunkDocs documents per chunk
   constexpr uint64_t kChunkDocs = 1ull << 20;
   std::vector<std::pair<uint64_t, uint64_t>> chunks;
   for (uint64_t d0 = 0; d0 < n;) {
     uint64_t d1 = d0 + 1;
-    while (d1 < n && d1 - d0 < kChunkDocs && offsets[d1 + 1] - offsets[d0] <= kChunkBytes) ++d1;
+    const uint64_t cap = h2d_chunk_bytes(ctx->fam, chunks.size());
+    while (d1 < n && d1 - d0 < kChunkDocs && offsets[d1 + 1] - offsets[d0] <= cap) ++d1;
     chunks.push_back({d0, d1});
     d0 = d1;
   }
@@ -165,10 +184,13 @@ void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets,
     ND_CUDA(cudaMemcpyAsync(dtext, bytes + offsets[d0], tb, cudaMemcpyHostToDevice, ctx->h2d));
     ND_CUDA(cudaMemcpyAsync(doff, ho, (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->h2d));
     ND_CUDA(cudaEventRecord(sl.h2d_done, ctx->h2d));
-    ND_CUDA(cudaStreamWaitEvent(sl.comp, sl.h2d_done, 0));
+    // K1j runs its chunks one after another on one stream: two pass-major
+    // launches side by side would interleave their passes' code again
+    cudaStream_t comp = ctx->fam.jit ? ctx->slot[0].comp : sl.comp;
+    ND_CUDA(cudaStreamWaitEvent(comp, sl.h2d_done, 0));
     launch_signatures(ctx->fam, dtext, doff, m, bands, rows, K, dsig, dband, sl.scratch,
-                      sl.comp, /*check_short=*/false, ho);
-    ND_CUDA(cudaEventRecord(sl.comp_done, sl.comp));
+                      comp, /*check_short=*/false, ho);
+    ND_CUDA(cudaEventRecord(sl.comp_done, comp));
     ND_CUDA(cudaStreamWaitEvent(ctx->d2h, sl.comp_done, 0));
     ND_CUDA(cudaMemcpyAsync(sig_out + d0 * H, dsig, m * H * sizeof(uint32_t),
                             cudaMemcpyDeviceToHost, ctx->d2h));

@@ -53,6 +53,7 @@ struct nd_ctx {
 
 namespace ndb {
 int guarded_impl(nd_ctx* ctx, const std::function<void()>& fn);
+uint64_t h2d_chunk_bytes(const DevFamily& fam, size_t chunk_index);
 // nd_signatures' host pipeline (chunks in, signature rows + band ids out)
 void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
                      uint32_t bands, uint32_t rows, uint32_t K, uint32_t* sig_out,

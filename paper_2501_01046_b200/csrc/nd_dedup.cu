@@ -114,7 +114,7 @@ uint64_t id_of(const DedupState& st, uint32_t row) {
 
 }  // namespace
 
-// Host text -> device signatures/band keys: chunks of <= 64 MB are copied
+// Host text -> device signatures/band keys: chunks (h2d_chunk_bytes) are copied
 // on the h2d stream into a ring of chunk buffers and signed on the ctx stream
 // as each lands (PCIe overlaps K1; the paper's double buffering).
 void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uint64_t* offsets,
@@ -127,13 +127,13 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   uint64_t* d_off = st.offs.as<uint64_t>(n + 1);
   uint64_t* h_off = static_cast<uint64_t*>(ctx->pinned_off.get((n + 1) * sizeof(uint64_t)));
   for (uint64_t i = 0; i <= n; ++i) h_off[i] = offsets[i] - offsets[0];
-  // chunks of <= 64 MB of text (a longer document is a chunk of its own)
-  constexpr uint64_t kChunk = 64ull << 20;
+  // chunks of <= h2d_chunk_bytes of text (a longer document is a chunk of its own)
   std::vector<std::pair<uint64_t, uint64_t>> chunks;
   uint64_t max_bytes = 0;
   for (uint64_t d0 = 0; d0 < n;) {
     uint64_t d1 = d0 + 1;
-    while (d1 < n && h_off[d1 + 1] - h_off[d0] <= kChunk) ++d1;
+    const uint64_t cap = h2d_chunk_bytes(ctx->fam, chunks.size());
+    while (d1 < n && h_off[d1 + 1] - h_off[d0] <= cap) ++d1;
     chunks.push_back({d0, d1});
     max_bytes = std::max(max_bytes, h_off[d1] - h_off[d0]);
     d0 = d1;
@@ -157,7 +157,8 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   for (size_t c = 0; c < chunks.size(); ++c) {
     const auto [d0, d1] = chunks[c];
     const int r = static_cast<int>(c % kRing);
-    cudaStream_t cs = ctx->ring_stream[r];
+    // (K1j: one compute stream, see signatures_host)
+    cudaStream_t cs = ctx->fam.jit ? ctx->ring_stream[0] : ctx->ring_stream[r];
     if (c >= kRing) ND_CUDA(cudaStreamWaitEvent(ctx->h2d, k1_done[r], 0));  // slot free again
     ND_CUDA(cudaMemcpyAsync(ring[r], bytes + offsets[0] + h_off[d0], h_off[d1] - h_off[d0],
                             cudaMemcpyHostToDevice, ctx->h2d));

@@ -1,0 +1,135 @@
+"""K1j -- the family-specialised signature kernel compiled by NVRTC at family
+upload (csrc/k1_jit.cpp) -- against the register-constant K1 and the oracle.
+
+K1j walks each item per lane in aligned 32-bit words with single steps at
+both ends, so the shapes that matter are: every shingle length 1..16 (the
+ring of words above the current one), documents of exactly L .. L+8 bytes,
+every byte alignment of the text (4-byte words at absolute addresses), H not
+a multiple of the pass width, documents split into 8192-window items, and
+text ending at the very end of its buffer.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2501_01046_b200 import _lib, minhash
+
+pytestmark = pytest.mark.gpu
+
+
+def _kernel(ctx):
+    return ctx.lib.nd_k1_kernel(ctx.h).decode()
+
+
+def _both(ctx, monkeypatch, data, offs, fam, bands=0, rows=0, K=0):
+    out = {}
+    for jit in ("1", "0"):
+        monkeypatch.setenv("ND_K1_JIT", jit)
+        ctx._family_key = None
+        sig, band = minhash.signatures_packed(data, offs, fam, bands, rows, K, ctx=ctx,
+                                              want_bands=bool(bands))
+        out[jit] = (sig, band, _kernel(ctx))
+    monkeypatch.delenv("ND_K1_JIT")
+    ctx._family_key = None
+    assert out["1"][2] == "k1j", out["1"][2]
+    assert out["0"][2] == "k1"
+    return out
+
+
+def _docs(rng, lens, alphabet=256):
+    texts = [bytes(rng.integers(0, alphabet, size=int(n), dtype=np.uint8)) for n in lens]
+    offs = np.zeros(len(texts) + 1, np.uint64)
+    offs[1:] = np.cumsum([len(t) for t in texts])
+    return np.frombuffer(b"".join(texts), np.uint8).copy(), offs
+
+
+@pytest.mark.parametrize("L", list(range(1, 17)))
+def test_k1j_every_shingle_length(ctx, oracle, monkeypatch, L):
+    rng = np.random.default_rng(100 + L)
+    lens = [L + k for k in range(9)] + list(rng.integers(L, 3000, size=40)) + [20000]
+    data, offs = _docs(rng, lens)
+    fam = minhash.derive_family(5, 64, L)
+    out = _both(ctx, monkeypatch, data, offs, fam)
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][0], oracle.signatures(data, offs, oracle.derive_family(5, 64, L), L=L))
+
+
+@pytest.mark.parametrize("H,bands,rows", [(100, 10, 10), (128, 16, 8), (256, 32, 8), (40, 5, 8),
+                                          (512, 64, 8), (8, 2, 4)])
+def test_k1j_hash_counts_and_band_keys(ctx, oracle, monkeypatch, H, bands, rows):
+    rng = np.random.default_rng(H)
+    lens = list(rng.integers(5, 5000, size=300)) + [9000, 17000, 8196, 8197]
+    data, offs = _docs(rng, lens, alphabet=37)
+    fam = minhash.derive_family(5, H, 5)
+    out = _both(ctx, monkeypatch, data, offs, fam, bands, rows, 977)
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][1])
+    want = oracle.signatures(data, offs, oracle.derive_family(5, H))
+    assert np.array_equal(out["1"][0], want)
+    assert np.array_equal(out["1"][1], oracle.band_ids(want, bands, rows, 977))
+
+
+@pytest.mark.parametrize("shift", [0, 1, 2, 3, 5, 7])
+def test_k1j_text_alignment_and_buffer_end(ctx, oracle, monkeypatch, shift):
+    # device text starting `shift` bytes into an allocation whose last byte is
+    # the last document byte (no slack for whole-word reads past the end)
+    import torch
+
+    rng = np.random.default_rng(shift)
+    data, offs = _docs(rng, list(rng.integers(5, 700, size=257)) + [5, 6, 7])
+    n = len(offs) - 1
+    fam = minhash.derive_family(5, 128, 5)
+    buf = torch.zeros(len(data) + shift, dtype=torch.uint8, device="cuda")
+    buf[shift:] = torch.from_numpy(data).cuda()
+    d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
+    res = {}
+    for jit in ("1", "0"):
+        monkeypatch.setenv("ND_K1_JIT", jit)
+        ctx._family_key = None
+        sig = torch.empty((n, 128), dtype=torch.int32, device="cuda")
+        band = torch.empty((n, 16), dtype=torch.int32, device="cuda")
+        minhash.signatures_device(buf.data_ptr() + shift, d_offs.data_ptr(), n, fam, sig.data_ptr(),
+                                  band.data_ptr(), 16, 8, 0, ctx=ctx)
+        torch.cuda.synchronize()
+        res[jit] = (sig.cpu().numpy().view(np.uint32), band.cpu().numpy().view(np.uint32))
+    monkeypatch.delenv("ND_K1_JIT")
+    ctx._family_key = None
+    assert np.array_equal(res["1"][0], res["0"][0]) and np.array_equal(res["1"][1], res["0"][1])
+    assert np.array_equal(res["1"][0], oracle.signatures(data, offs, oracle.derive_family(5, 128)))
+
+
+def test_k1j_skewed_lengths_many_items(ctx, oracle, monkeypatch):
+    # lognormal lengths up to 60 KB: multi-item documents (atomicMin across
+    # items) mixed with short ones in one length-sorted work order
+    spec = _lib.NdSynthSpec(doc_count=3000, group_count=200, group_size_min=2, group_size_max=4,
+                            edit_num=1, edit_den=100, len_min=800, len_max=60000, seed=9, mode=1,
+                            len_law=1, sigma_milli=1400)
+    lib = _lib.load()
+    nb = C.c_uint64()
+    _lib.check(lib.nd_synth_generate(C.byref(spec), None, None, C.byref(nb)))
+    data = np.empty(nb.value, np.uint8)
+    offs = np.empty(spec.doc_count + 1, np.uint64)
+    _lib.check(lib.nd_synth_generate(C.byref(spec), data.ctypes.data_as(_lib.u8p),
+                                     offs.ctypes.data_as(_lib.u64p), C.byref(nb)))
+    assert np.diff(offs).max() > 3 * 8196
+    fam = minhash.derive_family(5, 128, 5)
+    out = _both(ctx, monkeypatch, data, offs, fam, 16, 8, 1500)
+    assert np.array_equal(out["1"][0], out["0"][0]) and np.array_equal(out["1"][1], out["0"][1])
+    sample = np.random.default_rng(0).choice(spec.doc_count, 200, replace=False)
+    for i in sample[:50]:
+        o = np.array([0, offs[i + 1] - offs[i]], np.uint64)
+        d = data[int(offs[i]):int(offs[i + 1])].copy()
+        assert np.array_equal(out["1"][0][i], oracle.signatures(d, o, oracle.derive_family(5, 128))[0])
+
+
+def test_k1j_not_used_outside_its_domain(ctx, monkeypatch):
+    # codepoint units and hand-built families keep their kernels
+    fam = minhash.derive_family(5, 32, 5, minhash.ShingleUnit.CODEPOINT)
+    ctx.upload_family(fam)
+    assert _kernel(ctx) == "k1w"
+    ctx._family_key = None
+    fam = minhash.derive_family(5, 32, 20)  # L > 16
+    ctx.upload_family(fam)
+    assert _kernel(ctx) == "k1"
+    ctx._family_key = None
