@@ -110,6 +110,18 @@ int nd_synth_text_device(nd_ctx* ctx, const nd_synth_spec* spec, const uint64_t*
 
 /* ---- device context ----------------------------------------------------- */
 int nd_ctx_create(int device, nd_ctx** out);
+/* One context over several devices (the reference's in-process
+ * parallel compare, pipeline.cpp:387-420, band_partition lsh.cpp:62-72):
+ * one host thread per shard, peer access enabled between distinct devices.
+ * nd_signatures and nd_dedup shard the batch by contiguous document ranges;
+ * nd_dedup exchanges (cell, row) records all-to-all over NVLink peer copies,
+ * every owner compares its cells reading signature rows in place from the
+ * owning GPU, and the pairs meet on the first device for the components.
+ * Outputs are identical for any device list; a device may repeat (several
+ * shards on one GPU).  The fetch / report calls work on the group context;
+ * other entry points run on the first device. */
+int nd_ctx_create_multi(const int* devices, int ndev, nd_ctx** out);
+int nd_ctx_shard_count(const nd_ctx* ctx);
 void nd_ctx_destroy(nd_ctx* ctx);
 const char* nd_last_error(const nd_ctx* ctx);
 /* stream all device work of this ctx is ordered on (cudaStream_t; NULL = own) */

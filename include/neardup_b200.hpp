@@ -54,12 +54,20 @@ namespace neardup::b200 {
   }
 }
 
-// One device context (streams, uploaded family, scratch).  Not reentrant.
+// One device context (streams, uploaded family, scratch), or one context over
+// a list of devices (nd_ctx_create_multi: signature_batch and run_dedup shard
+// their batches over the GPUs, one host thread per device).  Not reentrant.
 class Device {
  public:
   explicit Device(int device = 0) {
     if (int rc = nd_ctx_create(device, &ctx_); rc != ND_OK) rethrow(rc, nd_last_error_global());
   }
+  explicit Device(std::span<const int> devices) {
+    if (int rc = nd_ctx_create_multi(devices.data(), static_cast<int>(devices.size()), &ctx_);
+        rc != ND_OK)
+      rethrow(rc, nd_last_error_global());
+  }
+  int shards() const { return nd_ctx_shard_count(ctx_); }
   ~Device() { nd_ctx_destroy(ctx_); }
   Device(const Device&) = delete;
   Device& operator=(const Device&) = delete;

@@ -97,7 +97,23 @@ int main() {
   RunConfig cfg;
   uint64_t cand = 0;
   DedupReport rep = b200::dedup_in_memory(dev, clean, cfg, &cand);
-  (void)rep;
+  // the same through one context over three shards (nd_ctx_create_multi; on a
+  // one-GPU box the shards share device 0)
+  const int devs[3] = {0, 0, 0};
+  b200::Device multi(std::span<const int>(devs, 3));
+  if (multi.shards() != 3) return std::puts("FAIL shard count"), 1;
+  uint64_t cand_m = 0;
+  DedupReport rep_m = b200::dedup_in_memory(multi, clean, cfg, &cand_m);
+  if (cand_m != cand || rep_m.groups.size() != rep.groups.size() ||
+      rep_m.removals != rep.removals || rep_m.near_duplicates != rep.near_duplicates)
+    return std::puts("FAIL multi-device dedup"), 1;
+  for (size_t i = 0; i < rep.groups.size(); ++i)
+    if (rep.groups[i].representative != rep_m.groups[i].representative ||
+        rep.groups[i].members != rep_m.groups[i].members)
+      return std::puts("FAIL multi-device groups"), 1;
+  auto gm = b200::signature_batch(multi, docs, fam);
+  for (size_t i = 0; i < gm.size(); ++i)
+    if (gm[i].values != gpu[i].values) return std::puts("FAIL multi-device signatures"), 1;
 
   // the staged workflow: reference run_dedup vs b200::run_dedup, whole workspaces
   namespace fs = std::filesystem;

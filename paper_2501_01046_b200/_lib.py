@@ -97,6 +97,8 @@ SIGNATURES = {
     "nd_synth_generate": (C.c_int, [C.POINTER(NdSynthSpec), u8p, u64p, u64p]),
     "nd_synth_text_device": (C.c_int, [vp, C.POINTER(NdSynthSpec), vp, vp]),
     "nd_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+    "nd_ctx_create_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]),
+    "nd_ctx_shard_count": (C.c_int, [vp]),
     "nd_ctx_destroy": (None, [vp]),
     "nd_last_error": (C.c_char_p, [vp]),
     "nd_ctx_set_stream": (C.c_int, [vp, vp]),

@@ -438,10 +438,10 @@ __device__ __forceinline__ void join_check_blocks(const SigView sv, uint32_t H,
                                                   uint64_t* __restrict__ out_key,
                                                   uint32_t* __restrict__ out_m,
                                                   unsigned long long* __restrict__ count,
-                                                  uint64_t cap) {
+                                                  uint64_t cap, bool looked_up = false) {
   const uint32_t key = ((min(d, e) << 12) | max(d, e)) + 1u;
   // after an overflow the set is dropped (misses would probe long runs)
-  if (exact_set && pset_has(pset, smask, key)) return;  // identical at an earlier block
+  if (!looked_up && exact_set && pset_has(pset, smask, key)) return;  // identical at an earlier block
   const uint32_t ra = rowsm[d], rb = rowsm[e];
   const uint32_t* a = sv.row(ra);
   const uint32_t* b = sv.row(rb);
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
                   uint32_t join_max, uint32_t tbits, uint32_t sbits, uint32_t NB,
                   uint32_t min_match, int nb, uint64_t* __restrict__ out_key,
                   uint32_t* __restrict__ out_m, unsigned long long* __restrict__ count,
-                  uint64_t cap, bool two_barriers) {
+                  uint64_t cap, bool two_barriers, uint32_t qcap) {
   // VL values per document and group of BPL = VL / BW blocks: one 32-byte
   // sector (a 16-byte load would still move a whole sector), or 64 bytes
   // for the big-cell variant
@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
   constexpr int BPL = VL / BW;
   extern __shared__ uint32_t jsm[];
   __shared__ int pset_full;
+  __shared__ uint32_t qn[2];  // deferred-check queue fill, by block parity
   const uint32_t n = cell_len[blockIdx.x];
   if (n > join_max) return;  // big cells go to k_compare
   const uint32_t T = 1u << tbits;
@@ -488,6 +489,13 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
   // other half, so one barrier per block suffices (an insert of block k + 2
   // waits behind block k + 1's barrier, which every walker of k has passed)
   uint16_t* next2 = reinterpret_cast<uint16_t*>(rowsm + join_max);  // 2 x join_max (0xFFFF = end)
+  // deferred checks (qcap > 0): the walk only queues the chained pairs the
+  // handled-pair set does not answer; after a barrier the whole CTA drains
+  // the queue, so the row reads of one block's candidates are spread over
+  // every thread (many loads in flight) instead of gating the barrier behind
+  // the few walkers that found candidates
+  uint2* queue = reinterpret_cast<uint2*>(
+      (reinterpret_cast<uintptr_t>(next2 + 2 * join_max) + 7) & ~uintptr_t{7});
   const uint64_t s = cell_start[blockIdx.x];
   for (uint32_t i = threadIdx.x; i < n; i += TPB) rowsm[i] = rows[s + i];
   for (uint32_t i = threadIdx.x; i < T; i += TPB) {
@@ -495,7 +503,10 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
     head[i] = 0;
   }
   for (uint32_t i = threadIdx.x; i < S; i += TPB) pset[i] = 0;
-  if (threadIdx.x == 0) pset_full = 0;
+  if (threadIdx.x == 0) {
+    pset_full = 0;
+    qn[0] = qn[1] = 0;
+  }
   __syncthreads();
   const uint32_t mask = T - 1;
   const bool vec = (H & 3) == 0;
@@ -552,10 +563,34 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
       }
       __syncthreads();
       const bool exact_set = S > 1 && *static_cast<volatile int*>(&pset_full) == 0;
-      for (uint32_t d = threadIdx.x; d < n; d += TPB)
-        for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e])
-          join_check_blocks<BW>(sv, H, d, e, rowsm, k, vec, pset, S - 1, &pset_full, exact_set,
-                                min_match, nb, out_key, out_m, count, cap);
+      if (qcap) {
+        // qn[(k + 1) & 1] was last read by the drain of block k - 1, before
+        // this block's barrier: reset it for block k + 1
+        if (threadIdx.x == 0) qn[(k + 1) & 1] = 0;
+        uint32_t* q = &qn[k & 1];
+        for (uint32_t d = threadIdx.x; d < n; d += TPB)
+          for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e]) {
+            if (exact_set && pset_has(pset, S - 1, ((min(d, e) << 12) | max(d, e)) + 1u)) continue;
+            const uint32_t slot = atomicAdd(q, 1u);
+            if (slot < qcap)
+              queue[slot] = make_uint2(d, e);
+            else  // queue full: check inline
+              join_check_blocks<BW>(sv, H, d, e, rowsm, k, vec, pset, S - 1, &pset_full,
+                                    exact_set, min_match, nb, out_key, out_m, count, cap, true);
+          }
+        __syncthreads();
+        const uint32_t lim = min(*static_cast<volatile uint32_t*>(q), qcap);
+        for (uint32_t i = threadIdx.x; i < lim; i += TPB) {
+          const uint2 de = queue[i];
+          join_check_blocks<BW>(sv, H, de.x, de.y, rowsm, k, vec, pset, S - 1, &pset_full,
+                                exact_set, min_match, nb, out_key, out_m, count, cap, true);
+        }
+      } else {
+        for (uint32_t d = threadIdx.x; d < n; d += TPB)
+          for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e])
+            join_check_blocks<BW>(sv, H, d, e, rowsm, k, vec, pset, S - 1, &pset_full, exact_set,
+                                  min_match, nb, out_key, out_m, count, cap);
+      }
       if (two_barriers) __syncthreads();
     }
   }
@@ -610,8 +645,12 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
     const char* ps = getenv("ND_JOIN_PSET");  // 0: no set (HBM checks of earlier blocks)
     if (ps && ps[0] == '0') sbits = 0;
     const size_t smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
+    // deferred-check queue (ND_JOIN_DEFER = entries, 0 = check in the walk)
+    const char* jd = getenv("ND_JOIN_DEFER");
+    const uint32_t qcap = jd ? static_cast<uint32_t>(std::max(0, atoi(jd))) : 1024u;
     const size_t smem_b = (2u * (1u << tbits) + (sbits ? 1u << sbits : 1u)) * sizeof(uint32_t) +
-                          join_max * (sizeof(uint32_t) + 2 * sizeof(uint16_t));
+                          join_max * (sizeof(uint32_t) + 2 * sizeof(uint16_t)) +
+                          (qcap ? 8 + qcap * sizeof(uint2) : 0);
     const char* tb = getenv("ND_JOIN_TWO_BARRIERS");  // 1: the barrier after each walk too
     const bool two_barriers = tb && tb[0] == '1';
     if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
@@ -619,7 +658,8 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
     if (join_mode == 2 && BW > 1) {
       using JoinBFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                                const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
-                               int, uint64_t*, uint32_t*, unsigned long long*, uint64_t, bool);
+                               int, uint64_t*, uint32_t*, unsigned long long*, uint64_t, bool,
+                               uint32_t);
       // 512 threads per CTA for cells above 1024 documents: -33 % K3 time on
       // C3-sized cells; smaller cells are faster with 256
       const int tpb = join_max > 1024 ? 512 : 256;
@@ -637,7 +677,7 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
                                      static_cast<int>(smem_b)));
       fn<<<grid, tpb, smem_b, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
                                    join_max, tbits, sbits, NB, min_match, nb, out_key, out_m,
-                                   count, cap, two_barriers);
+                                   count, cap, two_barriers, qcap);
       ND_CHECK_LAUNCH();
     } else {
       using JoinFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,

@@ -898,11 +898,19 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     check_short = true;
   }
   uint32_t hflags[4] = {0, 0, 0, 0};
-  if (h_offsets) {  // host planning: only multi-item batches need the device plan
+  uint64_t host_items = n;  // work items, known on the host when h_offsets is
+  if (h_offsets) {  // host planning: no device round trip (the pipelines keep running)
+    host_items = 0;
     for (uint64_t d = 0; d < n; ++d) {
       uint64_t len = h_offsets[d + 1] - h_offsets[d];
-      if (len < fam.L) hflags[0] = 1;
-      else if (len - fam.L + 1 > kSeg) ++hflags[1];
+      if (len < fam.L) {
+        hflags[0] = 1;
+        ++host_items;
+        continue;
+      }
+      const uint64_t segs = (len - fam.L + 1 + kSeg - 1) / kSeg;
+      host_items += segs;
+      if (segs > 1) ++hflags[1];
     }
     if (check_short && hflags[0]) fail(ND_ERR_SHORT, "a document has fewer units than the shingle length");
   }
@@ -915,9 +923,11 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     k_plan<<<static_cast<unsigned>((n + tb - 1) / tb), tb, 0, s>>>(d_offsets, n, fam.L, seg_count,
                                                                     flags);
     ND_CHECK_LAUNCH();
-    ND_CUDA(cudaMemcpyAsync(hflags, flags, sizeof hflags, cudaMemcpyDeviceToHost, s));
-    ND_CUDA(cudaStreamSynchronize(s));
-    if (check_short && hflags[0]) fail(ND_ERR_SHORT, "a document has fewer units than the shingle length");
+    if (!h_offsets) {
+      ND_CUDA(cudaMemcpyAsync(hflags, flags, sizeof hflags, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaStreamSynchronize(s));
+      if (check_short && hflags[0]) fail(ND_ERR_SHORT, "a document has fewer units than the shingle length");
+    }
   }
 
   const uint32_t* item_doc = nullptr;
@@ -928,8 +938,12 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   if (nmulti) {
     uint64_t* off = sc.item_off.as<uint64_t>(n + 1);
     scan_u32_to_u64(seg_count, off, n, sc.scan_tmp, s);
-    ND_CUDA(cudaMemcpyAsync(&items, off + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    ND_CUDA(cudaStreamSynchronize(s));
+    if (h_offsets) {
+      items = host_items;
+    } else {
+      ND_CUDA(cudaMemcpyAsync(&items, off + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaStreamSynchronize(s));
+    }
     uint32_t* idoc = sc.item_doc.as<uint32_t>(items);
     multi_docs = sc.multi_docs.as<uint32_t>(nmulti + 1);
     uint32_t* counter = flags + 2;

@@ -60,6 +60,7 @@ nd_ctx::~nd_ctx() {
     if (slot[i].comp) cudaStreamDestroy(slot[i].comp);
   }
   pinned_off.release();
+  multi.release();
   for (void* p : peer.opened) cudaIpcCloseMemHandle(p);
   for (auto* b : {&peer.own, &peer.bases, &peer.row_base}) b->release();
   for (auto& r : ring) r.release();
@@ -302,6 +303,8 @@ int nd_ctx_create(int device, nd_ctx** out) {
 
 void nd_ctx_destroy(nd_ctx* ctx) {
   if (!ctx) return;
+  for (nd_ctx* c : ctx->shards) nd_ctx_destroy(c);
+  ctx->shards.clear();
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   delete ctx;
@@ -327,6 +330,16 @@ int nd_ctx_set_stream(nd_ctx* ctx, void* stream) {
 
 int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L, uint32_t unit) {
   return guarded_impl(ctx, [&] {
+    family_upload_one(ctx, fns, H, L, unit);
+    if (is_group(ctx)) multi_family_upload(ctx, fns, H, L, unit);
+  });
+}
+
+}  // extern "C"
+
+namespace ndb {
+void family_upload_one(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L, uint32_t unit) {
+  {
     if (H == 0 || L == 0) fail(ND_ERR_CONFIG, "hash count and shingle length must be positive");
     if (unit > 1) fail(ND_ERR_CONFIG, "unknown shingle unit");
     if (L > 64) fail(ND_ERR_CONFIG, "shingle length above 64 is not supported on the GPU path");
@@ -433,11 +446,15 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L,
     ctx->fam.L = L;
     ctx->family_host.assign(fns, fns + H);
     ctx->family_derived = false;
-  });
+  }
 }
+}  // namespace ndb
+
+extern "C" {
 
 const char* nd_k1_kernel(nd_ctx* ctx) {
   static thread_local std::string out;
+  if (is_group(ctx)) ctx = ctx->shards[0];
   if (!ctx || !ctx->fam.q) return "";
   out = ctx->fam.exact ? "k1x" : ctx->fam.jit ? "k1j" : ctx->fam.unit == 1 ? "k1w" : "k1";
   if (!ctx->k1_note.empty()) out += ": " + ctx->k1_note;
@@ -448,6 +465,11 @@ int nd_signatures(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, ui
                   uint32_t bands, uint32_t rows, uint32_t K, uint32_t* sig_out,
                   uint32_t* band_out) {
   return guarded_impl(ctx, [&] {
+    if (is_group(ctx)) {
+      ctx->require_family();
+      multi_signatures(ctx, bytes, offsets, n, bands, rows, K, sig_out, band_out);
+      return;
+    }
     signatures_host(ctx, bytes, offsets, n, bands, rows, K, sig_out, band_out);
   });
 }

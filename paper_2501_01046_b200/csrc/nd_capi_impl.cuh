@@ -39,6 +39,24 @@ struct nd_ctx {
     uint32_t world = 0, H = 0;
     uint64_t rows = 0;
   } peer;
+  // multi-device group (nd_ctx_create_multi): one sub-context per shard;
+  // the group's own fields serve single-device calls on its first device
+  std::vector<nd_ctx*> shards;
+  struct Multi {                // per-shard exchange buffers (nd_multi.cu)
+    ndb::DevBuf send_keys, send_vals, first_cell, split, bases, row_base, pair_lo, pair_hi,
+        pair_m;
+    ndb::SortScratch sort;
+    ndb::PairSet final_pairs;
+    std::vector<uint64_t> ranges;  // group: document range of each shard, last dedup
+    bool last_valid = false;
+    void release() {
+      for (auto* b : {&send_keys, &send_vals, &first_cell, &split, &bases, &row_base, &pair_lo,
+                      &pair_hi, &pair_m})
+        b->release();
+      sort.release();
+      final_pairs.release();
+    }
+  } multi;
   uint64_t hbm_budget = 0;      // compare-stage HBM budget (0 = 70 % of free memory)
   uint64_t family_seed = 0;
   bool family_derived = false;  // family came from derive_family(family_seed, ...)
@@ -53,6 +71,16 @@ struct nd_ctx {
 
 namespace ndb {
 int guarded_impl(nd_ctx* ctx, const std::function<void()>& fn);
+// multi-device group contexts (nd_multi.cu)
+bool is_group(const nd_ctx* ctx);
+void family_upload_one(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t L, uint32_t unit);
+void multi_family_upload(nd_ctx* g, const nd_hash_fn* fns, uint32_t H, uint32_t L, uint32_t unit);
+void multi_signatures(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                      uint32_t bands, uint32_t rows, uint32_t K, uint32_t* sig_out,
+                      uint32_t* band_out);
+void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
+                 const uint64_t* doc_ids, uint64_t n, const nd_params& p, nd_dedup_stats* stats);
+void multi_fetch_signatures(nd_ctx* g, uint32_t* sig, uint32_t* band);
 uint64_t h2d_chunk_bytes(const DevFamily& fam, size_t chunk_index);
 // nd_signatures' host pipeline (chunks in, signature rows + band ids out)
 void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,

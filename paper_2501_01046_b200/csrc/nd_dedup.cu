@@ -157,8 +157,14 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   for (size_t c = 0; c < chunks.size(); ++c) {
     const auto [d0, d1] = chunks[c];
     const int r = static_cast<int>(c % kRing);
-    // (K1j: one compute stream, see signatures_host)
-    cudaStream_t cs = ctx->fam.jit ? ctx->ring_stream[0] : ctx->ring_stream[r];
+    // (ND_K1J_STREAMS=1: K1j chunks on one stream, as signatures_host does;
+    // here the ring's three streams measured faster: C3 10M docs from host
+    // 1.39 s vs 1.60 s, C2 82 vs 85 ms)
+    static const bool one = [] {
+      const char* v = getenv("ND_K1J_STREAMS");
+      return v && v[0] == '1';
+    }();
+    cudaStream_t cs = (ctx->fam.jit && one) ? ctx->ring_stream[0] : ctx->ring_stream[r];
     if (c >= kRing) ND_CUDA(cudaStreamWaitEvent(ctx->h2d, k1_done[r], 0));  // slot free again
     ND_CUDA(cudaMemcpyAsync(ring[r], bytes + offsets[0] + h_off[d0], h_off[d1] - h_off[d0],
                             cudaMemcpyHostToDevice, ctx->h2d));
@@ -409,6 +415,10 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
   return guarded_impl(ctx, [&] {
     const nd_params p = *params;
     validate(p);
+    if (is_group(ctx)) {  // sharded over the group's devices (nd_multi.cu)
+      multi_dedup(ctx, bytes, offsets, doc_ids, n, p, stats);
+      return;
+    }
     ensure_family(ctx, p);
     DedupState& st = ctx->dedup;
     st.valid = false;
@@ -455,6 +465,9 @@ int nd_dedup_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offse
                     const uint64_t* doc_ids, uint64_t n, const nd_params* params,
                     nd_dedup_stats* stats) {
   return guarded_impl(ctx, [&] {
+    if (is_group(ctx))
+      fail(ND_ERR_CONFIG, "nd_dedup_device takes one device's buffers; use nd_dedup with host "
+                          "buffers on a multi-device context");
     const nd_params p = *params;
     validate(p);
     ensure_family(ctx, p);
@@ -480,6 +493,10 @@ int nd_dedup_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offse
 
 int nd_dedup_fetch_signatures(nd_ctx* ctx, uint32_t* sig, uint32_t* band) {
   return guarded_impl(ctx, [&] {
+    if (is_group(ctx)) {
+      multi_fetch_signatures(ctx, sig, band);
+      return;
+    }
     DedupState& st = ctx->dedup;
     if (!st.valid || !ctx->fam.q) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");
     cudaStream_t s = ctx->stream;
@@ -498,6 +515,11 @@ int nd_dedup_fetch_signatures(nd_ctx* ctx, uint32_t* sig, uint32_t* band) {
 }
 
 int nd_dedup_fetch_pairs(nd_ctx* ctx, uint64_t* lo, uint64_t* hi, uint32_t* match_count) {
+  if (is_group(ctx)) {  // the group's result lives in shard 0's state
+    const int rc = nd_dedup_fetch_pairs(ctx->shards[0], lo, hi, match_count);
+    if (rc != ND_OK) ctx->err = ctx->shards[0]->err;
+    return rc;
+  }
   return guarded_impl(ctx, [&] {
     DedupState& st = ctx->dedup;
     if (!st.valid) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");
@@ -516,6 +538,11 @@ int nd_dedup_fetch_pairs(nd_ctx* ctx, uint64_t* lo, uint64_t* hi, uint32_t* matc
 }
 
 int nd_dedup_fetch_groups(nd_ctx* ctx, uint64_t* members, uint64_t* group_start) {
+  if (is_group(ctx)) {  // the group's result lives in shard 0's state
+    const int rc = nd_dedup_fetch_groups(ctx->shards[0], members, group_start);
+    if (rc != ND_OK) ctx->err = ctx->shards[0]->err;
+    return rc;
+  }
   return guarded_impl(ctx, [&] {
     DedupState& st = ctx->dedup;
     if (!st.valid) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");
@@ -538,6 +565,11 @@ int nd_dedup_write_report(nd_ctx* ctx, const char* dir, uint64_t total_records) 
 
 int nd_dedup_write_report_ex(nd_ctx* ctx, const char* dir, uint64_t total_records,
                              int fsync_files) {
+  if (is_group(ctx)) {
+    const int rc = nd_dedup_write_report_ex(ctx->shards[0], dir, total_records, fsync_files);
+    if (rc != ND_OK) ctx->err = ctx->shards[0]->err;
+    return rc;
+  }
   return guarded_impl(ctx, [&] {
     DedupState& st = ctx->dedup;
     if (!st.valid) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");

@@ -17,20 +17,33 @@ def _p(a: np.ndarray, t):
 
 
 class Context:
-    """Owns an nd_ctx on ``device``.  Not reentrant (nd_ctx contract)."""
+    """Owns an nd_ctx on ``device``, or -- with ``devices`` -- one context over
+    several GPUs (nd_ctx_create_multi: signatures and dedup sharded over the
+    devices, records exchanged over NVLink peer copies; a device may repeat).
+    Not reentrant (nd_ctx contract)."""
 
-    def __init__(self, device: int = 0, stream: int | None = None):
+    def __init__(self, device: int = 0, stream: int | None = None, devices=None):
         self.lib = _lib.load()
         h = C.c_void_p()
-        check(self.lib.nd_ctx_create(device, C.byref(h)))
+        if devices is not None:
+            devs = (C.c_int * len(devices))(*devices)
+            check(self.lib.nd_ctx_create_multi(devs, len(devices), C.byref(h)))
+            device = devices[0]
+        else:
+            check(self.lib.nd_ctx_create(device, C.byref(h)))
         self.h = h
         self.device = device
+        self.devices = list(devices) if devices is not None else [device]
         self._family_key = None
         if stream is not None:
             self.set_stream(stream)
 
     def set_stream(self, stream: int | None) -> None:
         check(self.lib.nd_ctx_set_stream(self.h, C.c_void_p(stream or 0)), self.h)
+
+    @property
+    def shards(self) -> int:
+        return int(self.lib.nd_ctx_shard_count(self.h))
 
     def close(self) -> None:
         if self.h:

@@ -26,3 +26,21 @@ a = t(lambda: minhash.signatures_packed(data, offs, fam, 16, 8, 2000, ctx=ctx, s
 b = t(lambda: pipeline.dedup_packed(data, offs, pipeline.RunConfig(), bucket_count=2000, ctx=ctx, fetch="arrays"))
 print(json.dumps({"first_mb": os.environ.get("ND_H2D_FIRST_MB"), "max_mb": os.environ.get("ND_H2D_MAX_MB"),
                   "sig_e2e_ms": a, "sig_e2e_docs_s": n / a * 1e3, "dedup_e2e_ms": b}))
+if os.environ.get("C3"):
+    import ctypes as C
+    from paper_2501_01046_b200 import _lib
+    lib = _lib.load()
+    docs = int(os.environ.get("C3"))
+    spec = bench.c3_spec(_lib, docs)
+    offs3 = torch.empty(docs + 1, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+    nb = C.c_uint64()
+    _lib.check(lib.nd_synth_generate(C.byref(spec), None, offs3.ctypes.data_as(_lib.u64p), C.byref(nb)))
+    d_offs = torch.from_numpy(offs3.view(np.int64)).cuda()
+    d_text = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+    ctx.check(lib.nd_synth_text_device(ctx.h, C.byref(spec), C.c_void_p(d_offs.data_ptr()), C.c_void_p(d_text.data_ptr())))
+    host = torch.empty(nb.value, dtype=torch.uint8, pin_memory=True); host.copy_(d_text); torch.cuda.synchronize()
+    del d_text; torch.cuda.empty_cache()
+    h = host.numpy()
+    c = t(lambda: pipeline.dedup_packed(h, offs3, pipeline.RunConfig(), ctx=ctx, fetch="arrays"), reps=2)
+    print(json.dumps({"c3_docs": docs, "c3_e2e_ms": c, "c3_docs_s": docs / c * 1e3,
+                      "streams": os.environ.get("ND_K1J_STREAMS")}))
