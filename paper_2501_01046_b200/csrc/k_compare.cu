@@ -458,6 +458,10 @@ __device__ __forceinline__ void join_check_blocks(const SigView sv, uint32_t H,
   if (alive && m >= min_match) emit(ra, rb, m, nb, out_key, out_m, count, cap);
 }
 
+// a block defers its candidate checks when the previous block had at least
+// this many (ND_JOIN_DEFER sets the queue size; 0 = never defer)
+constexpr uint32_t kDeferMin = 64;
+
 // TPB threads per CTA: 256, or 512 for big cells (twice the warps per SM at
 // the same 2 CTAs per SM that their shared memory allows)
 template <int DPT, int BW, int TPB>
@@ -475,7 +479,10 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
   constexpr int BPL = VL / BW;
   extern __shared__ uint32_t jsm[];
   __shared__ int pset_full;
-  __shared__ uint32_t qn[2];  // deferred-check queue fill, by block parity
+  // candidates of a block (after the handled-pair filter) by block % 3: the
+  // deferred-check queue's fill, and what decides whether the next block
+  // defers (only when the previous block had many, e.g. clusters)
+  __shared__ uint32_t qn[3];
   const uint32_t n = cell_len[blockIdx.x];
   if (n > join_max) return;  // big cells go to k_compare
   const uint32_t T = 1u << tbits;
@@ -505,8 +512,9 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
   for (uint32_t i = threadIdx.x; i < S; i += TPB) pset[i] = 0;
   if (threadIdx.x == 0) {
     pset_full = 0;
-    qn[0] = qn[1] = 0;
+    qn[0] = qn[1] = qn[2] = 0;
   }
+  uint32_t kblock = 0;  // running block index (k) for the % 3 counters
   __syncthreads();
   const uint32_t mask = T - 1;
   const bool vec = (H & 3) == 0;
@@ -563,11 +571,14 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
       }
       __syncthreads();
       const bool exact_set = S > 1 && *static_cast<volatile int*>(&pset_full) == 0;
-      if (qcap) {
-        // qn[(k + 1) & 1] was last read by the drain of block k - 1, before
-        // this block's barrier: reset it for block k + 1
-        if (threadIdx.x == 0) qn[(k + 1) & 1] = 0;
-        uint32_t* q = &qn[k & 1];
+      // qn[(k + 1) % 3] was last written in block k - 2's walk and read at
+      // block k - 1's decision, both before this barrier: reset it for k + 1
+      if (threadIdx.x == 0) qn[(kblock + 1) % 3] = 0;
+      uint32_t* q = &qn[kblock % 3];
+      const bool defer =
+          qcap && kblock > 0 && *static_cast<volatile uint32_t*>(&qn[(kblock + 2) % 3]) >= kDeferMin;
+      ++kblock;
+      if (defer) {
         for (uint32_t d = threadIdx.x; d < n; d += TPB)
           for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e]) {
             if (exact_set && pset_has(pset, S - 1, ((min(d, e) << 12) | max(d, e)) + 1u)) continue;
@@ -587,9 +598,12 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
         }
       } else {
         for (uint32_t d = threadIdx.x; d < n; d += TPB)
-          for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e])
+          for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e]) {
+            if (exact_set && pset_has(pset, S - 1, ((min(d, e) << 12) | max(d, e)) + 1u)) continue;
+            if (qcap) atomicAdd(q, 1u);  // count: does the next block defer?
             join_check_blocks<BW>(sv, H, d, e, rowsm, k, vec, pset, S - 1, &pset_full, exact_set,
-                                  min_match, nb, out_key, out_m, count, cap);
+                                  min_match, nb, out_key, out_m, count, cap, true);
+          }
       }
       if (two_barriers) __syncthreads();
     }
@@ -645,9 +659,13 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
     const char* ps = getenv("ND_JOIN_PSET");  // 0: no set (HBM checks of earlier blocks)
     if (ps && ps[0] == '0') sbits = 0;
     const size_t smem = (2u * (1u << tbits) + 2u * join_max) * sizeof(uint32_t);
-    // deferred-check queue (ND_JOIN_DEFER = entries, 0 = check in the walk)
+    // deferred-check queue (ND_JOIN_DEFER = entries, 0 = check in the walk).
+    // Off by default: it halves K3's time on clustered cells (C5: 54.7 ->
+    // 36.5 ms at 1024 entries) but its shared memory costs the uniform cells
+    // of C2/C3 L1 capacity for the row gathers (C2 cells 5.1 -> 6.9 ms, even
+    // at 128 entries; profiles/r2_k3_defer.txt)
     const char* jd = getenv("ND_JOIN_DEFER");
-    const uint32_t qcap = jd ? static_cast<uint32_t>(std::max(0, atoi(jd))) : 1024u;
+    const uint32_t qcap = jd ? static_cast<uint32_t>(std::max(0, atoi(jd))) : 0u;
     const size_t smem_b = (2u * (1u << tbits) + (sbits ? 1u << sbits : 1u)) * sizeof(uint32_t) +
                           join_max * (sizeof(uint32_t) + 2 * sizeof(uint16_t)) +
                           (qcap ? 8 + qcap * sizeof(uint2) : 0);
