@@ -138,8 +138,10 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t hash_count,
                      uint32_t shingle_len, uint32_t unit);
 /* Which signature kernel the uploaded family runs: "k1j" (family-specialised,
  * compiled by NVRTC at upload), "k1" (per-lane register constants), "k1w"
- * (codepoint units) or "k1x" (exact 64-bit Barrett); when K1j was eligible but
- * could not be compiled the reason follows after ": ". */
+ * (codepoint units), "k1j+k1w" / "k1+k1w" (codepoint units: documents whose
+ * code points are all < 256 on the byte kernel, the others on K1w) or "k1x"
+ * (exact 64-bit Barrett); when K1j was eligible but could not be compiled the
+ * reason follows after ": ". */
 const char* nd_k1_kernel(nd_ctx* ctx);
 
 /* signature_of_document over a packed batch + band_bucket_ids

@@ -357,7 +357,9 @@ std::shared_ptr<JitKernel> compile(const nd_hash_fn* fns, uint32_t H, uint32_t L
 bool k1_jit_eligible(const DevFamily& fam) {
   const char* v = getenv("ND_K1_JIT");  // 0: the register-constant K1
   if (v && v[0] == '0') return false;
-  return fam.unit == 0 && !fam.exact && fam.L >= 1 && fam.L <= 16 && fam.H >= 1 && fam.H <= 1024;
+  // codepoint families compile too when narrow documents can use them
+  return (fam.unit == 0 || fam.narrow_ok) && !fam.exact && fam.L >= 1 && fam.L <= 16 &&
+         fam.H >= 1 && fam.H <= 1024;
 }
 
 // Compiles (or finds) the family's kernel; the cache outlives contexts so a

@@ -140,6 +140,37 @@ __global__ void k_fill_multi(const uint32_t* __restrict__ multi_docs, uint32_t n
   }
 }
 
+// Codepoint documents whose units are all < 256 (ASCII / Latin-1 text) hash
+// exactly like bytes: wide[d] = 1 when document d has a unit >= 256; cnt[0]
+// counts them, cnt[1] the units of the batch (device-side totals)
+__global__ void k_wide_docs(const uint32_t* __restrict__ units, const uint64_t* __restrict__ uoff,
+                            uint64_t n, uint32_t* __restrict__ wide, uint32_t* __restrict__ cnt) {
+  const uint64_t d = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (d >= n) return;
+  bool w = false;
+  for (uint64_t i = uoff[d] + lane; i < uoff[d + 1] && !w; i += 32) w = units[i] >= 256u;
+  w = __any_sync(0xFFFFFFFFu, w);
+  if (lane == 0) {
+    wide[d] = w ? 1u : 0u;
+    if (w) atomicAdd(cnt, 1u);
+  }
+}
+
+__global__ void k_units_to_u8(const uint32_t* __restrict__ units, uint64_t m,
+                              uint8_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<uint8_t>(units[i]);
+}
+
+// seg_count of the documents the wide pass skips -> 0 (no items)
+__global__ void k_keep_wide(const uint32_t* __restrict__ wide, uint64_t n,
+                            uint32_t* __restrict__ seg_count) {
+  const uint64_t d = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (d < n && !wide[d]) seg_count[d] = 0;
+}
+
 // K1j work order: items by descending window count (stable), so the 32
 // items a warp takes have nearly equal lengths
 __global__ void k_item_len_keys(const uint64_t* __restrict__ offsets,
@@ -885,6 +916,7 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   if (n > 0xFFFFFFFFull) fail(ND_ERR_CONFIG, "batch exceeds 2^32 documents");
   unsigned tb = 256;
   const void* d_text = d_bytes;
+  const uint32_t* wide_mask = nullptr;  // codepoint: only the wide documents run K1w
   if (fam.unit == 1) {
     // codepoint units: decode, then plan and sign over the u32 unit arrays;
     // unit counts are only known on the device, so the short check runs there
@@ -896,6 +928,41 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     d_offsets = uoff;
     h_offsets = nullptr;
     check_short = true;
+    static const bool narrow_on = [] {
+      const char* v = getenv("ND_K1_NARROW");  // 0: every codepoint document through K1w
+      return !(v && v[0] == '0');
+    }();
+    if (fam.narrow_ok && narrow_on) {
+      // Documents whose code points are all < 256 hash exactly like bytes
+      // (the fq arithmetic's domain: units < 256, 2^21 <= p < 2^23): narrow
+      // every unit to a byte and run the byte kernels (K1j / fq) over the
+      // whole batch; then K1w redoes only the documents with a wider unit
+      // (their rows from the byte pass are overwritten).
+      uint32_t* wide = sc.wide.as<uint32_t>(n);
+      uint32_t* cnt = sc.flags.as<uint32_t>(4);
+      ND_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), s));
+      k_wide_docs<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, s>>>(units, uoff, n, wide,
+                                                                              cnt);
+      ND_CHECK_LAUNCH();
+      uint32_t nwide = 0;
+      uint64_t total = 0;
+      ND_CUDA(cudaMemcpyAsync(&nwide, cnt, 4, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaMemcpyAsync(&total, uoff + n, 8, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaStreamSynchronize(s));
+      if (nwide < n) {
+        uint8_t* u8 = sc.units8.as<uint8_t>(total + 16);
+        if (total)
+          k_units_to_u8<<<4 * sm_count(), 256, 0, s>>>(units, total, u8);
+        ND_CHECK_LAUNCH();
+        DevFamily byte_view = fam;
+        byte_view.unit = 0;
+        byte_view.narrow_ok = false;
+        launch_signatures(byte_view, u8, uoff, n, bands, rows, K, d_sig, d_band, sc, s,
+                          /*check_short=*/true, nullptr);
+        if (nwide == 0) return;
+        wide_mask = wide;  // K1w below: the wide documents only
+      }
+    }
   }
   uint32_t hflags[4] = {0, 0, 0, 0};
   uint64_t host_items = n;  // work items, known on the host when h_offsets is
@@ -916,7 +983,7 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   }
   uint32_t* seg_count = nullptr;
   uint32_t* flags = nullptr;
-  if (!h_offsets || hflags[1]) {
+  if (!h_offsets || hflags[1] || wide_mask) {
     seg_count = sc.seg_count.as<uint32_t>(n);
     flags = sc.flags.as<uint32_t>(4);
     ND_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(uint32_t), s));
@@ -928,6 +995,10 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
       ND_CUDA(cudaStreamSynchronize(s));
       if (check_short && hflags[0]) fail(ND_ERR_SHORT, "a document has fewer units than the shingle length");
     }
+    if (wide_mask) {
+      k_keep_wide<<<static_cast<unsigned>((n + tb - 1) / tb), tb, 0, s>>>(wide_mask, n, seg_count);
+      ND_CHECK_LAUNCH();
+    }
   }
 
   const uint32_t* item_doc = nullptr;
@@ -935,7 +1006,7 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   uint64_t items = n;
   uint32_t nmulti = hflags[1];
   uint32_t* multi_docs = nullptr;
-  if (nmulti) {
+  if (nmulti || wide_mask) {
     uint64_t* off = sc.item_off.as<uint64_t>(n + 1);
     scan_u32_to_u64(seg_count, off, n, sc.scan_tmp, s);
     if (h_offsets) {
@@ -951,6 +1022,10 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     k_item_scatter<<<static_cast<unsigned>((n + tb - 1) / tb), tb, 0, s>>>(off, n, idoc, multi_docs,
                                                                            counter);
     ND_CHECK_LAUNCH();
+    if (wide_mask) {  // the multi-item documents among the wide ones
+      ND_CUDA(cudaMemcpyAsync(&nmulti, counter, 4, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaStreamSynchronize(s));
+    }
     k_fill_multi<<<1024, 256, 0, s>>>(multi_docs, nmulti, fam.H, d_sig);
     ND_CHECK_LAUNCH();
     item_doc = idoc;

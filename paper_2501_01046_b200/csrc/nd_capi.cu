@@ -354,6 +354,7 @@ void family_upload_one(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t 
     // struct) that breaks them makes the reference compute something other
     // than the window hash, which no exact GPU evaluation can reproduce.
     bool fast = true;
+    bool narrow = unit == 1;  // codepoint family inside the byte fq domain
     for (uint32_t i = 0; i < H; ++i) {
       const nd_hash_fn& f = fns[i];
       const uint64_t p = f.modulus;
@@ -381,6 +382,8 @@ void family_upload_one(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t 
                                 ": reduce_factor is not floor(2^64 / modulus)");
       const uint64_t p_lo = unit == 1 ? 0x110000ull : (1ull << 21);
       if (p < p_lo || p >= (1ull << 23) || f.base == 0 || f.base >= (1u << 16)) fast = false;
+      if (p < (1ull << 21) || p >= (1ull << 23) || f.base == 0 || f.base >= (1u << 16))
+        narrow = false;
     }
     const char* fe = getenv("ND_K1_EXACT");  // 1: exact arithmetic for every family (tests)
     if (fe && fe[0] == '1') fast = false;
@@ -427,6 +430,7 @@ void family_upload_one(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t 
     ctx->fam.p = d + 9 * Hp;
     ctx->fam.rf = reinterpret_cast<unsigned long long*>(d + 10 * Hp);
     ctx->fam.exact = !fast;
+    ctx->fam.narrow_ok = narrow && fast;
     ctx->fam.unit = unit;
     ctx->fam.H = H;
     ctx->fam.L = L;
@@ -456,7 +460,9 @@ const char* nd_k1_kernel(nd_ctx* ctx) {
   static thread_local std::string out;
   if (is_group(ctx)) ctx = ctx->shards[0];
   if (!ctx || !ctx->fam.q) return "";
-  out = ctx->fam.exact ? "k1x" : ctx->fam.jit ? "k1j" : ctx->fam.unit == 1 ? "k1w" : "k1";
+  if (ctx->fam.exact) out = "k1x";
+  else if (ctx->fam.unit == 1) out = ctx->fam.jit ? "k1j+k1w" : ctx->fam.narrow_ok ? "k1+k1w" : "k1w";
+  else out = ctx->fam.jit ? "k1j" : "k1";
   if (!ctx->k1_note.empty()) out += ": " + ctx->k1_note;
   return out.c_str();
 }

@@ -51,6 +51,9 @@ struct DevFamily {
   uint32_t L = 0;
   uint32_t unit = 0;         // 0 = byte, 1 = codepoint (ShingleUnit, text.hpp:23-26)
   void* jit = nullptr;        // K1j kernel specialised for this family (k1_jit.cpp), or null
+  // codepoint family whose functions all lie in the byte fq domain: documents
+  // whose code points are all < 256 run the byte kernels over narrowed units
+  bool narrow_ok = false;
   // true when some function lies outside the domain the fast arithmetics are
   // proven for (byte fq: 2^21 <= p < 2^23, q < 2^16; codepoint wide:
   // 0x10FFFF < p < 2^23, q < 2^16): K1 then runs the 64-bit Barrett
@@ -116,11 +119,12 @@ struct SortScratch {
 };
 struct SigScratch {
   DevBuf seg_count, item_off, item_doc, flags, multi_docs, scan_tmp, units, unit_off, unit_cnt,
-      item_counter, order_keys, order_vals;
+      item_counter, order_keys, order_vals, units8, wide;
   SortScratch sort;  // K1j: items ordered by length
   void release() {
     for (DevBuf* b : {&seg_count, &item_off, &item_doc, &flags, &multi_docs, &scan_tmp, &units,
-                      &unit_off, &unit_cnt, &item_counter, &order_keys, &order_vals})
+                      &unit_off, &unit_cnt, &item_counter, &order_keys, &order_vals, &units8,
+                      &wide})
       b->release();
     sort.release();
   }

@@ -124,12 +124,45 @@ def test_k1j_skewed_lengths_many_items(ctx, oracle, monkeypatch):
 
 
 def test_k1j_not_used_outside_its_domain(ctx, monkeypatch):
-    # codepoint units and hand-built families keep their kernels
+    # codepoint units: K1j for the documents below U+0100, K1w for the rest;
+    # L > 16: the register-constant kernel
     fam = minhash.derive_family(5, 32, 5, minhash.ShingleUnit.CODEPOINT)
     ctx.upload_family(fam)
-    assert _kernel(ctx) == "k1w"
+    assert _kernel(ctx) == "k1j+k1w"
     ctx._family_key = None
     fam = minhash.derive_family(5, 32, 20)  # L > 16
     ctx.upload_family(fam)
     assert _kernel(ctx) == "k1"
     ctx._family_key = None
+
+
+@pytest.mark.parametrize("mix", ["ascii", "latin1", "mixed"])
+def test_codepoint_narrow_documents_take_the_byte_kernels(ctx, oracle, monkeypatch, mix):
+    # codepoint units < 256 (ASCII, and Latin-1 whose UTF-8 is two bytes)
+    # hash exactly like bytes: those documents run K1j over narrowed units,
+    # the rest K1w; every row must equal K1w-only and the oracle
+    rng = np.random.default_rng({"ascii": 1, "latin1": 2, "mixed": 3}[mix])
+    latin = [chr(c) for c in range(0xA0, 0x100)] + list("abcdefgh ")
+    wide = [chr(c) for c in range(0x400, 0x450)] + [chr(c) for c in range(0x4E00, 0x4E40)]
+    texts = []
+    for i in range(400):
+        k = int(rng.integers(5, 3000)) if i % 50 else 12000  # some multi-item documents
+        if mix == "ascii" or (mix == "mixed" and i % 3 == 0):
+            texts.append("".join(rng.choice(list("abcdefghijklmnop qrstuvwxyz"), size=k)))
+        elif mix == "latin1" or (mix == "mixed" and i % 3 == 1):
+            texts.append("".join(rng.choice(latin, size=k)))
+        else:
+            texts.append("".join(rng.choice(latin + wide, size=k)))
+    raw = [t.encode() for t in texts]
+    offs = np.zeros(len(raw) + 1, np.uint64)
+    offs[1:] = np.cumsum([len(b) for b in raw])
+    data = np.frombuffer(b"".join(raw), np.uint8).copy()
+    fam = minhash.derive_family(5, 128, 5, minhash.ShingleUnit.CODEPOINT)
+    res = {}
+    for narrow in ("1", "0"):
+        monkeypatch.setenv("ND_K1_NARROW", narrow)
+        res[narrow] = minhash.signatures_packed(data, offs, fam, 16, 8, 1000, ctx=ctx)
+    monkeypatch.delenv("ND_K1_NARROW")
+    assert np.array_equal(res["1"][0], res["0"][0]) and np.array_equal(res["1"][1], res["0"][1])
+    want = oracle.signatures(data, offs, oracle.derive_family(5, 128), unit=1)
+    assert np.array_equal(res["1"][0], want)
