@@ -159,7 +159,7 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
   std::ostringstream s;
   s << "typedef unsigned int u32; typedef unsigned long long u64; typedef unsigned char u8;\n"
        "typedef long long i64;\n"
-       "#define L " << L << "\n#define H " << H << "\n#define KSEG 8192ll\n"
+       "#define L " << L << "\n#define H " << H << "\n"
        "#define NPASS " << (H + kJitF - 1) / kJitF << "\n"
        "static __device__ __forceinline__ u32 umin(u32 a, u32 b) { return a < b ? a : b; }\n"
        "static __device__ __forceinline__ u32 rol(u32 C, u32 ci, u32 co, float cf, u32 q,\n"
@@ -175,9 +175,9 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "extern \"C\" __global__ void __launch_bounds__(" << kJitThreads << ", " << min_blocks << ")\n"
        "k1j(const u8* __restrict__ text, const u64* __restrict__ offsets,\n"
        "    const u32* __restrict__ order, const u32* __restrict__ item_doc,\n"
-       "    const u64* __restrict__ item_off, u32 n_items, u32 bands, u32 rows, u32 K,\n"
-       "    u32* __restrict__ sig, u32* __restrict__ band, u64* __restrict__ counter,\n"
-       "    float c5) {\n"
+       "    const u64* __restrict__ item_off, u32 n_items, u32 seg_len,\n"
+       "    u32* __restrict__ sig, u64* __restrict__ counter, float c5) {\n"
+       "  const i64 KSEG = seg_len;  // windows per work item\n"
        "  // c5 = 2^-5 arrives as a parameter so that it sits in a register and\n"
        "  // every FFMA keeps its function constant as the immediate\n"
        "  const u32 lane = threadIdx.x & 31;\n"
@@ -388,18 +388,23 @@ double k1_jit_compile_seconds(const void* handle) {
   return handle ? static_cast<const JitKernel*>(handle)->compile_seconds : 0.0;
 }
 
+uint64_t k1_jit_resident_warps(const void* handle) {
+  return static_cast<uint64_t>(static_cast<const JitKernel*>(handle)->per_sm) * sm_count() *
+         (kJitThreads / 32);
+}
+
 void k1_jit_launch(const void* handle, const uint8_t* d_text, const uint64_t* d_offsets,
                    const uint32_t* order, const uint32_t* item_doc, const uint64_t* item_off,
-                   uint32_t n_items, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
-                   uint32_t* d_band, unsigned long long* counter, cudaStream_t s) {
+                   uint32_t n_items, uint32_t seg_len, uint32_t* d_sig,
+                   unsigned long long* counter, cudaStream_t s) {
   const JitKernel* k = static_cast<const JitKernel*>(handle);
   const uint64_t warps = (static_cast<uint64_t>(n_items) + 31) / 32;
   uint64_t blocks = (warps + kJitThreads / 32 - 1) / (kJitThreads / 32);
   blocks = std::min<uint64_t>(blocks, static_cast<uint64_t>(k->per_sm) * sm_count());
   ND_CUDA(cudaMemsetAsync(counter, 0, k->passes * sizeof(unsigned long long), s));  // one per pass
   float c5 = 0.03125f;
-  void* args[] = {&d_text, &d_offsets, &order, &item_doc, &item_off, &n_items, &bands, &rows, &K,
-                  &d_sig, &d_band, &counter, &c5};
+  void* args[] = {&d_text, &d_offsets, &order, &item_doc, &item_off, &n_items, &seg_len, &d_sig,
+                  &counter, &c5};
   ND_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(k->fn), dim3(static_cast<unsigned>(blocks)),
                            dim3(kJitThreads), args, 0, s));
   ND_CHECK_LAUNCH();

@@ -105,7 +105,8 @@ struct FamPtrs {
 // ---------------------------------------------------------------------------
 // planning: per-document segment counts, short-document detection
 __global__ void k_plan(const uint64_t* __restrict__ offsets, uint64_t n, uint32_t L,
-                       uint32_t* __restrict__ seg_count, uint32_t* __restrict__ flags) {
+                       uint32_t* __restrict__ seg_count, uint32_t* __restrict__ flags,
+                       uint32_t seg_len) {
   uint64_t d = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (d >= n) return;
   uint64_t len = offsets[d + 1] - offsets[d];
@@ -114,7 +115,7 @@ __global__ void k_plan(const uint64_t* __restrict__ offsets, uint64_t n, uint32_
     atomicOr(&flags[0], 1u);  // ShortDocumentError
   } else {
     uint64_t nwin = len - L + 1;
-    uint64_t s = (nwin + kSeg - 1) / kSeg;
+    uint64_t s = (nwin + seg_len - 1) / seg_len;
     nseg = static_cast<uint32_t>(s);
     if (s > 1) atomicAdd(&flags[1], 1u);  // multi-item document count
   }
@@ -176,16 +177,17 @@ __global__ void k_keep_wide(const uint32_t* __restrict__ wide, uint64_t n,
 __global__ void k_item_len_keys(const uint64_t* __restrict__ offsets,
                                 const uint32_t* __restrict__ item_doc,
                                 const uint64_t* __restrict__ item_off, uint64_t n_items, uint32_t L,
-                                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                                uint32_t seg_len, uint32_t* __restrict__ keys,
+                                uint32_t* __restrict__ vals) {
   uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= n_items) return;
   uint64_t doc = i, ws = 0;
   if (item_doc) {
     doc = item_doc[i];
-    ws = (i - item_off[doc]) * kSeg;
+    ws = (i - item_off[doc]) * seg_len;
   }
   const uint64_t nwin = offsets[doc + 1] - offsets[doc] - L + 1;
-  const uint64_t w = min(nwin - ws, static_cast<uint64_t>(kSeg));
+  const uint64_t w = min(nwin - ws, static_cast<uint64_t>(seg_len));
   keys[i] = 16383u - static_cast<uint32_t>(w);  // kSeg < 2^14
   vals[i] = static_cast<uint32_t>(i);
 }
@@ -964,6 +966,30 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
       }
     }
   }
+  // K1j splits documents into items of seg_len windows; a small batch gets
+  // shorter items so that the pass-major grid still fills the GPU (~1.5
+  // items per resident lane; the register kernels keep kSeg)
+  uint32_t seg_len = kSeg;
+  const bool jit_path = fam.jit && fam.unit == 0;
+  if (jit_path) {
+    const uint64_t target = static_cast<uint64_t>(3 * 32 / 2) * k1_jit_resident_warps(fam.jit);
+    if (n < target) {
+      uint64_t bytes = 0;
+      if (h_offsets) {
+        bytes = h_offsets[n] - h_offsets[0];
+      } else {
+        uint64_t ends[2] = {0, 0};
+        ND_CUDA(cudaMemcpyAsync(&ends[0], d_offsets, 8, cudaMemcpyDeviceToHost, s));
+        ND_CUDA(cudaMemcpyAsync(&ends[1], d_offsets + n, 8, cudaMemcpyDeviceToHost, s));
+        ND_CUDA(cudaStreamSynchronize(s));
+        bytes = ends[1] - ends[0];
+      }
+      const uint64_t per = (bytes + target - 1) / target;  // ~windows per item
+      const char* ms = getenv("ND_K1J_MIN_SEG");           // tuning
+      const uint64_t lo = ms ? std::max(64, atoi(ms)) : 512;
+      seg_len = static_cast<uint32_t>(std::min<uint64_t>(kSeg, std::max<uint64_t>(lo, (per + 63) / 64 * 64)));
+    }
+  }
   uint32_t hflags[4] = {0, 0, 0, 0};
   uint64_t host_items = n;  // work items, known on the host when h_offsets is
   if (h_offsets) {  // host planning: no device round trip (the pipelines keep running)
@@ -975,7 +1001,7 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
         ++host_items;
         continue;
       }
-      const uint64_t segs = (len - fam.L + 1 + kSeg - 1) / kSeg;
+      const uint64_t segs = (len - fam.L + 1 + seg_len - 1) / seg_len;
       host_items += segs;
       if (segs > 1) ++hflags[1];
     }
@@ -988,7 +1014,7 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     flags = sc.flags.as<uint32_t>(4);
     ND_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(uint32_t), s));
     k_plan<<<static_cast<unsigned>((n + tb - 1) / tb), tb, 0, s>>>(d_offsets, n, fam.L, seg_count,
-                                                                    flags);
+                                                                    flags, seg_len);
     ND_CHECK_LAUNCH();
     if (!h_offsets) {
       ND_CUDA(cudaMemcpyAsync(hflags, flags, sizeof hflags, cudaMemcpyDeviceToHost, s));
@@ -1048,12 +1074,12 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     uint32_t* keys = sc.order_keys.as<uint32_t>(items);
     uint32_t* order = sc.order_vals.as<uint32_t>(items);
     k_item_len_keys<<<static_cast<unsigned>((items + tb - 1) / tb), tb, 0, s>>>(
-        d_offsets, item_doc, item_off, items, fam.L, keys, order);
+        d_offsets, item_doc, item_off, items, fam.L, seg_len, keys, order);
     ND_CHECK_LAUNCH();
     radix_sort_u32(keys, order, items, 14, sc.sort, s);
     k1_jit_launch(fam.jit, static_cast<const uint8_t*>(d_text), d_offsets, order, item_doc,
-                  item_off, static_cast<uint32_t>(items), d_band ? bands : 0, rows, K, d_sig,
-                  d_band, sc.item_counter.as<unsigned long long>(k1_jit_passes(fam.jit)), s);
+                  item_off, static_cast<uint32_t>(items), seg_len, d_sig,
+                  sc.item_counter.as<unsigned long long>(k1_jit_passes(fam.jit)), s);
     // band keys of every document from its finished row (keys is free again)
     if (d_band) launch_band_keys(d_sig, n, fam.H, bands, rows, K, d_band, keys, s);
     return;

@@ -135,10 +135,11 @@ void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L);
 double k1_jit_compile_seconds(const void* handle);
 uint32_t k1_jit_passes(const void* handle);
 std::string k1_jit_source(const nd_hash_fn* fns, uint32_t H, uint32_t L);
+uint64_t k1_jit_resident_warps(const void* handle);
 void k1_jit_launch(const void* handle, const uint8_t* d_text, const uint64_t* d_offsets,
                    const uint32_t* order, const uint32_t* item_doc, const uint64_t* item_off,
-                   uint32_t n_items, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
-                   uint32_t* d_band, unsigned long long* counter, cudaStream_t s);
+                   uint32_t n_items, uint32_t seg_len, uint32_t* d_sig,
+                   unsigned long long* counter, cudaStream_t s);
 // UTF-8 -> codepoint units (k_utf8.cu): units_out[unit_off_out[d] ..
 // unit_off_out[d+1]) are document d's units (decode_codepoints, text.cpp:101-113).
 void decode_codepoints_device(const uint8_t* d_text, const uint64_t* d_offsets, uint64_t n,
