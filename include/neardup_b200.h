@@ -349,6 +349,18 @@ int nd_union_stage(nd_ctx* ctx, const char* const* pair_paths, uint32_t nfiles,
 int nd_stage_cell_records(nd_ctx* ctx, const uint32_t* d_band, uint64_t n, uint32_t bands,
                           uint32_t bucket_count, uint32_t doc_base, uint32_t* d_keys,
                           uint32_t* d_vals);
+/* The same records packed for one all-to-all: d_rec[i] = cell << 32 | row,
+ * sorted by cell, and owner_split[world + 1] (host) = where each owner's run
+ * starts (owner of a cell = nd_cell_partition(bands, K, world)).
+ * Synchronous (the splits are read back). */
+int nd_stage_records_packed(nd_ctx* ctx, const uint32_t* d_band, uint64_t n, uint32_t bands,
+                            uint32_t bucket_count, uint32_t doc_base, uint32_t world,
+                            uint64_t* d_rec, uint64_t* owner_split);
+/* nd_stage_compare_peer over m packed records (arrival order = rank order). */
+int nd_stage_compare_peer_packed(nd_ctx* ctx, const uint64_t* d_rec, uint64_t m,
+                                 uint64_t key_limit, uint64_t threshold_num,
+                                 uint64_t threshold_den, uint64_t* npairs_out,
+                                 uint64_t* candidate_pairs_out);
 /* compare_pass over the cells of m (cell, row) records (any order; stable by
  * arrival) against signature rows d_sig[nrows*H]; keeps the sorted distinct
  * pairs in the ctx; synchronous; *npairs_out = their count. */

@@ -98,6 +98,10 @@ SIGNATURES = {
     "nd_synth_text_device": (C.c_int, [vp, C.POINTER(NdSynthSpec), vp, vp]),
     "nd_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
     "nd_ctx_create_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]),
+    "nd_stage_records_packed": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          C.c_uint32, vp, u64p]),
+    "nd_stage_compare_peer_packed": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, C.c_uint64,
+                                               C.c_uint64, u64p, u64p]),
     "nd_ctx_shard_count": (C.c_int, [vp]),
     "nd_ctx_destroy": (None, [vp]),
     "nd_last_error": (C.c_char_p, [vp]),

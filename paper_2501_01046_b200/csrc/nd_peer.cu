@@ -13,7 +13,86 @@
 
 using namespace ndb;
 
+namespace {
+__global__ void k_pack_records(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                               uint64_t m, uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = (static_cast<uint64_t>(keys[i]) << 32) | vals[i];
+}
+__global__ void k_unpack_records(const uint64_t* __restrict__ in, uint64_t m,
+                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = in[i];
+    keys[i] = static_cast<uint32_t>(r >> 32);
+    vals[i] = static_cast<uint32_t>(r);
+  }
+}
+// owner run starts in the cell-sorted keys: lower_bound of each owner's first cell
+__global__ void k_splits(const uint32_t* __restrict__ keys, uint64_t m,
+                         const uint64_t* __restrict__ first_cell, uint32_t G,
+                         uint64_t* __restrict__ split) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > G) return;
+  uint64_t lo = 0, hi = m;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < first_cell[g]) lo = mid + 1; else hi = mid;
+  }
+  split[g] = lo;
+}
+}  // namespace
+
 extern "C" {
+
+int nd_stage_records_packed(nd_ctx* ctx, const uint32_t* d_band, uint64_t n, uint32_t bands,
+                            uint32_t K, uint32_t doc_base, uint32_t world, uint64_t* d_rec,
+                            uint64_t* owner_split) {
+  return guarded_impl(ctx, [&] {
+    if (bands == 0 || K == 0) fail(ND_ERR_CONFIG, "bands and bucket count must be positive");
+    if (world == 0) fail(ND_ERR_CONFIG, "world size must be positive");
+    cudaStream_t s = ctx->stream;
+    const uint64_t m = n * bands;
+    const uint64_t cells = static_cast<uint64_t>(bands) * K;
+    uint32_t* keys = ctx->multi.send_keys.as<uint32_t>(m + 1);
+    uint32_t* vals = ctx->multi.send_vals.as<uint32_t>(m + 1);
+    make_records(d_band, n, bands, K, doc_base, keys, vals, s);
+    radix_sort_u32(keys, vals, m, bits_for(cells - 1), ctx->stage_sort, s);
+    if (m) {
+      k_pack_records<<<4 * sm_count(), 256, 0, s>>>(keys, vals, m, d_rec);
+      ND_CHECK_LAUNCH();
+    }
+    std::vector<uint64_t> first(world + 1);
+    for (uint32_t g = 0; g <= world; ++g)
+      first[g] = static_cast<uint64_t>((static_cast<unsigned __int128>(cells) * g + world - 1) / world);
+    uint64_t* d_first = ctx->multi.first_cell.as<uint64_t>(world + 1);
+    uint64_t* d_split = ctx->multi.split.as<uint64_t>(world + 1);
+    ND_CUDA(cudaMemcpyAsync(d_first, first.data(), (world + 1) * 8, cudaMemcpyHostToDevice, s));
+    k_splits<<<1, 64 * ((world + 64) / 64), 0, s>>>(keys, m, d_first, world, d_split);
+    ND_CHECK_LAUNCH();
+    ND_CUDA(cudaMemcpyAsync(owner_split, d_split, (world + 1) * 8, cudaMemcpyDeviceToHost, s));
+    ND_CUDA(cudaStreamSynchronize(s));
+    owner_split[world] = m;
+  });
+}
+
+int nd_stage_compare_peer_packed(nd_ctx* ctx, const uint64_t* d_rec, uint64_t m,
+                                 uint64_t key_limit, uint64_t num, uint64_t den,
+                                 uint64_t* npairs_out, uint64_t* cand_out) {
+  return guarded_impl(ctx, [&] {
+    cudaStream_t s = ctx->stream;
+    uint32_t* k = ctx->multi.send_keys.as<uint32_t>(m + 1);
+    uint32_t* v = ctx->multi.send_vals.as<uint32_t>(m + 1);
+    if (m) {
+      k_unpack_records<<<4 * sm_count(), 256, 0, s>>>(d_rec, m, k, v);
+      ND_CHECK_LAUNCH();
+    }
+    const int rc = nd_stage_compare_peer(ctx, k, v, m, key_limit, num, den, npairs_out, cand_out);
+    if (rc != ND_OK) fail(rc, ctx->err);
+  });
+}
+
 
 int nd_peer_export(nd_ctx* ctx, const uint32_t* d_sig, uint64_t rows, uint32_t H,
                    uint8_t* handle_out) {

@@ -121,6 +121,35 @@ class GpuStages:
         self.ctx.check(self.ctx.lib.nd_peer_open(self.ctx.h, hb, rb.ctypes.data_as(_lib.u64p),
                                                  world, rank))
 
+    # ---- packed records: one u64 per (cell, row), sorted by cell, with the owner
+    # splits found on the device (one all-to-all instead of two)
+    packed_capable = True
+
+    def records_packed(self, band, bands, K, doc_base, world):
+        t = self.torch
+        n = band.shape[0]
+        rec = self.tensor((max(n * bands, 1),), t.int64)
+        split = np.zeros(world + 1, np.uint64)
+        self.ctx.check(self.ctx.lib.nd_stage_records_packed(
+            self.ctx.h, C.c_void_p(band.data_ptr()), n, bands, K, doc_base, world,
+            C.c_void_p(rec.data_ptr()), split.ctypes.data_as(_lib.u64p)))
+        return rec[: n * bands], [int(x) for x in split]
+
+    def compare_peer_packed(self, rec, key_limit, threshold):
+        t = self.torch
+        num, den = threshold
+        npairs, cand = C.c_uint64(), C.c_uint64()
+        self.ctx.check(self.ctx.lib.nd_stage_compare_peer_packed(
+            self.ctx.h, C.c_void_p(rec.data_ptr()), rec.shape[0], key_limit, num, den,
+            C.byref(npairs), C.byref(cand)))
+        k = npairs.value
+        lo, hi, m = (self.tensor((max(k, 1),), t.int32) for _ in range(3))
+        self.ctx.check(self.ctx.lib.nd_stage_pairs_copy(
+            self.ctx.h, C.c_void_p(lo.data_ptr()), C.c_void_p(hi.data_ptr()),
+            C.c_void_p(m.data_ptr())))
+        self.ctx_sync()
+        return lo[:k], hi[:k], m[:k], cand.value
+
     def compare_peer(self, keys, vals, key_limit, threshold):
         t = self.torch
         num, den = threshold
@@ -171,6 +200,26 @@ def _all_gather_var(dist, t, group, torch):
     return torch.cat([o[:s] for o, s in zip(outs, sizes)]), sizes
 
 
+def _all_gather_v(dist, t, group, torch):
+    """all_gather of tensors whose first dimension differs per rank without
+    padding: every rank sends its whole tensor to every rank through one
+    all-to-all (NCCL's all-gather-v); gloo groups fall back to the padded form."""
+    world = dist.get_world_size(group)
+    if world == 1:
+        return t, [t.shape[0]]
+    if _host_collectives(dist, group, t.device):
+        return _all_gather_var(dist, t, group, torch)
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    flat = t.reshape(t.shape[0], -1)
+    out = torch.empty((sum(sizes), flat.shape[1]), dtype=t.dtype, device=t.device)
+    send = flat.repeat(world, 1) if t.shape[0] else flat
+    dist.all_to_all_single(out, send, [s for s in sizes], [t.shape[0]] * world, group=group)
+    return out.reshape((sum(sizes),) + tuple(t.shape[1:])), sizes
+
+
 def _events(torch, dev, timings):
     if timings is None or dev.type != "cuda":
         return None
@@ -219,30 +268,51 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists",
     # 2. K1 on the shard
     sig, band = stages.signatures(data, offsets, fam, b, config.rows, K)
     # 3. records -> owners
-    keys, vals = stages.cell_records(band, b, K, doc_base)
-    first = cell_partition(b, K, world)
-    bounds = torch.tensor(first[1:-1], dtype=torch.int64, device=dev)
-    splits = torch.searchsorted(keys.to(torch.int64), bounds) if world > 1 else \
-        torch.zeros(0, dtype=torch.int64, device=dev)
-    edges = [0] + [int(x) for x in splits.tolist()] + [keys.shape[0]]
-    send = [edges[i + 1] - edges[i] for i in range(world)]
+    packed = getattr(stages, "packed_capable", False) and os.environ.get("ND_PEER_SIGS", "1") != "0"
+    ev = _events(torch, dev, timings)
+    if packed:
+        # one u64 per (cell, row), sorted by cell, owner splits from the device
+        rec, split = stages.records_packed(band, b, K, doc_base, world)
+        send = [split[i + 1] - split[i] for i in range(world)]
+    else:
+        keys, vals = stages.cell_records(band, b, K, doc_base)
+        first = cell_partition(b, K, world)
+        bounds = torch.tensor(first[1:-1], dtype=torch.int64, device=dev)
+        splits = torch.searchsorted(keys.to(torch.int64), bounds) if world > 1 else \
+            torch.zeros(0, dtype=torch.int64, device=dev)
+        edges = [0] + [int(x) for x in splits.tolist()] + [keys.shape[0]]
+        send = [edges[i + 1] - edges[i] for i in range(world)]
     send_t = torch.tensor(send, dtype=torch.int64, device=cdev)
     recv_t = torch.empty_like(send_t)
     dist.all_to_all_single(recv_t, send_t, group=group)
     recv = [int(x) for x in recv_t.tolist()]
-    rkeys = torch.empty(sum(recv), dtype=keys.dtype, device=cdev)
-    rvals = torch.empty(sum(recv), dtype=vals.dtype, device=cdev)
-    ev = _events(torch, dev, timings)
     if ev:
         ev[0].record()
-    dist.all_to_all_single(rkeys, keys.to(cdev), recv, send, group=group)
-    dist.all_to_all_single(rvals, vals.to(cdev), recv, send, group=group)
+    if packed:
+        rrec = torch.empty(sum(recv), dtype=torch.int64, device=cdev)
+        dist.all_to_all_single(rrec, rec.to(cdev), recv, send, group=group)
+        rec_bytes = 8
+    else:
+        rkeys = torch.empty(sum(recv), dtype=keys.dtype, device=cdev)
+        rvals = torch.empty(sum(recv), dtype=vals.dtype, device=cdev)
+        dist.all_to_all_single(rkeys, keys.to(cdev), recv, send, group=group)
+        dist.all_to_all_single(rvals, vals.to(cdev), recv, send, group=group)
+        rec_bytes = keys.element_size() + vals.element_size()
     if ev:
         ev[1].record()
-    rkeys, rvals = rkeys.to(dev), rvals.to(dev)
-    rec_bytes = keys.element_size() + vals.element_size()
     thr = _ratio(config.threshold)
-    if getattr(stages, "peer_capable", False) and os.environ.get("ND_PEER_SIGS", "1") != "0":
+    if packed:
+        h = torch.tensor(list(stages.export_rows(sig)), dtype=torch.uint8, device=cdev)
+        hs = [torch.empty_like(h) for _ in range(world)]
+        dist.all_gather(hs, h, group=group)
+        handles = b"".join(bytes(x.cpu().tolist()) for x in hs)
+        row_base = [sum(counts[:r]) for r in range(world + 1)]
+        stages.open_peers(handles, row_base, world, rank)
+        lo, hi, m, cand_local = stages.compare_peer_packed(rrec.to(dev), b * K, thr)
+        dist.barrier(group=group)
+        stages.close_peers()
+    elif getattr(stages, "peer_capable", False) and os.environ.get("ND_PEER_SIGS", "1") != "0":
+        rkeys, rvals = rkeys.to(dev), rvals.to(dev)
         # 4+5. compare the owned cells reading every rank's rows in peer memory:
         # exchange IPC handles, map, compare, and keep the rows alive until
         # every rank is done (barrier)
@@ -256,6 +326,7 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists",
         dist.barrier(group=group)
         stages.close_peers()
     else:
+        rkeys, rvals = rkeys.to(dev), rvals.to(dev)
         # 4. all signature rows on every rank
         sig_all, _ = _all_gather_var(dist, sig, group, torch)
         # 5. compare the owned cells
@@ -269,7 +340,7 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists",
     trip = torch.stack([lo, hi, m], dim=1) if lo.numel() else torch.zeros((0, 3), dtype=lo.dtype, device=dev)
     if ev:
         ev[2].record()
-    all_trip, _ = _all_gather_var(dist, trip, group, torch)
+    all_trip, _ = _all_gather_v(dist, trip, group, torch)
     if ev:
         ev[3].record()
         torch.cuda.synchronize(dev)
