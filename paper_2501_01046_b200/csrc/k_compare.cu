@@ -399,6 +399,22 @@ __device__ __forceinline__ bool same_block(const uint32_t* __restrict__ a,
   return eq;
 }
 
+// Block fingerprints of every signature row, computed once per compare:
+// fps[row * NB + k] = block_fp of block k.  The join then reads 4 bytes per
+// (document, cell, block) instead of the block's BW values -- each document is
+// in one cell per band, so its row would otherwise be gathered b times.
+template <int BW>
+__global__ void k_block_fps(const uint32_t* __restrict__ sig, uint64_t nrows, uint32_t H,
+                            uint32_t NB, uint32_t* __restrict__ fps) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nrows * NB) return;
+  const uint64_t row = i / NB;
+  const uint32_t k = static_cast<uint32_t>(i % NB);
+  uint32_t v[BW];
+  load_block<BW>(sig + row * H + static_cast<uint64_t>(k) * BW, (H & 3) == 0, v);
+  fps[i] = block_fp<BW>(v);
+}
+
 // Pairs of one cell already handled at an earlier block (open addressing over
 // (d << 12 | e) + 1, d < e < kJoinMax).  A near-duplicate pair shares almost
 // every block, so it is rediscovered in almost every block's chains; the set
@@ -471,7 +487,8 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
                   uint32_t join_max, uint32_t tbits, uint32_t sbits, uint32_t NB,
                   uint32_t min_match, int nb, uint64_t* __restrict__ out_key,
                   uint32_t* __restrict__ out_m, unsigned long long* __restrict__ count,
-                  uint64_t cap, bool two_barriers, uint32_t qcap) {
+                  uint64_t cap, bool two_barriers, uint32_t qcap,
+                  const uint32_t* __restrict__ fps) {
   // VL values per document and group of BPL = VL / BW blocks: one 32-byte
   // sector (a 16-byte load would still move a whole sector), or 64 bytes
   // for the big-cell variant
@@ -521,12 +538,23 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
   for (uint32_t k0 = 0; k0 < NB; k0 += BPL) {
     // fingerprints of blocks k0 .. k0+BPL-1 of this thread's documents
     uint32_t fp[DPT][BPL];
+    if (fps) {  // from the precomputed table (k_block_fps): 4 bytes per block
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) {
+        const uint32_t d = threadIdx.x + j * TPB;
+        if (d < n) {
+          const uint32_t* f = fps + static_cast<uint64_t>(rowsm[d]) * NB + k0;
+#pragma unroll
+          for (int b = 0; b < BPL; ++b) fp[j][b] = k0 + b < NB ? __ldg(f + b) : 0u;
+        }
+      }
+    }
     const uint32_t p0 = k0 * BW;
     const bool full = vec && p0 + VL <= H;
 #pragma unroll
     for (int j = 0; j < DPT; ++j) {
       const uint32_t d = threadIdx.x + j * TPB;
-      if (d < n) {
+      if (!fps && d < n) {
         const uint32_t* r = sv.row(rowsm[d]) + p0;
         uint32_t v[VL];
         if (full) {
@@ -626,7 +654,7 @@ int compare_prefilter_width(uint32_t H, uint32_t min_match) {
 
 void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_match,
                     int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,
-                    uint64_t cap, cudaStream_t s) {
+                    uint64_t cap, cudaStream_t s, uint64_t nrows) {
   if (cs.ncells == 0 || min_match > H) return;
   // cells of <= kJoinMax documents: hash join (one CTA per cell)
   const uint32_t P = H - min_match + 1;
@@ -677,7 +705,21 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
       using JoinBFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                                const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
                                int, uint64_t*, uint32_t*, unsigned long long*, uint64_t, bool,
-                               uint32_t);
+                               uint32_t, const uint32_t*);
+      // block fingerprints of every row, once (one-table views; the peer
+      // views of the multi-GPU paths read the blocks in place)
+      const uint32_t* fps = nullptr;
+      const char* jf = getenv("ND_JOIN_FPS");  // 0: fingerprints from the rows in the join
+      if (!(jf && jf[0] == '0') && d_sig.world <= 1 && nrows > 0 && nrows * NB < (1ull << 40)) {
+        uint32_t* f = cs.fps.as<uint32_t>(nrows * NB);
+        const uint64_t total = nrows * NB;
+        const unsigned blocks = static_cast<unsigned>((total + 255) / 256);
+        if (BW == 2) k_block_fps<2><<<blocks, 256, 0, s>>>(d_sig.base0, nrows, H, NB, f);
+        else if (BW == 4) k_block_fps<4><<<blocks, 256, 0, s>>>(d_sig.base0, nrows, H, NB, f);
+        else k_block_fps<8><<<blocks, 256, 0, s>>>(d_sig.base0, nrows, H, NB, f);
+        ND_CHECK_LAUNCH();
+        fps = f;
+      }
       // 512 threads per CTA for cells above 1024 documents: -33 % K3 time on
       // C3-sized cells; smaller cells are faster with 256
       const int tpb = join_max > 1024 ? 512 : 256;
@@ -695,7 +737,7 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
                                      static_cast<int>(smem_b)));
       fn<<<grid, tpb, smem_b, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
                                    join_max, tbits, sbits, NB, min_match, nb, out_key, out_m,
-                                   count, cap, two_barriers, qcap);
+                                   count, cap, two_barriers, qcap, fps);
       ND_CHECK_LAUNCH();
     } else {
       using JoinFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,

@@ -89,7 +89,7 @@ void compare_pairs(DedupState& st, const SigView& d_sig, uint32_t H, uint32_t mm
     ps.keys = ps.dkeys.as<uint64_t>(ps.cap);
     ps.vals = ps.dvals.as<uint32_t>(ps.cap);
     ND_CUDA(cudaMemsetAsync(ps.counter, 0, sizeof(unsigned long long), s));
-    launch_compare(st.cells, d_sig, H, mm, ps.nb, ps.keys, ps.vals, ps.counter, ps.cap, s);
+    launch_compare(st.cells, d_sig, H, mm, ps.nb, ps.keys, ps.vals, ps.counter, ps.cap, s, nrows);
     unsigned long long got = 0;
     ND_CUDA(cudaMemcpyAsync(&got, ps.counter, sizeof got, cudaMemcpyDeviceToHost, s));
     ND_CUDA(cudaStreamSynchronize(s));

@@ -167,7 +167,7 @@ constexpr uint32_t kJoinMax = 4096;  // largest cell the hash join (k_join) take
 constexpr uint32_t kJoinMaxP = 510;  // largest H - min_matches + 1 the joins' 9-bit tags take
 struct CellSet {
   DevBuf rec_keys, rec_vals, flag, run_idx, run_start, cstart, clen, ckey, cpairs, ctiles, pair_off,
-      ioff, icell, scan, maxbuf;
+      ioff, icell, scan, maxbuf, fps;
   bool join_enabled = true;     // cells <= kJoinMax use the hash join
   uint64_t max_len = 0;         // largest non-singleton cell
   SortScratch sort;
@@ -182,7 +182,7 @@ struct CellSet {
   uint32_t* item_cell = nullptr;          // per item: its cell
   void release() {
     for (DevBuf* b : {&rec_keys, &rec_vals, &flag, &run_idx, &run_start, &cstart, &clen, &ckey,
-                      &cpairs, &ctiles, &pair_off, &ioff, &icell, &scan, &maxbuf})
+                      &cpairs, &ctiles, &pair_off, &ioff, &icell, &scan, &maxbuf, &fps})
       b->release();
     sort.release();
   }
@@ -235,9 +235,10 @@ struct SigView {
     return bases[r] + (static_cast<uint64_t>(g) - row_base[r]) * H;
   }
 };
+// nrows: rows of d_sig (block fingerprints are precomputed for a one-table view)
 void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_match,
                     int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,
-                    uint64_t cap, cudaStream_t s);
+                    uint64_t cap, cudaStream_t s, uint64_t nrows = 0);
 uint64_t unique_pairs(PairSet& ps, cudaStream_t s);
 // packs (lo, hi, m) triples (lo < hi not required) into ps.keys/ps.vals
 void pack_pairs(PairSet& ps, const uint32_t* lo, const uint32_t* hi, const uint32_t* m,
