@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
                   uint32_t min_match, int nb, uint64_t* __restrict__ out_key,
                   uint32_t* __restrict__ out_m, unsigned long long* __restrict__ count,
                   uint64_t cap, bool two_barriers, uint32_t qcap,
-                  const uint32_t* __restrict__ fps) {
+                  const uint32_t* __restrict__ fps, bool exch) {
   // VL values per document and group of BPL = VL / BW blocks: one 32-byte
   // sector (a 16-byte load would still move a whole sector), or 64 bytes
   // for the big-cell variant
@@ -582,17 +582,24 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
       for (int j = 0; j < DPT; ++j) {
         const uint32_t d = threadIdx.x + j * TPB;
         if (d >= n) continue;  // (not break: keeps fp[][] in registers)
-        const uint32_t key = (tag << 23) | fp[j][b];
         uint32_t h = (fp[j][b] * 0x9E3779B1u) >> (32 - tbits);
-        for (;;) {
-          const uint32_t cur = keys[h];
-          if (cur == key) break;
-          if ((cur >> 23) == tag) {  // another fingerprint of this block: probe on
-            h = (h + 1) & mask;
-            continue;
+        if (exch) {
+          // one chain per slot, whatever the fingerprint: the walk skips the
+          // chained documents whose fingerprint differs (kept in fpk, which
+          // reuses the key table's words: T >= 2 * join_max)
+          keys[(k & 1) * join_max + d] = fp[j][b];
+        } else {
+          const uint32_t key = (tag << 23) | fp[j][b];
+          for (;;) {
+            const uint32_t cur = keys[h];
+            if (cur == key) break;
+            if ((cur >> 23) == tag) {  // another fingerprint of this block: probe on
+              h = (h + 1) & mask;
+              continue;
+            }
+            const uint32_t old = atomicCAS(&keys[h], cur, key);
+            if (old == cur || old == key) break;
           }
-          const uint32_t old = atomicCAS(&keys[h], cur, key);
-          if (old == cur || old == key) break;
         }
         const uint32_t prev = atomicExch(&head[h], (tag << 16) | d);
         next[d] = (prev >> 16) == tag ? static_cast<uint16_t>(prev) : uint16_t{0xFFFF};
@@ -606,9 +613,11 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
       const bool defer =
           qcap && kblock > 0 && *static_cast<volatile uint32_t*>(&qn[(kblock + 2) % 3]) >= kDeferMin;
       ++kblock;
+      const uint32_t* fpk = keys + (k & 1) * join_max;
       if (defer) {
         for (uint32_t d = threadIdx.x; d < n; d += TPB)
           for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e]) {
+            if (exch && fpk[e] != fpk[d]) continue;
             if (exact_set && pset_has(pset, S - 1, ((min(d, e) << 12) | max(d, e)) + 1u)) continue;
             const uint32_t slot = atomicAdd(q, 1u);
             if (slot < qcap)
@@ -627,6 +636,7 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
       } else {
         for (uint32_t d = threadIdx.x; d < n; d += TPB)
           for (uint32_t e = next[d]; e != 0xFFFFu; e = next[e]) {
+            if (exch && fpk[e] != fpk[d]) continue;
             if (exact_set && pset_has(pset, S - 1, ((min(d, e) << 12) | max(d, e)) + 1u)) continue;
             if (qcap) atomicAdd(q, 1u);  // count: does the next block defer?
             join_check_blocks<BW>(sv, H, d, e, rowsm, k, vec, pset, S - 1, &pset_full, exact_set,
@@ -697,6 +707,10 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
     const size_t smem_b = (2u * (1u << tbits) + (sbits ? 1u << sbits : 1u)) * sizeof(uint32_t) +
                           join_max * (sizeof(uint32_t) + 2 * sizeof(uint16_t)) +
                           (qcap ? 8 + qcap * sizeof(uint2) : 0);
+    // one chain per table slot, no key CAS loop (ND_JOIN_EXCH=0: the keyed
+    // table with probing); -20..-29 % K3 (profiles/r2_k3_defer.txt)
+    const char* je = getenv("ND_JOIN_EXCH");
+    const bool exch = !(je && je[0] == '0') && (1u << tbits) >= 2 * join_max;
     const char* tb = getenv("ND_JOIN_TWO_BARRIERS");  // 1: the barrier after each walk too
     const bool two_barriers = tb && tb[0] == '1';
     if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
@@ -705,7 +719,7 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
       using JoinBFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                                const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
                                int, uint64_t*, uint32_t*, unsigned long long*, uint64_t, bool,
-                               uint32_t, const uint32_t*);
+                               uint32_t, const uint32_t*, bool);
       // block fingerprints of every row, once (one-table views; the peer
       // views of the multi-GPU paths read the blocks in place)
       const uint32_t* fps = nullptr;
@@ -737,7 +751,7 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
                                      static_cast<int>(smem_b)));
       fn<<<grid, tpb, smem_b, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
                                    join_max, tbits, sbits, NB, min_match, nb, out_key, out_m,
-                                   count, cap, two_barriers, qcap, fps);
+                                   count, cap, two_barriers, qcap, fps, exch);
       ND_CHECK_LAUNCH();
     } else {
       using JoinFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
