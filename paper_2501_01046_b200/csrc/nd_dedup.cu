@@ -242,7 +242,8 @@ uint64_t hbm_budget_of(nd_ctx* ctx) {
 // alternates and the cell CSR (the same estimate as the staged compare's
 // interval plan, nd_stages.cu).
 constexpr uint64_t kRecBytes = 8 * 4;
-uint64_t row_bytes_of(const nd_params& p) { return 4ull * p.hash_count + 4ull * p.bands + 8; }
+// (+ 4H: K3's block-fingerprint table, at most one u32 per signature value)
+uint64_t row_bytes_of(const nd_params& p) { return 8ull * p.hash_count + 4ull * p.bands + 8; }
 
 // Out-of-core in-memory dedup (plan_gather's idea, sigstore.cpp:288-329,
 // applied to HBM instead of host RAM): when the signatures and cell records of
