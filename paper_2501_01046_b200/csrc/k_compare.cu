@@ -504,8 +504,11 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
   if (n > join_max) return;  // big cells go to k_compare
   const uint32_t T = 1u << tbits;
   const uint32_t S = 1u << sbits;
-  uint32_t* keys = jsm;                // T   (tag << 23 | fingerprint), tag 0 = empty
-  uint32_t* head = keys + T;           // T   (tag << 16 | doc)
+  // keyed table: T keys (tag << 23 | fingerprint, tag 0 = empty); one chain
+  // per slot (exch): the documents' fingerprints, double-buffered by parity
+  const uint32_t KW = exch ? 2 * join_max : T;
+  uint32_t* keys = jsm;                // KW
+  uint32_t* head = keys + KW;          // T   (tag << 16 | doc)
   uint32_t* pset = head + T;           // S   handled pairs (pset_has / pset_add)
   uint32_t* rowsm = pset + S;          // join_max
   // chain links, double-buffered by block parity: the walk of block k reads
@@ -522,10 +525,8 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
       (reinterpret_cast<uintptr_t>(next2 + 2 * join_max) + 7) & ~uintptr_t{7});
   const uint64_t s = cell_start[blockIdx.x];
   for (uint32_t i = threadIdx.x; i < n; i += TPB) rowsm[i] = rows[s + i];
-  for (uint32_t i = threadIdx.x; i < T; i += TPB) {
-    keys[i] = 0;
-    head[i] = 0;
-  }
+  for (uint32_t i = threadIdx.x; i < KW; i += TPB) keys[i] = 0;
+  for (uint32_t i = threadIdx.x; i < T; i += TPB) head[i] = 0;
   for (uint32_t i = threadIdx.x; i < S; i += TPB) pset[i] = 0;
   if (threadIdx.x == 0) {
     pset_full = 0;
@@ -585,8 +586,7 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
         uint32_t h = (fp[j][b] * 0x9E3779B1u) >> (32 - tbits);
         if (exch) {
           // one chain per slot, whatever the fingerprint: the walk skips the
-          // chained documents whose fingerprint differs (kept in fpk, which
-          // reuses the key table's words: T >= 2 * join_max)
+          // chained documents whose fingerprint differs (kept in fpk)
           keys[(k & 1) * join_max + d] = fp[j][b];
         } else {
           const uint32_t key = (tag << 23) | fp[j][b];
@@ -684,10 +684,23 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
     }
   if (cs.join_enabled && join_max >= 2 && P <= kJoinMaxP) {
     // table slots >= n / load; the default load 1/2 (ND_JOIN_LOAD = percent)
-    const char* jl = getenv("ND_JOIN_LOAD");
+    // one chain per table slot, no key CAS loop (ND_JOIN_EXCH=0: the keyed
+    // table with probing); -20..-29 % K3 (profiles/r2_k3_defer.txt).  Its
+    // table may be fuller (a shared slot only lengthens a chain):
+    // ND_JOIN_EXCH_LOAD percent, default 50 (100 / 200 measured 5 / 19 % slower)
+    const char* je = getenv("ND_JOIN_EXCH");
+    const bool exch = !(je && je[0] == '0');
+    const char* jl = getenv("ND_JOIN_LOAD");  // keyed tables (k_join, keyed block join)
     const uint32_t load_pct = jl ? static_cast<uint32_t>(std::max(10, std::min(95, atoi(jl)))) : 50;
     uint32_t tbits = 4;
     while ((1ull << tbits) * load_pct < 100ull * join_max) ++tbits;
+    uint32_t tbits_b = tbits;  // block join's table
+    if (exch) {
+      const char* xl = getenv("ND_JOIN_EXCH_LOAD");
+      const uint32_t xpct = xl ? static_cast<uint32_t>(std::max(10, std::min(400, atoi(xl)))) : 50;
+      tbits_b = 4;
+      while ((1ull << tbits_b) * xpct < 100ull * join_max) ++tbits_b;
+    }
     // handled-pair set of the block join: 2^sbits >= join_max / 2 slots
     // (overflow only costs the HBM checks of earlier blocks)
     const char* sd = getenv("ND_JOIN_PSET_DIV");  // tuning: slots >= join_max / div
@@ -704,13 +717,10 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
     // at 128 entries; profiles/r2_k3_defer.txt)
     const char* jd = getenv("ND_JOIN_DEFER");
     const uint32_t qcap = jd ? static_cast<uint32_t>(std::max(0, atoi(jd))) : 0u;
-    const size_t smem_b = (2u * (1u << tbits) + (sbits ? 1u << sbits : 1u)) * sizeof(uint32_t) +
+    const size_t smem_b = ((exch ? 2u * join_max : (1u << tbits_b)) + (1u << tbits_b) +
+                           (sbits ? 1u << sbits : 1u)) * sizeof(uint32_t) +
                           join_max * (sizeof(uint32_t) + 2 * sizeof(uint16_t)) +
                           (qcap ? 8 + qcap * sizeof(uint2) : 0);
-    // one chain per table slot, no key CAS loop (ND_JOIN_EXCH=0: the keyed
-    // table with probing); -20..-29 % K3 (profiles/r2_k3_defer.txt)
-    const char* je = getenv("ND_JOIN_EXCH");
-    const bool exch = !(je && je[0] == '0') && (1u << tbits) >= 2 * join_max;
     const char* tb = getenv("ND_JOIN_TWO_BARRIERS");  // 1: the barrier after each walk too
     const bool two_barriers = tb && tb[0] == '1';
     if (cs.ncells > 0x7FFFFFFFull) fail(ND_ERR_CONFIG, "too many cells");
@@ -750,7 +760,7 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
         ND_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem_b)));
       fn<<<grid, tpb, smem_b, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
-                                   join_max, tbits, sbits, NB, min_match, nb, out_key, out_m,
+                                   join_max, tbits_b, sbits, NB, min_match, nb, out_key, out_m,
                                    count, cap, two_barriers, qcap, fps, exch);
       ND_CHECK_LAUNCH();
     } else {
