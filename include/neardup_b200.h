@@ -143,6 +143,11 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t hash_count,
  * (exact 64-bit Barrett); when K1j was eligible but could not be compiled the
  * reason follows after ": ". */
 const char* nd_k1_kernel(nd_ctx* ctx);
+/* The CUDA source K1j compiles for a family (no device needed): writes up to
+ * cap bytes (NUL-terminated) into out and returns the full length, or -1
+ * when the family is outside K1j's domain. */
+int64_t nd_k1j_source(const nd_hash_fn* fns, uint32_t hash_count, uint32_t shingle_len, char* out,
+                      uint64_t cap);
 
 /* signature_of_document over a packed batch + band_bucket_ids
  * (minhash.hpp:71-78, lsh.hpp:38-40; caller pipeline.cpp:214-218).

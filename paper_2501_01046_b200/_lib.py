@@ -108,6 +108,8 @@ SIGNATURES = {
     "nd_ctx_set_stream": (C.c_int, [vp, vp]),
     "nd_family_upload": (C.c_int, [vp, C.POINTER(NdHashFn), C.c_uint32, C.c_uint32, C.c_uint32]),
     "nd_k1_kernel": (C.c_char_p, [vp]),
+    "nd_k1j_source": (C.c_int64, [C.POINTER(NdHashFn), C.c_uint32, C.c_uint32, C.c_char_p,
+                                  C.c_uint64]),
     "nd_signatures": (C.c_int, [vp, u8p, u64p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                 u32p, u32p]),
     "nd_signatures_h2d": (C.c_int, [vp, u8p, u64p, C.c_uint64, C.c_uint32, C.c_uint32,

@@ -415,3 +415,19 @@ std::string k1_jit_source(const nd_hash_fn* fns, uint32_t H, uint32_t L) {
 }
 
 }  // namespace ndb
+
+extern "C" int64_t nd_k1j_source(const nd_hash_fn* fns, uint32_t H, uint32_t L, char* out,
+                                 uint64_t cap) {
+  if (!fns || H == 0 || H > 1024 || L == 0 || L > 16) return -1;
+  for (uint32_t i = 0; i < H; ++i)  // the fq domain (derive_family's)
+    if (fns[i].modulus < (1u << 21) || fns[i].modulus >= (1u << 23) || fns[i].base == 0 ||
+        fns[i].base >= (1u << 16))
+      return -1;
+  const std::string s = ndb::k1_jit_source(fns, H, L);
+  if (out && cap) {
+    const uint64_t n = std::min<uint64_t>(cap - 1, s.size());
+    std::memcpy(out, s.data(), n);
+    out[n] = '\0';
+  }
+  return static_cast<int64_t>(s.size());
+}
