@@ -43,15 +43,15 @@ struct nd_ctx {
   // the group's own fields serve single-device calls on its first device
   std::vector<nd_ctx*> shards;
   struct Multi {                // per-shard exchange buffers (nd_multi.cu)
-    ndb::DevBuf send_keys, send_vals, first_cell, split, bases, row_base, pair_lo, pair_hi,
-        pair_m;
+    ndb::DevBuf send_keys, send_vals, first_cell, split, bases, row_bases, row_base, pair_lo,
+        pair_hi, pair_m;
     ndb::SortScratch sort;
     ndb::PairSet final_pairs;
     std::vector<uint64_t> ranges;  // group: document range of each shard, last dedup
     bool last_valid = false;
     void release() {
-      for (auto* b : {&send_keys, &send_vals, &first_cell, &split, &bases, &row_base, &pair_lo,
-                      &pair_hi, &pair_m})
+      for (auto* b : {&send_keys, &send_vals, &first_cell, &split, &bases, &row_bases, &row_base,
+                      &pair_lo, &pair_hi, &pair_m})
         b->release();
       sort.release();
       final_pairs.release();

@@ -5,16 +5,19 @@
 //
 // nd_dedup on a group context:
 //   A. every shard signs a contiguous, byte-balanced range of the batch (its
-//      own H2D ring + K1, K from the GLOBAL document count, pipeline.cpp:300),
-//      emits (cell, global row) records and stably radix-sorts them by cell;
-//      the cell owner is floor(cell * G / (bands * K)) (nd_cell_partition),
-//      so each shard's sorted records split into G contiguous runs;
-//   B. all-to-all over NVLink/NVSwitch: shard d pulls run d of every source
-//      s with peer copies (cudaMemcpyPeerAsync, source order s = 0..G-1, so
-//      each cell's rows stay ascending as scan_gather requires,
-//      sigstore.cpp:259-262), builds its cells (K2) and compares them (K3)
-//      reading every signature row in place from the owning GPU's HBM through
-//      a SigView over the G shards' row arrays;
+//      own H2D ring + K1, K from the GLOBAL document count, pipeline.cpp:300)
+//      and stably partitions its (document, band) records by owner -- one
+//      radix digit; the cell owner is floor(cell * G / (bands * K)), the
+//      inverse of nd_cell_partition;
+//   B. the all-to-all is fused into that partition's scatter: each record is
+//      formed from its band id and stored straight into its owner's receive
+//      buffer (peer stores over NVLink/NVSwitch), at the owner's offset for
+//      the source -- source order s = 0..G-1, then document order, so each
+//      cell's rows stay ascending as scan_gather requires
+//      (sigstore.cpp:259-262).  Each owner then builds its cells (K2, the
+//      only full sort of the records) and compares them (K3) reading every
+//      signature row in place from the GPU that computed it, through a
+//      SigView over the G shards' row arrays;
 //   C. the shards' distinct pairs are gathered on shard 0 over peer copies,
 //      sorted + uniqued once more and clustered (K4).
 // Outputs are identical for any shard count (the union of pairs is
@@ -47,6 +50,44 @@ __global__ void k_owner_splits(const uint32_t* __restrict__ keys, uint64_t m,
     if (keys[mid] < target) lo = mid + 1; else hi = mid;
   }
   split[g] = lo;
+}
+
+// owner of each (document, band) record, and its index: the key/value pair of
+// the one-digit stable partition by owner.  owner(cell) = floor(cell * G /
+// cells) is the inverse of nd_cell_partition's first_cell = ceil(cells * o / G)
+__global__ void k_owner_keys(const uint32_t* __restrict__ band, uint64_t m, uint32_t bands,
+                             uint32_t K, uint64_t cells, uint32_t G, uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t cell = static_cast<uint64_t>(i % bands) * K + band[i];
+    keys[i] = static_cast<uint32_t>(cell * G / cells);
+    vals[i] = static_cast<uint32_t>(i);
+  }
+}
+
+// The exchange itself, fused into the partition's scatter: record p of the
+// owner-sorted order goes straight into its owner's receive buffer (a peer
+// store over NVLink when the owner is another GPU), at the owner's offset
+// for this source plus the record's rank among this source's records for
+// that owner -- source order, then document order, as scan_gather's rows.
+struct OwnerDst {
+  uint32_t* keys[64];
+  uint32_t* vals[64];
+  uint64_t base[64];   // this source's first slot in each owner's buffer
+  uint64_t start[65];  // where each owner's run starts in the sorted order
+};
+__global__ void k_scatter_owners(const uint32_t* __restrict__ okeys,
+                                 const uint32_t* __restrict__ oidx, uint64_t m,
+                                 const uint32_t* __restrict__ band, uint32_t bands, uint32_t K,
+                                 uint32_t doc_base, const OwnerDst* __restrict__ dst) {
+  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t o = okeys[p], i = oidx[p];
+    const uint64_t q = dst->base[o] + (p - dst->start[o]);
+    dst->keys[o][q] = (i % bands) * K + band[i];
+    dst->vals[o][q] = doc_base + i / bands;
+  }
 }
 
 // runs fn(shard index) on one host thread per shard; rethrows the first error
@@ -157,14 +198,21 @@ void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
     if (m) h2d_signatures(c, st, bytes, offsets + d0, m, B, p.rows, K, sig, band);
     ND_CUDA(cudaStreamSynchronize(cs));
     t_k1[s] = since(t0);
+    // one-digit stable partition of the records by owner (their cell order
+    // is the owner's business): keys = owner, values = record index
     const uint64_t recs = m * B;
     uint32_t* keys = c->multi.send_keys.as<uint32_t>(recs + 1);
     uint32_t* vals = c->multi.send_vals.as<uint32_t>(recs + 1);
-    make_records(band, m, B, K, static_cast<uint32_t>(d0), keys, vals, cs);
-    radix_sort_u32(keys, vals, recs, bits_for(cells_total - 1), c->multi.sort, cs);
+    if (recs) {
+      k_owner_keys<<<4 * sm_count(), 256, 0, cs>>>(band, recs, B, K, cells_total, G, keys, vals);
+      ND_CHECK_LAUNCH();
+      radix_sort_u32(keys, vals, recs, std::max(1, bits_for(G - 1)), c->multi.sort, cs);
+    }
+    std::vector<uint64_t> owner_ids(G + 1);
+    for (uint32_t o = 0; o <= G; ++o) owner_ids[o] = o;
     uint64_t* d_fc = c->multi.first_cell.as<uint64_t>(G + 1);
     uint64_t* d_split = c->multi.split.as<uint64_t>(G + 1);
-    ND_CUDA(cudaMemcpyAsync(d_fc, first_cell.data(), (G + 1) * 8, cudaMemcpyHostToDevice, cs));
+    ND_CUDA(cudaMemcpyAsync(d_fc, owner_ids.data(), (G + 1) * 8, cudaMemcpyHostToDevice, cs));
     k_owner_splits<<<1, 64 * ((G + 64) / 64), 0, cs>>>(keys, recs, d_fc, G, d_split);
     ND_CHECK_LAUNCH();
     ND_CUDA(cudaMemcpyAsync(split[s].data(), d_split, (G + 1) * 8, cudaMemcpyDeviceToHost, cs));
@@ -174,7 +222,7 @@ void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
   });
   const double sec_a = since(ta);
 
-  // ---- B: all-to-all of records over peer copies, K2 + K3 per owner ---------
+  // ---- B: receive buffers, the fused exchange, K2 + K3 per owner -------------
   std::vector<const uint32_t*> bases(G);
   std::vector<uint64_t> row_base(G + 1);
   for (uint32_t s = 0; s < G; ++s) {
@@ -182,29 +230,52 @@ void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
     row_base[s] = r[s];
   }
   row_base[G] = n;
+  // owner o receives source s's run at recv_base[s][o] (source order)
+  std::vector<std::vector<uint64_t>> recv_base(G, std::vector<uint64_t>(G, 0));
+  std::vector<uint64_t> recv_total(G, 0);
+  for (uint32_t o = 0; o < G; ++o)
+    for (uint32_t s = 0; s < G; ++s) {
+      recv_base[s][o] = recv_total[o];
+      recv_total[o] += split[s][o + 1] - split[s][o];
+    }
+  std::vector<uint32_t*> rkeys(G), rvals(G);
+  run_shards(g, [&](uint32_t d) {  // allocate on the owner's device
+    CellSet& cs = g->shards[d]->dedup.cells;
+    rkeys[d] = cs.rec_keys.as<uint32_t>(recv_total[d] + 1);
+    rvals[d] = cs.rec_vals.as<uint32_t>(recv_total[d] + 1);
+  });
   auto tb = std::chrono::steady_clock::now();
+  run_shards(g, [&](uint32_t s) {  // every source scatters into every owner
+    nd_ctx* c = g->shards[s];
+    cudaStream_t cs = c->stream;
+    const uint64_t recs = (r[s + 1] - r[s]) * B;
+    if (!recs) return;
+    OwnerDst h{};
+    for (uint32_t o = 0; o < G; ++o) {
+      h.keys[o] = rkeys[o];
+      h.vals[o] = rvals[o];
+      h.base[o] = recv_base[s][o];
+    }
+    for (uint32_t o = 0; o <= G; ++o) h.start[o] = split[s][o];
+    OwnerDst* d_h = reinterpret_cast<OwnerDst*>(c->multi.bases.as<uint8_t>(sizeof(OwnerDst)));
+    ND_CUDA(cudaMemcpyAsync(d_h, &h, sizeof h, cudaMemcpyHostToDevice, cs));
+    k_scatter_owners<<<4 * sm_count(), 256, 0, cs>>>(
+        static_cast<const uint32_t*>(c->multi.send_keys.ptr),
+        static_cast<const uint32_t*>(c->multi.send_vals.ptr), recs,
+        static_cast<const uint32_t*>(c->dedup.band.ptr), B, K, static_cast<uint32_t>(r[s]), d_h);
+    ND_CHECK_LAUNCH();
+    ND_CUDA(cudaStreamSynchronize(cs));  // the peer stores have landed
+  });
   run_shards(g, [&](uint32_t d) {
     nd_ctx* c = g->shards[d];
     auto t0 = std::chrono::steady_clock::now();
     DedupState& st = c->dedup;
     cudaStream_t cs = c->stream;
-    uint64_t m = 0;
-    for (uint32_t s = 0; s < G; ++s) m += split[s][d + 1] - split[s][d];
-    uint32_t* rk = st.cells.rec_keys.as<uint32_t>(m + 1);
-    uint32_t* rv = st.cells.rec_vals.as<uint32_t>(m + 1);
-    uint64_t at = 0;
-    for (uint32_t s = 0; s < G; ++s) {  // source order: rows ascend within every cell
-      const uint64_t a = split[s][d], cnt = split[s][d + 1] - a;
-      if (!cnt) continue;
-      nd_ctx* src = g->shards[s];
-      ND_CUDA(cudaMemcpyPeerAsync(rk + at, c->device, static_cast<const uint32_t*>(src->multi.send_keys.ptr) + a,
-                                  src->device, cnt * 4, cs));
-      ND_CUDA(cudaMemcpyPeerAsync(rv + at, c->device, static_cast<const uint32_t*>(src->multi.send_vals.ptr) + a,
-                                  src->device, cnt * 4, cs));
-      at += cnt;
-    }
+    const uint64_t m = recv_total[d];
+    uint32_t* rk = rkeys[d];
+    uint32_t* rv = rvals[d];
     // every shard's signature rows, read in place (peer memory over NVLink)
-    auto** d_bases = c->multi.bases.as<const uint32_t*>(G);
+    auto** d_bases = c->multi.row_bases.as<const uint32_t*>(G);
     uint64_t* d_rb = c->multi.row_base.as<uint64_t>(G + 1);
     ND_CUDA(cudaMemcpyAsync(d_bases, bases.data(), G * sizeof(void*), cudaMemcpyHostToDevice, cs));
     ND_CUDA(cudaMemcpyAsync(d_rb, row_base.data(), (G + 1) * 8, cudaMemcpyHostToDevice, cs));
