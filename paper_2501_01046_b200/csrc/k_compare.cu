@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
                   uint32_t min_match, int nb, uint64_t* __restrict__ out_key,
                   uint32_t* __restrict__ out_m, unsigned long long* __restrict__ count,
                   uint64_t cap, bool two_barriers, uint32_t qcap,
-                  const uint32_t* __restrict__ fps, bool exch) {
+                  bool use_fps, bool exch) {
   // VL values per document and group of BPL = VL / BW blocks: one 32-byte
   // sector (a 16-byte load would still move a whole sector), or 64 bytes
   // for the big-cell variant
@@ -539,12 +539,12 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
   for (uint32_t k0 = 0; k0 < NB; k0 += BPL) {
     // fingerprints of blocks k0 .. k0+BPL-1 of this thread's documents
     uint32_t fp[DPT][BPL];
-    if (fps) {  // from the precomputed table (k_block_fps): 4 bytes per block
+    if (use_fps) {  // from the precomputed table (k_block_fps): 4 bytes per block
 #pragma unroll
       for (int j = 0; j < DPT; ++j) {
         const uint32_t d = threadIdx.x + j * TPB;
         if (d < n) {
-          const uint32_t* f = fps + static_cast<uint64_t>(rowsm[d]) * NB + k0;
+          const uint32_t* f = sv.fp(rowsm[d]) + k0;
 #pragma unroll
           for (int b = 0; b < BPL; ++b) fp[j][b] = k0 + b < NB ? __ldg(f + b) : 0u;
         }
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(TPB, TPB == 512 ? 2 : 8)
 #pragma unroll
     for (int j = 0; j < DPT; ++j) {
       const uint32_t d = threadIdx.x + j * TPB;
-      if (!fps && d < n) {
+      if (!use_fps && d < n) {
         const uint32_t* r = sv.row(rowsm[d]) + p0;
         uint32_t v[VL];
         if (full) {
@@ -654,6 +654,27 @@ using CmpFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
 
 }  // namespace
 
+void join_block_shape(uint32_t H, uint32_t min_match, uint32_t* NB, int* BW) {
+  *NB = H - min_match + 1;  // A + 1 blocks
+  *BW = 1;
+  for (int w : {8, 4, 2})
+    if (static_cast<uint64_t>(*NB) * w <= H) {
+      *BW = w;
+      break;
+    }
+}
+
+void block_fingerprints(const uint32_t* sig, uint64_t nrows, uint32_t H, uint32_t NB, int BW,
+                        uint32_t* fps, cudaStream_t s) {
+  const uint64_t total = nrows * NB;
+  if (!total) return;
+  const unsigned blocks = static_cast<unsigned>((total + 255) / 256);
+  if (BW == 2) k_block_fps<2><<<blocks, 256, 0, s>>>(sig, nrows, H, NB, fps);
+  else if (BW == 4) k_block_fps<4><<<blocks, 256, 0, s>>>(sig, nrows, H, NB, fps);
+  else k_block_fps<8><<<blocks, 256, 0, s>>>(sig, nrows, H, NB, fps);
+  ND_CHECK_LAUNCH();
+}
+
 // Smallest compiled prefilter width >= H - min_matches + 1 that fits in H.
 int compare_prefilter_width(uint32_t H, uint32_t min_match) {
   const uint32_t P = H - min_match + 1;
@@ -675,13 +696,9 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
   const uint32_t join_max = static_cast<uint32_t>(std::min<uint64_t>(cs.max_len, kJoinMax));
   const char* jb = getenv("ND_JOIN_BLOCKS");  // read per call: tests switch it
   const int join_mode = jb && std::string(jb) == "0" ? 1 : 2;  // 2 = blocks, 1 = per position
-  const uint32_t NB = H - min_match + 1;  // A + 1 blocks
+  uint32_t NB = 0;
   int BW = 1;
-  for (int w : {8, 4, 2})
-    if (static_cast<uint64_t>(NB) * w <= H) {
-      BW = w;
-      break;
-    }
+  join_block_shape(H, min_match, &NB, &BW);
   if (cs.join_enabled && join_max >= 2 && P <= kJoinMaxP) {
     // table slots >= n / load; the default load 1/2 (ND_JOIN_LOAD = percent)
     // one chain per table slot, no key CAS loop (ND_JOIN_EXCH=0: the keyed
@@ -729,21 +746,20 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
       using JoinBFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,
                                const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
                                int, uint64_t*, uint32_t*, unsigned long long*, uint64_t, bool,
-                               uint32_t, const uint32_t*, bool);
-      // block fingerprints of every row, once (one-table views; the peer
-      // views of the multi-GPU paths read the blocks in place)
-      const uint32_t* fps = nullptr;
+                               uint32_t, bool, bool);
+      // block fingerprints of every row, once: computed here for a one-table
+      // view; the multi-GPU paths hand in per-rank tables (sv.fp_bases)
+      SigView sv = d_sig;
       const char* jf = getenv("ND_JOIN_FPS");  // 0: fingerprints from the rows in the join
-      if (!(jf && jf[0] == '0') && d_sig.world <= 1 && nrows > 0 && nrows * NB < (1ull << 40)) {
+      const bool fps_on = !(jf && jf[0] == '0');
+      if (fps_on && sv.world <= 1 && nrows > 0 && nrows * NB < (1ull << 40)) {
         uint32_t* f = cs.fps.as<uint32_t>(nrows * NB);
-        const uint64_t total = nrows * NB;
-        const unsigned blocks = static_cast<unsigned>((total + 255) / 256);
-        if (BW == 2) k_block_fps<2><<<blocks, 256, 0, s>>>(d_sig.base0, nrows, H, NB, f);
-        else if (BW == 4) k_block_fps<4><<<blocks, 256, 0, s>>>(d_sig.base0, nrows, H, NB, f);
-        else k_block_fps<8><<<blocks, 256, 0, s>>>(d_sig.base0, nrows, H, NB, f);
-        ND_CHECK_LAUNCH();
-        fps = f;
+        block_fingerprints(sv.base0, nrows, H, NB, BW, f, s);
+        sv.fp0 = f;
+        sv.fpNB = NB;
       }
+      const bool use_fps = fps_on && sv.fpNB == NB && (sv.world <= 1 ? sv.fp0 != nullptr
+                                                                       : sv.fp_bases != nullptr);
       // 512 threads per CTA for cells above 1024 documents: -33 % K3 time on
       // C3-sized cells; smaller cells are faster with 256
       const int tpb = join_max > 1024 ? 512 : 256;
@@ -759,9 +775,9 @@ void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_
       if (smem_b > 48 * 1024)
         ND_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem_b)));
-      fn<<<grid, tpb, smem_b, s>>>(d_sig, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
+      fn<<<grid, tpb, smem_b, s>>>(sv, H, cs.sorted_rows, cs.cell_start, cs.cell_len,
                                    join_max, tbits_b, sbits, NB, min_match, nb, out_key, out_m,
-                                   count, cap, two_barriers, qcap, fps, exch);
+                                   count, cap, two_barriers, qcap, use_fps, exch);
       ND_CHECK_LAUNCH();
     } else {
       using JoinFn = void (*)(SigView, uint32_t, const uint32_t*, const uint64_t*,

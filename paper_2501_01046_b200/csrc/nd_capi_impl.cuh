@@ -44,14 +44,14 @@ struct nd_ctx {
   std::vector<nd_ctx*> shards;
   struct Multi {                // per-shard exchange buffers (nd_multi.cu)
     ndb::DevBuf send_keys, send_vals, first_cell, split, bases, row_bases, row_base, pair_lo,
-        pair_hi, pair_m;
+        pair_hi, pair_m, fps, fp_bases;
     ndb::SortScratch sort;
     ndb::PairSet final_pairs;
     std::vector<uint64_t> ranges;  // group: document range of each shard, last dedup
     bool last_valid = false;
     void release() {
       for (auto* b : {&send_keys, &send_vals, &first_cell, &split, &bases, &row_bases, &row_base,
-                      &pair_lo, &pair_hi, &pair_m})
+                      &pair_lo, &pair_hi, &pair_m, &fps, &fp_bases})
         b->release();
       sort.release();
       final_pairs.release();

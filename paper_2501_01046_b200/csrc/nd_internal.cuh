@@ -222,19 +222,38 @@ struct SigView {
   const uint64_t* row_base = nullptr;      // device array [world + 1]
   uint32_t world = 1;
   uint32_t H = 0;
+  // K3's block fingerprints of the same rows (k_block_fps), fpNB per row:
+  // one table (fp0) or one per rank (fp_bases, peer memory); fpNB = 0: none
+  const uint32_t* fp0 = nullptr;
+  const uint32_t* const* fp_bases = nullptr;
+  uint32_t fpNB = 0;
   __host__ __device__ SigView() {}
   __host__ __device__ SigView(const uint32_t* b, uint32_t h) : base0(b), H(h) {}
-  __device__ __forceinline__ const uint32_t* row(uint32_t g) const {
-    if (world <= 1) return base0 + static_cast<uint64_t>(g) * H;
-    // the rank r with row_base[r] <= g < row_base[r + 1]: binary search over
-    // the world + 1 bases (3 probes for 8 ranks, world <= 64)
+  // the rank r with row_base[r] <= g < row_base[r + 1]: binary search over
+  // the world + 1 bases (3 probes for 8 ranks, world <= 64)
+  __device__ __forceinline__ uint32_t rank_of(uint32_t g) const {
     uint32_t r = 0;
 #pragma unroll
     for (uint32_t step = 32; step > 0; step >>= 1)
       if (r + step < world && g >= row_base[r + step]) r += step;
+    return r;
+  }
+  __device__ __forceinline__ const uint32_t* row(uint32_t g) const {
+    if (world <= 1) return base0 + static_cast<uint64_t>(g) * H;
+    const uint32_t r = rank_of(g);
     return bases[r] + (static_cast<uint64_t>(g) - row_base[r]) * H;
   }
+  __device__ __forceinline__ const uint32_t* fp(uint32_t g) const {
+    if (world <= 1) return fp0 + static_cast<uint64_t>(g) * fpNB;
+    const uint32_t r = rank_of(g);
+    return fp_bases[r] + (static_cast<uint64_t>(g) - row_base[r]) * fpNB;
+  }
 };
+// K3's block shape for (H, min_matches): NB = H - min_matches + 1 blocks of
+// BW positions (1 = the per-position join); k_block_fps of n rows into fps
+void join_block_shape(uint32_t H, uint32_t min_match, uint32_t* NB, int* BW);
+void block_fingerprints(const uint32_t* sig, uint64_t nrows, uint32_t H, uint32_t NB, int BW,
+                        uint32_t* fps, cudaStream_t s);
 // nrows: rows of d_sig (block fingerprints are precomputed for a one-table view)
 void launch_compare(CellSet& cs, const SigView& d_sig, uint32_t H, uint32_t min_match,
                     int nb, uint64_t* out_key, uint32_t* out_m, unsigned long long* count,

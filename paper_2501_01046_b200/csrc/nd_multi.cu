@@ -173,6 +173,14 @@ void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
   if (cells_total > 0xFFFFFFFFull) fail(ND_ERR_CONFIG, "bands * bucket_count exceeds 2^32 cells");
   const uint32_t mm = min_matches(H, p.threshold_num, p.threshold_den);
   const auto r = shard_ranges(offsets, n, G);
+  // K3's block fingerprints are computed by each shard for its own rows (A)
+  // and read by every owner through peer memory (B), like the rows
+  uint32_t fpNB = 0;
+  int fpBW = 1;
+  join_block_shape(H, mm, &fpNB, &fpBW);
+  const char* jf = getenv("ND_JOIN_FPS");
+  const bool fps_on = fpBW > 1 && !(jf && jf[0] == '0');
+  std::vector<const uint32_t*> fp_bases(G, nullptr);
   std::vector<uint64_t> first_cell(G + 1);
   for (uint32_t s = 0; s <= G; ++s)
     first_cell[s] = static_cast<uint64_t>(
@@ -196,6 +204,11 @@ void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
     uint32_t* sig = st.sig.as<uint32_t>(m * H + 1);
     uint32_t* band = st.band.as<uint32_t>(m * B + 1);
     if (m) h2d_signatures(c, st, bytes, offsets + d0, m, B, p.rows, K, sig, band);
+    if (fps_on) {
+      uint32_t* f = c->multi.fps.as<uint32_t>(m * fpNB + 1);
+      block_fingerprints(sig, m, H, fpNB, fpBW, f, cs);
+      fp_bases[s] = f;
+    }
     ND_CUDA(cudaStreamSynchronize(cs));
     t_k1[s] = since(t0);
     // one-digit stable partition of the records by owner (their cell order
@@ -283,6 +296,12 @@ void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
     view.bases = d_bases;
     view.row_base = d_rb;
     view.world = G;
+    if (fps_on) {
+      auto** d_fpb = c->multi.fp_bases.as<const uint32_t*>(G);
+      ND_CUDA(cudaMemcpyAsync(d_fpb, fp_bases.data(), G * sizeof(void*), cudaMemcpyHostToDevice, cs));
+      view.fp_bases = d_fpb;
+      view.fpNB = fpNB;
+    }
     build_cells_from_records(st.cells, rk, rv, m, cells_total, kCmpRows, cs);
     compare_and_unique(st, view, H, mm, n, cs);
     ND_CUDA(cudaStreamSynchronize(cs));
