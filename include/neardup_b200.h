@@ -143,6 +143,11 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t hash_count,
  * (exact 64-bit Barrett); when K1j was eligible but could not be compiled the
  * reason follows after ": ". */
 const char* nd_k1_kernel(nd_ctx* ctx);
+/* How the last nd_dedup / nd_dedup_device compared: "global" (one block join
+ * over all rows, the cells counted for the reference's counters; the
+ * in-memory single-device default), "cells" (the per-cell joins: out-of-core
+ * intervals, device groups, ND_K3=cells) or "" (no valid dedup). */
+const char* nd_dedup_compare_kind(nd_ctx* ctx);
 /* The CUDA source K1j compiles for a family (no device needed): writes up to
  * cap bytes (NUL-terminated) into out and returns the full length, or -1
  * when the family is outside K1j's domain. */
@@ -225,6 +230,14 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
 int nd_dedup_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offsets,
                     const uint64_t* doc_ids, uint64_t n, const nd_params* params,
                     nd_dedup_stats* stats);
+/* The same dedup from signature rows already computed (e.g. read from .feds
+ * files with nd_feds_read): sig n*hash_count u32, band n*bands u32 host
+ * arrays, every band id below the bucket count (params->bucket_count, or
+ * choose_bucket_count(n)); compare + distinct pairs + components in HBM
+ * (run_compare_stage + run_union_stage, pipeline.cpp:347-476, in memory). */
+int nd_dedup_signatures(nd_ctx* ctx, const uint32_t* sig, const uint32_t* band,
+                        const uint64_t* doc_ids, uint64_t n, const nd_params* params,
+                        nd_dedup_stats* stats);
 /* distinct pairs (doc ids, sorted by (lo, hi)) of the last dedup */
 int nd_dedup_fetch_pairs(nd_ctx* ctx, uint64_t* lo, uint64_t* hi, uint32_t* match_count);
 /* signatures (n*H u32) and band ids (n*bands u32) the last dedup computed,

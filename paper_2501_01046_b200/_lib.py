@@ -108,6 +108,7 @@ SIGNATURES = {
     "nd_ctx_set_stream": (C.c_int, [vp, vp]),
     "nd_family_upload": (C.c_int, [vp, C.POINTER(NdHashFn), C.c_uint32, C.c_uint32, C.c_uint32]),
     "nd_k1_kernel": (C.c_char_p, [vp]),
+    "nd_dedup_compare_kind": (C.c_char_p, [vp]),
     "nd_k1j_source": (C.c_int64, [C.POINTER(NdHashFn), C.c_uint32, C.c_uint32, C.c_char_p,
                                   C.c_uint64]),
     "nd_signatures": (C.c_int, [vp, u8p, u64p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
@@ -128,6 +129,8 @@ SIGNATURES = {
                            C.POINTER(NdDedupStats)]),
     "nd_dedup_device": (C.c_int, [vp, vp, vp, u64p, C.c_uint64, C.POINTER(NdParams),
                                   C.POINTER(NdDedupStats)]),
+    "nd_dedup_signatures": (C.c_int, [vp, u32p, u32p, u64p, C.c_uint64, C.POINTER(NdParams),
+                                      C.POINTER(NdDedupStats)]),
     "nd_dedup_fetch_pairs": (C.c_int, [vp, u64p, u64p, u32p]),
     "nd_dedup_fetch_signatures": (C.c_int, [vp, u32p, u32p]),
     "nd_dedup_fetch_groups": (C.c_int, [vp, u64p, u64p]),

@@ -24,38 +24,12 @@
 #include <string>
 
 #include "nd_internal.cuh"
+#include "k_compare_util.cuh"
 
 namespace ndb {
 namespace {
 
 constexpr int kCols = 64;  // columns staged per batch
-
-__device__ __forceinline__ uint32_t full_matches(const uint32_t* __restrict__ a,
-                                                 const uint32_t* __restrict__ b, uint32_t H,
-                                                 uint32_t allowed, bool& alive) {
-  uint32_t matches = 0;
-  alive = true;
-  for (uint32_t h0 = 0; h0 < H; h0 += 32) {
-    const uint32_t hi = min(H, h0 + 32);
-    for (uint32_t h = h0; h < hi; ++h) matches += __ldg(a + h) == __ldg(b + h);
-    if (hi - matches > allowed) {  // accepting count unreachable (oracle.cpp:81-92)
-      alive = false;
-      return matches;
-    }
-  }
-  return matches;
-}
-
-__device__ __forceinline__ void emit(uint32_t ra, uint32_t rb, uint32_t m, int nb,
-                                     uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
-                                     unsigned long long* __restrict__ count, uint64_t cap) {
-  const uint32_t lo = min(ra, rb), hi = max(ra, rb);
-  unsigned long long slot = atomicAdd(count, 1ull);
-  if (slot < cap) {
-    out_key[slot] = (static_cast<uint64_t>(lo) << nb) | hi;
-    out_m[slot] = m;
-  }
-}
 
 // Warp-cooperative exact count of one candidate pair: lanes compare 32
 // consecutive positions per step (coalesced 128-byte row reads) and a
@@ -358,25 +332,6 @@ __global__ void __launch_bounds__(kJoinThreads)
 // instead of ~q per position (q = chance two minima coincide, ~1/3000 here),
 // which removes almost all spurious candidates.
 template <int BW>
-__device__ __forceinline__ void load_block(const uint32_t* __restrict__ p, bool vec, uint32_t (&v)[BW]) {
-  if constexpr (BW % 4 == 0) {
-    if (vec) {
-#pragma unroll
-      for (int q = 0; q < BW / 4; ++q) {
-        const uint4 x = __ldg(reinterpret_cast<const uint4*>(p) + q);
-        v[4 * q] = x.x;
-        v[4 * q + 1] = x.y;
-        v[4 * q + 2] = x.z;
-        v[4 * q + 3] = x.w;
-      }
-      return;
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < BW; ++t) v[t] = __ldg(p + t);
-}
-
-template <int BW>
 __device__ __forceinline__ uint32_t block_fp(const uint32_t (&v)[BW]) {
   uint32_t h = 0x9E3779B9u;
 #pragma unroll
@@ -385,18 +340,6 @@ __device__ __forceinline__ uint32_t block_fp(const uint32_t (&v)[BW]) {
     h ^= h >> 15;
   }
   return h & 0x7FFFFFu;
-}
-
-template <int BW>
-__device__ __forceinline__ bool same_block(const uint32_t* __restrict__ a,
-                                           const uint32_t* __restrict__ b, bool vec) {
-  uint32_t x[BW], y[BW];
-  load_block<BW>(a, vec, x);
-  load_block<BW>(b, vec, y);
-  bool eq = true;
-#pragma unroll
-  for (int t = 0; t < BW; ++t) eq &= x[t] == y[t];
-  return eq;
 }
 
 // Block fingerprints of every signature row, computed once per compare:

@@ -467,6 +467,12 @@ const char* nd_k1_kernel(nd_ctx* ctx) {
   return out.c_str();
 }
 
+const char* nd_dedup_compare_kind(nd_ctx* ctx) {
+  if (!ctx) return "";
+  if (is_group(ctx)) return ctx->multi.last_valid ? "cells" : "";
+  return ctx->dedup.valid ? ctx->dedup.compare_kind : "";
+}
+
 int nd_signatures(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
                   uint32_t bands, uint32_t rows, uint32_t K, uint32_t* sig_out,
                   uint32_t* band_out) {

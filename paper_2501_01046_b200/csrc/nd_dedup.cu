@@ -196,11 +196,45 @@ void dedup_tail(nd_ctx* ctx, DedupState& st, const nd_params& p, uint64_t n, nd_
   cudaStream_t s = ctx->stream;
   const uint32_t H = p.hash_count;
   const uint32_t mm = min_matches(H, p.threshold_num, p.threshold_den);
-  build_cells_from_bands(st.cells, st.band.as<uint32_t>(n * p.bands), n, p.bands, st.K, kCmpRows,
-                         s);
-  t.mark();  // 2
-  compare_pairs(st, SigView(st.sig.as<uint32_t>(n * H), H), H, mm, n, s);
-  t.mark();  // 3
+  const uint32_t* sig = st.sig.as<uint32_t>(n * H);
+  const uint32_t* band = st.band.as<uint32_t>(n * p.bands);
+  uint64_t emitted = 0;
+  if (global_join_eligible(n, H, p.bands, st.K, mm)) {
+    // K3g: the cells only for the reference's counters, every block joined
+    // once over all rows (k_gjoin.cu)
+    gj_cell_counts(st.gj, band, n, p.bands, st.K, s);
+    t.mark();  // 2
+    PairSet& ps = st.pairs;
+    ps.nb = std::max(1, bits_for(n ? n - 1 : 0));
+    ps.counter = ps.dcount.as<unsigned long long>(1);
+    if (ps.cap == 0) ps.cap = std::max<uint64_t>(1 << 20, 2 * n);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      ps.keys = ps.dkeys.as<uint64_t>(ps.cap);
+      ps.vals = ps.dvals.as<uint32_t>(ps.cap);
+      ND_CUDA(cudaMemsetAsync(ps.counter, 0, sizeof(unsigned long long), s));
+      gj_pairs(st.gj, sig, band, n, H, p.bands, mm, ps.nb, ps.keys, ps.vals, ps.counter, ps.cap, s);
+      unsigned long long got = 0;
+      ND_CUDA(cudaMemcpyAsync(&got, ps.counter, sizeof got, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaStreamSynchronize(s));
+      ps.count = got;
+      if (got <= ps.cap) break;
+      ps.cap = got + got / 4;
+    }
+    t.mark();  // 3
+    const GJoinCounts c = gj_read(st.gj, s);
+    st.cells.ncells = c.ncells;
+    st.cells.candidate_pairs = c.candidate_pairs;
+    st.cells.cell_records = c.cell_records;
+    emitted = c.emitted;
+    st.compare_kind = "global";
+  } else {
+    build_cells_from_bands(st.cells, band, n, p.bands, st.K, kCmpRows, s);
+    t.mark();  // 2
+    compare_pairs(st, SigView(sig, H), H, mm, n, s);
+    t.mark();  // 3
+    emitted = st.pairs.count;
+    st.compare_kind = "cells";
+  }
   unique_pairs(st.pairs, s);
   t.mark();  // 4
   components(st.groups, st.pairs.lo, st.pairs.hi, st.pairs.distinct, n, s);
@@ -208,13 +242,14 @@ void dedup_tail(nd_ctx* ctx, DedupState& st, const nd_params& p, uint64_t n, nd_
   ND_CUDA(cudaStreamSynchronize(s));
   st.documents = n;
   st.bands = p.bands;
+  st.H = H;
   st.valid = true;
   if (stats) {
     stats->documents = n;
     stats->bucket_count = st.K;
     stats->nonsingleton_cells = st.cells.ncells;
     stats->candidate_pairs = st.cells.candidate_pairs;
-    stats->emitted_pairs = st.pairs.count;
+    stats->emitted_pairs = emitted;
     stats->distinct_pairs = st.pairs.distinct;
     stats->duplicate_groups = st.groups.groups;
     stats->near_duplicates = st.groups.members;
@@ -369,7 +404,9 @@ void dedup_out_of_core(nd_ctx* ctx, DedupState& st, const nd_params& p, const ui
   st.sig_on_host = true;
   st.documents = n;
   st.bands = B;
+  st.H = H;
   st.intervals = static_cast<uint32_t>(intervals.size());
+  st.compare_kind = "cells";
   st.valid = true;
   if (stats) {
     *stats = nd_dedup_stats{};
@@ -492,6 +529,39 @@ int nd_dedup_device(nd_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offse
   });
 }
 
+int nd_dedup_signatures(nd_ctx* ctx, const uint32_t* sig, const uint32_t* band,
+                        const uint64_t* doc_ids, uint64_t n, const nd_params* params,
+                        nd_dedup_stats* stats) {
+  return guarded_impl(ctx, [&] {
+    if (is_group(ctx)) fail(ND_ERR_CONFIG, "nd_dedup_signatures runs on one device");
+    const nd_params p = *params;
+    validate(p);
+    DedupState& st = ctx->dedup;
+    st.valid = false;
+    set_doc_ids(st, doc_ids, n);
+    if (n == 0) fail(ND_ERR_CONFIG, "no documents survive preprocessing; nothing to deduplicate");
+    st.K = bucket_count_for(p, n);
+    for (uint64_t i = 0; i < n * p.bands; ++i)
+      if (band[i] >= st.K)
+        fail(ND_ERR_CONFIG, "band id " + std::to_string(band[i]) + " of row " +
+                                std::to_string(i / p.bands) + " is not below the bucket count " +
+                                std::to_string(st.K));
+    st.sig_on_host = false;
+    st.host_sig.clear();
+    st.host_band.clear();
+    st.intervals = 1;
+    cudaStream_t s = ctx->stream;
+    uint32_t* d_sig = st.sig.as<uint32_t>(n * p.hash_count);
+    uint32_t* d_band = st.band.as<uint32_t>(n * p.bands);
+    ND_CUDA(cudaMemcpyAsync(d_sig, sig, n * p.hash_count * 4, cudaMemcpyHostToDevice, s));
+    ND_CUDA(cudaMemcpyAsync(d_band, band, n * p.bands * 4, cudaMemcpyHostToDevice, s));
+    EventTimer t(s);
+    t.mark();
+    t.mark();  // (no K1)
+    dedup_tail(ctx, st, p, n, stats, t);
+  });
+}
+
 int nd_dedup_fetch_signatures(nd_ctx* ctx, uint32_t* sig, uint32_t* band) {
   return guarded_impl(ctx, [&] {
     if (is_group(ctx)) {
@@ -501,7 +571,7 @@ int nd_dedup_fetch_signatures(nd_ctx* ctx, uint32_t* sig, uint32_t* band) {
     DedupState& st = ctx->dedup;
     if (!st.valid || !ctx->fam.q) fail(ND_ERR_PREREQ, "no dedup result; run nd_dedup first");
     cudaStream_t s = ctx->stream;
-    const uint64_t n = st.documents, H = ctx->fam.H;
+    const uint64_t n = st.documents, H = st.H;
     if (st.sig_on_host) {  // out-of-core run: rows in host memory
       if (sig && n) std::memcpy(sig, st.host_sig.data(), n * H * 4);
       if (band && n) std::memcpy(band, st.host_band.data(), n * st.bands * 4);

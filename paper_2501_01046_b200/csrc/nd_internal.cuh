@@ -285,9 +285,36 @@ void components(GroupSet& gs, const uint32_t* lo, const uint32_t* hi, uint64_t e
 
 // State of the last dedup run held by a context (results stay on device
 // until fetched).
+// K3g, the global block join of the in-memory dedup (k_gjoin.cu)
+constexpr uint32_t kGJoinMaxBlocks = 64;
+struct GJoin {
+  DevBuf fps_buf, table_buf, link_buf, cnt, acc;
+  uint32_t* fps = nullptr;                  // [NB][n] block fingerprints
+  unsigned long long* table = nullptr;      // 2^tbits chain heads
+  unsigned long long* link = nullptr;       // [n] (fingerprint << 32 | row) chained before
+  unsigned long long* acc_d = nullptr;      // candidate pairs, cells, records, emitted
+  int tbits = 10;
+  void release() {
+    for (DevBuf* b : {&fps_buf, &table_buf, &link_buf, &cnt, &acc}) b->release();
+  }
+};
+struct GJoinCounts {
+  uint64_t candidate_pairs, ncells, cell_records, emitted;
+};
+bool global_join_eligible(uint64_t n, uint32_t H, uint32_t B, uint32_t K, uint32_t mm);
+// reference counters from a histogram of the cells (async, into g.acc_d)
+void gj_cell_counts(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint32_t K,
+                    cudaStream_t s);
+// accepted pairs, each once, and the emitted-pairs counter (async)
+void gj_pairs(GJoin& g, const uint32_t* sig, const uint32_t* band, uint64_t n, uint32_t H,
+              uint32_t B, uint32_t mm, int nb, uint64_t* out_key, uint32_t* out_m,
+              unsigned long long* count, uint64_t cap, cudaStream_t s);
+GJoinCounts gj_read(GJoin& g, cudaStream_t s);
+
 struct DedupState {
   DevBuf sig, band, text, offs;
   CellSet cells;
+  GJoin gj;
   PairSet pairs;
   GroupSet groups;
   SigScratch sig_scratch;
@@ -296,13 +323,16 @@ struct DedupState {
   std::vector<uint32_t> host_sig, host_band;
   bool sig_on_host = false;
   uint32_t intervals = 1;         // bucket intervals of the last dedup
+  const char* compare_kind = "";  // K3 of the last dedup: "global" (K3g) or "cells"
   uint64_t documents = 0;
   uint32_t K = 0;
   uint32_t bands = 0;             // band keys per row in band
+  uint32_t H = 0;                 // hashes per row in sig
   bool valid = false;
   void release() {
     for (DevBuf* b : {&sig, &band, &text, &offs}) b->release();
     cells.release();
+    gj.release();
     pairs.release();
     groups.release();
     sig_scratch.release();

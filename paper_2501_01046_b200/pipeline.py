@@ -170,6 +170,40 @@ def dedup_packed(data: np.ndarray, offsets: np.ndarray, config: RunConfig | None
     return _fetch_report(ctx, stats, lists=(fetch != "arrays"))
 
 
+def dedup_signatures(sig: np.ndarray, band: np.ndarray, config: RunConfig | None = None,
+                     doc_ids: np.ndarray | None = None, bucket_count: int = 0,
+                     ctx: Context | None = None, fetch="lists") -> DedupReport:
+    """In-memory compare + union over signature rows already computed (n x H
+    sig, n x bands band ids, e.g. from read_sig_file): the compare and union
+    stages of run_dedup (pipeline.cpp:347-476) without their files."""
+    config = config or RunConfig()
+    config.validate()
+    ctx = ctx or default_context()
+    sig = np.ascontiguousarray(sig, np.uint32)
+    band = np.ascontiguousarray(band, np.uint32)
+    n = sig.shape[0]
+    if sig.shape != (n, config.hash_count) or band.shape != (n, config.bands):
+        raise _lib.ConfigError(_lib.ND_ERR_CONFIG, "signature / band id shapes do not match the config")
+    ids = None if doc_ids is None else np.ascontiguousarray(doc_ids, np.uint64)
+    stats = NdDedupStats()
+    params = config.to_params(bucket_count)
+    ctx.check(ctx.lib.nd_dedup_signatures(ctx.h, sig.ctypes.data_as(_lib.u32p),
+                                          band.ctypes.data_as(_lib.u32p),
+                                          ids.ctypes.data_as(u64p) if ids is not None else None, n,
+                                          C.byref(params), C.byref(stats)))
+    if not fetch:
+        rep = DedupReport(total_documents=stats.documents, distinct_pairs=stats.distinct_pairs)
+        rep.candidate_pairs = stats.candidate_pairs
+        return rep
+    return _fetch_report(ctx, stats, lists=(fetch != "arrays"))
+
+
+def dedup_compare_kind(ctx: Context | None = None) -> str:
+    """How the last in-memory dedup on ctx compared: "global" or "cells"."""
+    ctx = ctx or default_context()
+    return ctx.lib.nd_dedup_compare_kind(ctx.h).decode()
+
+
 def dedup_pairs(distinct_pairs: int, ctx: Context | None = None):
     """Sorted distinct duplicate pairs (doc ids) of the last dedup on ctx."""
     from .compare import DuplicatePair

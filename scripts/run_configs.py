@@ -104,7 +104,8 @@ def main():
            "cells": stats.nonsingleton_cells, "candidate_pairs": stats.candidate_pairs,
            "emitted_pairs": stats.emitted_pairs, "distinct_pairs": stats.distinct_pairs,
            "groups": stats.duplicate_groups, "near_duplicates": stats.near_duplicates,
-           "host_lengths_s": t_len, "device_text_s": t_gen - t_len}
+           "host_lengths_s": t_len, "device_text_s": t_gen - t_len,
+           "compare": lib.nd_dedup_compare_kind(ctx.h).decode()}
     res["k1_hwe_per_s"] = res["hwe"] / stats.seconds[0] if stats.seconds[0] else None
     res["candidate_pairs_per_s"] = stats.candidate_pairs / stats.seconds[2] if stats.seconds[2] else None
     print(json.dumps(res), flush=True)
