@@ -59,6 +59,7 @@ struct JitShape {
   int F = 16;
   int min_blocks = 6;
   int prefetch = 1;
+  int unroll = 1;  // whole words per loop iteration (2: ND_K1J_UNROLL=2, slower)
 };
 
 JitShape jit_shape() {
@@ -66,6 +67,7 @@ JitShape jit_shape() {
   if (const char* v = getenv("ND_K1J_F")) j.F = std::max(4, std::min(64, atoi(v)));
   if (const char* v = getenv("ND_K1J_MINB")) j.min_blocks = std::max(1, std::min(16, atoi(v)));
   if (const char* v = getenv("ND_K1J_PREFETCH")) j.prefetch = std::max(1, std::min(2, atoi(v)));
+  if (const char* v = getenv("ND_K1J_UNROLL")) j.unroll = std::max(1, std::min(2, atoi(v)));
   return j;
 }
 
@@ -233,7 +235,7 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
          "        }\n"
          "        if (phase == 1) break;\n";
     // whole aligned words
-    s << "        if (p - 3 >= wlo) {\n"
+    s << "        if (p - " << (js.unroll == 2 ? 7 : 3) << " >= wlo) {\n"
          "          const u32* wp = (const u32*)(abase + (u64)(p - 3));\n"
          "          i64 q = p - 3;\n"
          "          u32 cur = wp[0];\n";
@@ -247,42 +249,66 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
         << "            if (nv > 0) r" << k << " = wp[" << k
         << "] & (nv >= 4 ? 0xffffffffu : ((1u << (8 * (u32)nv)) - 1u)); }\n";
     }
-    if (js.prefetch >= 2)
-      s << "          u32 nx1 = (q - 4 >= wlo) ? wp[-1] : 0u;\n";
-    s << "          for (;;) {\n"
-         "            const bool more = q - 4 >= wlo;\n";
-    if (js.prefetch >= 2)
-      s << "            const u32 nx = nx1;\n"
-           "            nx1 = (q - 8 >= wlo) ? wp[-2] : 0u;\n";
-    else
-      s << "            const u32 nx = more ? wp[-1] : 0u;\n";
-    for (int i = 3; i >= 0; --i) {
-      const int pos = i + static_cast<int>(L), k = pos >> 2, j = pos & 3;
-      const std::string src = k == 0 ? "cur" : "r" + std::to_string(k);
-      char sel_in[8], sel_out[8];
-      std::snprintf(sel_in, sizeof sel_in, "0x44%d4", i);
-      std::snprintf(sel_out, sizeof sel_out, "0x444%d", j);
-      s << "            const u32 ci" << i << " = __byte_perm(cur, 0u, " << sel_in << ");\n"
-        << "            const u32 co" << i << " = __byte_perm(" << src << ", 0u, " << sel_out << ");\n"
-        << "            const float cf" << i << " = __uint2float_rn(co" << i << ");\n";
+    // one word: 4 windows of every function of the pass, then the ring
+    // shifts down one word and `next` becomes the current word
+    auto word = [&](const std::string& next) {
+      for (int i = 3; i >= 0; --i) {
+        const int pos = i + static_cast<int>(L), k = pos >> 2, j = pos & 3;
+        const std::string src = k == 0 ? "cur" : "r" + std::to_string(k);
+        char sel_in[8], sel_out[8];
+        std::snprintf(sel_in, sizeof sel_in, "0x44%d4", i);
+        std::snprintf(sel_out, sizeof sel_out, "0x444%d", j);
+        s << "            { const u32 ci" << i << " = __byte_perm(cur, 0u, " << sel_in << ");\n"
+          << "            const u32 co" << i << " = __byte_perm(" << src << ", 0u, " << sel_out
+          << ");\n"
+          << "            const float cf" << i << " = __uint2float_rn(co" << i << ");\n";
+      }
+      for (int f = 0; f < n; ++f) {
+        const std::string sf = "s" + std::to_string(f), mf = "m" + std::to_string(f);
+        s << "            { const u32 a3 = " << rol_call(sf, 3, cs[fb + f]) << ";\n"
+          << "              const u32 a2 = " << rol_call("a3", 2, cs[fb + f]) << ";\n"
+          << "              const u32 a1 = " << rol_call("a2", 1, cs[fb + f]) << ";\n"
+          << "              const u32 a0 = " << rol_call("a1", 0, cs[fb + f]) << ";\n"
+          << "              " << sf << " = a0; " << mf << " = __vimin3_u32(" << mf << ", a3, a2); "
+          << mf << " = __vimin3_u32(" << mf << ", a1, a0); }\n";
+      }
+      s << "            }}}}\n";
+      for (int k = R; k >= 2; --k) s << "            r" << k << " = r" << k - 1 << ";\n";
+      if (R >= 1) s << "            r1 = cur;\n";
+      s << "            cur = " << next << ";\n";
+    };
+    if (js.unroll == 2) {
+      // pairs of words while two remain (a 32-bit pair count); an odd last
+      // word goes to the single steps below
+      s << "          u32 npair = (u32)((q - wlo + 4) >> 3);\n"
+           "          do {\n"
+           "            const u32 nx = wp[-1];\n";
+      word("nx");
+      s << "            const u32 nx2 = (q - 8 >= wlo) ? wp[-2] : 0u;\n";
+      word("nx2");
+      s << "            wp -= 2; q -= 8;\n"
+           "          } while (--npair);\n"
+           "          p = q + 3;\n"
+           "        }\n"
+           "      }\n";
+    } else {
+      if (js.prefetch >= 2)
+        s << "          u32 nx1 = (q - 4 >= wlo) ? wp[-1] : 0u;\n";
+      s << "          for (;;) {\n"
+           "            const bool more = q - 4 >= wlo;\n";
+      if (js.prefetch >= 2)
+        s << "            const u32 nx = nx1;\n"
+             "            nx1 = (q - 8 >= wlo) ? wp[-2] : 0u;\n";
+      else
+        s << "            const u32 nx = more ? wp[-1] : 0u;\n";
+      word("nx");
+      s << "            --wp; q -= 4;\n"
+           "            if (!more) break;\n"
+           "          }\n"
+           "          p = q + 3;\n"
+           "        }\n"
+           "      }\n";
     }
-    for (int f = 0; f < n; ++f) {
-      const std::string sf = "s" + std::to_string(f), mf = "m" + std::to_string(f);
-      s << "            { const u32 a3 = " << rol_call(sf, 3, cs[fb + f]) << ";\n"
-        << "              const u32 a2 = " << rol_call("a3", 2, cs[fb + f]) << ";\n"
-        << "              const u32 a1 = " << rol_call("a2", 1, cs[fb + f]) << ";\n"
-        << "              const u32 a0 = " << rol_call("a1", 0, cs[fb + f]) << ";\n"
-        << "              " << sf << " = a0; " << mf << " = __vimin3_u32(" << mf << ", a3, a2); "
-        << mf << " = __vimin3_u32(" << mf << ", a1, a0); }\n";
-    }
-    for (int k = R; k >= 2; --k) s << "            r" << k << " = r" << k - 1 << ";\n";
-    if (R >= 1) s << "            r1 = cur;\n";
-    s << "            cur = nx; --wp; q -= 4;\n"
-         "            if (!more) break;\n"
-         "          }\n"
-         "          p = q + 3;\n"
-         "        }\n"
-         "      }\n";
     // store the canonical minima (state scaled by 256)
     s << "      if (active) {\n        if (multi) {\n";
     for (int f = 0; f < n; ++f)
@@ -368,7 +394,8 @@ void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L) {
   std::string key(reinterpret_cast<const char*>(fns), sizeof(nd_hash_fn) * H);
   const JitShape js = jit_shape();
   key += "|" + std::to_string(H) + "|" + std::to_string(L) + "|" + std::to_string(js.F) + "|" +
-         std::to_string(js.min_blocks) + "|" + std::to_string(js.prefetch);
+         std::to_string(js.min_blocks) + "|" + std::to_string(js.prefetch) + "|" +
+         std::to_string(js.unroll);
   int dev = 0;
   cudaGetDevice(&dev);
   key += "|" + std::to_string(dev);

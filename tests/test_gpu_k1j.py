@@ -166,3 +166,17 @@ def test_codepoint_narrow_documents_take_the_byte_kernels(ctx, oracle, monkeypat
     assert np.array_equal(res["1"][0], res["0"][0]) and np.array_equal(res["1"][1], res["0"][1])
     want = oracle.signatures(data, offs, oracle.derive_family(5, 128), unit=1)
     assert np.array_equal(res["1"][0], want)
+
+
+@pytest.mark.parametrize("L", [1, 4, 5, 9, 16])
+def test_k1j_two_words_per_iteration(ctx, oracle, monkeypatch, L):
+    # ND_K1J_UNROLL=2 (pairs of words, the odd last word on single steps):
+    # not the default, but a compiled shape must still be exact
+    monkeypatch.setenv("ND_K1J_UNROLL", "2")
+    rng = np.random.default_rng(700 + L)
+    lens = [L + k for k in range(12)] + list(rng.integers(L, 3000, size=60)) + [20000]
+    data, offs = _docs(rng, lens)
+    fam = minhash.derive_family(5, 64, L)
+    out = _both(ctx, monkeypatch, data, offs, fam)
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][0], oracle.signatures(data, offs, oracle.derive_family(5, 64, L), L=L))
