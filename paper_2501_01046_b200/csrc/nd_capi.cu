@@ -48,7 +48,7 @@ using ndb::fail;
 
 nd_ctx::~nd_ctx() {
   for (auto* b : {&fam_buf, &sig_in_text, &sig_in_off}) b->release();
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kSlots; ++i) {
     slot[i].text.release();
     slot[i].off.release();
     slot[i].sig.release();
@@ -83,7 +83,7 @@ void nd_ctx::ensure_streams() {
   if (h2d) return;
   ND_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
   ND_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kSlots; ++i) {
     ND_CUDA(cudaStreamCreateWithFlags(&slot[i].comp, cudaStreamNonBlocking));
     ND_CUDA(cudaEventCreateWithFlags(&slot[i].h2d_done, cudaEventDisableTiming));
     ND_CUDA(cudaEventCreateWithFlags(&slot[i].comp_done, cudaEventDisableTiming));
@@ -110,7 +110,7 @@ namespace ndb {
 uint64_t h2d_chunk_bytes(const DevFamily& fam, size_t chunk_index) {
   static const uint64_t first_mb = [] {
     const char* v = getenv("ND_H2D_FIRST_MB");  // tuning
-    return v ? std::max(1, atoi(v)) : 64;
+    return v ? std::max(1, atoi(v)) : 32;
   }();
   static const uint64_t max_mb = [] {
     const char* v = getenv("ND_H2D_MAX_MB");  // tuning
@@ -136,13 +136,29 @@ void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets,
   if (band_out && (bands == 0 || rows == 0 || static_cast<uint64_t>(bands) * rows != H))
     fail(ND_ERR_CONFIG, "signature has " + std::to_string(H) + " values, banding needs " +
                             std::to_string(bands) + "*" + std::to_string(rows));
-  for (uint64_t i = 0; i < n; ++i) {
-    if (offsets[i + 1] < offsets[i]) fail(ND_ERR_CONFIG, "offsets must be non-decreasing");
-    if (offsets[i + 1] - offsets[i] < L)
-      fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has " +
-                             std::to_string(offsets[i + 1] - offsets[i]) + " units, needs " +
-                             std::to_string(L));
-  }
+  // a bad document stops the run after the chunks already issued have
+  // drained (no copy into the caller's buffers after the error returns)
+  auto drain_and_fail = [&](int code, const std::string& msg) {
+    if (ctx->h2d) {
+      cudaStreamSynchronize(ctx->h2d);
+      for (auto& sl : ctx->slot) cudaStreamSynchronize(sl.comp);
+      cudaStreamSynchronize(ctx->d2h);
+    }
+    fail(code, msg);
+  };
+  auto check_docs = [&](uint64_t a, uint64_t b) {
+    for (uint64_t i = a; i < b; ++i) {
+      if (offsets[i + 1] < offsets[i]) drain_and_fail(ND_ERR_CONFIG, "offsets must be non-decreasing");
+      if (offsets[i + 1] - offsets[i] < L)
+        drain_and_fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has " +
+                                         std::to_string(offsets[i + 1] - offsets[i]) +
+                                         " units, needs " + std::to_string(L));
+    }
+  };
+  // the offsets are checked chunk by chunk as the chunks are issued (the
+  // first copy starts after one chunk's worth of host work, not n's); the
+  // chunk boundaries need them ascending, checked once, cheaply, up front
+  if (offsets[n] < offsets[0]) fail(ND_ERR_CONFIG, "offsets must be non-decreasing");
   ctx->ensure_streams();
   cudaEvent_t start;
   ND_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
@@ -150,55 +166,129 @@ void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets,
   ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
 
   // chunking: <= chunk_bytes(c) of text and <= kChunkDocs documents per chunk
+  // (binary search over the offsets; a longer document is a chunk of its own)
   constexpr uint64_t kChunkDocs = 1ull << 20;
-  std::vector<std::pair<uint64_t, uint64_t>> chunks;
-  for (uint64_t d0 = 0; d0 < n;) {
-    uint64_t d1 = d0 + 1;
-    const uint64_t cap = h2d_chunk_bytes(ctx->fam, chunks.size());
-    while (d1 < n && d1 - d0 < kChunkDocs && offsets[d1 + 1] - offsets[d0] <= cap) ++d1;
-    chunks.push_back({d0, d1});
-    d0 = d1;
-  }
+  // optional ramp down at the end (ND_H2D_TAIL_DIV=d: a chunk takes at most
+  // 1/d of the text left, down to the first chunk's size; measured no faster
+  // on the C2 shard, the extra launch tails cost what the shorter last copy
+  // saves)
+  static const uint64_t tail_div = [] {
+    const char* v = getenv("ND_H2D_TAIL_DIV");
+    return static_cast<uint64_t>(v ? std::max(0, atoi(v)) : 0);
+  }();
+  const uint64_t first_cap = h2d_chunk_bytes(ctx->fam, 0);
+  auto chunk_end = [&](uint64_t d0, size_t index) {
+    uint64_t cap = h2d_chunk_bytes(ctx->fam, index);
+    if (tail_div && ctx->fam.jit)
+      cap = std::min(cap, std::max(first_cap, (offsets[n] - offsets[d0]) / tail_div));
+    const uint64_t lim = std::min(n, d0 + kChunkDocs);
+    // largest d1 in (d0, lim] with offsets[d1] - offsets[d0] <= cap
+    const uint64_t* it = std::upper_bound(offsets + d0 + 1, offsets + lim + 1, offsets[d0] + cap);
+    return std::max<uint64_t>(d0 + 1, static_cast<uint64_t>(it - offsets) - 1);
+  };
+  // slot buffers sized for the largest chunk the ramp can produce
   uint64_t max_docs = 0, max_bytes = 0;
-  for (auto [a, b] : chunks) {
-    max_docs = std::max(max_docs, b - a);
-    max_bytes = std::max(max_bytes, offsets[b] - offsets[a]);
+  {
+    uint64_t d0 = 0;
+    for (size_t c = 0; d0 < n; ++c) {
+      const uint64_t d1 = chunk_end(d0, c);
+      if (offsets[d1] < offsets[d0]) fail(ND_ERR_CONFIG, "offsets must be non-decreasing");
+      max_docs = std::max(max_docs, d1 - d0);
+      max_bytes = std::max(max_bytes, offsets[d1] - offsets[d0]);
+      d0 = d1;
+    }
   }
-  uint64_t* hoff = static_cast<uint64_t*>(ctx->pinned_off.get(2 * (max_docs + 1) * sizeof(uint64_t)));
-  bool first_use[2] = {true, true};
-  for (size_t c = 0; c < chunks.size(); ++c) {
-    auto& sl = ctx->slot[c & 1];
-    const uint64_t d0 = chunks[c].first, d1 = chunks[c].second, m = d1 - d0;
+  // slots in flight: with three, chunk c+3's copy in waits only for chunk
+  // c's results to leave, so the copies run ahead of the kernels through the
+  // ramp (ND_H2D_SLOTS=2: double buffering)
+  static const int nslots = [] {
+    const char* v = getenv("ND_H2D_SLOTS");
+    return v ? std::max(2, std::min(nd_ctx::kSlots, atoi(v))) : nd_ctx::kSlots;
+  }();
+  uint64_t* hoff = static_cast<uint64_t*>(
+      ctx->pinned_off.get(nslots * (max_docs + 1) * sizeof(uint64_t)));
+  bool first_use[nd_ctx::kSlots] = {true, true, true};
+  // ND_PIPE_TRACE=1: per chunk, device times (ms from the call's start) of
+  // copy in / kernel / copy out, on stderr
+  const bool trace = [] {
+    const char* v = getenv("ND_PIPE_TRACE");
+    return v && v[0] == '1';
+  }();
+  struct Tr { cudaEvent_t e[6]; uint64_t bytes; };
+  std::vector<Tr> tr;
+  cudaEvent_t t0ev = nullptr;
+  if (trace) {
+    ND_CUDA(cudaEventCreate(&t0ev));
+    ND_CUDA(cudaEventRecord(t0ev, ctx->stream));
+  }
+  auto mark = [&](size_t c, int k, cudaStream_t st) {
+    if (!trace) return;
+    if (tr.size() <= c) {
+      tr.resize(c + 1);
+      for (auto& e : tr[c].e) cudaEventCreate(&e);
+    }
+    cudaEventRecord(tr[c].e[k], st);
+  };
+  uint64_t next_d0 = 0;
+  for (size_t c = 0; next_d0 < n; ++c) {
+    const int si = static_cast<int>(c % nslots);
+    auto& sl = ctx->slot[si];
+    const uint64_t d0 = next_d0, d1 = chunk_end(d0, c), m = d1 - d0;
+    next_d0 = d1;
+    check_docs(d0, d1);
     const uint64_t tb = offsets[d1] - offsets[d0];
     uint8_t* dtext = sl.text.as<uint8_t>(max_bytes + 16);
     uint64_t* doff = sl.off.as<uint64_t>(max_docs + 1);
     uint32_t* dsig = sl.sig.as<uint32_t>(max_docs * H);
     uint32_t* dband = band_out ? sl.band.as<uint32_t>(max_docs * bands) : nullptr;
-    uint64_t* ho = hoff + (c & 1) * (max_docs + 1);
+    uint64_t* ho = hoff + si * (max_docs + 1);
     // the slot is free once its previous chunk's results left the device
-    if (!first_use[c & 1]) {
+    if (!first_use[si]) {
       ND_CUDA(cudaEventSynchronize(sl.d2h_done));  // host offsets buffer reuse
       ND_CUDA(cudaStreamWaitEvent(ctx->h2d, sl.d2h_done, 0));
     }
-    first_use[c & 1] = false;
+    first_use[si] = false;
     for (uint64_t i = 0; i <= m; ++i) ho[i] = offsets[d0 + i] - offsets[d0];
+    mark(c, 0, ctx->h2d);
     ND_CUDA(cudaMemcpyAsync(dtext, bytes + offsets[d0], tb, cudaMemcpyHostToDevice, ctx->h2d));
     ND_CUDA(cudaMemcpyAsync(doff, ho, (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->h2d));
     ND_CUDA(cudaEventRecord(sl.h2d_done, ctx->h2d));
+    mark(c, 1, ctx->h2d);
+    if (trace) tr[c].bytes = tb;
     // K1j runs its chunks one after another on one stream: two pass-major
     // launches side by side would interleave their passes' code again
-    cudaStream_t comp = ctx->fam.jit ? ctx->slot[0].comp : sl.comp;
+    // (ND_K1J_SIG_STREAMS=3: one stream per slot, for A/B runs)
+    static const bool per_slot = [] {
+      const char* v = getenv("ND_K1J_SIG_STREAMS");
+      return v && v[0] == '3';
+    }();
+    cudaStream_t comp = (ctx->fam.jit && !per_slot) ? ctx->slot[0].comp : sl.comp;
     ND_CUDA(cudaStreamWaitEvent(comp, sl.h2d_done, 0));
+    mark(c, 2, comp);
     launch_signatures(ctx->fam, dtext, doff, m, bands, rows, K, dsig, dband, sl.scratch,
                       comp, /*check_short=*/false, ho);
     ND_CUDA(cudaEventRecord(sl.comp_done, comp));
+    mark(c, 3, comp);
     ND_CUDA(cudaStreamWaitEvent(ctx->d2h, sl.comp_done, 0));
+    mark(c, 4, ctx->d2h);
     ND_CUDA(cudaMemcpyAsync(sig_out + d0 * H, dsig, m * H * sizeof(uint32_t),
                             cudaMemcpyDeviceToHost, ctx->d2h));
     if (band_out)
       ND_CUDA(cudaMemcpyAsync(band_out + d0 * bands, dband, m * bands * sizeof(uint32_t),
                               cudaMemcpyDeviceToHost, ctx->d2h));
     ND_CUDA(cudaEventRecord(sl.d2h_done, ctx->d2h));
+    mark(c, 5, ctx->d2h);
+  }
+  if (trace) {
+    ND_CUDA(cudaStreamSynchronize(ctx->d2h));
+    for (size_t c = 0; c < tr.size(); ++c) {
+      float t[6];
+      for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&t[k], t0ev, tr[c].e[k]);
+      fprintf(stderr, "chunk %zu %6.1f MB  in %7.2f-%7.2f  k1 %7.2f-%7.2f  out %7.2f-%7.2f ms\n", c,
+              tr[c].bytes / 1048576.0, t[0], t[1], t[2], t[3], t[4], t[5]);
+      for (auto& e : tr[c].e) cudaEventDestroy(e);
+    }
+    cudaEventDestroy(t0ev);
   }
   cudaEvent_t end;
   ND_CUDA(cudaEventCreateWithFlags(&end, cudaEventDisableTiming));

@@ -13,12 +13,13 @@ struct nd_ctx {
   cudaStream_t stream = nullptr;  // ordering stream for all device work
   bool own_stream = false;
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy engines for host entry points
-  struct Slot {  // double-buffered chunk of the host pipeline
+  static constexpr int kSlots = 3;
+  struct Slot {  // triple-buffered chunk of the host pipeline (nd_signatures)
     ndb::DevBuf text, off, sig, band;
     ndb::SigScratch scratch;
     cudaStream_t comp = nullptr;
     cudaEvent_t h2d_done = nullptr, comp_done = nullptr, d2h_done = nullptr;
-  } slot[2];
+  } slot[kSlots];
   ndb::PinnedBuf pinned_off;
   ndb::DevBuf ring[3];          // text chunks streaming through h2d_signatures
   cudaStream_t ring_stream[3] = {nullptr, nullptr, nullptr};

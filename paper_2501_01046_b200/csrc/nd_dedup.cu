@@ -124,18 +124,25 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   cudaStream_t s = ctx->stream;
   ctx->ensure_streams();
   const uint32_t H = ctx->fam.H;
+  const uint32_t L = ctx->fam.L;
+  if (offsets[n] < offsets[0])
+    fail(ND_ERR_SHORT, "document offsets decrease: a document has fewer units than the shingle length");
   uint64_t* d_off = st.offs.as<uint64_t>(n + 1);
   uint64_t* h_off = static_cast<uint64_t*>(ctx->pinned_off.get((n + 1) * sizeof(uint64_t)));
-  for (uint64_t i = 0; i <= n; ++i) h_off[i] = offsets[i] - offsets[0];
-  // chunks of <= h2d_chunk_bytes of text (a longer document is a chunk of its own)
+  // chunks of <= h2d_chunk_bytes of text (a longer document is a chunk of its
+  // own), bounds by binary search; each chunk's relative offsets are filled,
+  // its documents checked and its offsets copied just before its text, so the
+  // first copy waits for one chunk's host work, not the batch's
   std::vector<std::pair<uint64_t, uint64_t>> chunks;
   uint64_t max_bytes = 0;
   for (uint64_t d0 = 0; d0 < n;) {
-    uint64_t d1 = d0 + 1;
     const uint64_t cap = h2d_chunk_bytes(ctx->fam, chunks.size());
-    while (d1 < n && h_off[d1 + 1] - h_off[d0] <= cap) ++d1;
+    const uint64_t* it = std::upper_bound(offsets + d0 + 1, offsets + n + 1, offsets[d0] + cap);
+    const uint64_t d1 = std::max<uint64_t>(d0 + 1, static_cast<uint64_t>(it - offsets) - 1);
+    if (offsets[d1] < offsets[d0])
+      fail(ND_ERR_SHORT, "document offsets decrease: a document has fewer units than the shingle length");
     chunks.push_back({d0, d1});
-    max_bytes = std::max(max_bytes, h_off[d1] - h_off[d0]);
+    max_bytes = std::max(max_bytes, offsets[d1] - offsets[d0]);
     d0 = d1;
   }
   // the text streams through a ring of kRing chunk buffers: only signatures
@@ -152,11 +159,28 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   for (auto& e : k1_done) ND_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   ND_CUDA(cudaEventRecord(start, s));
   ND_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
-  ND_CUDA(cudaMemcpyAsync(d_off, h_off, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->h2d));
   std::vector<cudaEvent_t> evs;
+  auto drain_and_fail = [&](int code, const std::string& msg) {
+    cudaStreamSynchronize(ctx->h2d);
+    for (auto rs : ctx->ring_stream) cudaStreamSynchronize(rs);
+    for (auto ev : evs) cudaEventDestroy(ev);
+    for (auto e : k1_done) cudaEventDestroy(e);
+    cudaEventDestroy(start);
+    fail(code, msg);
+  };
   for (size_t c = 0; c < chunks.size(); ++c) {
     const auto [d0, d1] = chunks[c];
     const int r = static_cast<int>(c % kRing);
+    for (uint64_t i = d0; i < d1; ++i) {
+      // (every document is checked before its chunk is signed; as before, a
+      // decreasing offset reads as a short document)
+      if (offsets[i + 1] < offsets[i] || offsets[i + 1] - offsets[i] < L)
+        drain_and_fail(ND_ERR_SHORT, "document " + std::to_string(i) +
+                                         " has fewer units than the shingle length");
+    }
+    for (uint64_t i = (c == 0 ? d0 : d0 + 1); i <= d1; ++i) h_off[i] = offsets[i] - offsets[0];
+    ND_CUDA(cudaMemcpyAsync(d_off + d0, h_off + d0, (d1 - d0 + 1) * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice, ctx->h2d));
     // (ND_K1J_STREAMS=1: K1j chunks on one stream, as signatures_host does;
     // here the ring's three streams measured faster: C3 10M docs from host
     // 1.39 s vs 1.60 s, C2 82 vs 85 ms)
@@ -462,9 +486,6 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
     st.valid = false;
     set_doc_ids(st, doc_ids, n);
     if (n == 0) fail(ND_ERR_CONFIG, "no documents survive preprocessing; nothing to deduplicate");
-    for (uint64_t i = 0; i < n; ++i)
-      if (offsets[i + 1] < offsets[i] || offsets[i + 1] - offsets[i] < p.shingle_len)
-        fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has fewer units than the shingle length");
     st.K = bucket_count_for(p, n);
     st.sig_on_host = false;
     st.host_sig.clear();
@@ -472,6 +493,9 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
     st.intervals = 1;
     const uint64_t budget = hbm_budget_of(ctx);
     if (n * row_bytes_of(p) + n * p.bands * kRecBytes > budget) {
+      for (uint64_t i = 0; i < n; ++i)
+        if (offsets[i + 1] < offsets[i] || offsets[i + 1] - offsets[i] < p.shingle_len)
+          fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has fewer units than the shingle length");
       dedup_out_of_core(ctx, st, p, bytes, offsets, n, budget, stats);
       return;
     }
@@ -491,9 +515,6 @@ int nd_signatures_h2d(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets
     ctx->require_family();
     if (d_band && (bands == 0 || rows == 0 || static_cast<uint64_t>(bands) * rows != ctx->fam.H))
       fail(ND_ERR_CONFIG, "banding shape does not match the hash count");
-    for (uint64_t i = 0; i < n; ++i)
-      if (offsets[i + 1] < offsets[i] || offsets[i + 1] - offsets[i] < ctx->fam.L)
-        fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has fewer units than the shingle length");
     h2d_signatures(ctx, ctx->h2d_state, bytes, offsets, n, bands, rows, K, d_sig, d_band);
     ND_CUDA(cudaStreamSynchronize(ctx->stream));
   });
