@@ -178,7 +178,8 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "k1j(const u8* __restrict__ text, const u64* __restrict__ offsets,\n"
        "    const u32* __restrict__ order, const u32* __restrict__ item_doc,\n"
        "    const u64* __restrict__ item_off, u32 n_items, u32 seg_len,\n"
-       "    u32* __restrict__ sig, u64* __restrict__ counter, float c5) {\n"
+       "    u32* __restrict__ sig, u64* __restrict__ counter, float c5,\n"
+       "    u32* __restrict__ pass_flag, u32 epoch) {\n"
        "  const i64 KSEG = seg_len;  // windows per work item\n"
        "  // c5 = 2^-5 arrives as a parameter so that it sits in a register and\n"
        "  // every FFMA keeps its function constant as the immediate\n"
@@ -188,6 +189,8 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "  // execute one pass's code at a time (the instruction cache holds one\n"
        "  // pass, not all of them)\n"
        "  for (u32 P = 0; P < NPASS; ++P) {\n"
+       "  // the chunk gate (K1Gate): the next launch may start filling SMs\n"
+       "  if (P == NPASS - 1 && lane == 0 && pass_flag) atomicMax(pass_flag, epoch);\n"
        "  u64 base = 0;\n"
        "  if (lane == 0) base = atomicAdd(counter + P, 32ull);\n"
        "  base = __shfl_sync(0xffffffffu, base, 0);\n"
@@ -423,15 +426,17 @@ uint64_t k1_jit_resident_warps(const void* handle) {
 void k1_jit_launch(const void* handle, const uint8_t* d_text, const uint64_t* d_offsets,
                    const uint32_t* order, const uint32_t* item_doc, const uint64_t* item_off,
                    uint32_t n_items, uint32_t seg_len, uint32_t* d_sig,
-                   unsigned long long* counter, cudaStream_t s) {
+                   unsigned long long* counter, cudaStream_t s, const K1Gate* gate) {
   const JitKernel* k = static_cast<const JitKernel*>(handle);
   const uint64_t warps = (static_cast<uint64_t>(n_items) + 31) / 32;
   uint64_t blocks = (warps + kJitThreads / 32 - 1) / (kJitThreads / 32);
   blocks = std::min<uint64_t>(blocks, static_cast<uint64_t>(k->per_sm) * sm_count());
   ND_CUDA(cudaMemsetAsync(counter, 0, k->passes * sizeof(unsigned long long), s));  // one per pass
   float c5 = 0.03125f;
+  unsigned int* pass_flag = gate ? gate->flag : nullptr;
+  unsigned int epoch = gate ? gate->epoch : 0u;
   void* args[] = {&d_text, &d_offsets, &order, &item_doc, &item_off, &n_items, &seg_len, &d_sig,
-                  &counter, &c5};
+                  &counter, &c5, &pass_flag, &epoch};
   ND_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(k->fn), dim3(static_cast<unsigned>(blocks)),
                            dim3(kJitThreads), args, 0, s));
   ND_CHECK_LAUNCH();

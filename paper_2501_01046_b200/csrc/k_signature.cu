@@ -192,6 +192,16 @@ __global__ void k_item_len_keys(const uint64_t* __restrict__ offsets,
   vals[i] = static_cast<uint32_t>(i);
 }
 
+// one thread holds its stream until *flag >= epoch (bounded: after ~4 s it
+// gives up, and the next launch simply runs alongside)
+__global__ void k_gate_wait(const unsigned int* __restrict__ flag, unsigned int epoch) {
+  const long long t0 = clock64();
+  while (*reinterpret_cast<const volatile unsigned int*>(flag) < epoch) {
+    if (clock64() - t0 > 8000000000ll) break;
+    __nanosleep(1000);
+  }
+}
+
 __global__ void k_iota_docs(uint32_t* __restrict__ v, uint64_t n) {
   uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i < n) v[i] = static_cast<uint32_t>(i);
@@ -908,10 +918,15 @@ Launcher pick_launcher(bool int_arith, uint32_t Hp, bool codepoint, bool exact) 
 }  // namespace
 
 
+void k1_gate_wait(const unsigned int* flag, unsigned int epoch, cudaStream_t s) {
+  k_gate_wait<<<1, 1, 0, s>>>(flag, epoch);
+  ND_CHECK_LAUNCH();
+}
+
 void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint64_t* d_offsets,
                        uint64_t n, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
                        uint32_t* d_band, SigScratch& sc, cudaStream_t s, bool check_short,
-                       const uint64_t* h_offsets) {
+                       const uint64_t* h_offsets, const K1Gate* gate) {
   if (n == 0) return;
   if (fam.L == 0 || fam.L > static_cast<uint32_t>(kLMax))
     fail(ND_ERR_CONFIG, "shingle length must be in [1, 64] on the GPU path");
@@ -1079,7 +1094,7 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     radix_sort_u32(keys, order, items, 14, sc.sort, s);
     k1_jit_launch(fam.jit, static_cast<const uint8_t*>(d_text), d_offsets, order, item_doc,
                   item_off, static_cast<uint32_t>(items), seg_len, d_sig,
-                  sc.item_counter.as<unsigned long long>(k1_jit_passes(fam.jit)), s);
+                  sc.item_counter.as<unsigned long long>(k1_jit_passes(fam.jit)), s, gate);
     // band keys of every document from its finished row (keys is free again)
     if (d_band) launch_band_keys(d_sig, n, fam.H, bands, rows, K, d_band, keys, s);
     return;

@@ -47,7 +47,7 @@ int guarded_impl(nd_ctx* ctx, const std::function<void()>& fn) {
 using ndb::fail;
 
 nd_ctx::~nd_ctx() {
-  for (auto* b : {&fam_buf, &sig_in_text, &sig_in_off}) b->release();
+  for (auto* b : {&fam_buf, &sig_in_text, &sig_in_off, &gate_flag}) b->release();
   for (int i = 0; i < kSlots; ++i) {
     slot[i].text.release();
     slot[i].off.release();
@@ -77,6 +77,23 @@ nd_ctx::~nd_ctx() {
   if (h2d) cudaStreamDestroy(h2d);
   if (d2h) cudaStreamDestroy(d2h);
   if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+bool nd_ctx::gate_on() const {
+  const char* v = getenv("ND_K1J_GATE");  // read per call (A/B runs in one process)
+  const bool on = !(v && v[0] == '0');
+  return on && fam.jit && fam.unit == 0;
+}
+
+ndb::K1Gate* nd_ctx::next_gate(ndb::K1Gate& g) {
+  if (!gate_on()) return nullptr;
+  if (!gate_flag.ptr) {
+    ND_CUDA(cudaMemset(gate_flag.as<unsigned int>(1), 0, sizeof(unsigned int)));
+    gate_epoch = 0;
+  }
+  g.flag = static_cast<unsigned int*>(gate_flag.ptr);
+  g.epoch = ++gate_epoch;
+  return &g;
 }
 
 void nd_ctx::ensure_streams() {
@@ -168,18 +185,19 @@ void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets,
   // chunking: <= chunk_bytes(c) of text and <= kChunkDocs documents per chunk
   // (binary search over the offsets; a longer document is a chunk of its own)
   constexpr uint64_t kChunkDocs = 1ull << 20;
-  // optional ramp down at the end (ND_H2D_TAIL_DIV=d: a chunk takes at most
-  // 1/d of the text left, down to the first chunk's size; measured no faster
-  // on the C2 shard, the extra launch tails cost what the shorter last copy
-  // saves)
-  static const uint64_t tail_div = [] {
+  // ramp down at the end (ND_H2D_TAIL_DIV=d, default 2: a chunk takes at
+  // most 1/d of the text left, down to the first chunk's size) so the last
+  // copy out is short; with the chunk gate the extra launches' tails overlap
+  // (C2 shard: 74.7 -> 72.1 ms; without the gate no faster)
+  const uint64_t tail_div = [] {
     const char* v = getenv("ND_H2D_TAIL_DIV");
-    return static_cast<uint64_t>(v ? std::max(0, atoi(v)) : 0);
+    return static_cast<uint64_t>(v ? std::max(0, atoi(v)) : 2);
   }();
   const uint64_t first_cap = h2d_chunk_bytes(ctx->fam, 0);
+  const bool gated = ctx->gate_on();
   auto chunk_end = [&](uint64_t d0, size_t index) {
     uint64_t cap = h2d_chunk_bytes(ctx->fam, index);
-    if (tail_div && ctx->fam.jit)
+    if (tail_div && ctx->fam.jit && gated)
       cap = std::min(cap, std::max(first_cap, (offsets[n] - offsets[d0]) / tail_div));
     const uint64_t lim = std::min(n, d0 + kChunkDocs);
     // largest d1 in (d0, lim] with offsets[d1] - offsets[d0] <= cap
@@ -255,18 +273,25 @@ void signatures_host(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets,
     ND_CUDA(cudaEventRecord(sl.h2d_done, ctx->h2d));
     mark(c, 1, ctx->h2d);
     if (trace) tr[c].bytes = tb;
-    // K1j runs its chunks one after another on one stream: two pass-major
-    // launches side by side would interleave their passes' code again
-    // (ND_K1J_SIG_STREAMS=3: one stream per slot, for A/B runs)
+    // K1j chunks: two pass-major launches side by side would interleave
+    // their passes' code, so chunk c+1 is gated (K1Gate) until chunk c's
+    // first warp enters its last pass, on the other of two streams; the next
+    // launch then fills the SMs the last pass frees (ND_K1J_GATE=0: one
+    // stream, launches back to back; ND_K1J_SIG_STREAMS=3: ungated streams)
     static const bool per_slot = [] {
       const char* v = getenv("ND_K1J_SIG_STREAMS");
       return v && v[0] == '3';
     }();
-    cudaStream_t comp = (ctx->fam.jit && !per_slot) ? ctx->slot[0].comp : sl.comp;
+    K1Gate gate_buf;
+    K1Gate* gate = ctx->fam.jit && !per_slot ? ctx->next_gate(gate_buf) : nullptr;
+    cudaStream_t comp = !ctx->fam.jit || per_slot ? sl.comp
+                        : gate                   ? ctx->slot[c & 1].comp
+                                                 : ctx->slot[0].comp;
     ND_CUDA(cudaStreamWaitEvent(comp, sl.h2d_done, 0));
+    if (gate && c > 0) k1_gate_wait(gate->flag, gate->epoch - 1, comp);
     mark(c, 2, comp);
     launch_signatures(ctx->fam, dtext, doff, m, bands, rows, K, dsig, dband, sl.scratch,
-                      comp, /*check_short=*/false, ho);
+                      comp, /*check_short=*/false, ho, gate);
     ND_CUDA(cudaEventRecord(sl.comp_done, comp));
     mark(c, 3, comp);
     ND_CUDA(cudaStreamWaitEvent(ctx->d2h, sl.comp_done, 0));

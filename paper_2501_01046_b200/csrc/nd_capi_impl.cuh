@@ -21,6 +21,12 @@ struct nd_ctx {
     cudaEvent_t h2d_done = nullptr, comp_done = nullptr, d2h_done = nullptr;
   } slot[kSlots];
   ndb::PinnedBuf pinned_off;
+  ndb::DevBuf gate_flag;        // K1Gate flag of this context's chunked K1j launches
+  unsigned int gate_epoch = 0;
+  // a gate for the next chunked K1j launch (null flag: gating off,
+  // ND_K1J_GATE=0, or not a K1j family)
+  ndb::K1Gate* next_gate(ndb::K1Gate& g);
+  bool gate_on() const;
   ndb::DevBuf ring[3];          // text chunks streaming through h2d_signatures
   cudaStream_t ring_stream[3] = {nullptr, nullptr, nullptr};
   ndb::SigScratch ring_scratch[3];

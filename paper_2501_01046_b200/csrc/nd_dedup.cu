@@ -117,6 +117,13 @@ uint64_t id_of(const DedupState& st, uint32_t row) {
 // Host text -> device signatures/band keys: chunks (h2d_chunk_bytes) are copied
 // on the h2d stream into a ring of chunk buffers and signed on the ctx stream
 // as each lands (PCIe overlaps K1; the paper's double buffering).
+namespace {
+bool k1j_one_stream() {  // read per call (A/B runs in one process)
+  const char* v = getenv("ND_K1J_STREAMS");
+  return v && v[0] == '1';
+}
+}  // namespace
+
 void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uint64_t* offsets,
                     uint64_t n, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
                     uint32_t* d_band) {
@@ -135,8 +142,15 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
   // first copy waits for one chunk's host work, not the batch's
   std::vector<std::pair<uint64_t, uint64_t>> chunks;
   uint64_t max_bytes = 0;
+  // gated K1j chunks (K1Gate, as in signatures_host) also ramp down at the end
+  // (off by default here: C3 from host 3.452 s gated vs 3.451 s ungated, C2
+  // 74.4 vs 73.2 ms; ND_K1J_RING_GATE=1 turns it on)
+  const char* rg = getenv("ND_K1J_RING_GATE");
+  const bool gated = ctx->gate_on() && !k1j_one_stream() && rg && rg[0] == '1';
+  const uint64_t first_cap = h2d_chunk_bytes(ctx->fam, 0);
   for (uint64_t d0 = 0; d0 < n;) {
-    const uint64_t cap = h2d_chunk_bytes(ctx->fam, chunks.size());
+    uint64_t cap = h2d_chunk_bytes(ctx->fam, chunks.size());
+    if (gated) cap = std::min(cap, std::max(first_cap, (offsets[n] - offsets[d0]) / 2));
     const uint64_t* it = std::upper_bound(offsets + d0 + 1, offsets + n + 1, offsets[d0] + cap);
     const uint64_t d1 = std::max<uint64_t>(d0 + 1, static_cast<uint64_t>(it - offsets) - 1);
     if (offsets[d1] < offsets[d0])
@@ -181,13 +195,9 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
     for (uint64_t i = (c == 0 ? d0 : d0 + 1); i <= d1; ++i) h_off[i] = offsets[i] - offsets[0];
     ND_CUDA(cudaMemcpyAsync(d_off + d0, h_off + d0, (d1 - d0 + 1) * sizeof(uint64_t),
                             cudaMemcpyHostToDevice, ctx->h2d));
-    // (ND_K1J_STREAMS=1: K1j chunks on one stream, as signatures_host does;
-    // here the ring's three streams measured faster: C3 10M docs from host
-    // 1.39 s vs 1.60 s, C2 82 vs 85 ms)
-    static const bool one = [] {
-      const char* v = getenv("ND_K1J_STREAMS");
-      return v && v[0] == '1';
-    }();
+    // (ND_K1J_STREAMS=1: K1j chunks on one stream; the ring's three streams
+    // measured faster: C3 from host 3.45 vs 3.64 s, C2 73 vs 75 ms)
+    const bool one = k1j_one_stream();
     cudaStream_t cs = (ctx->fam.jit && one) ? ctx->ring_stream[0] : ctx->ring_stream[r];
     if (c >= kRing) ND_CUDA(cudaStreamWaitEvent(ctx->h2d, k1_done[r], 0));  // slot free again
     ND_CUDA(cudaMemcpyAsync(ring[r], bytes + offsets[0] + h_off[d0], h_off[d1] - h_off[d0],
@@ -197,11 +207,14 @@ void h2d_signatures(nd_ctx* ctx, DedupState& st, const uint8_t* bytes, const uin
     ND_CUDA(cudaEventRecord(ev, ctx->h2d));
     ND_CUDA(cudaStreamWaitEvent(cs, ev, 0));
     evs.push_back(ev);
+    K1Gate gate_buf;
+    K1Gate* gate = gated ? ctx->next_gate(gate_buf) : nullptr;
+    if (gate && c > 0) k1_gate_wait(gate->flag, gate->epoch - 1, cs);
     // offsets stay batch-absolute: the kernel reads text + offset, so the
     // text pointer is the slot shifted back by the chunk's first offset
     launch_signatures(ctx->fam, ring[r] - h_off[d0], d_off + d0, d1 - d0, bands, rows, K,
                       d_sig + d0 * H, d_band ? d_band + d0 * bands : nullptr,
-                      ctx->ring_scratch[r], cs, false, h_off + d0);
+                      ctx->ring_scratch[r], cs, false, h_off + d0, gate);
     ND_CUDA(cudaEventRecord(k1_done[r], cs));
   }
   for (int r = 0; r < kRing; ++r) ND_CUDA(cudaStreamWaitEvent(s, k1_done[r], 0));

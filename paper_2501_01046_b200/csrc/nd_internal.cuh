@@ -136,10 +136,19 @@ double k1_jit_compile_seconds(const void* handle);
 uint32_t k1_jit_passes(const void* handle);
 std::string k1_jit_source(const nd_hash_fn* fns, uint32_t H, uint32_t L);
 uint64_t k1_jit_resident_warps(const void* handle);
+// Chunk gate: a K1j launch raises *flag to its epoch when its first warp
+// enters the last pass; k1_gate_wait holds a stream until then, so the next
+// chunk's launch fills the SMs the last pass frees instead of interleaving
+// its passes with the running launch's (k_signature.cu)
+struct K1Gate {
+  unsigned int* flag = nullptr;
+  unsigned int epoch = 0;
+};
+void k1_gate_wait(const unsigned int* flag, unsigned int epoch, cudaStream_t s);
 void k1_jit_launch(const void* handle, const uint8_t* d_text, const uint64_t* d_offsets,
                    const uint32_t* order, const uint32_t* item_doc, const uint64_t* item_off,
                    uint32_t n_items, uint32_t seg_len, uint32_t* d_sig,
-                   unsigned long long* counter, cudaStream_t s);
+                   unsigned long long* counter, cudaStream_t s, const K1Gate* gate = nullptr);
 // UTF-8 -> codepoint units (k_utf8.cu): units_out[unit_off_out[d] ..
 // unit_off_out[d+1]) are document d's units (decode_codepoints, text.cpp:101-113).
 void decode_codepoints_device(const uint8_t* d_text, const uint64_t* d_offsets, uint64_t n,
@@ -151,7 +160,8 @@ void decode_codepoints_device(const uint8_t* d_text, const uint64_t* d_offsets, 
 void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint64_t* d_offsets,
                        uint64_t n, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
                        uint32_t* d_band, SigScratch& scratch, cudaStream_t stream,
-                       bool check_short, const uint64_t* h_offsets);
+                       bool check_short, const uint64_t* h_offsets,
+                       const K1Gate* gate = nullptr);
 
 // Stable LSD radix sort of (key, value) pairs by the low key_bits bits.
 void radix_sort_u32(uint32_t* keys, uint32_t* vals, uint64_t n, int key_bits, SortScratch& sc,

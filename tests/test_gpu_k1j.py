@@ -180,3 +180,47 @@ def test_k1j_two_words_per_iteration(ctx, oracle, monkeypatch, L):
     out = _both(ctx, monkeypatch, data, offs, fam)
     assert np.array_equal(out["1"][0], out["0"][0])
     assert np.array_equal(out["1"][0], oracle.signatures(data, offs, oracle.derive_family(5, 64, L), L=L))
+
+
+def test_chunk_gate_host_pipelines(ctx, oracle, monkeypatch):
+    # ~150 MB of text: several chunks through nd_signatures (gated K1j
+    # launches on two streams, ramp down at the end) and through nd_dedup's
+    # ring (gated on request); every configuration gives the same rows
+    from paper_2501_01046_b200 import pipeline
+
+    rng = np.random.default_rng(77)
+    n = 70000
+    lens = rng.integers(1200, 3000, size=n)
+    offs = np.zeros(n + 1, np.uint64)
+    offs[1:] = np.cumsum(lens)
+    data = rng.integers(97, 123, size=int(offs[-1]), dtype=np.uint8)
+    fam = minhash.derive_family(5, 128, 5)
+    res = {}
+    for name, env in {"gate": {}, "nogate": {"ND_K1J_GATE": "0"},
+                      "notail": {"ND_H2D_TAIL_DIV": "0"}}.items():
+        for k in ("ND_K1J_GATE", "ND_H2D_TAIL_DIV"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        res[name] = minhash.signatures_packed(data, offs, fam, 16, 8, 1000, ctx=ctx)
+    for k in ("ND_K1J_GATE", "ND_H2D_TAIL_DIV"):
+        monkeypatch.delenv(k, raising=False)
+    for name in ("nogate", "notail"):
+        assert np.array_equal(res[name][0], res["gate"][0]) and np.array_equal(res[name][1], res["gate"][1])
+    idx = rng.choice(n, 300, replace=False)
+    for i in idx[:40]:
+        o = np.array([0, offs[i + 1] - offs[i]], np.uint64)
+        assert np.array_equal(res["gate"][0][i], oracle.signatures(
+            data[int(offs[i]):int(offs[i + 1])].copy(), o, oracle.derive_family(5, 128))[0])
+    got = {}
+    for name, env in {"ring": {}, "ring_gate": {"ND_K1J_RING_GATE": "1"}}.items():
+        monkeypatch.delenv("ND_K1J_RING_GATE", raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        rep = pipeline.dedup_packed(data, offs, pipeline.RunConfig(), bucket_count=1000, ctx=ctx)
+        sig = np.empty((n, 128), np.uint32)
+        ctx.check(ctx.lib.nd_dedup_fetch_signatures(ctx.h, sig.ctypes.data_as(_lib.u32p), None))
+        got[name] = (rep.stats["candidate_pairs"], sig)
+    monkeypatch.delenv("ND_K1J_RING_GATE", raising=False)
+    assert got["ring"][0] == got["ring_gate"][0]
+    assert np.array_equal(got["ring"][1], res["gate"][0]) and np.array_equal(got["ring_gate"][1], res["gate"][0])
