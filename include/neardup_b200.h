@@ -145,8 +145,9 @@ int nd_family_upload(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t hash_count,
 const char* nd_k1_kernel(nd_ctx* ctx);
 /* How the last nd_dedup / nd_dedup_device compared: "global" (one block join
  * over all rows, the cells counted for the reference's counters; the
- * in-memory single-device default), "cells" (the per-cell joins: out-of-core
- * intervals, device groups, ND_K3=cells) or "" (no valid dedup). */
+ * in-memory default, on a device group each block joined by one shard),
+ * "cells" (the per-cell joins: out-of-core intervals, thresholds with more
+ * than 64 blocks, ND_K3=cells) or "" (no valid dedup). */
 const char* nd_dedup_compare_kind(nd_ctx* ctx);
 /* The CUDA source K1j compiles for a family (no device needed): writes up to
  * cap bytes (NUL-terminated) into out and returns the full length, or -1

@@ -74,31 +74,30 @@ __global__ void k_gj_fps(const uint32_t* __restrict__ sig, uint64_t n, uint32_t 
 
 // chain row i into the slot of its fingerprint: table entries and links are
 // (fingerprint << 32 | row) of the row chained before (kNoRow: end)
-__global__ void k_gj_insert(const uint32_t* __restrict__ fp, uint64_t n,
-                            unsigned long long* __restrict__ table, int tbits,
-                            unsigned long long* __restrict__ link) {
+__global__ void k_gj_insert(const FpCol fc, uint64_t n, unsigned long long* __restrict__ table,
+                            int tbits, unsigned long long* __restrict__ link) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
-  const uint32_t f = fp[i];
+  const uint32_t f = fc.get(i);
   const uint32_t slot = (f * 0x9E3779B1u) >> (32 - tbits);
   link[i] = atomicExch(&table[slot], (static_cast<unsigned long long>(f) << 32) | i);
 }
 
 template <int BW>
-__device__ __noinline__ void gj_check(const uint32_t* __restrict__ sig, uint32_t H,
-                                      const uint32_t* __restrict__ band, uint32_t B, uint32_t d,
+__device__ __noinline__ void gj_check(const SigView& sv, const SigView& bv, uint32_t d,
                                       uint32_t e, uint32_t k, uint32_t min_match, int nb,
                                       uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
                                       unsigned long long* __restrict__ count, uint64_t cap,
                                       unsigned long long* __restrict__ emitted) {
+  const uint32_t H = sv.H, B = bv.H;
   const bool vec = (H & 3) == 0;
-  const uint32_t* a = sig + static_cast<uint64_t>(d) * H;
-  const uint32_t* b = sig + static_cast<uint64_t>(e) * H;
+  const uint32_t* a = sv.row(d);
+  const uint32_t* b = sv.row(e);
   if (!same_block<BW>(a + k * BW, b + k * BW, vec)) return;  // fingerprint collision
   for (uint32_t j = 0; j < k; ++j)
     if (same_block<BW>(a + j * BW, b + j * BW, vec)) return;  // checked at block j
-  const uint32_t* ba = band + static_cast<uint64_t>(d) * B;
-  const uint32_t* bb = band + static_cast<uint64_t>(e) * B;
+  const uint32_t* ba = bv.row(d);
+  const uint32_t* bb = bv.row(e);
   uint32_t shared = 0;
   for (uint32_t j = 0; j < B; ++j) shared += __ldg(ba + j) == __ldg(bb + j);
   if (shared == 0) return;  // no common cell: the reference never compares them
@@ -110,22 +109,20 @@ __device__ __noinline__ void gj_check(const uint32_t* __restrict__ sig, uint32_t
 }
 
 template <int BW>
-__global__ void k_gj_walk(const uint32_t* __restrict__ fp, uint64_t n,
-                          const unsigned long long* __restrict__ link,
-                          const uint32_t* __restrict__ sig, uint32_t H,
-                          const uint32_t* __restrict__ band, uint32_t B, uint32_t k,
-                          uint32_t min_match, int nb, uint64_t* __restrict__ out_key,
-                          uint32_t* __restrict__ out_m, unsigned long long* __restrict__ count,
-                          uint64_t cap, unsigned long long* __restrict__ emitted) {
+__global__ void k_gj_walk(const FpCol fc, uint64_t n, const unsigned long long* __restrict__ link,
+                          const SigView sv, const SigView bv, uint32_t k, uint32_t min_match,
+                          int nb, uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_m,
+                          unsigned long long* __restrict__ count, uint64_t cap,
+                          unsigned long long* __restrict__ emitted) {
   const uint64_t d = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (d >= n) return;
-  const uint32_t f = fp[d];
+  const uint32_t f = fc.get(d);
   unsigned long long c = link[d];
   while (static_cast<uint32_t>(c) != kNoRow) {
     const uint32_t e = static_cast<uint32_t>(c);
     if (static_cast<uint32_t>(c >> 32) == f)
-      gj_check<BW>(sig, H, band, B, static_cast<uint32_t>(d), e, k, min_match, nb, out_key, out_m,
-                   count, cap, emitted);
+      gj_check<BW>(sv, bv, static_cast<uint32_t>(d), e, k, min_match, nb, out_key, out_m, count,
+                   cap, emitted);
     c = __ldg(link + e);
   }
 }
@@ -137,13 +134,17 @@ __global__ void k_cell_hist(const uint32_t* __restrict__ band, uint64_t n, uint3
     atomicAdd(&cnt[static_cast<uint64_t>(i % B) * K + band[i]], 1u);
 }
 
-// out[0] = sum n(n-1)/2, out[1] = cells with n >= 2, out[2] = their records
-__global__ void k_cell_stats(const uint32_t* __restrict__ cnt, uint64_t cells,
-                             unsigned long long* __restrict__ out) {
+// out[0] = sum n(n-1)/2, out[1] = cells with n >= 2, out[2] = their records;
+// n = the sum over `parts` histograms (one per shard of a device group)
+__global__ void k_cell_stats(const uint32_t* __restrict__ cnt0, const uint32_t* const* __restrict__ cnts,
+                             uint32_t parts, uint64_t cells, unsigned long long* __restrict__ out) {
   unsigned long long p = 0, c = 0, r = 0;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < cells;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long v = cnt[i];
+    unsigned long long v = 0;
+    if (cnt0) v = cnt0[i];
+    else
+      for (uint32_t q = 0; q < parts; ++q) v += cnts[q][i];
     if (v >= 2) {
       p += v * (v - 1) / 2;
       c += 1;
@@ -164,24 +165,36 @@ __global__ void k_cell_stats(const uint32_t* __restrict__ cnt, uint64_t cells,
 }
 
 template <int BW>
-void gj_blocks(GJoin& g, const uint32_t* sig, const uint32_t* band, uint64_t n, uint32_t H,
-               uint32_t B, uint32_t NB, uint32_t mm, int nb, uint64_t* out_key, uint32_t* out_m,
-               unsigned long long* count, uint64_t cap, unsigned long long* emitted,
-               cudaStream_t s) {
+void gj_blocks(GJoin& g, const FpCols& fc, const SigView& sv, const SigView& bv, uint64_t n,
+               const std::vector<uint32_t>& blocks, uint32_t mm, int nb, uint64_t* out_key,
+               uint32_t* out_m, unsigned long long* count, uint64_t cap,
+               unsigned long long* emitted, cudaStream_t s) {
   const unsigned tb = 256;
-  const unsigned blocks = static_cast<unsigned>((n + tb - 1) / tb);
-  k_gj_fps<BW><<<std::min<uint64_t>(blocks, 64ull * sm_count()), tb, 0, s>>>(sig, n, H, NB,
-                                                                           g.fps);
-  ND_CHECK_LAUNCH();
-  for (uint32_t k = 0; k < NB; ++k) {
-    const uint32_t* f = g.fps + static_cast<uint64_t>(k) * n;
+  const unsigned grid = static_cast<unsigned>((n + tb - 1) / tb);
+  for (uint32_t k : blocks) {
+    FpCol col;
+    col.base = fc.base0 ? fc.base0 + static_cast<uint64_t>(k) * n : nullptr;
+    col.bases = fc.bases;
+    col.row_base = fc.row_base;
+    col.world = fc.world;
+    col.k = k;
     ND_CUDA(cudaMemsetAsync(g.table, 0xFF, (uint64_t{1} << g.tbits) * 8, s));
-    k_gj_insert<<<blocks, tb, 0, s>>>(f, n, g.table, g.tbits, g.link);
+    k_gj_insert<<<grid, tb, 0, s>>>(col, n, g.table, g.tbits, g.link);
     ND_CHECK_LAUNCH();
-    k_gj_walk<BW><<<blocks, tb, 0, s>>>(f, n, g.link, sig, H, band, B, k, mm, nb, out_key, out_m,
-                                        count, cap, emitted);
+    k_gj_walk<BW><<<grid, tb, 0, s>>>(col, n, g.link, sv, bv, k, mm, nb, out_key, out_m, count,
+                                      cap, emitted);
     ND_CHECK_LAUNCH();
   }
+}
+
+template <int BW>
+void gj_fps_launch(const uint32_t* sig, uint64_t n, uint32_t H, uint32_t NB, uint32_t* fps,
+                   cudaStream_t s) {
+  const unsigned tb = 256;
+  const uint64_t blocks = (n + tb - 1) / tb;
+  k_gj_fps<BW><<<static_cast<unsigned>(std::min<uint64_t>(blocks, 64ull * sm_count())), tb, 0,
+                 s>>>(sig, n, H, NB, fps);
+  ND_CHECK_LAUNCH();
 }
 
 }  // namespace
@@ -202,20 +215,70 @@ bool global_join_eligible(uint64_t n, uint32_t H, uint32_t B, uint32_t K, uint32
   return need < free_b / 10 * 8;
 }
 
-void gj_cell_counts(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint32_t K,
-                    cudaStream_t s) {
+void gj_cell_hist(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint32_t K,
+                  cudaStream_t s) {
   const uint64_t cells = static_cast<uint64_t>(B) * K;
   uint32_t* cnt = g.cnt.as<uint32_t>(cells + 1);
-  g.acc_d = reinterpret_cast<unsigned long long*>(g.acc.as<uint64_t>(4));
-  ND_CUDA(cudaMemsetAsync(g.acc_d, 0, 4 * sizeof(uint64_t), s));
   ND_CUDA(cudaMemsetAsync(cnt, 0, cells * 4, s));
-  const int grid = 8 * sm_count();
   if (n) {
-    k_cell_hist<<<grid, 256, 0, s>>>(band, n, B, K, cnt);
+    k_cell_hist<<<8 * sm_count(), 256, 0, s>>>(band, n, B, K, cnt);
     ND_CHECK_LAUNCH();
   }
-  k_cell_stats<<<grid, 256, 0, s>>>(cnt, cells, g.acc_d);
+}
+
+void gj_reset(GJoin& g, cudaStream_t s) {
+  g.acc_d = reinterpret_cast<unsigned long long*>(g.acc.as<uint64_t>(4));
+  ND_CUDA(cudaMemsetAsync(g.acc_d, 0, 4 * sizeof(uint64_t), s));
+}
+
+void gj_cell_stats(GJoin& g, const uint32_t* const* d_cnts, uint32_t parts, uint64_t cells,
+                   cudaStream_t s) {
+  k_cell_stats<<<8 * sm_count(), 256, 0, s>>>(nullptr, d_cnts, parts, cells, g.acc_d);
   ND_CHECK_LAUNCH();
+}
+
+void gj_cell_counts(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint32_t K,
+                    cudaStream_t s) {
+  gj_reset(g, s);
+  gj_cell_hist(g, band, n, B, K, s);
+  k_cell_stats<<<8 * sm_count(), 256, 0, s>>>(static_cast<const uint32_t*>(g.cnt.ptr), nullptr, 1,
+                                              static_cast<uint64_t>(B) * K, g.acc_d);
+  ND_CHECK_LAUNCH();
+}
+
+void gj_fps(const uint32_t* sig, uint64_t n, uint32_t H, uint32_t mm, uint32_t* fps,
+            cudaStream_t s) {
+  uint32_t NB = 0;
+  int BW = 1;
+  if (mm <= H) join_block_shape(H, mm, &NB, &BW);
+  if (!n || !NB) return;
+  switch (BW) {
+    case 8: gj_fps_launch<8>(sig, n, H, NB, fps, s); break;
+    case 4: gj_fps_launch<4>(sig, n, H, NB, fps, s); break;
+    case 2: gj_fps_launch<2>(sig, n, H, NB, fps, s); break;
+    default: gj_fps_launch<1>(sig, n, H, NB, fps, s);
+  }
+}
+
+void gj_join(GJoin& g, const FpCols& fc, const SigView& sv, const SigView& bv, uint64_t n,
+             uint32_t mm, const std::vector<uint32_t>& blocks, int nb, uint64_t* out_key,
+             uint32_t* out_m, unsigned long long* count, uint64_t cap, cudaStream_t s) {
+  const uint32_t H = sv.H;
+  uint32_t NB = 0;
+  int BW = 1;
+  if (mm <= H) join_block_shape(H, mm, &NB, &BW);
+  ND_CUDA(cudaMemsetAsync(g.acc_d + 3, 0, sizeof(uint64_t), s));
+  if (n < 2 || NB == 0 || blocks.empty()) return;
+  g.tbits = std::max(10, bits_for(n - 1));
+  g.table = reinterpret_cast<unsigned long long*>(g.table_buf.as<uint64_t>(uint64_t{1} << g.tbits));
+  g.link = reinterpret_cast<unsigned long long*>(g.link_buf.as<uint64_t>(n));
+  unsigned long long* emitted = g.acc_d + 3;
+  switch (BW) {
+    case 8: gj_blocks<8>(g, fc, sv, bv, n, blocks, mm, nb, out_key, out_m, count, cap, emitted, s); break;
+    case 4: gj_blocks<4>(g, fc, sv, bv, n, blocks, mm, nb, out_key, out_m, count, cap, emitted, s); break;
+    case 2: gj_blocks<2>(g, fc, sv, bv, n, blocks, mm, nb, out_key, out_m, count, cap, emitted, s); break;
+    default: gj_blocks<1>(g, fc, sv, bv, n, blocks, mm, nb, out_key, out_m, count, cap, emitted, s);
+  }
 }
 
 void gj_pairs(GJoin& g, const uint32_t* sig, const uint32_t* band, uint64_t n, uint32_t H,
@@ -224,19 +287,18 @@ void gj_pairs(GJoin& g, const uint32_t* sig, const uint32_t* band, uint64_t n, u
   uint32_t NB = 0;
   int BW = 1;
   if (mm <= H) join_block_shape(H, mm, &NB, &BW);
-  ND_CUDA(cudaMemsetAsync(g.acc_d + 3, 0, sizeof(uint64_t), s));
-  if (n < 2 || NB == 0) return;
-  g.tbits = std::max(10, bits_for(n - 1));
-  g.fps = g.fps_buf.as<uint32_t>(n * NB);
-  g.table = reinterpret_cast<unsigned long long*>(g.table_buf.as<uint64_t>(uint64_t{1} << g.tbits));
-  g.link = reinterpret_cast<unsigned long long*>(g.link_buf.as<uint64_t>(n));
-  unsigned long long* emitted = g.acc_d + 3;
-  switch (BW) {
-    case 8: gj_blocks<8>(g, sig, band, n, H, B, NB, mm, nb, out_key, out_m, count, cap, emitted, s); break;
-    case 4: gj_blocks<4>(g, sig, band, n, H, B, NB, mm, nb, out_key, out_m, count, cap, emitted, s); break;
-    case 2: gj_blocks<2>(g, sig, band, n, H, B, NB, mm, nb, out_key, out_m, count, cap, emitted, s); break;
-    default: gj_blocks<1>(g, sig, band, n, H, B, NB, mm, nb, out_key, out_m, count, cap, emitted, s);
+  if (n < 2 || NB == 0) {
+    ND_CUDA(cudaMemsetAsync(g.acc_d + 3, 0, sizeof(uint64_t), s));
+    return;
   }
+  g.fps = g.fps_buf.as<uint32_t>(n * NB);
+  gj_fps(sig, n, H, mm, g.fps, s);
+  FpCols fc;
+  fc.base0 = g.fps;
+  std::vector<uint32_t> blocks(NB);
+  for (uint32_t k = 0; k < NB; ++k) blocks[k] = k;
+  gj_join(g, fc, SigView(sig, H), SigView(band, B), n, mm, blocks, nb, out_key, out_m, count, cap,
+          s);
 }
 
 GJoinCounts gj_read(GJoin& g, cudaStream_t s) {

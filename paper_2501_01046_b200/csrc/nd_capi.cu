@@ -584,7 +584,7 @@ const char* nd_k1_kernel(nd_ctx* ctx) {
 
 const char* nd_dedup_compare_kind(nd_ctx* ctx) {
   if (!ctx) return "";
-  if (is_group(ctx)) return ctx->multi.last_valid ? "cells" : "";
+  if (is_group(ctx)) return ctx->multi.last_valid ? ctx->shards[0]->dedup.compare_kind : "";
   return ctx->dedup.valid ? ctx->dedup.compare_kind : "";
 }
 

@@ -297,6 +297,32 @@ void components(GroupSet& gs, const uint32_t* lo, const uint32_t* hi, uint64_t e
 // until fetched).
 // K3g, the global block join of the in-memory dedup (k_gjoin.cu)
 constexpr uint32_t kGJoinMaxBlocks = 64;
+// block-major fingerprints of a batch's rows, fps[k * m + i] for the m rows
+// of one table, or one such table per shard of a device group (peer memory;
+// shard r holds rows row_base[r] .. row_base[r+1])
+struct FpCols {
+  const uint32_t* base0 = nullptr;
+  const uint32_t* const* bases = nullptr;
+  const uint64_t* row_base = nullptr;
+  uint32_t world = 1;
+};
+// block k's column of FpCols: fingerprint of global row g
+struct FpCol {
+  const uint32_t* base = nullptr;  // world == 1: fps + k * n
+  const uint32_t* const* bases = nullptr;
+  const uint64_t* row_base = nullptr;
+  uint32_t world = 1;
+  uint32_t k = 0;
+  __device__ __forceinline__ uint32_t get(uint64_t g) const {
+    if (world <= 1) return base[g];
+    uint32_t r = 0;
+#pragma unroll
+    for (uint32_t step = 32; step > 0; step >>= 1)
+      if (r + step < world && g >= row_base[r + step]) r += step;
+    const uint64_t m = row_base[r + 1] - row_base[r];
+    return bases[r][static_cast<uint64_t>(k) * m + (g - row_base[r])];
+  }
+};
 struct GJoin {
   DevBuf fps_buf, table_buf, link_buf, cnt, acc;
   uint32_t* fps = nullptr;                  // [NB][n] block fingerprints
@@ -315,6 +341,20 @@ bool global_join_eligible(uint64_t n, uint32_t H, uint32_t B, uint32_t K, uint32
 // reference counters from a histogram of the cells (async, into g.acc_d)
 void gj_cell_counts(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint32_t K,
                     cudaStream_t s);
+// the pieces, for device groups (nd_multi.cu): reset the counters, one
+// shard's cell histogram, the counters from `parts` histograms (device array
+// of pointers), block-major fingerprints of m rows, and the join of the given
+// blocks over fingerprint columns / rows / band ids that may live on peers
+void gj_reset(GJoin& g, cudaStream_t s);
+void gj_cell_hist(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint32_t K,
+                  cudaStream_t s);
+void gj_cell_stats(GJoin& g, const uint32_t* const* d_cnts, uint32_t parts, uint64_t cells,
+                   cudaStream_t s);
+void gj_fps(const uint32_t* sig, uint64_t n, uint32_t H, uint32_t mm, uint32_t* fps,
+            cudaStream_t s);
+void gj_join(GJoin& g, const FpCols& fc, const SigView& sv, const SigView& bv, uint64_t n,
+             uint32_t mm, const std::vector<uint32_t>& blocks, int nb, uint64_t* out_key,
+             uint32_t* out_m, unsigned long long* count, uint64_t cap, cudaStream_t s);
 // accepted pairs, each once, and the emitted-pairs counter (async)
 void gj_pairs(GJoin& g, const uint32_t* sig, const uint32_t* band, uint64_t n, uint32_t H,
               uint32_t B, uint32_t mm, int nb, uint64_t* out_key, uint32_t* out_m,

@@ -156,6 +156,76 @@ void multi_signatures(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets, 
   });
 }
 
+// C (both compares): the owners' distinct pairs gathered on shard 0 over peer
+// copies, sorted + uniqued once more, components (K4); stats
+void multi_finish(nd_ctx* g, const std::vector<uint64_t>& r, const uint64_t* doc_ids, uint64_t n,
+                  uint32_t B, uint32_t K, nd_dedup_stats* stats, const std::vector<double>& t_k1,
+                  double sec_a, double sec_b, uint64_t ncells, uint64_t cand, uint64_t crec,
+                  uint64_t emitted, const char* kind) {
+  // ---- C: the pairs of every owner -> shard 0, distinct + components ----------
+  const uint32_t G = static_cast<uint32_t>(g->shards.size());
+  auto tc = std::chrono::steady_clock::now();
+  nd_ctx* c0 = g->shards[0];
+  ND_CUDA(cudaSetDevice(c0->device));
+  DedupState& st0 = c0->dedup;
+  cudaStream_t s0 = c0->stream;
+  uint64_t np = 0;
+  for (uint32_t s = 0; s < G; ++s) np += g->shards[s]->dedup.pairs.distinct;
+  uint32_t* glo = c0->multi.pair_lo.as<uint32_t>(np + 1);
+  uint32_t* ghi = c0->multi.pair_hi.as<uint32_t>(np + 1);
+  uint32_t* gm = c0->multi.pair_m.as<uint32_t>(np + 1);
+  for (uint32_t s = 0, at = 0; s < G; ++s) {
+    const PairSet& ps = g->shards[s]->dedup.pairs;
+    if (!ps.distinct) continue;
+    const int dev = g->shards[s]->device;
+    ND_CUDA(cudaMemcpyPeerAsync(glo + at, c0->device, ps.lo, dev, ps.distinct * 4, s0));
+    ND_CUDA(cudaMemcpyPeerAsync(ghi + at, c0->device, ps.hi, dev, ps.distinct * 4, s0));
+    ND_CUDA(cudaMemcpyPeerAsync(gm + at, c0->device, ps.mc, dev, ps.distinct * 4, s0));
+    at += static_cast<uint32_t>(ps.distinct);
+  }
+  PairSet& fin = c0->multi.final_pairs;
+  fin.nb = std::max(1, bits_for(n - 1));
+  pack_pairs(fin, glo, ghi, gm, np, s0);
+  unique_pairs(fin, s0);
+  components(st0.groups, fin.lo, fin.hi, fin.distinct, n, s0);
+  ND_CUDA(cudaStreamSynchronize(s0));
+  // the result lives in shard 0's state (pairs, groups) -- the fetch calls of
+  // the group context read it there
+  std::swap(st0.pairs, fin);
+  st0.doc_ids.clear();
+  if (doc_ids) st0.doc_ids.assign(doc_ids, doc_ids + n);
+  st0.documents = n;
+  st0.bands = B;
+  st0.K = K;
+  st0.intervals = 1;
+  st0.valid = true;
+  g->multi.ranges = r;
+  g->multi.last_valid = true;
+  const double sec_c = since(tc);
+  st0.compare_kind = kind;
+  if (stats) {
+    *stats = nd_dedup_stats{};
+    stats->documents = n;
+    stats->bucket_count = K;
+    stats->nonsingleton_cells = ncells;
+    stats->candidate_pairs = cand;
+    stats->emitted_pairs = emitted;
+    stats->cell_records = crec;
+    stats->distinct_pairs = st0.pairs.distinct;
+    stats->duplicate_groups = st0.groups.groups;
+    stats->near_duplicates = st0.groups.members;
+    stats->removals = st0.groups.removals;
+    // wall clock per phase (max over shards): signatures, records + exchange
+    // setup, exchange + K2 + K3, gather + K4
+    stats->seconds[0] = *std::max_element(t_k1.begin(), t_k1.end());
+    stats->seconds[1] = sec_a - stats->seconds[0];
+    stats->seconds[2] = sec_b;
+    stats->seconds[3] = 0;
+    stats->seconds[4] = sec_c;
+    stats->intervals = 1;
+  }
+}
+
 void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
                  const uint64_t* doc_ids, uint64_t n, const nd_params& p, nd_dedup_stats* stats) {
   const uint32_t G = static_cast<uint32_t>(g->shards.size());
@@ -181,6 +251,15 @@ void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
   const char* jf = getenv("ND_JOIN_FPS");
   const bool fps_on = fpBW > 1 && !(jf && jf[0] == '0');
   std::vector<const uint32_t*> fp_bases(G, nullptr);
+  // the global block join (K3g) when the single-device dedup would use it:
+  // every shard fingerprints its rows (block-major) and counts its cells; the
+  // owner of block k (k mod G) joins that block over ALL rows, reading the
+  // fingerprints, rows and band ids in place on the shards that computed them
+  const bool global = [&] {
+    ND_CUDA(cudaSetDevice(g->shards[0]->device));
+    return global_join_eligible(n, H, B, K, mm);
+  }();
+  std::vector<const uint32_t*> gfp_bases(G, nullptr), cnt_bases(G, nullptr);
   std::vector<uint64_t> first_cell(G + 1);
   for (uint32_t s = 0; s <= G; ++s)
     first_cell[s] = static_cast<uint64_t>(
@@ -204,6 +283,16 @@ void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
     uint32_t* sig = st.sig.as<uint32_t>(m * H + 1);
     uint32_t* band = st.band.as<uint32_t>(m * B + 1);
     if (m) h2d_signatures(c, st, bytes, offsets + d0, m, B, p.rows, K, sig, band);
+    if (global) {
+      uint32_t* f = st.gj.fps_buf.as<uint32_t>(m * fpNB + 1);
+      gj_fps(sig, m, H, mm, f, cs);
+      gj_cell_hist(st.gj, band, m, B, K, cs);
+      gfp_bases[s] = f;
+      cnt_bases[s] = static_cast<const uint32_t*>(st.gj.cnt.ptr);
+      ND_CUDA(cudaStreamSynchronize(cs));
+      t_k1[s] = t_a[s] = since(t0);
+      return;
+    }
     if (fps_on) {
       uint32_t* f = c->multi.fps.as<uint32_t>(m * fpNB + 1);
       block_fingerprints(sig, m, H, fpNB, fpBW, f, cs);
@@ -252,6 +341,72 @@ void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
       recv_total[o] += split[s][o + 1] - split[s][o];
     }
   std::vector<uint32_t*> rkeys(G), rvals(G);
+  if (global) {  // ---- B': the blocks, each joined by its owner over all rows
+    std::vector<const uint32_t*> band_bases(G);
+    for (uint32_t s = 0; s < G; ++s)
+      band_bases[s] = static_cast<const uint32_t*>(g->shards[s]->dedup.band.ptr);
+    std::vector<GJoinCounts> counts(G);
+    auto tb = std::chrono::steady_clock::now();
+    run_shards(g, [&](uint32_t d) {
+      nd_ctx* c = g->shards[d];
+      auto t0 = std::chrono::steady_clock::now();
+      DedupState& st = c->dedup;
+      cudaStream_t cs = c->stream;
+      auto** d_sb = c->multi.row_bases.as<const uint32_t*>(G);
+      auto** d_bb = c->multi.bases.as<const uint32_t*>(G);
+      auto** d_fb = c->multi.fp_bases.as<const uint32_t*>(G);
+      auto** d_cb = c->multi.first_cell.as<const uint32_t*>(G);
+      uint64_t* d_rb = c->multi.row_base.as<uint64_t>(G + 1);
+      ND_CUDA(cudaMemcpyAsync(d_sb, bases.data(), G * sizeof(void*), cudaMemcpyHostToDevice, cs));
+      ND_CUDA(cudaMemcpyAsync(d_bb, band_bases.data(), G * sizeof(void*), cudaMemcpyHostToDevice, cs));
+      ND_CUDA(cudaMemcpyAsync(d_fb, gfp_bases.data(), G * sizeof(void*), cudaMemcpyHostToDevice, cs));
+      ND_CUDA(cudaMemcpyAsync(d_cb, cnt_bases.data(), G * sizeof(void*), cudaMemcpyHostToDevice, cs));
+      ND_CUDA(cudaMemcpyAsync(d_rb, row_base.data(), (G + 1) * 8, cudaMemcpyHostToDevice, cs));
+      SigView sv(bases[0], H), bv(band_bases[0], B);
+      sv.bases = d_sb;
+      bv.bases = d_bb;
+      sv.row_base = bv.row_base = d_rb;
+      sv.world = bv.world = G;
+      FpCols fc;
+      fc.bases = d_fb;
+      fc.row_base = d_rb;
+      fc.world = G;
+      if (G == 1) fc.base0 = gfp_bases[0];  // one table: [NB][n]
+      std::vector<uint32_t> mine;
+      for (uint32_t k = d; k < fpNB && mm <= H; k += G) mine.push_back(k);
+      gj_reset(st.gj, cs);
+      if (d == 0) gj_cell_stats(st.gj, d_cb, G, cells_total, cs);
+      PairSet& ps = st.pairs;
+      ps.nb = std::max(1, bits_for(n - 1));
+      ps.counter = ps.dcount.as<unsigned long long>(1);
+      if (ps.cap == 0) ps.cap = std::max<uint64_t>(1 << 20, 2 * n / G);
+      for (int attempt = 0; attempt < 2; ++attempt) {
+        ps.keys = ps.dkeys.as<uint64_t>(ps.cap);
+        ps.vals = ps.dvals.as<uint32_t>(ps.cap);
+        ND_CUDA(cudaMemsetAsync(ps.counter, 0, sizeof(unsigned long long), cs));
+        gj_join(st.gj, fc, sv, bv, n, mm, mine, ps.nb, ps.keys, ps.vals, ps.counter, ps.cap, cs);
+        unsigned long long got = 0;
+        ND_CUDA(cudaMemcpyAsync(&got, ps.counter, sizeof got, cudaMemcpyDeviceToHost, cs));
+        ND_CUDA(cudaStreamSynchronize(cs));
+        ps.count = got;
+        if (got <= ps.cap) break;
+        ps.cap = got + got / 4;
+      }
+      unique_pairs(ps, cs);
+      counts[d] = gj_read(st.gj, cs);
+      st.compare_kind = "global";
+      t_b[d] = since(t0);
+    });
+    const double sec_b = since(tb);
+    multi_finish(g, r, doc_ids, n, B, K, stats, t_k1, sec_a, sec_b, counts[0].ncells,
+                 counts[0].candidate_pairs, counts[0].cell_records,
+                 [&] {
+                   uint64_t e = 0;
+                   for (auto& c : counts) e += c.emitted;
+                   return e;
+                 }(), "global");
+    return;
+  }
   run_shards(g, [&](uint32_t d) {  // allocate on the owner's device
     CellSet& cs = g->shards[d]->dedup.cells;
     rkeys[d] = cs.rec_keys.as<uint32_t>(recv_total[d] + 1);
@@ -313,68 +468,14 @@ void multi_dedup(nd_ctx* g, const uint8_t* bytes, const uint64_t* offsets,
   });
   const double sec_b = since(tb);
 
-  // ---- C: the pairs of every owner -> shard 0, distinct + components ----------
-  auto tc = std::chrono::steady_clock::now();
-  nd_ctx* c0 = g->shards[0];
-  ND_CUDA(cudaSetDevice(c0->device));
-  DedupState& st0 = c0->dedup;
-  cudaStream_t s0 = c0->stream;
-  uint64_t np = 0;
-  for (uint32_t s = 0; s < G; ++s) np += g->shards[s]->dedup.pairs.distinct;
-  uint32_t* glo = c0->multi.pair_lo.as<uint32_t>(np + 1);
-  uint32_t* ghi = c0->multi.pair_hi.as<uint32_t>(np + 1);
-  uint32_t* gm = c0->multi.pair_m.as<uint32_t>(np + 1);
-  for (uint32_t s = 0, at = 0; s < G; ++s) {
-    const PairSet& ps = g->shards[s]->dedup.pairs;
-    if (!ps.distinct) continue;
-    const int dev = g->shards[s]->device;
-    ND_CUDA(cudaMemcpyPeerAsync(glo + at, c0->device, ps.lo, dev, ps.distinct * 4, s0));
-    ND_CUDA(cudaMemcpyPeerAsync(ghi + at, c0->device, ps.hi, dev, ps.distinct * 4, s0));
-    ND_CUDA(cudaMemcpyPeerAsync(gm + at, c0->device, ps.mc, dev, ps.distinct * 4, s0));
-    at += static_cast<uint32_t>(ps.distinct);
+  uint64_t sc = 0, sn = 0, sr = 0, se = 0;
+  for (uint32_t s = 0; s < G; ++s) {
+    sn += ncells[s];
+    sc += cand[s];
+    se += emitted[s];
+    sr += crec[s];
   }
-  PairSet& fin = c0->multi.final_pairs;
-  fin.nb = std::max(1, bits_for(n - 1));
-  pack_pairs(fin, glo, ghi, gm, np, s0);
-  unique_pairs(fin, s0);
-  components(st0.groups, fin.lo, fin.hi, fin.distinct, n, s0);
-  ND_CUDA(cudaStreamSynchronize(s0));
-  // the result lives in shard 0's state (pairs, groups) -- the fetch calls of
-  // the group context read it there
-  std::swap(st0.pairs, fin);
-  st0.doc_ids.clear();
-  if (doc_ids) st0.doc_ids.assign(doc_ids, doc_ids + n);
-  st0.documents = n;
-  st0.bands = B;
-  st0.K = K;
-  st0.intervals = 1;
-  st0.valid = true;
-  g->multi.ranges = r;
-  g->multi.last_valid = true;
-  const double sec_c = since(tc);
-  if (stats) {
-    *stats = nd_dedup_stats{};
-    stats->documents = n;
-    stats->bucket_count = K;
-    for (uint32_t s = 0; s < G; ++s) {
-      stats->nonsingleton_cells += ncells[s];
-      stats->candidate_pairs += cand[s];
-      stats->emitted_pairs += emitted[s];
-      stats->cell_records += crec[s];
-    }
-    stats->distinct_pairs = st0.pairs.distinct;
-    stats->duplicate_groups = st0.groups.groups;
-    stats->near_duplicates = st0.groups.members;
-    stats->removals = st0.groups.removals;
-    // wall clock per phase (max over shards): signatures, records + exchange
-    // setup, exchange + K2 + K3, gather + K4
-    stats->seconds[0] = *std::max_element(t_k1.begin(), t_k1.end());
-    stats->seconds[1] = sec_a - stats->seconds[0];
-    stats->seconds[2] = sec_b;
-    stats->seconds[3] = 0;
-    stats->seconds[4] = sec_c;
-    stats->intervals = 1;
-  }
+  multi_finish(g, r, doc_ids, n, B, K, stats, t_k1, sec_a, sec_b, sn, sc, sr, se, "cells");
 }
 
 void multi_fetch_signatures(nd_ctx* g, uint32_t* sig, uint32_t* band) {

@@ -42,6 +42,7 @@ def test_multi_dedup_byte_identical(corpus, tmp_path, shards):
     assert ctx.shards == shards
     rep = pipeline.dedup_packed(data, offs, pipeline.RunConfig(), ctx=ctx)
     assert rep.candidate_pairs == cand
+    assert pipeline.dedup_compare_kind(ctx) == "global"
     ws = str(tmp_path / "g")
     pipeline.write_report(ws, ctx=ctx)
     assert _files(ws) == want
@@ -89,3 +90,34 @@ def test_multi_more_shards_than_documents(ref):
     assert [g.members for g in r.groups] == [g.members for g in r1.groups]
     one.close()
     ctx.close()
+
+
+@pytest.mark.parametrize("shards,thr", [(3, (4, 5)), (16, (9, 10))])
+def test_multi_global_and_cell_joins_agree(corpus, monkeypatch, shards, thr):
+    # K3g on a device group (block k joined by shard k mod G over every
+    # shard's rows, read in place; 16 shards > 13 blocks leaves owners idle)
+    # against the per-cell joins on the group and K3g on one device: pairs,
+    # groups and every counter equal
+    data, offs, _, _ = corpus
+    cfg = pipeline.RunConfig(threshold=thr)
+    res = {}
+    for name, devs, env in (("group", [0] * shards, None), ("group_cells", [0] * shards, "cells"),
+                            ("one", [0], None)):
+        if env:
+            monkeypatch.setenv("ND_K3", env)
+        else:
+            monkeypatch.delenv("ND_K3", raising=False)
+        ctx = Context(devices=devs) if len(devs) > 1 else Context(0)
+        r = pipeline.dedup_packed(data, offs, cfg, ctx=ctx)
+        kind = pipeline.dedup_compare_kind(ctx)
+        st = {k: v for k, v in r.stats.items() if k not in ("seconds",)}
+        res[name] = (st, pipeline.dedup_pairs(r.distinct_pairs, ctx=ctx),
+                     [(g.representative, g.members) for g in r.groups])
+        assert kind == ("cells" if env else "global"), (name, kind)
+        ctx.close()
+    monkeypatch.delenv("ND_K3", raising=False)
+    assert res["group"] == res["one"]
+    assert res["group"][1:] == res["group_cells"][1:]
+    for k in ("candidate_pairs", "emitted_pairs", "nonsingleton_cells", "cell_records",
+              "distinct_pairs"):
+        assert res["group"][0][k] == res["group_cells"][0][k], k
