@@ -403,6 +403,21 @@ int nd_stage_compare_peer(nd_ctx* ctx, const uint32_t* d_keys, const uint32_t* d
                           uint64_t m, uint64_t key_limit, uint64_t threshold_num,
                           uint64_t threshold_den, uint64_t* npairs_out, uint64_t* candidate_pairs_out);
 int nd_peer_close(nd_ctx* ctx);
+/* K3g over peer memory (the global block join, one process per GPU): each
+ * rank exports, in one IPC allocation, its signature rows, its band ids and
+ * the block fingerprints of its rows for the threshold; after nd_peer_open,
+ * nd_stage_gjoin_peer joins the blocks k = self (mod world) over ALL ranks'
+ * rows (global row ids) -- every accepted pair of the batch is found by
+ * exactly one rank -- leaving distinct pairs for nd_stage_pairs_copy and the
+ * rank's share of the emitted-pairs counter.  nd_stage_cell_hist writes this
+ * rank's cell histogram (bands*K u32, d_cnt) for an all-reduce: the
+ * reference's counters (pipeline.cpp:406-411) come from the summed one. */
+int nd_peer_export_gjoin(nd_ctx* ctx, const uint32_t* d_sig, const uint32_t* d_band, uint64_t rows,
+                         uint32_t hash_count, uint32_t bands, uint64_t threshold_num,
+                         uint64_t threshold_den, uint8_t* handle_out);
+int nd_stage_gjoin_peer(nd_ctx* ctx, uint32_t self, uint64_t* npairs_out, uint64_t* emitted_out);
+int nd_stage_cell_hist(nd_ctx* ctx, const uint32_t* d_band, uint64_t n, uint32_t bands, uint32_t K,
+                       uint32_t* d_cnt);
 /* copies the pairs of the last nd_stage_compare into device buffers */
 int nd_stage_pairs_copy(nd_ctx* ctx, uint32_t* d_lo, uint32_t* d_hi, uint32_t* d_match);
 /* union stage over gathered pairs (rows < nnodes, repeats allowed): distinct

@@ -174,6 +174,10 @@ SIGNATURES = {
     "nd_stage_compare_peer": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64,
                                         C.c_uint64, u64p, u64p]),
     "nd_peer_close": (C.c_int, [vp]),
+    "nd_peer_export_gjoin": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_uint32, C.c_uint32,
+                                       C.c_uint64, C.c_uint64, u8p]),
+    "nd_stage_gjoin_peer": (C.c_int, [vp, C.c_uint32, u64p, u64p]),
+    "nd_stage_cell_hist": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, vp]),
     "nd_stage_pairs_copy": (C.c_int, [vp, vp, vp, vp]),
     "nd_stage_union": (C.c_int, [vp, vp, vp, vp, C.c_uint64, C.c_uint64,
                                  C.POINTER(NdDedupStats)]),

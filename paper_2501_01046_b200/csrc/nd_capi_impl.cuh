@@ -40,10 +40,14 @@ struct nd_ctx {
   ndb::DedupState h2d_state;    // text staging of nd_signatures_h2d
   ndb::SortScratch stage_sort;  // nd_stage_cell_records
   struct Peer {                 // signature rows of every rank in peer memory (nd_peer.cu)
-    ndb::DevBuf own, bases, row_base;
+    ndb::DevBuf own, bases, row_base, band_bases, fp_bases;
     std::vector<void*> opened;  // IPC mappings of the other ranks' rows
     ndb::SigView view;
-    uint32_t world = 0, H = 0;
+    // nd_peer_export_gjoin: each rank's allocation also holds its band ids
+    // and block fingerprints (K3g over peer memory)
+    ndb::SigView band_view;
+    ndb::FpCols fps;
+    uint32_t world = 0, H = 0, B = 0, mm = 0, NB = 0;
     uint64_t rows = 0;
   } peer;
   // multi-device group (nd_ctx_create_multi): one sub-context per shard;

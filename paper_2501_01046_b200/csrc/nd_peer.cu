@@ -110,6 +110,43 @@ int nd_peer_export(nd_ctx* ctx, const uint32_t* d_sig, uint64_t rows, uint32_t H
     static_assert(sizeof(h) == ND_IPC_HANDLE_BYTES, "IPC handle size");
     std::memcpy(handle_out, &h, sizeof h);
     ctx->peer.H = H;
+    ctx->peer.B = 0;  // rows only (the cell compare)
+  });
+}
+
+namespace {
+uint64_t align256(uint64_t b) { return (b + 255) & ~uint64_t{255}; }
+}  // namespace
+
+int nd_peer_export_gjoin(nd_ctx* ctx, const uint32_t* d_sig, const uint32_t* d_band, uint64_t rows,
+                         uint32_t H, uint32_t bands, uint64_t num, uint64_t den,
+                         uint8_t* handle_out) {
+  return guarded_impl(ctx, [&] {
+    if (H == 0 || bands == 0) fail(ND_ERR_CONFIG, "hash count and bands must be positive");
+    if (den == 0) fail(ND_ERR_CONFIG, "ratio denominator must be positive");
+    const uint32_t mm = min_matches(H, num, den);
+    uint32_t NB = 0;
+    int BW = 1;
+    if (mm <= H) join_block_shape(H, mm, &NB, &BW);
+    if (NB > kGJoinMaxBlocks) fail(ND_ERR_CONFIG, "threshold needs more than 64 blocks: use the cell compare");
+    // one allocation: [rows x H signatures][rows x bands band ids][NB x rows fingerprints]
+    const uint64_t sb = align256(rows * H * 4), bb = align256(rows * bands * 4);
+    ctx->peer.own.release();
+    uint8_t* own = ctx->peer.own.as<uint8_t>(sb + bb + rows * NB * 4 + 256);
+    cudaStream_t s = ctx->stream;
+    if (rows) {
+      ND_CUDA(cudaMemcpyAsync(own, d_sig, rows * H * 4, cudaMemcpyDeviceToDevice, s));
+      ND_CUDA(cudaMemcpyAsync(own + sb, d_band, rows * bands * 4, cudaMemcpyDeviceToDevice, s));
+      gj_fps(d_sig, rows, H, mm, reinterpret_cast<uint32_t*>(own + sb + bb), s);
+    }
+    ND_CUDA(cudaStreamSynchronize(s));
+    cudaIpcMemHandle_t h;
+    ND_CUDA(cudaIpcGetMemHandle(&h, own));
+    std::memcpy(handle_out, &h, sizeof h);
+    ctx->peer.H = H;
+    ctx->peer.B = bands;
+    ctx->peer.mm = mm;
+    ctx->peer.NB = NB;
   });
 }
 
@@ -147,6 +184,82 @@ int nd_peer_open(nd_ctx* ctx, const uint8_t* handles, const uint64_t* row_base, 
     P.view.bases = d_bases;
     P.view.row_base = d_rb;
     P.view.world = world;
+    if (P.B) {  // nd_peer_export_gjoin's layout: band ids and fingerprints follow
+      std::vector<const uint32_t*> bb(world), fb(world);
+      for (uint32_t r = 0; r < world; ++r) {
+        const uint64_t rows = row_base[r + 1] - row_base[r];
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(bases[r]);
+        const uint64_t sb = align256(rows * P.H * 4), bsz = align256(rows * P.B * 4);
+        bb[r] = reinterpret_cast<const uint32_t*>(b + sb);
+        fb[r] = reinterpret_cast<const uint32_t*>(b + sb + bsz);
+      }
+      auto** d_bb = P.band_bases.as<const uint32_t*>(world);
+      auto** d_fb = P.fp_bases.as<const uint32_t*>(world);
+      ND_CUDA(cudaMemcpyAsync(d_bb, bb.data(), world * sizeof(void*), cudaMemcpyHostToDevice,
+                              ctx->stream));
+      ND_CUDA(cudaMemcpyAsync(d_fb, fb.data(), world * sizeof(void*), cudaMemcpyHostToDevice,
+                              ctx->stream));
+      ND_CUDA(cudaStreamSynchronize(ctx->stream));
+      P.band_view = SigView(bb[0], P.B);
+      P.band_view.bases = d_bb;
+      P.band_view.row_base = d_rb;
+      P.band_view.world = world;
+      P.fps = FpCols{};
+      P.fps.bases = d_fb;
+      P.fps.row_base = d_rb;
+      P.fps.world = world;
+      if (world == 1) P.fps.base0 = fb[0];
+    }
+  });
+}
+
+int nd_stage_gjoin_peer(nd_ctx* ctx, uint32_t self, uint64_t* npairs_out, uint64_t* emitted_out) {
+  return guarded_impl(ctx, [&] {
+    auto& P = ctx->peer;
+    if (P.world == 0 || P.B == 0)
+      fail(ND_ERR_PREREQ, "no peer rows mapped with nd_peer_export_gjoin + nd_peer_open");
+    if (self >= P.world) fail(ND_ERR_CONFIG, "bad peer rank");
+    DedupState& st = ctx->api;
+    cudaStream_t s = ctx->stream;
+    st.valid = false;
+    std::vector<uint32_t> mine;  // the blocks this rank joins: k = self (mod world)
+    for (uint32_t k = self; k < P.NB; k += P.world) mine.push_back(k);
+    const uint64_t n = P.rows;
+    gj_reset(st.gj, s);
+    PairSet& ps = st.pairs;
+    ps.nb = std::max(1, bits_for(n ? n - 1 : 0));
+    ps.counter = ps.dcount.as<unsigned long long>(1);
+    if (ps.cap == 0) ps.cap = std::max<uint64_t>(1 << 20, 2 * n / P.world);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      ps.keys = ps.dkeys.as<uint64_t>(ps.cap);
+      ps.vals = ps.dvals.as<uint32_t>(ps.cap);
+      ND_CUDA(cudaMemsetAsync(ps.counter, 0, sizeof(unsigned long long), s));
+      gj_join(st.gj, P.fps, P.view, P.band_view, n, P.mm, mine, ps.nb, ps.keys, ps.vals,
+              ps.counter, ps.cap, s);
+      unsigned long long got = 0;
+      ND_CUDA(cudaMemcpyAsync(&got, ps.counter, sizeof got, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaStreamSynchronize(s));
+      ps.count = got;
+      if (got <= ps.cap) break;
+      ps.cap = got + got / 4;
+    }
+    unique_pairs(ps, s);
+    const GJoinCounts c = gj_read(st.gj, s);
+    st.valid = true;
+    *npairs_out = ps.distinct;
+    if (emitted_out) *emitted_out = c.emitted;
+  });
+}
+
+int nd_stage_cell_hist(nd_ctx* ctx, const uint32_t* d_band, uint64_t n, uint32_t bands, uint32_t K,
+                       uint32_t* d_cnt) {
+  return guarded_impl(ctx, [&] {
+    if (bands == 0 || K == 0) fail(ND_ERR_CONFIG, "bands and bucket count must be positive");
+    GJoin& g = ctx->api.gj;
+    gj_cell_hist(g, d_band, n, bands, K, ctx->stream);
+    ND_CUDA(cudaMemcpyAsync(d_cnt, g.cnt.ptr, static_cast<uint64_t>(bands) * K * 4,
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+    ND_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -181,6 +294,7 @@ int nd_peer_close(nd_ctx* ctx) {
     for (void* p : P.opened) cudaIpcCloseMemHandle(p);
     P.opened.clear();
     P.world = 0;
+    P.B = 0;
     P.own.release();
   });
 }

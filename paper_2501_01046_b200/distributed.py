@@ -168,6 +168,38 @@ class GpuStages:
     def close_peers(self) -> None:
         self.ctx.check(self.ctx.lib.nd_peer_close(self.ctx.h))
 
+    # ---- K3g over peer memory: every rank's rows, band ids and block
+    # fingerprints mapped in place; rank r joins the blocks k = r (mod world)
+    gjoin_capable = True
+
+    def cell_hist(self, band, bands, K):
+        cnt = self.tensor((bands * K,), self.torch.int32)
+        self.ctx.check(self.ctx.lib.nd_stage_cell_hist(
+            self.ctx.h, C.c_void_p(band.data_ptr()), band.shape[0], bands, K,
+            C.c_void_p(cnt.data_ptr())))
+        return cnt
+
+    def export_gjoin(self, sig, band, threshold) -> bytes:
+        h = (C.c_uint8 * 64)()
+        num, den = threshold
+        self.ctx.check(self.ctx.lib.nd_peer_export_gjoin(
+            self.ctx.h, C.c_void_p(sig.data_ptr()), C.c_void_p(band.data_ptr()), sig.shape[0],
+            sig.shape[1], band.shape[1], num, den, h))
+        return bytes(h)
+
+    def gjoin_peer(self, rank: int):
+        t = self.torch
+        npairs, emitted = C.c_uint64(), C.c_uint64()
+        self.ctx.check(self.ctx.lib.nd_stage_gjoin_peer(self.ctx.h, rank, C.byref(npairs),
+                                                        C.byref(emitted)))
+        k = npairs.value
+        lo, hi, m = (self.tensor((max(k, 1),), t.int32) for _ in range(3))
+        self.ctx.check(self.ctx.lib.nd_stage_pairs_copy(
+            self.ctx.h, C.c_void_p(lo.data_ptr()), C.c_void_p(hi.data_ptr()),
+            C.c_void_p(m.data_ptr())))
+        self.ctx_sync()
+        return lo[:k], hi[:k], m[:k], emitted.value
+
     def union(self, lo, hi, m, nnodes):
         st = NdDedupStats()
         ptr = (lambda x: C.c_void_p(x.data_ptr()) if x.numel() else None)
@@ -267,9 +299,16 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists",
     fam = derive_family(config.seed, config.hash_count, config.shingle_len, config.unit)
     # 2. K1 on the shard
     sig, band = stages.signatures(data, offsets, fam, b, config.rows, K)
+    thr = _ratio(config.threshold)
+    ev = _events(torch, dev, timings)
+    mm = _lib.load().nd_min_matches(config.hash_count, thr[0], thr[1])
+    nblocks = config.hash_count - mm + 1 if mm <= config.hash_count else 0
+    if (getattr(stages, "gjoin_capable", False) and os.environ.get("ND_K3", "") != "cells"
+            and os.environ.get("ND_PEER_SIGS", "1") != "0" and nblocks <= 64):
+        return _dedup_gjoin(stages, sig, band, counts, N, K, b, thr, rank, world, group, dev,
+                            cdev, ev, timings, fetch, dist, torch)
     # 3. records -> owners
     packed = getattr(stages, "packed_capable", False) and os.environ.get("ND_PEER_SIGS", "1") != "0"
-    ev = _events(torch, dev, timings)
     if packed:
         # one u64 per (cell, row), sorted by cell, owner splits from the device
         rec, split = stages.records_packed(band, b, K, doc_base, world)
@@ -300,7 +339,6 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists",
         rec_bytes = keys.element_size() + vals.element_size()
     if ev:
         ev[1].record()
-    thr = _ratio(config.threshold)
     if packed:
         h = torch.tensor(list(stages.export_rows(sig)), dtype=torch.uint8, device=cdev)
         hs = [torch.empty_like(h) for _ in range(world)]
@@ -356,3 +394,51 @@ def dedup_sharded(data, offsets, config, stages, group=None, fetch="lists",
     if rep is not None:
         rep.candidate_pairs = int(cand.item())
     return ShardResult(rep, int(cand.item()), int(emitted.item()), st.distinct_pairs, K, N)
+
+
+def _dedup_gjoin(stages, sig, band, counts, N, K, b, thr, rank, world, group, dev, cdev, ev,
+                 timings, fetch, dist, torch) -> ShardResult:
+    """K3g across ranks (nd_stage_gjoin_peer): no record exchange -- the cell
+    histograms are all-reduced for the reference's counters, and each rank
+    joins its blocks over every rank's rows, band ids and fingerprints read in
+    place through CUDA IPC mappings (NVLink peer memory)."""
+    cnt = stages.cell_hist(band, b, K)
+    if ev:
+        ev[0].record()
+    c = cnt.to(cdev)
+    dist.all_reduce(c, group=group)
+    if ev:
+        ev[1].record()
+    c = c.to(torch.int64)
+    cand_total = int((c * (c - 1) // 2).sum().item())
+    h = torch.tensor(list(stages.export_gjoin(sig, band, thr)), dtype=torch.uint8, device=cdev)
+    hs = [torch.empty_like(h) for _ in range(world)]
+    dist.all_gather(hs, h, group=group)
+    handles = b"".join(bytes(x.cpu().tolist()) for x in hs)
+    row_base = [sum(counts[:r]) for r in range(world + 1)]
+    stages.open_peers(handles, row_base, world, rank)
+    lo, hi, m, emitted_local = stages.gjoin_peer(rank)
+    dist.barrier(group=group)
+    stages.close_peers()
+    emitted = torch.tensor([emitted_local], dtype=torch.int64, device=cdev)
+    dist.all_reduce(emitted, group=group)
+    trip = torch.stack([lo, hi, m], dim=1) if lo.numel() else torch.zeros((0, 3), dtype=lo.dtype, device=dev)
+    if ev:
+        ev[2].record()
+    all_trip, _ = _all_gather_v(dist, trip, group, torch)
+    if ev:
+        ev[3].record()
+        torch.cuda.synchronize(dev)
+        timings.update(
+            exchange_ms=ev[0].elapsed_time(ev[1]),
+            exchange_sent_bytes=int(c.numel()) * 4,
+            exchange_recv_bytes=int(c.numel()) * 4,
+            edges_ms=ev[2].elapsed_time(ev[3]),
+            edges_bytes=int(all_trip.numel()) * all_trip.element_size(),
+            compare="global")
+    st = stages.union(all_trip[:, 0].contiguous(), all_trip[:, 1].contiguous(),
+                      all_trip[:, 2].contiguous(), N)
+    rep = stages.report(st, fetch) if (rank == 0 and fetch) else None
+    if rep is not None:
+        rep.candidate_pairs = cand_total
+    return ShardResult(rep, cand_total, int(emitted.item()), st.distinct_pairs, K, N)

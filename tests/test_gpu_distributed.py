@@ -65,13 +65,14 @@ def _gpu_worker(rank, world, port, data, offs, out_path):
     if rank == 0:
         with open(out_path, "w") as f:
             json.dump({"groups": [[g.representative, g.members] for g in res.report.groups],
-                       "distinct": res.distinct_pairs, "cand": res.candidate_pairs}, f)
+                       "distinct": res.distinct_pairs, "cand": res.candidate_pairs,
+                       "emitted": res.emitted_pairs}, f)
     dist.destroy_process_group()
     ctx.close()
 
 
-@pytest.mark.parametrize("world,peer", [(2, "1"), (3, "1"), (2, "0")])
-def test_sharded_cuda_stages_several_ranks(ctx, ref, tmp_path, monkeypatch, world, peer):
+@pytest.mark.parametrize("world,peer,k3", [(2, "1", ""), (3, "1", ""), (2, "0", ""), (2, "1", "cells")])
+def test_sharded_cuda_stages_several_ranks(ctx, ref, tmp_path, monkeypatch, world, peer, k3):
     # the multi-rank protocol over the REAL device stages: `world` processes
     # share the one GPU (gloo moves the collective buffers through the host;
     # NCCL refuses two ranks on one device) -- owner split, all-to-all of cell
@@ -81,6 +82,10 @@ def test_sharded_cuda_stages_several_ranks(ctx, ref, tmp_path, monkeypatch, worl
     import torch.multiprocessing as mp
 
     monkeypatch.setenv("ND_PEER_SIGS", peer)
+    if k3:
+        monkeypatch.setenv("ND_K3", k3)
+    else:
+        monkeypatch.delenv("ND_K3", raising=False)
     from paper_2501_01046_b200 import pipeline
 
     data, offs = ref.generate_synthetic(2500, 200, gmin=2, gmax=4, edit=(2, 100), len_min=300,
@@ -93,6 +98,12 @@ def test_sharded_cuda_stages_several_ranks(ctx, ref, tmp_path, monkeypatch, worl
     assert got["groups"]
     assert got["distinct"] == single.distinct_pairs
     assert got["cand"] == single.candidate_pairs
+    if peer == "1" and not k3:
+        # K3g over IPC peer memory: each rank joins its blocks over all rows;
+        # the emitted-pairs counter (one per shared cell) equals one device's
+        monkeypatch.delenv("ND_K3", raising=False)
+        one = pipeline.dedup_packed(data, offs, pipeline.RunConfig(), ctx=ctx)
+        assert got["emitted"] == one.stats["emitted_pairs"]
 
 
 def test_bench_two_ranks_harness(tmp_path):
