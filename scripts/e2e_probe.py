@@ -44,7 +44,8 @@ for _ in range(8):
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(s); run(); e1.record(s); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
 h = int(np.frombuffer(sig.tobytes(), np.uint64).sum() % (1 << 61))
-print(json.dumps({"ms": min(ts), "ms_med": sorted(ts)[4], "sum": h}))
+print(json.dumps({"ms": min(ts), "ms_med": sorted(ts)[4], "ms_mean": sum(ts) / len(ts),
+                  "ms_max": max(ts), "sum": h}))
 """
 
 
@@ -65,6 +66,8 @@ def main():
     for k, v in res.items():
         good = [x for x in v if isinstance(x, dict)]
         print(json.dumps({"variant": k, "env": envs[k], "best_ms": min(x["ms"] for x in good) if good else None,
+                          "mean_ms": [round(x["ms_mean"], 2) for x in good],
+                          "max_ms": [round(x["ms_max"], 2) for x in good],
                           "all": [x["ms"] if isinstance(x, dict) else x for x in v],
                           "sums": sorted({x["sum"] for x in good})}))
 
