@@ -86,6 +86,7 @@ def _both(ctx, monkeypatch, sig, band, cfg, K):
     (16, 4, 4, (1, 10), "global"),     # NB 15, BW 1
     (256, 32, 8, (4, 5), "global"),    # NB 52, BW 4
     (96, 12, 8, (3, 4), "global"),     # NB 24, BW 4
+    (100, 10, 10, (4, 5), "global"),   # H % 4 != 0 (scalar block loads), NB 20, BW 4
     (128, 16, 8, (1, 4), "cells"),     # NB 96 > 64: the per-cell joins
     (128, 16, 8, (1, 1), "global"),    # min_matches > H: no block, no pair
 ])
@@ -189,3 +190,24 @@ def test_dedup_signatures_validates(ctx):
         pipeline.dedup_signatures(sig, band, pipeline.RunConfig(), bucket_count=50, ctx=ctx)
     with pytest.raises(_lib.ConfigError):
         pipeline.dedup_signatures(sig[:, :64], band, pipeline.RunConfig(), bucket_count=50, ctx=ctx)
+
+
+def test_global_join_identical_rows_and_tiny_batches(ctx, ref, monkeypatch):
+    # every row identical (one chain of n rows in every block's slot: the
+    # pairs are checked at block 0 and rejected at every later block), then
+    # batches of 2 and 3 rows
+    H, bands, rows = 128, 16, 8
+    rng = np.random.default_rng(3)
+    base = rng.integers(0, 1 << 22, size=H).astype(np.uint32)
+    cfg = pipeline.RunConfig(hash_count=H, bands=bands, rows=rows)
+    for n in (2500, 2, 3):
+        sig = np.tile(base, (n, 1))
+        if n == 3:
+            sig[2] = rng.integers(0, 1 << 22, size=H)
+        band = np.tile(rng.integers(0, 7, size=bands).astype(np.uint32), (n, 1))
+        out = _both(ctx, monkeypatch, sig, band, cfg, 7)
+        assert out["global"][0] == "global"
+        assert out["global"][1:] == out["cells"][1:]
+        want_pairs = n * (n - 1) // 2 if n != 3 else 1
+        assert out["global"][1]["distinct_pairs"] == want_pairs
+        assert out["global"][1]["emitted_pairs"] == want_pairs * bands
