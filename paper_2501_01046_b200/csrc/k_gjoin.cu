@@ -127,11 +127,15 @@ __global__ void k_gj_walk(const FpCol fc, uint64_t n, const unsigned long long* 
   }
 }
 
+// (a band id >= K is not counted; bad != nullptr counts them)
 __global__ void k_cell_hist(const uint32_t* __restrict__ band, uint64_t n, uint32_t B, uint32_t K,
-                            uint32_t* __restrict__ cnt) {
+                            uint32_t* __restrict__ cnt, unsigned int* __restrict__ bad) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n * B;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    atomicAdd(&cnt[static_cast<uint64_t>(i % B) * K + band[i]], 1u);
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t b = band[i];
+    if (b < K) atomicAdd(&cnt[static_cast<uint64_t>(i % B) * K + b], 1u);
+    else if (bad) atomicAdd(bad, 1u);
+  }
 }
 
 // out[0] = sum n(n-1)/2, out[1] = cells with n >= 2, out[2] = their records;
@@ -216,12 +220,12 @@ bool global_join_eligible(uint64_t n, uint32_t H, uint32_t B, uint32_t K, uint32
 }
 
 void gj_cell_hist(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint32_t K,
-                  cudaStream_t s) {
+                  cudaStream_t s, unsigned int* bad) {
   const uint64_t cells = static_cast<uint64_t>(B) * K;
   uint32_t* cnt = g.cnt.as<uint32_t>(cells + 1);
   ND_CUDA(cudaMemsetAsync(cnt, 0, cells * 4, s));
   if (n) {
-    k_cell_hist<<<8 * sm_count(), 256, 0, s>>>(band, n, B, K, cnt);
+    k_cell_hist<<<8 * sm_count(), 256, 0, s>>>(band, n, B, K, cnt, bad);
     ND_CHECK_LAUNCH();
   }
 }

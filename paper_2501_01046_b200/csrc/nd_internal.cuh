@@ -347,7 +347,7 @@ void gj_cell_counts(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint
 // blocks over fingerprint columns / rows / band ids that may live on peers
 void gj_reset(GJoin& g, cudaStream_t s);
 void gj_cell_hist(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint32_t K,
-                  cudaStream_t s);
+                  cudaStream_t s, unsigned int* bad = nullptr);
 void gj_cell_stats(GJoin& g, const uint32_t* const* d_cnts, uint32_t parts, uint64_t cells,
                    cudaStream_t s);
 void gj_fps(const uint32_t* sig, uint64_t n, uint32_t H, uint32_t mm, uint32_t* fps,

@@ -256,10 +256,15 @@ int nd_stage_cell_hist(nd_ctx* ctx, const uint32_t* d_band, uint64_t n, uint32_t
   return guarded_impl(ctx, [&] {
     if (bands == 0 || K == 0) fail(ND_ERR_CONFIG, "bands and bucket count must be positive");
     GJoin& g = ctx->api.gj;
-    gj_cell_hist(g, d_band, n, bands, K, ctx->stream);
+    unsigned int* bad = reinterpret_cast<unsigned int*>(g.acc.as<uint64_t>(4));
+    ND_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned int), ctx->stream));
+    gj_cell_hist(g, d_band, n, bands, K, ctx->stream, bad);
     ND_CUDA(cudaMemcpyAsync(d_cnt, g.cnt.ptr, static_cast<uint64_t>(bands) * K * 4,
                             cudaMemcpyDeviceToDevice, ctx->stream));
+    unsigned int h_bad = 0;
+    ND_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof h_bad, cudaMemcpyDeviceToHost, ctx->stream));
     ND_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h_bad) fail(ND_ERR_CONFIG, std::to_string(h_bad) + " band ids are not below the bucket count");
   });
 }
 

@@ -211,3 +211,25 @@ def test_global_join_identical_rows_and_tiny_batches(ctx, ref, monkeypatch):
         want_pairs = n * (n - 1) // 2 if n != 3 else 1
         assert out["global"][1]["distinct_pairs"] == want_pairs
         assert out["global"][1]["emitted_pairs"] == want_pairs * bands
+
+
+def test_stage_cell_hist_counts_and_rejects_bad_ids(ctx):
+    import ctypes as C
+
+    import torch
+
+    rng = np.random.default_rng(11)
+    n, B, K = 5000, 16, 300
+    band = rng.integers(0, K, size=(n, B)).astype(np.uint32)
+    d_band = torch.from_numpy(band.view(np.int32)).cuda()
+    cnt = torch.empty(B * K, dtype=torch.int32, device="cuda")
+    ctx.check(ctx.lib.nd_stage_cell_hist(ctx.h, C.c_void_p(d_band.data_ptr()), n, B, K,
+                                         C.c_void_p(cnt.data_ptr())))
+    want = np.zeros(B * K, np.int64)
+    np.add.at(want, (np.arange(B)[None, :] * K + band).ravel(), 1)
+    assert np.array_equal(cnt.cpu().numpy(), want)
+    band[17, 3] = K
+    d_band = torch.from_numpy(band.view(np.int32)).cuda()
+    with pytest.raises(_lib.ConfigError, match="bucket count"):
+        ctx.check(ctx.lib.nd_stage_cell_hist(ctx.h, C.c_void_p(d_band.data_ptr()), n, B, K,
+                                             C.c_void_p(cnt.data_ptr())))
