@@ -154,6 +154,13 @@ const char* nd_dedup_compare_kind(nd_ctx* ctx);
  * when the family is outside K1j's domain. */
 int64_t nd_k1j_source(const nd_hash_fn* fns, uint32_t hash_count, uint32_t shingle_len, char* out,
                       uint64_t cap);
+/* K1j's dn plan for a family (no device needed): per function one row of 12
+ * u32 {pass, class, g, w, function, q, QLn, Kb multiplier, p, A bits, B bits,
+ * M bits} (csrc/k1_jit.cpp, the denormal-state arithmetic), written up to
+ * cap_rows rows; returns the row count (= hash_count) or -1 when the family
+ * runs another arithmetic (outside the fq domain, ND_K1J_ARITH=fq). */
+int64_t nd_k1j_plan(const nd_hash_fn* fns, uint32_t hash_count, uint32_t shingle_len, uint32_t* out,
+                    uint64_t cap_rows);
 
 /* signature_of_document over a packed batch + band_bucket_ids
  * (minhash.hpp:71-78, lsh.hpp:38-40; caller pipeline.cpp:214-218).

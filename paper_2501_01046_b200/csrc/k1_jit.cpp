@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -60,6 +61,8 @@ struct JitShape {
   int min_blocks = 6;
   int prefetch = 1;
   int unroll = 1;  // whole words per loop iteration (2: ND_K1J_UNROLL=2, slower)
+  int arith = 1;   // 1: denormal-state arithmetic (dn, default); 0: the fq state of K1 (ND_K1J_ARITH=fq)
+  int classes = 4; // dn: most w classes (c_in extractions per window) in one pass
 };
 
 JitShape jit_shape() {
@@ -68,6 +71,8 @@ JitShape jit_shape() {
   if (const char* v = getenv("ND_K1J_MINB")) j.min_blocks = std::max(1, std::min(16, atoi(v)));
   if (const char* v = getenv("ND_K1J_PREFETCH")) j.prefetch = std::max(1, std::min(2, atoi(v)));
   if (const char* v = getenv("ND_K1J_UNROLL")) j.unroll = std::max(1, std::min(2, atoi(v)));
+  if (const char* v = getenv("ND_K1J_ARITH")) j.arith = std::strcmp(v, "fq") == 0 ? 0 : 1;
+  if (const char* v = getenv("ND_K1J_CLASSES")) j.classes = std::max(1, std::min(8, atoi(v)));
   return j;
 }
 
@@ -152,18 +157,271 @@ std::string rol_call(const std::string& st, int i, const FnConst& c) {
   return o.str();
 }
 
-std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitShape& js) {
+// ---- dn arithmetic: the state as a negative denormal -------------------------
+// The fq roll spends one instruction per HWE converting the state to float
+// (I2FP) for the quotient estimate.  dn keeps the state as the bit pattern
+// z = 0x80000000 + c (c < p < 2^23), which *is* the float -c * 2^-149 (sign
+// set, exponent field 0: a denormal), so the estimate FFMA reads the state
+// register directly:
+//
+//   t1 = (c_out + 256 g) * B                       FMUL  (shared float c_out)
+//   R  = z_f * A + t1      = (c q/p + t1) U        FFMA  (A = -fl(q/p) 2^(e-1))
+//   Kb = bits(R + M, round-down) = v +- floor(R/U) FADD.RM
+//   z' = c_out*QLn + (c_in + w) + z*q + Kb*(-+p)   3 IMAD (0x80000000*q == 0x80000000)
+//   z' = min_s32(z' + p, z')                       VIADDMNMX.S32 (the wrap at INT_MIN
+//                                                  canonicalises r in [-p, p))
+//
+// U = 2^(e-150) is the ulp of M's binade e, so the FADD leaves k' = floor(R/U)
+// in the low bits of Kb.  The float sees c_out + 256g where the integers see
+// c_out: R/U = u/p + n + f + eps with n + f = 256 g QLn / p (n integer,
+// f in [1/64, 63/64], g <= 64) and |eps| < 0.0094 (rounding of fl(q/p) and of
+// R < 2^17: 2^-8 each; t1 < 2^15: 2^-10; fl(QLn/p): 2^-11; the dropped
+// c_in/p < 2^-13), so
+// floor(R/U) - n = k' in {Q, Q+1} and r = u - k' p in [-p, p).  The integer
+// chain cancels both Kb's bias and the offset n through w: Kb = t + k' with
+// t = w p^-1 (mod 2^32), so Kb*(-p) = -w - k' p against the +w the c_in
+// extraction (one PRMT: c_in in byte 0, w's bytes 1..3) adds.  For each
+// function, v = t - n (M > 0) or v = n - t (M < 0, multiplier +p) must be a
+// normal float with e in [30, ehi] and room for floor(R/U) in its mantissa;
+// that holds for ~38% of random w, so the functions of a pass are grouped
+// into a few classes sharing w (one c_in PRMT per class and window) by a
+// seeded search.  Per HWE: FMUL, FFMA, FADD, 3 IMAD, VIADDMNMX + half a
+// VIMNMX3 = 7.5 (fq: 8.5).  The running minima are min_s32 of the z's; the
+// signature value is m ^ 0x80000000.
+struct DnFn {
+  uint32_t fn, cls;
+  uint32_t q, qln, kp, p;
+  uint32_t a_bits, b_bits, m_bits;
+};
+
+struct DnPass {
+  uint32_t g = 1;
+  std::vector<uint32_t> w;
+  std::vector<DnFn> fns;
+};
+
+struct DnInfo {
+  uint32_t p, q, qln, pinv;
+  float qp, qlnp;
+  int ehi;
+};
+
+constexpr int kDnElo = 30;
+constexpr uint32_t kDnMaxG = 64;  // offsets 256g: t1 < 2^15 units keeps |eps| < 0.0094
+
+DnInfo dn_info(const nd_hash_fn& f, uint32_t L) {
+  DnInfo d;
+  d.p = f.modulus;
+  d.q = f.base;
+  uint64_t qL = 1;
+  for (uint32_t i = 0; i < L; ++i) qL = qL * d.q % d.p;
+  d.qln = static_cast<uint32_t>((d.p - qL) % d.p);
+  uint32_t inv = d.p;  // p^-1 mod 2^32 by Newton (3 -> 6 -> 12 -> 24 -> 48 bits)
+  for (int i = 0; i < 5; ++i) inv *= 2u - d.p * inv;
+  d.pinv = inv;
+  d.qp = static_cast<float>(static_cast<double>(d.q) / d.p);
+  d.qlnp = static_cast<float>(static_cast<double>(d.qln) / d.p);
+  int ex = 0;
+  std::frexp(d.qp, &ex);  // qp < 2^ex
+  d.ehi = 128 - ex;       // |A| = qp 2^(e-1) < 2^127
+  return d;
+}
+
+bool dn_offset_ok(const DnInfo& d, uint32_t g) {
+  const uint64_t rem = (256ull * g * d.qln) % d.p;
+  return rem * 64 >= d.p && rem * 64 <= 63ull * d.p;  // f in [1/64, 63/64]
+}
+
+bool dn_fit(const DnInfo& d, uint32_t g, uint32_t w, DnFn* out) {
+  const uint64_t n = 256ull * g * d.qln / d.p;
+  const uint32_t qb = d.q + 257u + 256u * g;  // floor(R/U) <= q + 256 + n + 1
+  const uint32_t t = w * d.pinv;
+  const uint32_t vp = t - static_cast<uint32_t>(n), vn = static_cast<uint32_t>(n) - t;
+  auto ok_e = [&](uint32_t x) {
+    const int e = static_cast<int>((x >> 23) & 0xFF);
+    return e >= kDnElo && e <= d.ehi;
+  };
+  uint32_t v;
+  bool neg;
+  if (vp < 0x80000000u && ok_e(vp) && (vp & 0x7FFFFFu) + qb <= 0x7FFFFFu) {
+    v = vp;
+    neg = false;
+  } else if (vn >= 0x80000000u && ok_e(vn) && (vn & 0x7FFFFFu) >= qb) {
+    v = vn;
+    neg = true;
+  } else {
+    return false;
+  }
+  if (out) {
+    const int e = static_cast<int>((v >> 23) & 0xFF);
+    const float A = -std::ldexp(d.qp, e - 1);   // exact (power-of-two scaling, normal)
+    const float B = std::ldexp(d.qlnp, e - 150);
+    out->q = d.q;
+    out->qln = d.qln;
+    out->p = d.p;
+    out->kp = neg ? d.p : 0u - d.p;
+    std::memcpy(&out->a_bits, &A, 4);
+    std::memcpy(&out->b_bits, &B, 4);
+    out->m_bits = v;
+  }
+  return true;
+}
+
+// Groups the family's functions into passes of at most F functions, each pass
+// with one offset g and at most `classes` values of w.  Deterministic for a
+// family (seeded).  Functions that fit no offset g <= 64 (256 g QLn within
+// p/64 of a multiple of p for every g -- rare) or no w go to `fq`: they run
+// fq passes of the same kernel.
+struct DnPlan {
+  std::vector<DnPass> passes;
+  std::vector<uint32_t> fq;
+};
+
+DnPlan dn_plan(const nd_hash_fn* fns, uint32_t H, uint32_t L, int F, int classes) {
+  DnPlan plan;
+  std::vector<DnInfo> info(H);
+  for (uint32_t i = 0; i < H; ++i) info[i] = dn_info(fns[i], L);
+  std::vector<uint32_t> rest;
+  for (uint32_t i = 0; i < H; ++i) {
+    bool any = false;
+    for (uint32_t g = 1; g <= kDnMaxG && !any; ++g) any = dn_offset_ok(info[i], g);
+    (any ? rest : plan.fq).push_back(i);
+  }
+  uint64_t rng = 0x9E3779B97F4A7C15ull;
+  auto next = [&] {  // splitmix64
+    uint64_t z = (rng += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return static_cast<uint32_t>((z ^ (z >> 31)) >> 16);
+  };
+  while (!rest.empty()) {
+    const size_t want = std::min<size_t>(static_cast<size_t>(F), rest.size());
+    DnPass pass;
+    size_t best_elig = 0;
+    for (uint32_t g = 1; g <= kDnMaxG && best_elig < rest.size(); ++g) {
+      size_t c = 0;
+      for (uint32_t j : rest) c += dn_offset_ok(info[j], g);
+      if (c > best_elig) {
+        best_elig = c;
+        pass.g = g;
+      }
+    }
+    std::vector<char> taken(H, 0);
+    std::vector<uint32_t> cand;
+    for (uint32_t j : rest)
+      if (dn_offset_ok(info[j], pass.g)) cand.push_back(j);
+    while (pass.fns.size() < want && static_cast<int>(pass.w.size()) < classes) {
+      const size_t need = want - pass.fns.size();
+      uint32_t best_w = 0;
+      size_t best = 0;
+      for (int trial = 0; trial < 8192 && best < need; ++trial) {
+        const uint32_t w = next() << 8;  // low byte 0: c_in goes there
+        size_t c = 0;
+        for (uint32_t j : cand)
+          if (!taken[j] && dn_fit(info[j], pass.g, w, nullptr)) ++c;
+        if (c > best) {
+          best = c;
+          best_w = w;
+        }
+      }
+      if (best == 0) break;
+      const uint32_t cls = static_cast<uint32_t>(pass.w.size());
+      pass.w.push_back(best_w);
+      for (uint32_t j : cand) {
+        if (pass.fns.size() >= want) break;
+        DnFn f;
+        if (taken[j] || !dn_fit(info[j], pass.g, best_w, &f)) continue;
+        f.fn = j;
+        f.cls = cls;
+        taken[j] = 1;
+        pass.fns.push_back(f);
+      }
+    }
+    if (pass.fns.empty()) {  // nothing of the rest fits this pass's g
+      bool moved = false;
+      std::vector<uint32_t> left;
+      for (uint32_t j : rest) {
+        if (!moved && dn_offset_ok(info[j], pass.g)) {
+          plan.fq.push_back(j);  // one function at a time keeps the loop finite
+          moved = true;
+        } else {
+          left.push_back(j);
+        }
+      }
+      if (!moved) {
+        plan.fq.insert(plan.fq.end(), left.begin(), left.end());
+        left.clear();
+      }
+      rest.swap(left);
+      continue;
+    }
+    std::sort(pass.fns.begin(), pass.fns.end(),
+              [](const DnFn& a, const DnFn& b) { return a.fn < b.fn; });
+    std::vector<uint32_t> left;
+    for (uint32_t j : rest)
+      if (!taken[j]) left.push_back(j);
+    rest.swap(left);
+    plan.passes.push_back(std::move(pass));
+  }
+  std::sort(plan.fq.begin(), plan.fq.end());
+  return plan;
+}
+
+std::string fbits(uint32_t v) { return "__uint_as_float(" + hex(v) + ")"; }
+
+std::string rold_call(const std::string& st, int i, const DnFn& c) {
+  std::ostringstream o;
+  o << "rold(" << st << ", x" << c.cls << "_" << i << ", co" << i << ", cf" << i << ", "
+    << hex(c.q) << ", " << hex(c.qln) << ", " << hex(c.kp) << ", " << hex(c.p) << ", "
+    << fbits(c.a_bits) << ", " << fbits(c.b_bits) << ", " << fbits(c.m_bits) << ")";
+  return o.str();
+}
+
+// One pass's functions in either arithmetic (fq: fb.., dn: an explicit list).
+struct PassFns {
+  std::vector<uint32_t> fn;   // signature positions
+  std::vector<FnConst> fq;    // arith 0
+  const DnPass* dn = nullptr; // arith 1
+};
+
+std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitShape& js,
+                     uint32_t* passes_out = nullptr) {
   const uint32_t kJitF = static_cast<uint32_t>(js.F);
   const int min_blocks = js.min_blocks;
-  std::vector<FnConst> cs(H);
-  for (uint32_t f = 0; f < H; ++f) cs[f] = fn_const(fns[f], L);
+  DnPlan dn;
+  if (js.arith == 1) {
+    dn = dn_plan(fns, H, L, js.F, js.classes);
+  } else {
+    for (uint32_t f = 0; f < H; ++f) dn.fq.push_back(f);
+  }
+  std::vector<PassFns> passes;
+  for (const DnPass& dp : dn.passes) {
+    PassFns pf;
+    for (const DnFn& f : dp.fns) pf.fn.push_back(f.fn);
+    pf.dn = &dp;
+    passes.push_back(std::move(pf));
+  }
+  for (size_t i = 0; i < dn.fq.size(); i += kJitF) {  // fq passes
+    PassFns pf;
+    for (size_t k = i; k < std::min(dn.fq.size(), i + kJitF); ++k) {
+      pf.fn.push_back(dn.fq[k]);
+      pf.fq.push_back(fn_const(fns[dn.fq[k]], L));
+    }
+    passes.push_back(std::move(pf));
+  }
+  if (passes_out) *passes_out = static_cast<uint32_t>(passes.size());
   const int R = (3 + static_cast<int>(L)) >> 2;  // ring words above the current one
   std::ostringstream s;
   s << "typedef unsigned int u32; typedef unsigned long long u64; typedef unsigned char u8;\n"
        "typedef long long i64;\n"
        "#define L " << L << "\n#define H " << H << "\n"
-       "#define NPASS " << (H + kJitF - 1) / kJitF << "\n"
+       "#define NPASS " << passes.size() << "\n"
+       "// arithmetic: " << dn.passes.size() << " dn passes, " << dn.fq.size()
+    << " fq functions\n"
        "static __device__ __forceinline__ u32 umin(u32 a, u32 b) { return a < b ? a : b; }\n"
+       "static __device__ __forceinline__ u32 smin(u32 a, u32 b) {\n"
+       "  return (u32)min((int)a, (int)b);\n"
+       "}\n"
        "static __device__ __forceinline__ u32 rol(u32 C, u32 ci, u32 co, float cf, u32 q,\n"
        "    u32 qln256, u32 negp256, float qp256, float qlnp, float c5) {\n"
        "  const float t1 = __fmaf_rn(cf, qlnp, c5);\n"
@@ -174,6 +432,17 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "  x = kb * negp256 + x;\n"
        "  return umin(x, x + negp256);\n"
        "}\n"
+       "// dn: z = 0x80000000 + c is the float -c*2^-149 (see k1_jit.cpp)\n"
+       "static __device__ __forceinline__ u32 rold(u32 z, u32 X, u32 co, float cf, u32 q,\n"
+       "    u32 qln, u32 kp, u32 p, float A, float B, float M) {\n"
+       "  const float t1 = __fmul_rn(cf, B);\n"
+       "  const float R = __fmaf_rn(__uint_as_float(z), A, t1);\n"
+       "  const u32 kb = __float_as_uint(__fadd_rd(R, M));\n"
+       "  u32 x = co * qln + X;\n"
+       "  x = z * q + x;\n"
+       "  x = kb * kp + x;\n"
+       "  return (u32)__viaddmin_s32((int)x, (int)p, (int)x);\n"
+       "}\n"
        "extern \"C\" __global__ void __launch_bounds__(" << kJitThreads << ", " << min_blocks << ")\n"
        "k1j(const u8* __restrict__ text, const u64* __restrict__ offsets,\n"
        "    const u32* __restrict__ order, const u32* __restrict__ item_doc,\n"
@@ -182,12 +451,11 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "    u32* __restrict__ pass_flag, u32 epoch) {\n"
        "  const i64 KSEG = seg_len;  // windows per work item\n"
        "  // c5 = 2^-5 arrives as a parameter so that it sits in a register and\n"
-       "  // every FFMA keeps its function constant as the immediate\n"
+       "  // every FFMA keeps its function constant as the immediate (fq)\n"
        "  const u32 lane = threadIdx.x & 31;\n"
-       "  // pass-major: every warp of the grid works on pass P (functions\n"
-       "  // P*F .. P*F+F-1) until pass P's items are exhausted, so the SMs\n"
-       "  // execute one pass's code at a time (the instruction cache holds one\n"
-       "  // pass, not all of them)\n"
+       "  // pass-major: every warp of the grid works on pass P until pass P's\n"
+       "  // items are exhausted, so the SMs execute one pass's code at a time\n"
+       "  // (the instruction cache holds one pass, not all of them)\n"
        "  for (u32 P = 0; P < NPASS; ++P) {\n"
        "  // the chunk gate (K1Gate): the next launch may start filling SMs\n"
        "  if (P == NPASS - 1 && lane == 0 && pass_flag) atomicMax(pass_flag, epoch);\n"
@@ -195,8 +463,8 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "  if (lane == 0) base = atomicAdd(counter + P, 32ull);\n"
        "  base = __shfl_sync(0xffffffffu, base, 0);\n"
        "  while (base < n_items) {\n"
-       "    u64 nxt = 0;\n"
-       "    if (lane == 0) nxt = atomicAdd(counter + P, 32ull);\n"
+       "    u32 nxt = 0;  // < 2^32 (n_items is u32): one register across the pass\n"
+       "    if (lane == 0) nxt = (u32)atomicAdd(counter + P, 32ull);\n"
        "    const bool active = base + lane < n_items;\n"
        "    const u32 item = active ? order[base + lane] : 0u;\n"
        "    u64 doc = item; i64 ws = 0; bool multi = false;\n"
@@ -216,23 +484,45 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "    const u64 abase = (u64)bp;\n"
        "    u32* row = sig + doc * H;\n"
        "    switch (P) {\n";
-  int pass = 0;
-  for (uint32_t fb = 0; fb < H; fb += kJitF, ++pass) {
-    const int n = static_cast<int>(std::min<uint32_t>(kJitF, H - fb));
-    s << "    case " << pass << ": { // functions " << fb << " .. " << fb + n - 1 << "\n";
-    for (int f = 0; f < n; ++f) s << "      u32 s" << f << " = 0u, m" << f << " = 0xffffffffu;\n";
+  for (size_t pass = 0; pass < passes.size(); ++pass) {
+    const PassFns& pf = passes[pass];
+    const bool isdn = pf.dn != nullptr;
+    const int n = static_cast<int>(pf.fn.size());
+    const int ncls = isdn ? static_cast<int>(pf.dn->w.size()) : 0;
+    s << "    case " << pass << ": { // functions";
+    for (int f = 0; f < n; ++f) s << " " << pf.fn[f];
+    s << "\n";
+    if (isdn) {
+      s << "      const u32 GG = " << hex(pf.dn->g << 8) << ";  // float c_out offset 256g\n";
+      for (int c = 0; c < ncls; ++c) s << "      const u32 W" << c << " = " << hex(pf.dn->w[c]) << ";\n";
+      for (int f = 0; f < n; ++f)
+        s << "      u32 s" << f << " = 0x80000000u, m" << f << " = 0x7fffffffu;\n";
+    } else {
+      for (int f = 0; f < n; ++f) s << "      u32 s" << f << " = 0u, m" << f << " = 0xffffffffu;\n";
+    }
+    auto call = [&](const std::string& st, int i, int f) {
+      return isdn ? rold_call(st, i, pf.dn->fns[f]) : rol_call(st, i, pf.fq[f]);
+    };
+    const char* mn = isdn ? "smin" : "umin";
     // one single-step loop, run twice: phase 0 = warm-up (no min) + steps to
     // a 4-byte-aligned word boundary; phase 1 = the tail below the words
     s << "      i64 p = e - 1;\n"
          "      for (int phase = 0; phase < 2; ++phase) {\n"
-         "        while (p >= wlo && (phase == 1 || p > e - L || ((abase + (u64)p + 1) & 3))) {\n"
-         "          const u32 ci0 = ((u32)bp[p]) << 8;\n"
-         "          const u32 co0 = (p + L < e) ? (u32)bp[p + L] : 0u;\n"
-         "          const float cf0 = __uint2float_rn(co0);\n"
-         "          const bool cnt = p <= e - L;\n";
+         "        while (p >= wlo && (phase == 1 || p > e - L || ((abase + (u64)p + 1) & 3))) {\n";
+    if (isdn) {
+      s << "          const u32 ci0 = (u32)bp[p];\n";
+      for (int c = 0; c < ncls; ++c) s << "          const u32 x" << c << "_0 = ci0 | W" << c << ";\n";
+      s << "          const u32 co0 = (p + L < e) ? (u32)bp[p + L] : 0u;\n"
+           "          const float cf0 = __uint2float_rn(co0 + GG);\n";
+    } else {
+      s << "          const u32 ci0 = ((u32)bp[p]) << 8;\n"
+           "          const u32 co0 = (p + L < e) ? (u32)bp[p + L] : 0u;\n"
+           "          const float cf0 = __uint2float_rn(co0);\n";
+    }
+    s << "          const bool cnt = p <= e - L;\n";
     for (int f = 0; f < n; ++f) {
-      s << "          s" << f << " = " << rol_call("s" + std::to_string(f), 0, cs[fb + f]) << ";\n"
-        << "          if (cnt) m" << f << " = umin(m" << f << ", s" << f << ");\n";
+      s << "          s" << f << " = " << call("s" + std::to_string(f), 0, f) << ";\n"
+        << "          if (cnt) m" << f << " = " << mn << "(m" << f << ", s" << f << ");\n";
     }
     s << "          --p;\n"
          "        }\n"
@@ -258,22 +548,38 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
       for (int i = 3; i >= 0; --i) {
         const int pos = i + static_cast<int>(L), k = pos >> 2, j = pos & 3;
         const std::string src = k == 0 ? "cur" : "r" + std::to_string(k);
-        char sel_in[8], sel_out[8];
+        char sel_in[8], sel_out[8], sel_x[8], sel_f[8];
         std::snprintf(sel_in, sizeof sel_in, "0x44%d4", i);
         std::snprintf(sel_out, sizeof sel_out, "0x444%d", j);
-        s << "            { const u32 ci" << i << " = __byte_perm(cur, 0u, " << sel_in << ");\n"
-          << "            const u32 co" << i << " = __byte_perm(" << src << ", 0u, " << sel_out
-          << ");\n"
-          << "            const float cf" << i << " = __uint2float_rn(co" << i << ");\n";
+        std::snprintf(sel_x, sizeof sel_x, "0x765%d", i);  // c_in + (w & ~0xff)
+        std::snprintf(sel_f, sizeof sel_f, "0x445%d", j);  // c_out + 256g
+        s << "            {";
+        if (isdn) {
+          for (int c = 0; c < ncls; ++c)
+            s << " const u32 x" << c << "_" << i << " = __byte_perm(cur, W" << c << ", " << sel_x
+              << ");\n";
+          s << "            const u32 co" << i << " = __byte_perm(" << src << ", 0u, " << sel_out
+            << ");\n"
+            << "            const float cf" << i << " = __uint2float_rn(__byte_perm(" << src
+            << ", GG, " << sel_f << "));\n";
+        } else {
+          s << " const u32 ci" << i << " = __byte_perm(cur, 0u, " << sel_in << ");\n"
+            << "            const u32 co" << i << " = __byte_perm(" << src << ", 0u, " << sel_out
+            << ");\n"
+            << "            const float cf" << i << " = __uint2float_rn(co" << i << ");\n";
+        }
       }
+      const char* mn3 = isdn ? "(u32)__vimin3_s32((int)" : "__vimin3_u32(";
+      const char* cst = isdn ? "(int)" : "";
       for (int f = 0; f < n; ++f) {
         const std::string sf = "s" + std::to_string(f), mf = "m" + std::to_string(f);
-        s << "            { const u32 a3 = " << rol_call(sf, 3, cs[fb + f]) << ";\n"
-          << "              const u32 a2 = " << rol_call("a3", 2, cs[fb + f]) << ";\n"
-          << "              const u32 a1 = " << rol_call("a2", 1, cs[fb + f]) << ";\n"
-          << "              const u32 a0 = " << rol_call("a1", 0, cs[fb + f]) << ";\n"
-          << "              " << sf << " = a0; " << mf << " = __vimin3_u32(" << mf << ", a3, a2); "
-          << mf << " = __vimin3_u32(" << mf << ", a1, a0); }\n";
+        s << "            { const u32 a3 = " << call(sf, 3, f) << ";\n"
+          << "              const u32 a2 = " << call("a3", 2, f) << ";\n"
+          << "              const u32 a1 = " << call("a2", 1, f) << ";\n"
+          << "              const u32 a0 = " << call("a1", 0, f) << ";\n"
+          << "              " << sf << " = a0; " << mf << " = " << mn3 << mf << ", " << cst
+          << "a3, " << cst << "a2); " << mf << " = " << mn3 << mf << ", " << cst << "a1, " << cst
+          << "a0); }\n";
       }
       s << "            }}}}\n";
       for (int k = R; k >= 2; --k) s << "            r" << k << " = r" << k - 1 << ";\n";
@@ -312,17 +618,24 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
            "        }\n"
            "      }\n";
     }
-    // store the canonical minima (state scaled by 256)
+    // store the canonical minima (fq: state scaled by 256; dn: biased by 2^31)
+    auto val = [&](int f) {
+      return isdn ? "(m" + std::to_string(f) + " ^ 0x80000000u)" : "(m" + std::to_string(f) + " >> 8)";
+    };
     s << "      if (active) {\n        if (multi) {\n";
-    for (int f = 0; f < n; ++f)
-      s << "          atomicMin(row + " << fb + f << ", m" << f << " >> 8);\n";
+    for (int f = 0; f < n; ++f) s << "          atomicMin(row + " << pf.fn[f] << ", " << val(f) << ");\n";
     s << "        } else {\n";
-    if (H % 4 == 0 && n % 4 == 0) {
-      for (int f = 0; f < n; f += 4)
-        s << "          *(uint4*)(row + " << fb + f << ") = make_uint4(m" << f << " >> 8, m" << f + 1
-          << " >> 8, m" << f + 2 << " >> 8, m" << f + 3 << " >> 8);\n";
-    } else {
-      for (int f = 0; f < n; ++f) s << "          row[" << fb + f << "] = m" << f << " >> 8;\n";
+    for (int f = 0; f < n;) {
+      const bool vec = f + 4 <= n && pf.fn[f] % 4 == 0 && pf.fn[f + 1] == pf.fn[f] + 1 &&
+                       pf.fn[f + 2] == pf.fn[f] + 2 && pf.fn[f + 3] == pf.fn[f] + 3 && H % 4 == 0;
+      if (vec) {
+        s << "          *(uint4*)(row + " << pf.fn[f] << ") = make_uint4(" << val(f) << ", "
+          << val(f + 1) << ", " << val(f + 2) << ", " << val(f + 3) << ");\n";
+        f += 4;
+      } else {
+        s << "          row[" << pf.fn[f] << "] = " << val(f) << ";\n";
+        ++f;
+      }
     }
     s << "        }\n      }\n      break;\n    }\n";
   }
@@ -333,6 +646,7 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "}\n";
   return s.str();
 }
+
 
 struct JitKernel {
   cudaLibrary_t lib = nullptr;
@@ -349,13 +663,15 @@ std::shared_ptr<JitKernel> compile(const nd_hash_fn* fns, uint32_t H, uint32_t L
                                    const JitShape& js) {
   const Nvrtc& nv = nvrtc();
   if (!nv.ok) fail(ND_ERR_DEVICE, "K1j: " + nv.error);
-  const std::string src = generate(fns, H, L, js);
+  uint32_t passes = 0;
+  const std::string src = generate(fns, H, L, js, &passes);
   auto t0 = std::chrono::steady_clock::now();
   nvrtcProgram prog;
   if (nv.create(&prog, src.c_str(), "k1j.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     fail(ND_ERR_DEVICE, "K1j: nvrtcCreateProgram failed");
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17"};
-  const nvrtcResult rc = nv.compile(prog, 3, opts);
+  // denormals must survive: the dn state is a denormal float (no FTZ)
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17", "--ftz=false"};
+  const nvrtcResult rc = nv.compile(prog, 4, opts);
   if (rc != NVRTC_SUCCESS) {
     size_t n = 0;
     nv.log_size(prog, &n);
@@ -375,7 +691,7 @@ std::shared_ptr<JitKernel> compile(const nd_hash_fn* fns, uint32_t H, uint32_t L
   ND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &k->per_sm, reinterpret_cast<const void*>(k->fn), kJitThreads, 0));
   k->per_sm = std::max(k->per_sm, 1);
-  k->passes = (H + js.F - 1) / js.F;
+  k->passes = passes;
   k->compile_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return k;
@@ -398,7 +714,8 @@ void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L) {
   const JitShape js = jit_shape();
   key += "|" + std::to_string(H) + "|" + std::to_string(L) + "|" + std::to_string(js.F) + "|" +
          std::to_string(js.min_blocks) + "|" + std::to_string(js.prefetch) + "|" +
-         std::to_string(js.unroll);
+         std::to_string(js.unroll) + "|" + std::to_string(js.arith) + "|" +
+         std::to_string(js.classes);
   int dev = 0;
   cudaGetDevice(&dev);
   key += "|" + std::to_string(dev);
@@ -462,4 +779,35 @@ extern "C" int64_t nd_k1j_source(const nd_hash_fn* fns, uint32_t H, uint32_t L, 
     out[n] = '\0';
   }
   return static_cast<int64_t>(s.size());
+}
+
+extern "C" int64_t nd_k1j_plan(const nd_hash_fn* fns, uint32_t H, uint32_t L, uint32_t* out,
+                               uint64_t cap_rows) {
+  if (!fns || H == 0 || H > 1024 || L == 0 || L > 16) return -1;
+  for (uint32_t i = 0; i < H; ++i)  // the fq domain (derive_family's)
+    if (fns[i].modulus < (1u << 21) || fns[i].modulus >= (1u << 23) || fns[i].base == 0 ||
+        fns[i].base >= (1u << 16))
+      return -1;
+  const ndb::JitShape js = ndb::jit_shape();
+  if (js.arith != 1) return -1;
+  const ndb::DnPlan plan = ndb::dn_plan(fns, H, L, js.F, js.classes);
+  uint64_t row = 0;
+  auto put = [&](const uint32_t* v) {
+    if (out && row < cap_rows) std::memcpy(out + 12 * row, v, 12 * sizeof(uint32_t));
+    ++row;
+  };
+  for (size_t P = 0; P < plan.passes.size(); ++P)
+    for (const ndb::DnFn& f : plan.passes[P].fns) {
+      const ndb::DnPass& dp = plan.passes[P];
+      const uint32_t v[12] = {static_cast<uint32_t>(P), f.cls, dp.g, dp.w[f.cls], f.fn,
+                              f.q, f.qln, f.kp, f.p, f.a_bits, f.b_bits, f.m_bits};
+      put(v);
+    }
+  const uint32_t F = static_cast<uint32_t>(js.F);
+  for (size_t i = 0; i < plan.fq.size(); ++i) {  // fq passes: g = 0
+    const uint32_t v[12] = {static_cast<uint32_t>(plan.passes.size() + i / F), 0, 0, 0,
+                            plan.fq[i], fns[plan.fq[i]].base, 0, 0, fns[plan.fq[i]].modulus, 0, 0, 0};
+    put(v);
+  }
+  return static_cast<int64_t>(row);
 }
