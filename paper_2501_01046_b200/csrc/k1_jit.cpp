@@ -53,13 +53,18 @@ constexpr int kJitThreads = 128;
 // Tuning knobs of the generated kernel (part of the cache key): functions per
 // pass F (their states + minima stay in registers), the minimum resident
 // blocks per SM handed to ptxas, and how many words ahead the text is loaded.
-// (C2 shard, H=128: F=16 / 6 blocks 66.9 ms, F=32 / 4 blocks 67.6 ms,
-// F=24 / 5 blocks 67.7 ms, F=32 / 5 blocks 74.4 ms (spills), F=16 / 8 blocks
-// 73.4 ms; a second prefetched word changes nothing -- profiles/r2_k1j_variants.txt)
+// Defaults per arithmetic, measured on the C2 shard (1M docs, H=128, B200,
+// profiles/r2_k1j_variants.txt):
+//   fq: F=16 / 6 blocks 66.9 ms (F=32 / 4 blocks 67.6, F=24 / 5 blocks 67.7,
+//       F=32 / 5 blocks 74.4 (spills), F=16 / 8 blocks 73.4; prefetch 2: same)
+//   dn: F=32 / 4 blocks / 2 words prefetched 63.7 ms (F=16 / 6 blocks 65.9,
+//       F=20 / 5 64.8, F=32 / 4 / prefetch 1 64.1, F=40 / 4 65.1, F=48 / 4
+//       67.8, F=64 / 2 67.0): with 7.5 instructions per HWE the per-pass
+//       extraction and loop overhead and the exposed text load matter more
 struct JitShape {
-  int F = 16;
-  int min_blocks = 6;
-  int prefetch = 1;
+  int F = 32;
+  int min_blocks = 4;
+  int prefetch = 2;
   int unroll = 1;  // whole words per loop iteration (2: ND_K1J_UNROLL=2, slower)
   int arith = 1;   // 1: denormal-state arithmetic (dn, default); 0: the fq state of K1 (ND_K1J_ARITH=fq)
   int classes = 4; // dn: most w classes (c_in extractions per window) in one pass
@@ -67,11 +72,16 @@ struct JitShape {
 
 JitShape jit_shape() {
   JitShape j;
+  if (const char* v = getenv("ND_K1J_ARITH")) j.arith = std::strcmp(v, "fq") == 0 ? 0 : 1;
+  if (j.arith == 0) {
+    j.F = 16;
+    j.min_blocks = 6;
+    j.prefetch = 1;
+  }
   if (const char* v = getenv("ND_K1J_F")) j.F = std::max(4, std::min(64, atoi(v)));
   if (const char* v = getenv("ND_K1J_MINB")) j.min_blocks = std::max(1, std::min(16, atoi(v)));
   if (const char* v = getenv("ND_K1J_PREFETCH")) j.prefetch = std::max(1, std::min(2, atoi(v)));
   if (const char* v = getenv("ND_K1J_UNROLL")) j.unroll = std::max(1, std::min(2, atoi(v)));
-  if (const char* v = getenv("ND_K1J_ARITH")) j.arith = std::strcmp(v, "fq") == 0 ? 0 : 1;
   if (const char* v = getenv("ND_K1J_CLASSES")) j.classes = std::max(1, std::min(8, atoi(v)));
   return j;
 }

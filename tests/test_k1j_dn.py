@@ -65,10 +65,10 @@ def test_dn_plan_shape(seed, H, L):
     rows = allrows[allrows[:, 2] > 0]  # g = 0: the rare fq functions
     assert len(rows) >= H * 0.9
     for P in np.unique(allrows[:, 0]):
-        assert (allrows[:, 0] == P).sum() <= 16
+        assert (allrows[:, 0] == P).sum() <= 32  # F = 32 functions per pass (dn default)
     for P in np.unique(rows[:, 0]):
         sel = rows[rows[:, 0] == P]
-        assert len(sel) <= 16
+        assert len(sel) <= 32
         assert len(np.unique(sel[:, 2])) == 1  # one offset g per pass
         assert len(np.unique(sel[:, 1])) <= 4  # at most 4 w classes
         assert all((w & 0xFF) == 0 for w in sel[:, 3])
