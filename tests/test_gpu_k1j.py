@@ -224,3 +224,33 @@ def test_chunk_gate_host_pipelines(ctx, oracle, monkeypatch):
     monkeypatch.delenv("ND_K1J_RING_GATE", raising=False)
     assert got["ring"][0] == got["ring_gate"][0]
     assert np.array_equal(got["ring"][1], res["gate"][0]) and np.array_equal(got["ring_gate"][1], res["gate"][0])
+
+
+@pytest.mark.parametrize("seed,H,L", [(35, 128, 5), (8, 64, 3)])
+@pytest.mark.parametrize("shape", [
+    {},                                                        # dn, F=32, 4 CTAs, prefetch 2
+    {"ND_K1J_ARITH": "fq"},                                    # fq, F=16, 6 CTAs
+    {"ND_K1J_F": "16", "ND_K1J_MINB": "6", "ND_K1J_PREFETCH": "1"},  # round-2 dn shape
+    {"ND_K1J_CLASSES": "1", "ND_K1J_F": "20"},                 # one w class, partial passes
+])
+def test_k1j_shapes_and_dn_misfits(ctx, oracle, monkeypatch, seed, H, L, shape):
+    """families whose dn plan leaves one function to an fq pass of the same
+    kernel (nd_k1j_plan: seed 35 at H=128/L=5, seed 8 at H=64/L=3), under the
+    shipped shape and the knobs' other settings: identical to the oracle"""
+    fam = minhash.derive_family(seed, H, L)
+    plan = np.zeros((H, 12), np.uint32)
+    assert ctx.lib.nd_k1j_plan(fam.functions, H, L, plan.ctypes.data_as(C.POINTER(C.c_uint32)),
+                               H) == H
+    if not shape:
+        assert (plan[:, 2] == 0).sum() == 1  # one fq function
+    rng = np.random.default_rng(seed)
+    data, offs = _docs(rng, list(rng.integers(L, 5000, size=300)) + [L, L + 1, 30000])
+    for k, v in shape.items():
+        monkeypatch.setenv(k, v)
+    ctx._family_key = None
+    sig, _ = minhash.signatures_packed(data, offs, fam, 0, 0, 0, ctx=ctx, want_bands=False)
+    assert _kernel(ctx) == "k1j"
+    for k in shape:
+        monkeypatch.delenv(k)
+    ctx._family_key = None
+    assert np.array_equal(sig, oracle.signatures(data, offs, oracle.derive_family(seed, H, L), L=L))
