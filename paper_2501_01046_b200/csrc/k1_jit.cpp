@@ -68,6 +68,8 @@ struct JitShape {
   int unroll = 1;  // whole words per loop iteration (2: ND_K1J_UNROLL=2, slower)
   int arith = 1;   // 1: denormal-state arithmetic (dn, default); 0: the fq state of K1 (ND_K1J_ARITH=fq)
   int classes = 4; // dn: most w classes (c_in extractions per window) in one pass
+  int gptr = 0;    // 1: word pointer derived from the text pointer (LDG) instead of
+                   // an integer address (generic LD); ND_K1J_GPTR=1
 };
 
 JitShape jit_shape() {
@@ -83,6 +85,7 @@ JitShape jit_shape() {
   if (const char* v = getenv("ND_K1J_PREFETCH")) j.prefetch = std::max(1, std::min(2, atoi(v)));
   if (const char* v = getenv("ND_K1J_UNROLL")) j.unroll = std::max(1, std::min(2, atoi(v)));
   if (const char* v = getenv("ND_K1J_CLASSES")) j.classes = std::max(1, std::min(8, atoi(v)));
+  if (const char* v = getenv("ND_K1J_GPTR")) j.gptr = atoi(v) ? 1 : 0;
   return j;
 }
 
@@ -426,7 +429,9 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "typedef long long i64;\n"
        "#define L " << L << "\n#define H " << H << "\n"
        "#define NPASS " << passes.size() << "\n"
-       "// arithmetic: " << dn.passes.size() << " dn passes, " << dn.fq.size()
+    << (js.gptr ? "#define LW(a) __ldg(a)  // text words through the read-only path (LDG)\n"
+                : "#define LW(a) (*(a))\n")
+    << "// arithmetic: " << dn.passes.size() << " dn passes, " << dn.fq.size()
     << " fq functions\n"
        "static __device__ __forceinline__ u32 umin(u32 a, u32 b) { return a < b ? a : b; }\n"
        "static __device__ __forceinline__ u32 smin(u32 a, u32 b) {\n"
@@ -539,9 +544,9 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
          "        if (phase == 1) break;\n";
     // whole aligned words
     s << "        if (p - " << (js.unroll == 2 ? 7 : 3) << " >= wlo) {\n"
-         "          const u32* wp = (const u32*)(abase + (u64)(p - 3));\n"
+      << "          const u32* wp = (const u32*)(abase + (u64)(p - 3));\n"
          "          i64 q = p - 3;\n"
-         "          u32 cur = wp[0];\n";
+         "          u32 cur = LW(wp);\n";
     for (int k = 1; k <= R; ++k) {
       // the ring holds words q+4 .. q+4R (each shifts up one slot per word,
       // so every slot is loaded, not only those the first word reads); bytes
@@ -549,8 +554,8 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
       // e), and a word with no position below e is not loaded at all
       s << "          u32 r" << k << " = 0u;\n"
         << "          { const i64 nv = e - (q + " << 4 * k << ");\n"
-        << "            if (nv > 0) r" << k << " = wp[" << k
-        << "] & (nv >= 4 ? 0xffffffffu : ((1u << (8 * (u32)nv)) - 1u)); }\n";
+        << "            if (nv > 0) r" << k << " = LW(wp + " << k
+        << ") & (nv >= 4 ? 0xffffffffu : ((1u << (8 * (u32)nv)) - 1u)); }\n";
     }
     // one word: 4 windows of every function of the pass, then the ring
     // shifts down one word and `next` becomes the current word
@@ -601,9 +606,9 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
       // word goes to the single steps below
       s << "          u32 npair = (u32)((q - wlo + 4) >> 3);\n"
            "          do {\n"
-           "            const u32 nx = wp[-1];\n";
+           "            const u32 nx = LW(wp - 1);\n";
       word("nx");
-      s << "            const u32 nx2 = (q - 8 >= wlo) ? wp[-2] : 0u;\n";
+      s << "            const u32 nx2 = (q - 8 >= wlo) ? LW(wp - 2) : 0u;\n";
       word("nx2");
       s << "            wp -= 2; q -= 8;\n"
            "          } while (--npair);\n"
@@ -612,14 +617,14 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
            "      }\n";
     } else {
       if (js.prefetch >= 2)
-        s << "          u32 nx1 = (q - 4 >= wlo) ? wp[-1] : 0u;\n";
+        s << "          u32 nx1 = (q - 4 >= wlo) ? LW(wp - 1) : 0u;\n";
       s << "          for (;;) {\n"
            "            const bool more = q - 4 >= wlo;\n";
       if (js.prefetch >= 2)
         s << "            const u32 nx = nx1;\n"
-             "            nx1 = (q - 8 >= wlo) ? wp[-2] : 0u;\n";
+             "            nx1 = (q - 8 >= wlo) ? LW(wp - 2) : 0u;\n";
       else
-        s << "            const u32 nx = more ? wp[-1] : 0u;\n";
+        s << "            const u32 nx = more ? LW(wp - 1) : 0u;\n";
       word("nx");
       s << "            --wp; q -= 4;\n"
            "            if (!more) break;\n"
@@ -725,7 +730,7 @@ void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L) {
   key += "|" + std::to_string(H) + "|" + std::to_string(L) + "|" + std::to_string(js.F) + "|" +
          std::to_string(js.min_blocks) + "|" + std::to_string(js.prefetch) + "|" +
          std::to_string(js.unroll) + "|" + std::to_string(js.arith) + "|" +
-         std::to_string(js.classes);
+         std::to_string(js.classes) + "|" + std::to_string(js.gptr);
   int dev = 0;
   cudaGetDevice(&dev);
   key += "|" + std::to_string(dev);
