@@ -68,6 +68,9 @@ struct JitShape {
   int unroll = 1;  // whole words per loop iteration (2: ND_K1J_UNROLL=2, slower)
   int arith = 1;   // 1: denormal-state arithmetic (dn, default); 0: the fq state of K1 (ND_K1J_ARITH=fq)
   int classes = 4; // dn: most w classes (c_in extractions per window) in one pass
+  int pfw = 0;     // > 0: prefetch the text pfw words below the current one at every
+                   // word (ND_K1J_PFW; ND_K1J_PFL2=1: into L2 instead of L1)
+  int pfl2 = 0;
   int gptr = 0;    // 1: word pointer derived from the text pointer (LDG) instead of
                    // an integer address (generic LD); ND_K1J_GPTR=1
 };
@@ -86,6 +89,8 @@ JitShape jit_shape() {
   if (const char* v = getenv("ND_K1J_UNROLL")) j.unroll = std::max(1, std::min(2, atoi(v)));
   if (const char* v = getenv("ND_K1J_CLASSES")) j.classes = std::max(1, std::min(8, atoi(v)));
   if (const char* v = getenv("ND_K1J_GPTR")) j.gptr = atoi(v) ? 1 : 0;
+  if (const char* v = getenv("ND_K1J_PFW")) j.pfw = std::max(0, std::min(4096, atoi(v)));
+  if (const char* v = getenv("ND_K1J_PFL2")) j.pfl2 = atoi(v) ? 1 : 0;
   return j;
 }
 
@@ -620,6 +625,9 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
         s << "          u32 nx1 = (q - 4 >= wlo) ? LW(wp - 1) : 0u;\n";
       s << "          for (;;) {\n"
            "            const bool more = q - 4 >= wlo;\n";
+      if (js.pfw > 0)
+        s << "            if (q - " << 4 * js.pfw << " >= wlo) asm volatile(\"prefetch.global."
+          << (js.pfl2 ? "L2" : "L1") << " [%0];\" :: \"l\"(wp - " << js.pfw << "));\n";
       if (js.prefetch >= 2)
         s << "            const u32 nx = nx1;\n"
              "            nx1 = (q - 8 >= wlo) ? LW(wp - 2) : 0u;\n";
@@ -730,7 +738,8 @@ void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L) {
   key += "|" + std::to_string(H) + "|" + std::to_string(L) + "|" + std::to_string(js.F) + "|" +
          std::to_string(js.min_blocks) + "|" + std::to_string(js.prefetch) + "|" +
          std::to_string(js.unroll) + "|" + std::to_string(js.arith) + "|" +
-         std::to_string(js.classes) + "|" + std::to_string(js.gptr);
+         std::to_string(js.classes) + "|" + std::to_string(js.gptr) + "|" +
+         std::to_string(js.pfw) + "|" + std::to_string(js.pfl2);
   int dev = 0;
   cudaGetDevice(&dev);
   key += "|" + std::to_string(dev);
