@@ -71,6 +71,8 @@ struct JitShape {
   int pfw = 0;     // > 0: prefetch the text pfw words below the current one at every
                    // word (ND_K1J_PFW; ND_K1J_PFL2=1: into L2 instead of L1)
   int pfl2 = 0;
+  int sring = 0;   // 1: text lines staged per lane in a 2-line shared-memory ring by
+                   // cp.async one line ahead (ND_K1J_SRING=1)
   int gptr = 0;    // 1: word pointer derived from the text pointer (LDG) instead of
                    // an integer address (generic LD); ND_K1J_GPTR=1
 };
@@ -91,6 +93,8 @@ JitShape jit_shape() {
   if (const char* v = getenv("ND_K1J_GPTR")) j.gptr = atoi(v) ? 1 : 0;
   if (const char* v = getenv("ND_K1J_PFW")) j.pfw = std::max(0, std::min(4096, atoi(v)));
   if (const char* v = getenv("ND_K1J_PFL2")) j.pfl2 = atoi(v) ? 1 : 0;
+  if (const char* v = getenv("ND_K1J_SRING")) j.sring = atoi(v) ? 1 : 0;
+  if (j.unroll != 1) j.sring = 0;
   return j;
 }
 
@@ -463,6 +467,21 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "  x = kb * kp + x;\n"
        "  return (u32)__viaddmin_s32((int)x, (int)p, (int)x);\n"
        "}\n"
+       "// sring: the 128-byte line at g (aligned) into shared memory at s\n"
+       "static __device__ __forceinline__ void fetch_line(u32 s, const void* g) {\n"
+       "#pragma unroll\n"
+       "  for (int i = 0; i < 8; ++i)\n"
+       "    asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(s + 16 * i),\n"
+       "                 \"l\"((const char*)g + 16 * i) : \"memory\");\n"
+       "}\n"
+       "static __device__ __forceinline__ void ring_commit() {\n"
+       "  asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n"
+       "}\n"
+       "// all but the most recent group (the line fetched at the last line entry,\n"
+       "// first read >= 1 iteration later)\n"
+       "static __device__ __forceinline__ void ring_wait() {\n"
+       "  asm volatile(\"cp.async.wait_group 1;\" ::: \"memory\");\n"
+       "}\n"
        "extern \"C\" __global__ void __launch_bounds__(" << kJitThreads << ", " << min_blocks << ")\n"
        "k1j(const u8* __restrict__ text, const u64* __restrict__ offsets,\n"
        "    const u32* __restrict__ order, const u32* __restrict__ item_doc,\n"
@@ -473,6 +492,12 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "  // c5 = 2^-5 arrives as a parameter so that it sits in a register and\n"
        "  // every FFMA keeps its function constant as the immediate (fq)\n"
        "  const u32 lane = threadIdx.x & 31;\n"
+    << (js.sring ? "  // sring: per lane a 2-line ring (256 B) of its text, indexed by address & 255\n"
+                   "  __shared__ __align__(128) u32 sring_buf[" + std::to_string(kJitThreads * 64) + "];\n"
+                   "  const u32* myr = sring_buf + threadIdx.x * 64;\n"
+                   "  const u32 myr_s = (u32)__cvta_generic_to_shared(myr);\n"
+                 : std::string())
+    << ""
        "  // pass-major: every warp of the grid works on pass P until pass P's\n"
        "  // items are exhausted, so the SMs execute one pass's code at a time\n"
        "  // (the instruction cache holds one pass, not all of them)\n"
@@ -562,6 +587,13 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
         << "            if (nv > 0) r" << k << " = LW(wp + " << k
         << ") & (nv >= 4 ? 0xffffffffu : ((1u << (8 * (u32)nv)) - 1u)); }\n";
     }
+    if (js.sring && js.unroll == 1)
+      s << "          { // prime: the current word's line and the one below, then an empty\n"
+           "            // group so that the first ring_wait() waits for them\n"
+           "            const u64 lb = ((u64)wp) & ~127ull;\n"
+           "            fetch_line(myr_s + ((u32)lb & 255u), (const void*)lb);\n"
+           "            if (lb > abase + (u64)wlo) fetch_line(myr_s + ((u32)(lb - 128) & 255u), (const void*)(lb - 128));\n"
+           "            ring_commit(); ring_commit(); }\n";
     // one word: 4 windows of every function of the pass, then the ring
     // shifts down one word and `next` becomes the current word
     auto word = [&](const std::string& next) {
@@ -621,22 +653,32 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
            "        }\n"
            "      }\n";
     } else {
-      if (js.prefetch >= 2)
+      const bool pf2 = js.prefetch >= 2 && !js.sring;
+      if (pf2)
         s << "          u32 nx1 = (q - 4 >= wlo) ? LW(wp - 1) : 0u;\n";
       s << "          for (;;) {\n"
            "            const bool more = q - 4 >= wlo;\n";
       if (js.pfw > 0)
         s << "            if (q - " << 4 * js.pfw << " >= wlo) asm volatile(\"prefetch.global."
           << (js.pfl2 ? "L2" : "L1") << " [%0];\" :: \"l\"(wp - " << js.pfw << "));\n";
-      if (js.prefetch >= 2)
+      if (js.sring)
+        s << "            ring_wait();\n"
+             "            const u32 nx = myr[((u32)(u64)(wp - 1) & 255u) >> 2];\n";
+      else if (pf2)
         s << "            const u32 nx = nx1;\n"
              "            nx1 = (q - 8 >= wlo) ? LW(wp - 2) : 0u;\n";
       else
         s << "            const u32 nx = more ? LW(wp - 1) : 0u;\n";
       word("nx");
       s << "            --wp; q -= 4;\n"
-           "            if (!more) break;\n"
-           "          }\n"
+           "            if (!more) break;\n";
+      if (js.sring)
+        s << "            if (((u32)(u64)wp & 127u) == 124u) {  // entered a new line: fetch the one below\n"
+             "              const u64 lb = (((u64)wp) & ~127ull) - 128;\n"
+             "              if (lb + 128 > abase + (u64)wlo) fetch_line(myr_s + ((u32)lb & 255u), (const void*)lb);\n"
+             "            }\n"
+             "            ring_commit();\n";
+      s << "          }\n"
            "          p = q + 3;\n"
            "        }\n"
            "      }\n";
@@ -739,7 +781,7 @@ void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L) {
          std::to_string(js.min_blocks) + "|" + std::to_string(js.prefetch) + "|" +
          std::to_string(js.unroll) + "|" + std::to_string(js.arith) + "|" +
          std::to_string(js.classes) + "|" + std::to_string(js.gptr) + "|" +
-         std::to_string(js.pfw) + "|" + std::to_string(js.pfl2);
+         std::to_string(js.pfw) + "|" + std::to_string(js.pfl2) + "|" + std::to_string(js.sring);
   int dev = 0;
   cudaGetDevice(&dev);
   key += "|" + std::to_string(dev);
