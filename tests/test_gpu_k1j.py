@@ -232,6 +232,8 @@ def test_chunk_gate_host_pipelines(ctx, oracle, monkeypatch):
     {"ND_K1J_ARITH": "fq"},                                    # fq, F=16, 6 CTAs
     {"ND_K1J_F": "16", "ND_K1J_MINB": "6", "ND_K1J_PREFETCH": "1"},  # round-2 dn shape
     {"ND_K1J_CLASSES": "1", "ND_K1J_F": "20"},                 # one w class, partial passes
+    {"ND_K1J_SRING": "1"},                                     # text via a shared-memory ring
+    {"ND_K1J_GPTR": "1", "ND_K1J_PFW": "40"},                  # __ldg words + L1 prefetch
 ])
 def test_k1j_shapes_and_dn_misfits(ctx, oracle, monkeypatch, seed, H, L, shape):
     """families whose dn plan leaves one function to an fq pass of the same
