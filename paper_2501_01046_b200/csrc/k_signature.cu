@@ -987,7 +987,12 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   uint32_t seg_len = kSeg;
   const bool jit_path = fam.jit && fam.unit == 0;
   if (jit_path) {
-    const uint64_t target = static_cast<uint64_t>(3 * 32 / 2) * k1_jit_resident_warps(fam.jit);
+    // target items: 1.5 per resident lane (ND_K1J_HALF_ITEMS=h: h/2 per lane; tuning)
+    static const uint64_t half_items = [] {
+      const char* v = getenv("ND_K1J_HALF_ITEMS");
+      return static_cast<uint64_t>(v ? std::max(1, std::min(16, atoi(v))) : 3);
+    }();
+    const uint64_t target = half_items * 32 / 2 * k1_jit_resident_warps(fam.jit);
     if (n < target) {
       uint64_t bytes = 0;
       if (h_offsets) {
