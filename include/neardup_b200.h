@@ -154,6 +154,11 @@ const char* nd_dedup_compare_kind(nd_ctx* ctx);
  * when the family is outside K1j's domain. */
 int64_t nd_k1j_source(const nd_hash_fn* fns, uint32_t hash_count, uint32_t shingle_len, char* out,
                       uint64_t cap);
+/* The same for K1j over 16-bit units (unit_bytes = 2: codepoint documents
+ * whose code points are all < 2^16, the fq arithmetic; unit_bytes = 1 is
+ * nd_k1j_source). */
+int64_t nd_k1j_source_units(const nd_hash_fn* fns, uint32_t hash_count, uint32_t shingle_len,
+                            uint32_t unit_bytes, char* out, uint64_t cap);
 /* K1j's dn plan for a family (no device needed): per function one row of 12
  * u32 {pass, class, g, w, function, q, QLn, Kb multiplier, p, A bits, B bits,
  * M bits} (csrc/k1_jit.cpp, the denormal-state arithmetic), written up to

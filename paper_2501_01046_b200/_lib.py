@@ -111,6 +111,8 @@ SIGNATURES = {
     "nd_dedup_compare_kind": (C.c_char_p, [vp]),
     "nd_k1j_source": (C.c_int64, [C.POINTER(NdHashFn), C.c_uint32, C.c_uint32, C.c_char_p,
                                   C.c_uint64]),
+    "nd_k1j_source_units": (C.c_int64, [C.POINTER(NdHashFn), C.c_uint32, C.c_uint32, C.c_uint32,
+                                        C.c_char_p, C.c_uint64]),
     "nd_k1j_plan": (C.c_int64, [C.POINTER(NdHashFn), C.c_uint32, C.c_uint32,
                                 C.POINTER(C.c_uint32), C.c_uint64]),
     "nd_signatures": (C.c_int, [vp, u8p, u64p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,

@@ -73,6 +73,7 @@ struct JitShape {
   int pfl2 = 0;
   int sring = 0;   // 1: text lines staged per lane in a 2-line shared-memory ring by
                    // cp.async one line ahead (ND_K1J_SRING=1)
+  int uw = 1;      // bytes per text unit: 1 (bytes), 2 (code points < 2^16, fq only)
   int gptr = 0;    // 1: word pointer derived from the text pointer (LDG) instead of
                    // an integer address (generic LD); ND_K1J_GPTR=1
 };
@@ -432,12 +433,18 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
     passes.push_back(std::move(pf));
   }
   if (passes_out) *passes_out = static_cast<uint32_t>(passes.size());
-  const int R = (3 + static_cast<int>(L)) >> 2;  // ring words above the current one
+  const int UW = js.uw;                           // bytes per unit
+  const int WU = 4 / UW;                          // units per 4-byte word
+  const int R = (WU - 1 + static_cast<int>(L)) / WU;  // ring words above the current one
   std::ostringstream s;
   s << "typedef unsigned int u32; typedef unsigned long long u64; typedef unsigned char u8;\n"
        "typedef long long i64;\n"
        "#define L " << L << "\n#define H " << H << "\n"
        "#define NPASS " << passes.size() << "\n"
+       "#define UW " << UW << "  // bytes per unit\n"
+    << (UW == 2 ? "#define UNIT(i) ((u32)((const unsigned short*)bp)[i])\n"
+                : "#define UNIT(i) ((u32)bp[i])\n")
+    << ""
     << (js.gptr ? "#define LW(a) __ldg(a)  // text words through the read-only path (LDG)\n"
                 : "#define LW(a) (*(a))\n")
     << "// arithmetic: " << dn.passes.size() << " dn passes, " << dn.fq.size()
@@ -525,7 +532,7 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
        "    const i64 we = active ? (ws + KSEG < nwin ? ws + KSEG : nwin) : 0;\n"
        "    const i64 wlo = active ? ws : 0;\n"
        "    const i64 e = active ? we + L - 1 : 0;\n"
-       "    const u8* bp = text + off;\n"
+       "    const u8* bp = text + off * UW;\n"
        "    const u64 abase = (u64)bp;\n"
        "    u32* row = sig + doc * H;\n"
        "    switch (P) {\n";
@@ -553,15 +560,15 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
     // a 4-byte-aligned word boundary; phase 1 = the tail below the words
     s << "      i64 p = e - 1;\n"
          "      for (int phase = 0; phase < 2; ++phase) {\n"
-         "        while (p >= wlo && (phase == 1 || p > e - L || ((abase + (u64)p + 1) & 3))) {\n";
+         "        while (p >= wlo && (phase == 1 || p > e - L || ((abase + (u64)(p + 1) * UW) & 3))) {\n";
     if (isdn) {
-      s << "          const u32 ci0 = (u32)bp[p];\n";
+      s << "          const u32 ci0 = UNIT(p);\n";
       for (int c = 0; c < ncls; ++c) s << "          const u32 x" << c << "_0 = ci0 | W" << c << ";\n";
-      s << "          const u32 co0 = (p + L < e) ? (u32)bp[p + L] : 0u;\n"
+      s << "          const u32 co0 = (p + L < e) ? UNIT(p + L) : 0u;\n"
            "          const float cf0 = __uint2float_rn(co0 + GG);\n";
     } else {
-      s << "          const u32 ci0 = ((u32)bp[p]) << 8;\n"
-           "          const u32 co0 = (p + L < e) ? (u32)bp[p + L] : 0u;\n"
+      s << "          const u32 ci0 = UNIT(p) << 8;\n"
+           "          const u32 co0 = (p + L < e) ? UNIT(p + L) : 0u;\n"
            "          const float cf0 = __uint2float_rn(co0);\n";
     }
     s << "          const bool cnt = p <= e - L;\n";
@@ -573,9 +580,9 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
          "        }\n"
          "        if (phase == 1) break;\n";
     // whole aligned words
-    s << "        if (p - " << (js.unroll == 2 ? 7 : 3) << " >= wlo) {\n"
-      << "          const u32* wp = (const u32*)(abase + (u64)(p - 3));\n"
-         "          i64 q = p - 3;\n"
+    s << "        if (p - " << (js.unroll == 2 ? 2 * WU - 1 : WU - 1) << " >= wlo) {\n"
+      << "          const u32* wp = (const u32*)(abase + (u64)(p - " << WU - 1 << ") * UW);\n"
+      << "          i64 q = p - " << WU - 1 << ";\n"
          "          u32 cur = LW(wp);\n";
     for (int k = 1; k <= R; ++k) {
       // the ring holds words q+4 .. q+4R (each shifts up one slot per word,
@@ -583,9 +590,9 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
       // at positions >= e read as 0 (the first word's c_out can be position
       // e), and a word with no position below e is not loaded at all
       s << "          u32 r" << k << " = 0u;\n"
-        << "          { const i64 nv = e - (q + " << 4 * k << ");\n"
+        << "          { const i64 nv = e - (q + " << WU * k << ");\n"
         << "            if (nv > 0) r" << k << " = LW(wp + " << k
-        << ") & (nv >= 4 ? 0xffffffffu : ((1u << (8 * (u32)nv)) - 1u)); }\n";
+        << ") & (nv >= " << WU << " ? 0xffffffffu : ((1u << (8 * UW * (u32)nv)) - 1u)); }\n";
     }
     if (js.sring && js.unroll == 1)
       s << "          { // prime: the current word's line and the one below, then an empty\n"
@@ -597,12 +604,17 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
     // one word: 4 windows of every function of the pass, then the ring
     // shifts down one word and `next` becomes the current word
     auto word = [&](const std::string& next) {
-      for (int i = 3; i >= 0; --i) {
-        const int pos = i + static_cast<int>(L), k = pos >> 2, j = pos & 3;
+      for (int i = WU - 1; i >= 0; --i) {
+        const int pos = i + static_cast<int>(L), k = pos / WU, j = pos % WU;
         const std::string src = k == 0 ? "cur" : "r" + std::to_string(k);
         char sel_in[8], sel_out[8], sel_x[8], sel_f[8];
-        std::snprintf(sel_in, sizeof sel_in, "0x44%d4", i);
-        std::snprintf(sel_out, sizeof sel_out, "0x444%d", j);
+        if (UW == 2) {  // half-words: c_in << 8 from bytes 2i, 2i+1; c_out from 2j, 2j+1
+          std::snprintf(sel_in, sizeof sel_in, "0x4%d%d4", 2 * i + 1, 2 * i);
+          std::snprintf(sel_out, sizeof sel_out, "0x44%d%d", 2 * j + 1, 2 * j);
+        } else {
+          std::snprintf(sel_in, sizeof sel_in, "0x44%d4", i);
+          std::snprintf(sel_out, sizeof sel_out, "0x444%d", j);
+        }
         std::snprintf(sel_x, sizeof sel_x, "0x765%d", i);  // c_in + (w & ~0xff)
         std::snprintf(sel_f, sizeof sel_f, "0x445%d", j);  // c_out + 256g
         s << "            {";
@@ -625,15 +637,22 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
       const char* cst = isdn ? "(int)" : "";
       for (int f = 0; f < n; ++f) {
         const std::string sf = "s" + std::to_string(f), mf = "m" + std::to_string(f);
-        s << "            { const u32 a3 = " << call(sf, 3, f) << ";\n"
-          << "              const u32 a2 = " << call("a3", 2, f) << ";\n"
-          << "              const u32 a1 = " << call("a2", 1, f) << ";\n"
-          << "              const u32 a0 = " << call("a1", 0, f) << ";\n"
-          << "              " << sf << " = a0; " << mf << " = " << mn3 << mf << ", " << cst
-          << "a3, " << cst << "a2); " << mf << " = " << mn3 << mf << ", " << cst << "a1, " << cst
-          << "a0); }\n";
+        if (WU == 4) {
+          s << "            { const u32 a3 = " << call(sf, 3, f) << ";\n"
+            << "              const u32 a2 = " << call("a3", 2, f) << ";\n"
+            << "              const u32 a1 = " << call("a2", 1, f) << ";\n"
+            << "              const u32 a0 = " << call("a1", 0, f) << ";\n"
+            << "              " << sf << " = a0; " << mf << " = " << mn3 << mf << ", " << cst
+            << "a3, " << cst << "a2); " << mf << " = " << mn3 << mf << ", " << cst << "a1, " << cst
+            << "a0); }\n";
+        } else {  // two windows per word
+          s << "            { const u32 a1 = " << call(sf, 1, f) << ";\n"
+            << "              const u32 a0 = " << call("a1", 0, f) << ";\n"
+            << "              " << sf << " = a0; " << mf << " = " << mn3 << mf << ", " << cst
+            << "a1, " << cst << "a0); }\n";
+        }
       }
-      s << "            }}}}\n";
+      s << "            " << std::string(WU, '}') << "\n";
       for (int k = R; k >= 2; --k) s << "            r" << k << " = r" << k - 1 << ";\n";
       if (R >= 1) s << "            r1 = cur;\n";
       s << "            cur = " << next << ";\n";
@@ -655,22 +674,22 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
     } else {
       const bool pf2 = js.prefetch >= 2 && !js.sring;
       if (pf2)
-        s << "          u32 nx1 = (q - 4 >= wlo) ? LW(wp - 1) : 0u;\n";
+        s << "          u32 nx1 = (q - " << WU << " >= wlo) ? LW(wp - 1) : 0u;\n";
       s << "          for (;;) {\n"
-           "            const bool more = q - 4 >= wlo;\n";
+           "            const bool more = q - " << WU << " >= wlo;\n";
       if (js.pfw > 0)
-        s << "            if (q - " << 4 * js.pfw << " >= wlo) asm volatile(\"prefetch.global."
+        s << "            if (q - " << WU * js.pfw << " >= wlo) asm volatile(\"prefetch.global."
           << (js.pfl2 ? "L2" : "L1") << " [%0];\" :: \"l\"(wp - " << js.pfw << "));\n";
       if (js.sring)
         s << "            ring_wait();\n"
              "            const u32 nx = myr[((u32)(u64)(wp - 1) & 255u) >> 2];\n";
       else if (pf2)
         s << "            const u32 nx = nx1;\n"
-             "            nx1 = (q - 8 >= wlo) ? LW(wp - 2) : 0u;\n";
+             "            nx1 = (q - " << 2 * WU << " >= wlo) ? LW(wp - 2) : 0u;\n";
       else
         s << "            const u32 nx = more ? LW(wp - 1) : 0u;\n";
       word("nx");
-      s << "            --wp; q -= 4;\n"
+      s << "            --wp; q -= " << WU << ";\n"
            "            if (!more) break;\n";
       if (js.sring)
         s << "            if (((u32)(u64)wp & 127u) == 124u) {  // entered a new line: fetch the one below\n"
@@ -679,7 +698,7 @@ std::string generate(const nd_hash_fn* fns, uint32_t H, uint32_t L, const JitSha
              "            }\n"
              "            ring_commit();\n";
       s << "          }\n"
-           "          p = q + 3;\n"
+           "          p = q + " << WU - 1 << ";\n"
            "        }\n"
            "      }\n";
     }
@@ -719,6 +738,7 @@ struct JitKernel {
   int per_sm = 0;
   uint32_t passes = 0;
   double compile_seconds = 0;
+  float c5 = 0.03125f;  // fq's quotient offset: 2^-5 for bytes, 2^-3 for 16-bit units
 };
 
 std::mutex g_jit_mu;
@@ -757,6 +777,7 @@ std::shared_ptr<JitKernel> compile(const nd_hash_fn* fns, uint32_t H, uint32_t L
       &k->per_sm, reinterpret_cast<const void*>(k->fn), kJitThreads, 0));
   k->per_sm = std::max(k->per_sm, 1);
   k->passes = passes;
+  k->c5 = js.uw == 2 ? 0.125f : 0.03125f;
   k->compile_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return k;
@@ -774,14 +795,31 @@ bool k1_jit_eligible(const DevFamily& fam) {
 
 // Compiles (or finds) the family's kernel; the cache outlives contexts so a
 // family is compiled once per process.
-void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L) {
+// uw = 2: text of 16-bit units (code points < 2^16), the fq arithmetic with
+// c5 = 2^-3 (the error bound of DESIGN §3 with c_in, c_out < 2^16)
+JitShape unit_shape(JitShape js, int uw) {
+  if (uw == 2) {
+    js.uw = 2;
+    js.arith = 0;
+    js.F = 16;
+    js.min_blocks = 6;
+    js.prefetch = 1;
+    js.unroll = 1;
+    js.sring = 0;
+    js.pfw = 0;
+  }
+  return js;
+}
+
+void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L, int uw) {
   std::string key(reinterpret_cast<const char*>(fns), sizeof(nd_hash_fn) * H);
-  const JitShape js = jit_shape();
+  const JitShape js = unit_shape(jit_shape(), uw);
   key += "|" + std::to_string(H) + "|" + std::to_string(L) + "|" + std::to_string(js.F) + "|" +
          std::to_string(js.min_blocks) + "|" + std::to_string(js.prefetch) + "|" +
          std::to_string(js.unroll) + "|" + std::to_string(js.arith) + "|" +
          std::to_string(js.classes) + "|" + std::to_string(js.gptr) + "|" +
-         std::to_string(js.pfw) + "|" + std::to_string(js.pfl2) + "|" + std::to_string(js.sring);
+         std::to_string(js.pfw) + "|" + std::to_string(js.pfl2) + "|" + std::to_string(js.sring) +
+         "|u" + std::to_string(js.uw);
   int dev = 0;
   cudaGetDevice(&dev);
   key += "|" + std::to_string(dev);
@@ -815,7 +853,7 @@ void k1_jit_launch(const void* handle, const uint8_t* d_text, const uint64_t* d_
   uint64_t blocks = (warps + kJitThreads / 32 - 1) / (kJitThreads / 32);
   blocks = std::min<uint64_t>(blocks, static_cast<uint64_t>(k->per_sm) * sm_count());
   ND_CUDA(cudaMemsetAsync(counter, 0, k->passes * sizeof(unsigned long long), s));  // one per pass
-  float c5 = 0.03125f;
+  float c5 = k->c5;
   unsigned int* pass_flag = gate ? gate->flag : nullptr;
   unsigned int epoch = gate ? gate->epoch : 0u;
   void* args[] = {&d_text, &d_offsets, &order, &item_doc, &item_off, &n_items, &seg_len, &d_sig,
@@ -825,26 +863,32 @@ void k1_jit_launch(const void* handle, const uint8_t* d_text, const uint64_t* d_
   ND_CHECK_LAUNCH();
 }
 
-std::string k1_jit_source(const nd_hash_fn* fns, uint32_t H, uint32_t L) {
-  return generate(fns, H, L, jit_shape());
+std::string k1_jit_source(const nd_hash_fn* fns, uint32_t H, uint32_t L, int uw) {
+  return generate(fns, H, L, unit_shape(jit_shape(), uw));
 }
 
 }  // namespace ndb
 
-extern "C" int64_t nd_k1j_source(const nd_hash_fn* fns, uint32_t H, uint32_t L, char* out,
-                                 uint64_t cap) {
-  if (!fns || H == 0 || H > 1024 || L == 0 || L > 16) return -1;
+extern "C" int64_t nd_k1j_source_units(const nd_hash_fn* fns, uint32_t H, uint32_t L,
+                                       uint32_t unit_bytes, char* out, uint64_t cap) {
+  if (!fns || H == 0 || H > 1024 || L == 0 || L > 16 || (unit_bytes != 1 && unit_bytes != 2))
+    return -1;
   for (uint32_t i = 0; i < H; ++i)  // the fq domain (derive_family's)
     if (fns[i].modulus < (1u << 21) || fns[i].modulus >= (1u << 23) || fns[i].base == 0 ||
         fns[i].base >= (1u << 16))
       return -1;
-  const std::string s = ndb::k1_jit_source(fns, H, L);
+  const std::string s = ndb::k1_jit_source(fns, H, L, static_cast<int>(unit_bytes));
   if (out && cap) {
     const uint64_t n = std::min<uint64_t>(cap - 1, s.size());
     std::memcpy(out, s.data(), n);
     out[n] = '\0';
   }
   return static_cast<int64_t>(s.size());
+}
+
+extern "C" int64_t nd_k1j_source(const nd_hash_fn* fns, uint32_t H, uint32_t L, char* out,
+                                 uint64_t cap) {
+  return nd_k1j_source_units(fns, H, L, 1, out, cap);
 }
 
 extern "C" int64_t nd_k1j_plan(const nd_hash_fn* fns, uint32_t H, uint32_t L, uint32_t* out,

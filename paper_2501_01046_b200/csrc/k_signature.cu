@@ -142,20 +142,30 @@ __global__ void k_fill_multi(const uint32_t* __restrict__ multi_docs, uint32_t n
 }
 
 // Codepoint documents whose units are all < 256 (ASCII / Latin-1 text) hash
-// exactly like bytes: wide[d] = 1 when document d has a unit >= 256; cnt[0]
-// counts them, cnt[1] the units of the batch (device-side totals)
+// exactly like bytes, and those whose units are all < 2^16 (the BMP) run K1j
+// over 16-bit units: wide[d] = 0 (< 256), 1 (< 2^16) or 2 (a supplementary
+// code point); cnt[0] counts classes >= 1, cnt[1] class 2
 __global__ void k_wide_docs(const uint32_t* __restrict__ units, const uint64_t* __restrict__ uoff,
                             uint64_t n, uint32_t* __restrict__ wide, uint32_t* __restrict__ cnt) {
   const uint64_t d = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (d >= n) return;
-  bool w = false;
-  for (uint64_t i = uoff[d] + lane; i < uoff[d + 1] && !w; i += 32) w = units[i] >= 256u;
-  w = __any_sync(0xFFFFFFFFu, w);
+  uint32_t mx = 0;
+  for (uint64_t i = uoff[d] + lane; i < uoff[d + 1] && mx < 0x10000u; i += 32) mx = max(mx, units[i]);
+  mx = __reduce_max_sync(0xFFFFFFFFu, mx);
   if (lane == 0) {
-    wide[d] = w ? 1u : 0u;
-    if (w) atomicAdd(cnt, 1u);
+    const uint32_t c = mx >= 0x10000u ? 2u : mx >= 256u ? 1u : 0u;
+    wide[d] = c;
+    if (c) atomicAdd(cnt, 1u);
+    if (c == 2) atomicAdd(cnt + 1, 1u);
   }
+}
+
+__global__ void k_units_to_u16(const uint32_t* __restrict__ units, uint64_t m,
+                               uint16_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<uint16_t>(units[i]);
 }
 
 __global__ void k_units_to_u8(const uint32_t* __restrict__ units, uint64_t m,
@@ -165,11 +175,11 @@ __global__ void k_units_to_u8(const uint32_t* __restrict__ units, uint64_t m,
     out[i] = static_cast<uint8_t>(units[i]);
 }
 
-// seg_count of the documents the wide pass skips -> 0 (no items)
-__global__ void k_keep_wide(const uint32_t* __restrict__ wide, uint64_t n,
-                            uint32_t* __restrict__ seg_count) {
+// seg_count of the documents outside [lo, hi] of their class -> 0 (no items)
+__global__ void k_keep_class(const uint32_t* __restrict__ cls, uint64_t n, uint32_t lo,
+                             uint32_t hi, uint32_t* __restrict__ seg_count) {
   const uint64_t d = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (d < n && !wide[d]) seg_count[d] = 0;
+  if (d < n && (cls[d] < lo || cls[d] > hi)) seg_count[d] = 0;
 }
 
 // K1j work order: items by descending window count (stable), so the 32
@@ -926,14 +936,17 @@ void k1_gate_wait(const unsigned int* flag, unsigned int epoch, cudaStream_t s) 
 void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint64_t* d_offsets,
                        uint64_t n, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
                        uint32_t* d_band, SigScratch& sc, cudaStream_t s, bool check_short,
-                       const uint64_t* h_offsets, const K1Gate* gate) {
+                       const uint64_t* h_offsets, const K1Gate* gate,
+                       const uint32_t* doc_class, uint32_t class_lo, uint32_t class_hi) {
   if (n == 0) return;
   if (fam.L == 0 || fam.L > static_cast<uint32_t>(kLMax))
     fail(ND_ERR_CONFIG, "shingle length must be in [1, 64] on the GPU path");
   if (n > 0xFFFFFFFFull) fail(ND_ERR_CONFIG, "batch exceeds 2^32 documents");
   unsigned tb = 256;
   const void* d_text = d_bytes;
-  const uint32_t* wide_mask = nullptr;  // codepoint: only the wide documents run K1w
+  // only the documents whose class lies in [class_lo, class_hi] (codepoint
+  // batches: the u16 pass and K1w each take their own documents)
+  const uint32_t* wide_mask = doc_class;
   if (fam.unit == 1) {
     // codepoint units: decode, then plan and sign over the u32 unit arrays;
     // unit counts are only known on the device, so the short check runs there
@@ -952,9 +965,8 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
     if (fam.narrow_ok && narrow_on) {
       // Documents whose code points are all < 256 hash exactly like bytes
       // (the fq arithmetic's domain: units < 256, 2^21 <= p < 2^23): narrow
-      // every unit to a byte and run the byte kernels (K1j / fq) over the
-      // whole batch; then K1w redoes only the documents with a wider unit
-      // (their rows from the byte pass are overwritten).
+      // every unit to a byte and run the byte kernels (K1j / fq) over those
+      // documents; those below 2^16 run K1j over 16-bit units, the rest K1w.
       uint32_t* wide = sc.wide.as<uint32_t>(n);
       uint32_t* cnt = sc.flags.as<uint32_t>(4);
       ND_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), s));
@@ -963,9 +975,15 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
       ND_CHECK_LAUNCH();
       uint32_t nwide = 0;
       uint64_t total = 0;
+      uint32_t nastral = 0;
       ND_CUDA(cudaMemcpyAsync(&nwide, cnt, 4, cudaMemcpyDeviceToHost, s));
+      ND_CUDA(cudaMemcpyAsync(&nastral, cnt + 1, 4, cudaMemcpyDeviceToHost, s));
       ND_CUDA(cudaMemcpyAsync(&total, uoff + n, 8, cudaMemcpyDeviceToHost, s));
       ND_CUDA(cudaStreamSynchronize(s));
+      // K1w below: the documents with a code point >= 2^16 when the u16 pass
+      // ran, else every document with one >= 256
+      class_lo = fam.jit16 ? 2u : 1u;
+      class_hi = 2u;
       if (nwide < n) {
         uint8_t* u8 = sc.units8.as<uint8_t>(total + 16);
         if (total)
@@ -974,25 +992,43 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
         DevFamily byte_view = fam;
         byte_view.unit = 0;
         byte_view.narrow_ok = false;
+        // only the documents of class 0 when others exist (their rows come
+        // from the u16 pass or K1w); every document is still checked for length
         launch_signatures(byte_view, u8, uoff, n, bands, rows, K, d_sig, d_band, sc, s,
-                          /*check_short=*/true, nullptr);
+                          /*check_short=*/true, nullptr, nullptr, nwide ? wide : nullptr, 0u, 0u);
         if (nwide == 0) return;
-        wide_mask = wide;  // K1w below: the wide documents only
       }
+      if (fam.jit16 && nwide > nastral) {
+        // K1j over 16-bit units for the documents of class 1 (code points
+        // < 2^16, some >= 256); their rows from the byte pass are overwritten
+        uint16_t* u16 = sc.units16.as<uint16_t>(total + 16);
+        if (total) {
+          k_units_to_u16<<<4 * sm_count(), 256, 0, s>>>(units, total, u16);
+          ND_CHECK_LAUNCH();
+        }
+        DevFamily v16 = fam;
+        v16.unit = 2;
+        v16.narrow_ok = false;
+        launch_signatures(v16, reinterpret_cast<const uint8_t*>(u16), uoff, n, bands, rows, K, d_sig,
+                          d_band, sc, s, /*check_short=*/true, nullptr, nullptr, wide, 1u, 1u);
+        if (nastral == 0) return;
+      }
+      wide_mask = wide;  // K1w below: the documents of classes [class_lo, 2]
     }
   }
   // K1j splits documents into items of seg_len windows; a small batch gets
   // shorter items so that the pass-major grid still fills the GPU (~1.5
   // items per resident lane; the register kernels keep kSeg)
   uint32_t seg_len = kSeg;
-  const bool jit_path = fam.jit && fam.unit == 0;
+  const void* jit_handle = fam.unit == 0 ? fam.jit : fam.unit == 2 ? fam.jit16 : nullptr;
+  const bool jit_path = jit_handle != nullptr;
   if (jit_path) {
     // target items: 1.5 per resident lane (ND_K1J_HALF_ITEMS=h: h/2 per lane; tuning)
     static const uint64_t half_items = [] {
       const char* v = getenv("ND_K1J_HALF_ITEMS");
       return static_cast<uint64_t>(v ? std::max(1, std::min(16, atoi(v))) : 3);
     }();
-    const uint64_t target = half_items * 32 / 2 * k1_jit_resident_warps(fam.jit);
+    const uint64_t target = half_items * 32 / 2 * k1_jit_resident_warps(jit_handle);
     if (n < target) {
       uint64_t bytes = 0;
       if (h_offsets) {
@@ -1042,7 +1078,8 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
       if (check_short && hflags[0]) fail(ND_ERR_SHORT, "a document has fewer units than the shingle length");
     }
     if (wide_mask) {
-      k_keep_wide<<<static_cast<unsigned>((n + tb - 1) / tb), tb, 0, s>>>(wide_mask, n, seg_count);
+      k_keep_class<<<static_cast<unsigned>((n + tb - 1) / tb), tb, 0, s>>>(wide_mask, n, class_lo,
+                                                                          class_hi, seg_count);
       ND_CHECK_LAUNCH();
     }
   }
@@ -1089,7 +1126,7 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   }();
   unsigned long long* counter =
       persistent ? sc.item_counter.as<unsigned long long>(1) : nullptr;
-  if (fam.jit && fam.unit == 0) {
+  if (jit_path) {
     // K1j: items sorted by length, then the family-specialised kernel
     uint32_t* keys = sc.order_keys.as<uint32_t>(items);
     uint32_t* order = sc.order_vals.as<uint32_t>(items);
@@ -1097,9 +1134,9 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
         d_offsets, item_doc, item_off, items, fam.L, seg_len, keys, order);
     ND_CHECK_LAUNCH();
     radix_sort_u32(keys, order, items, 14, sc.sort, s);
-    k1_jit_launch(fam.jit, static_cast<const uint8_t*>(d_text), d_offsets, order, item_doc,
+    k1_jit_launch(jit_handle, static_cast<const uint8_t*>(d_text), d_offsets, order, item_doc,
                   item_off, static_cast<uint32_t>(items), seg_len, d_sig,
-                  sc.item_counter.as<unsigned long long>(k1_jit_passes(fam.jit)), s, gate);
+                  sc.item_counter.as<unsigned long long>(k1_jit_passes(jit_handle)), s, gate);
     // band keys of every document from its finished row (keys is free again)
     if (d_band) launch_band_keys(d_sig, n, fam.H, bands, rows, K, d_band, keys, s);
     return;

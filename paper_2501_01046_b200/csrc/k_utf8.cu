@@ -78,6 +78,139 @@ __device__ __forceinline__ bool starts_unit(const uint8_t* __restrict__ s, uint6
 
 constexpr int kWarps = 8;
 
+// Word-parallel walk (round 2): a warp reads its document as aligned 4-byte
+// words, 128 bytes per step (one LDG.32 per lane); every byte decides
+// "starts a unit?" and its value from the 3 bytes on either side, which come
+// from the neighbouring lanes' words (shuffles; lane 31 also reads the word
+// after the step, lane 0 gets the previous step's last word).  Bytes outside
+// the document read as 0 -- a non-trail byte, which ends a sequence exactly
+// where unit_at's length checks would (and no position outside is decoded).
+struct Ctx12 {
+  uint32_t prev, cur, next;  // bytes at offsets -4..-1, 0..3, 4..7 of the lane's word
+  __device__ __forceinline__ uint32_t at(int o) const {  // o in [-4, 7], unrolled
+    return o < 0 ? (prev >> (8 * (o + 4))) & 0xFFu
+         : o < 4 ? (cur >> (8 * o)) & 0xFFu
+                 : (next >> (8 * (o - 4))) & 0xFFu;
+  }
+};
+
+// byte K of the word as a lead: unit length (unit_at's; 0 for a trail byte)
+// and value (the scalar, or U+FFFD when ill-formed)
+template <int K>
+__device__ __forceinline__ uint32_t lead_at(const Ctx12& c, uint32_t& cp) {
+  const uint32_t b0 = c.at(K);
+  cp = b0;
+  if (b0 < 0x80u) return 1;
+  if (is_trail(b0)) {
+    cp = 0xFFFDu;  // only decoded when no lead covers it: a unit of its own
+    return 0;
+  }
+  int need;
+  uint32_t v, lo = 0x80u, hi = 0xBFu;
+  if (b0 >= 0xC2u && b0 <= 0xDFu) {
+    need = 1;
+    v = b0 & 0x1Fu;
+  } else if (b0 >= 0xE0u && b0 <= 0xEFu) {
+    need = 2;
+    v = b0 & 0x0Fu;
+    if (b0 == 0xE0u) lo = 0xA0u;
+    if (b0 == 0xEDu) hi = 0x9Fu;
+  } else if (b0 >= 0xF0u && b0 <= 0xF4u) {
+    need = 3;
+    v = b0 & 0x07u;
+    if (b0 == 0xF0u) lo = 0x90u;
+    if (b0 == 0xF4u) hi = 0x8Fu;
+  } else {
+    cp = 0xFFFDu;  // invalid lead (C0, C1, F5..FF)
+    return 1;
+  }
+  int k = 0;
+  const uint32_t b1 = c.at(K + 1);
+  if (b1 >= lo && b1 <= hi) {
+    v = (v << 6) | (b1 & 0x3Fu);
+    k = 1;
+    if (need >= 2) {
+      const uint32_t b2 = c.at(K + 2);
+      if (is_trail(b2)) {
+        v = (v << 6) | (b2 & 0x3Fu);
+        k = 2;
+        if (need == 3) {
+          const uint32_t b3 = c.at(K + 3);
+          if (is_trail(b3)) {
+            v = (v << 6) | (b3 & 0x3Fu);
+            k = 3;
+          }
+        }
+      }
+    }
+  }
+  cp = k == need ? v : 0xFFFDu;
+  return 1 + k;
+}
+
+// the lane's word: bytes at document positions pos .. pos+3, 0 outside [0, len)
+__device__ __forceinline__ uint32_t masked_word(const uint32_t* w, int64_t pos, int64_t len) {
+  if (pos + 3 < 0 || pos >= len) return 0u;
+  uint32_t v = __ldg(w);
+  if (pos < 0) v &= 0xFFFFFFFFu << (8 * static_cast<int>(-pos));
+  if (pos + 4 > len) v &= 0xFFFFFFFFu >> (8 * static_cast<int>(pos + 4 - len));
+  return v;
+}
+
+// one step of the walk: the 4 bytes of this lane -> start mask + values.
+// A byte starts a unit unless it is a trail byte covered by the nearest
+// non-trail byte j within 3 before it (len(j) > distance): non-trail bytes
+// end every sequence, so no other lead can cover it.  Unit lengths of the 3
+// bytes before the word come from the lane below (lane 0: the previous step).
+__device__ __forceinline__ uint32_t step_units(const uint32_t* aw, int64_t pos0, int64_t len,
+                                               int lane, uint32_t& carry, uint32_t& lcarry,
+                                               uint32_t (&cp)[4]) {
+  const int64_t pos = pos0 + 4 * lane;
+  const uint32_t w = masked_word(aw + lane, pos, len);
+  Ctx12 c;
+  c.cur = w;
+  c.prev = __shfl_up_sync(0xFFFFFFFFu, w, 1);
+  if (lane == 0) c.prev = carry;
+  c.next = __shfl_down_sync(0xFFFFFFFFu, w, 1);
+  if (lane == 31) c.next = masked_word(aw + 32, pos + 4, len);
+  carry = __shfl_sync(0xFFFFFFFFu, w, 31);
+  uint32_t valid = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) valid |= (pos + k >= 0 && pos + k < len) ? (1u << k) : 0u;
+  uint32_t l4;  // unit lengths of the 4 bytes, 3 bits each
+  if (((c.prev | c.cur | c.next) & 0x80808080u) == 0u) {  // ASCII context
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cp[k] = (w >> (8 * k)) & 0xFFu;
+    l4 = 01111u;
+  } else {
+    const uint32_t n0 = lead_at<0>(c, cp[0]), n1 = lead_at<1>(c, cp[1]);
+    const uint32_t n2 = lead_at<2>(c, cp[2]), n3 = lead_at<3>(c, cp[3]);
+    l4 = n0 | (n1 << 3) | (n2 << 6) | (n3 << 9);
+  }
+  uint32_t lp = __shfl_up_sync(0xFFFFFFFFu, l4, 1);
+  if (lane == 0) lp = lcarry;
+  lcarry = __shfl_sync(0xFFFFFFFFu, l4, 31);
+  if (l4 == 01111u) return valid;  // every byte leads a unit
+  // lens of positions -4..3 (a trail byte has length 0)
+  const uint32_t l8 = lp | (l4 << 12);
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t lk = (l8 >> (3 * (k + 4))) & 7u;
+    bool st = lk != 0;
+    if (!st) {
+      st = true;  // three trail bytes before it (or the document start): its own unit
+#pragma unroll
+      for (int d = 3; d >= 1; --d) {  // the nearest non-trail byte wins
+        const uint32_t lj = (l8 >> (3 * (k + 4 - d))) & 7u;
+        if (lj != 0) st = lj <= static_cast<uint32_t>(d);
+      }
+    }
+    m |= st ? (1u << k) : 0u;
+  }
+  return m & valid;
+}
+
 // pass 1: units per document (one warp per document)
 __global__ void __launch_bounds__(kWarps * 32)
     k_utf8_count(const uint8_t* __restrict__ text, const uint64_t* __restrict__ offsets,
@@ -86,9 +219,13 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int lane = threadIdx.x & 31;
   if (d >= n) return;
   const uint8_t* s = text + offsets[d];
-  const uint64_t len = offsets[d + 1] - offsets[d];
-  uint32_t count = 0;
-  for (uint64_t i = lane; i < len; i += 32) count += starts_unit(s, len, i);
+  const int64_t len = static_cast<int64_t>(offsets[d + 1] - offsets[d]);
+  const uint32_t* aw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s) & ~uintptr_t{3});
+  int64_t pos0 = -static_cast<int64_t>(reinterpret_cast<uintptr_t>(s) & 3);
+  uint32_t count = 0, carry = 0, lcarry = 01111u << 0;
+  uint32_t cp[4];
+  for (; pos0 < len; pos0 += 128, aw += 32)
+    count += __popc(step_units(aw, pos0, len, lane, carry, lcarry, cp));
 #pragma unroll
   for (int o = 16; o; o >>= 1) count += __shfl_xor_sync(0xFFFFFFFFu, count, o);
   if (lane == 0) units[d] = count;
@@ -102,21 +239,26 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int lane = threadIdx.x & 31;
   if (d >= n) return;
   const uint8_t* s = text + offsets[d];
-  const uint64_t len = offsets[d + 1] - offsets[d];
+  const int64_t len = static_cast<int64_t>(offsets[d + 1] - offsets[d]);
+  const uint32_t* aw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s) & ~uintptr_t{3});
+  int64_t pos0 = -static_cast<int64_t>(reinterpret_cast<uintptr_t>(s) & 3);
   uint32_t* o = out + unit_off[d];
   const unsigned below = (1u << lane) - 1u;
   uint64_t written = 0;
-  for (uint64_t b = 0; b < len; b += 32) {
-    const uint64_t i = b + lane;
-    bool st = false;
-    uint32_t cp = 0;
-    if (i < len) {
-      st = starts_unit(s, len, i);
-      if (st) unit_at(s, len, i, cp);
-    }
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, st);
-    if (st) o[written + __popc(m & below)] = cp;
-    written += __popc(m);
+  uint32_t carry = 0, lcarry = 01111u;
+  for (; pos0 < len; pos0 += 128, aw += 32) {
+    uint32_t cp[4];
+    const uint32_t m = step_units(aw, pos0, len, lane, carry, lcarry, cp);
+    const uint32_t cnt = __popc(m);  // 0..4: the lane's rank from three bit ballots
+    const unsigned b0 = __ballot_sync(0xFFFFFFFFu, cnt & 1u);
+    const unsigned b1 = __ballot_sync(0xFFFFFFFFu, cnt & 2u);
+    const unsigned b2 = __ballot_sync(0xFFFFFFFFu, cnt & 4u);
+    uint32_t at = __popc(b0 & below) + 2 * __popc(b1 & below) + 4 * __popc(b2 & below);
+    uint32_t* dst = o + written;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (m & (1u << k)) dst[at++] = cp[k];
+    written += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
   }
 }
 

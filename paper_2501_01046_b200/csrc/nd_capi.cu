@@ -552,10 +552,15 @@ void family_upload_one(nd_ctx* ctx, const nd_hash_fn* fns, uint32_t H, uint32_t 
     // K1j: compile (or find) the kernel specialised for this family; when
     // NVRTC is unavailable the register-constant K1 runs (same bits)
     ctx->fam.jit = nullptr;
+    ctx->fam.jit16 = nullptr;
     ctx->k1_note.clear();
     if (k1_jit_eligible(ctx->fam)) {
       try {
         ctx->fam.jit = k1_jit_prepare(fns, H, L);
+        // codepoint families: K1j over 16-bit units for documents whose code
+        // points are all < 2^16 (ND_K1J_U16=0: those run K1w)
+        const char* u16 = getenv("ND_K1J_U16");
+        if (unit == 1 && !(u16 && u16[0] == '0')) ctx->fam.jit16 = k1_jit_prepare(fns, H, L, 2);
       } catch (const NdError& e) {
         ctx->k1_note = e.what();
       }
@@ -576,7 +581,8 @@ const char* nd_k1_kernel(nd_ctx* ctx) {
   if (is_group(ctx)) ctx = ctx->shards[0];
   if (!ctx || !ctx->fam.q) return "";
   if (ctx->fam.exact) out = "k1x";
-  else if (ctx->fam.unit == 1) out = ctx->fam.jit ? "k1j+k1w" : ctx->fam.narrow_ok ? "k1+k1w" : "k1w";
+  else if (ctx->fam.unit == 1)
+    out = ctx->fam.jit16 ? "k1j+k1j16+k1w" : ctx->fam.jit ? "k1j+k1w" : ctx->fam.narrow_ok ? "k1+k1w" : "k1w";
   else out = ctx->fam.jit ? "k1j" : "k1";
   if (!ctx->k1_note.empty()) out += ": " + ctx->k1_note;
   return out.c_str();

@@ -49,8 +49,12 @@ struct DevFamily {
   uint32_t H = 0;            // real hash count
   uint32_t Hp = 0;           // padded hash count
   uint32_t L = 0;
-  uint32_t unit = 0;         // 0 = byte, 1 = codepoint (ShingleUnit, text.hpp:23-26)
+  uint32_t unit = 0;         // 0 = byte, 1 = codepoint (ShingleUnit, text.hpp:23-26);
+                             // 2 = internal view of code points < 2^16 as u16 units
   void* jit = nullptr;        // K1j kernel specialised for this family (k1_jit.cpp), or null
+  // codepoint family: K1j over 16-bit units (documents whose code points are
+  // all < 2^16 and some >= 256), or null
+  void* jit16 = nullptr;
   // codepoint family whose functions all lie in the byte fq domain: documents
   // whose code points are all < 256 run the byte kernels over narrowed units
   bool narrow_ok = false;
@@ -119,22 +123,23 @@ struct SortScratch {
 };
 struct SigScratch {
   DevBuf seg_count, item_off, item_doc, flags, multi_docs, scan_tmp, units, unit_off, unit_cnt,
-      item_counter, order_keys, order_vals, units8, wide;
+      item_counter, order_keys, order_vals, units8, units16, wide;
   SortScratch sort;  // K1j: items ordered by length
   void release() {
     for (DevBuf* b : {&seg_count, &item_off, &item_doc, &flags, &multi_docs, &scan_tmp, &units,
                       &unit_off, &unit_cnt, &item_counter, &order_keys, &order_vals, &units8,
-                      &wide})
+                      &units16, &wide})
       b->release();
     sort.release();
   }
 };
 // K1j: family-specialised signature kernel (k1_jit.cpp)
 bool k1_jit_eligible(const DevFamily& fam);
-void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L);
+// uw: bytes per text unit (1, or 2 for code points < 2^16)
+void* k1_jit_prepare(const nd_hash_fn* fns, uint32_t H, uint32_t L, int uw = 1);
 double k1_jit_compile_seconds(const void* handle);
 uint32_t k1_jit_passes(const void* handle);
-std::string k1_jit_source(const nd_hash_fn* fns, uint32_t H, uint32_t L);
+std::string k1_jit_source(const nd_hash_fn* fns, uint32_t H, uint32_t L, int uw = 1);
 uint64_t k1_jit_resident_warps(const void* handle);
 // Chunk gate: a K1j launch raises *flag to its epoch when its first warp
 // enters the last pass; k1_gate_wait holds a stream until then, so the next
@@ -161,7 +166,8 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
                        uint64_t n, uint32_t bands, uint32_t rows, uint32_t K, uint32_t* d_sig,
                        uint32_t* d_band, SigScratch& scratch, cudaStream_t stream,
                        bool check_short, const uint64_t* h_offsets,
-                       const K1Gate* gate = nullptr);
+                       const K1Gate* gate = nullptr, const uint32_t* doc_class = nullptr,
+                       uint32_t class_lo = 0, uint32_t class_hi = 0);
 
 // Stable LSD radix sort of (key, value) pairs by the low key_bits bits.
 void radix_sort_u32(uint32_t* keys, uint32_t* vals, uint64_t n, int key_bits, SortScratch& sc,

@@ -124,11 +124,17 @@ def test_k1j_skewed_lengths_many_items(ctx, oracle, monkeypatch):
 
 
 def test_k1j_not_used_outside_its_domain(ctx, monkeypatch):
-    # codepoint units: K1j for the documents below U+0100, K1w for the rest;
-    # L > 16: the register-constant kernel
+    # codepoint units: K1j for the documents below U+0100, K1j over 16-bit
+    # units for those below U+10000, K1w for the rest; L > 16: the
+    # register-constant kernel
     fam = minhash.derive_family(5, 32, 5, minhash.ShingleUnit.CODEPOINT)
     ctx.upload_family(fam)
+    assert _kernel(ctx) == "k1j+k1j16+k1w"
+    ctx._family_key = None
+    monkeypatch.setenv("ND_K1J_U16", "0")
+    ctx.upload_family(fam)
     assert _kernel(ctx) == "k1j+k1w"
+    monkeypatch.delenv("ND_K1J_U16")
     ctx._family_key = None
     fam = minhash.derive_family(5, 32, 20)  # L > 16
     ctx.upload_family(fam)
@@ -256,3 +262,53 @@ def test_k1j_shapes_and_dn_misfits(ctx, oracle, monkeypatch, seed, H, L, shape):
         monkeypatch.delenv(k)
     ctx._family_key = None
     assert np.array_equal(sig, oracle.signatures(data, offs, oracle.derive_family(seed, H, L), L=L))
+
+
+_ASCII = list("abcdefghijklmnop qrstuvwxyz")
+_LATIN = [chr(c) for c in range(0xA0, 0x100)]
+_BMP = ([chr(c) for c in range(0x400, 0x450)] + [chr(c) for c in range(0x4E00, 0x4E40)] +
+        [chr(c) for c in range(0xAC00, 0xAC20)] + [chr(0xFFFD), chr(0xFFEE), chr(0x100)])
+_ASTRAL = [chr(c) for c in range(0x1F600, 0x1F610)] + [chr(0x10FFFD), chr(0x10000)]
+
+
+def _cp_corpus(rng, n, L, kinds):
+    texts = []
+    for i in range(n):
+        k = int(rng.integers(L, 3000)) if i % 40 else 20000  # some multi-item documents
+        if i % 97 == 5:
+            k = L + i % 3  # documents of exactly L .. L+2 code points
+        kind = kinds[i % len(kinds)]
+        pool = {"ascii": _ASCII, "latin": _LATIN + _ASCII[:5], "bmp": _BMP + _ASCII[:8],
+                "cjk": _BMP[80:144], "astral": _BMP + _ASTRAL}[kind]
+        texts.append("".join(rng.choice(pool, size=k)))
+    raw = [t.encode() for t in texts]
+    offs = np.zeros(len(raw) + 1, np.uint64)
+    offs[1:] = np.cumsum([len(b) for b in raw])
+    return np.frombuffer(b"".join(raw), np.uint8).copy(), offs
+
+
+@pytest.mark.parametrize("L,H,kinds", [
+    (5, 128, ("bmp",)), (5, 128, ("cjk", "ascii", "bmp", "astral", "latin")),
+    (1, 40, ("bmp", "astral")), (2, 64, ("cjk",)), (9, 128, ("bmp", "ascii")),
+    (16, 100, ("cjk", "astral")),
+])
+def test_codepoint_bmp_documents_take_k1j16(ctx, oracle, monkeypatch, L, H, kinds):
+    """documents whose code points are all < 2^16 (Cyrillic, CJK, Hangul,
+    U+FFFD ...) run K1j over 16-bit units (fq arithmetic, c5 = 2^-3): every
+    row equals the oracle and the K1w-only path, next to ASCII / Latin-1
+    documents (byte K1j) and documents with supplementary code points (K1w)"""
+    rng = np.random.default_rng(1000 * L + H)
+    data, offs = _cp_corpus(rng, 240, L, kinds)
+    fam = minhash.derive_family(7, H, L, minhash.ShingleUnit.CODEPOINT)
+    bands = next(b for b in (16, 10, 8, 5, 4, 2, 1) if H % b == 0)
+    res = {}
+    for u16 in ("1", "0"):
+        monkeypatch.setenv("ND_K1J_U16", u16)
+        ctx._family_key = None
+        res[u16] = minhash.signatures_packed(data, offs, fam, bands, H // bands, 997, ctx=ctx)
+        assert _kernel(ctx) == ("k1j+k1j16+k1w" if u16 == "1" else "k1j+k1w")
+    monkeypatch.delenv("ND_K1J_U16")
+    ctx._family_key = None
+    want = oracle.signatures(data, offs, oracle.derive_family(7, H, L), L=L, unit=1)
+    assert np.array_equal(res["1"][0], want)
+    assert np.array_equal(res["1"][0], res["0"][0]) and np.array_equal(res["1"][1], res["0"][1])

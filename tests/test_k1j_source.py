@@ -101,3 +101,29 @@ def test_k1j_source_compiles_for_sm100a_without_loop_spills(tmp_path, arith):
         assert all(sum(x.startswith("I2FP") for x in b) <= 4 for b in words)
         per_hwe = min(len(b) for b in words) / hwe
         assert per_hwe < 7.9, per_hwe  # fq: 572 / 64 = 8.94
+
+
+@pytest.mark.skipif(shutil.which("nvcc") is None and not os.path.exists("/usr/local/cuda/bin/nvcc"),
+                    reason="nvcc not installed")
+@pytest.mark.parametrize("L", [1, 5, 16])
+def test_k1j_u16_source_compiles_without_spills(tmp_path, L):
+    """K1j over 16-bit units (codepoint documents below U+10000): the fq
+    arithmetic with c5 = 2^-3 passed at launch, two windows per word, <= 80
+    registers and no local memory"""
+    lib = _lib.load()
+    fam = minhash.derive_family(5, 128, L, minhash.ShingleUnit.CODEPOINT)
+    n = lib.nd_k1j_source_units(fam.functions, 128, L, 2, None, 0)
+    assert n > 0 and lib.nd_k1j_source_units(fam.functions, 128, L, 3, None, 0) == -1
+    buf = C.create_string_buffer(n + 1)
+    lib.nd_k1j_source_units(fam.functions, 128, L, 2, buf, n + 1)
+    src_text = buf.value.decode()
+    assert "#define UW 2" in src_text and "rold(" not in src_text.split("extern")[1]
+    src = tmp_path / "k1j16.cu"
+    src.write_text(src_text)
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    r = subprocess.run([nvcc, "-cubin", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                        "-Xptxas", "-v", str(src), "-o", str(tmp_path / "k.cubin")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert int(re.search(r"Used (\d+) registers", r.stderr).group(1)) <= 80
+    assert "0 bytes spill stores" in r.stderr
