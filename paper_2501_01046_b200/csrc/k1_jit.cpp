@@ -807,6 +807,9 @@ JitShape unit_shape(JitShape js, int uw) {
     js.unroll = 1;
     js.sring = 0;
     js.pfw = 0;
+    if (const char* v = getenv("ND_K1J16_F")) js.F = std::max(4, std::min(64, atoi(v)));  // tuning
+    if (const char* v = getenv("ND_K1J16_MINB")) js.min_blocks = std::max(1, std::min(16, atoi(v)));
+    if (const char* v = getenv("ND_K1J16_PREFETCH")) js.prefetch = std::max(1, std::min(2, atoi(v)));
   }
   return js;
 }

@@ -48,8 +48,16 @@ hwe = float((lens - 4).sum() * H)
 d_sig = torch.empty((n, H), dtype=torch.int32, device="cuda")
 d_band = torch.empty((n, 16), dtype=torch.int32, device="cuda")
 out = {}
-for variant in ("1", "0", "1", "0"):
-    os.environ["ND_K1J_U16"] = variant
+# PROBE_SHAPES="name:VAR=v,VAR=v name2:..." (K1j-u16 tuning) instead of u16 on/off
+shapes = [("u16", {"ND_K1J_U16": "1"}), ("k1w", {"ND_K1J_U16": "0"})]
+if os.environ.get("PROBE_SHAPES"):
+    shapes = [(sp.partition(":")[0], dict(x.split("=", 1) for x in sp.partition(":")[2].split(",") if x))
+              for sp in os.environ["PROBE_SHAPES"].split()]
+knobs = {k for _, e in shapes for k in e}
+for variant, env in shapes * 2:
+    for k in knobs:
+        os.environ.pop(k, None)
+    os.environ.update(env)
     ctx = Context(0)
     s = torch.cuda.Stream()
     torch.cuda.set_stream(s)
@@ -68,7 +76,7 @@ for variant in ("1", "0", "1", "0"):
     chk = int(np.frombuffer(d_sig.cpu().numpy().tobytes(), np.uint64).sum() % (1 << 61))
     kern = ctx.lib.nd_k1_kernel(ctx.h).decode()
     out.setdefault(variant, []).append(ms)
-    print(json.dumps({"u16": variant, "kernel": kern, "ms": round(ms, 3), "docs_per_s": n / ms * 1e3,
+    print(json.dumps({"variant": variant, "kernel": kern, "ms": round(ms, 3), "docs_per_s": n / ms * 1e3,
                       "T_hwe_s": hwe / ms / 1e9, "text_GB": len(buf) / 1e9, "checksum": chk}),
           flush=True)
     ctx.close()
