@@ -801,9 +801,13 @@ JitShape unit_shape(JitShape js, int uw) {
   if (uw == 2) {
     js.uw = 2;
     js.arith = 0;
-    js.F = 16;
-    js.min_blocks = 6;
-    js.prefetch = 1;
+    // 32 functions per pass, 4 CTAs, the word after next prefetched: two
+    // windows per word leave more per-word overhead to amortise (BMP text,
+    // 500k docs, whole call: F=16/6 CTAs 23.02 ms, F=20/5 22.68, F=24/5
+    // 22.77, F=32/4 22.65, F=32/4 + prefetch 2 22.34; profiles/r2_codepoint.txt)
+    js.F = 32;
+    js.min_blocks = 4;
+    js.prefetch = 2;
     js.unroll = 1;
     js.sring = 0;
     js.pfw = 0;

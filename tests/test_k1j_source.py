@@ -108,8 +108,8 @@ def test_k1j_source_compiles_for_sm100a_without_loop_spills(tmp_path, arith):
 @pytest.mark.parametrize("L", [1, 5, 16])
 def test_k1j_u16_source_compiles_without_spills(tmp_path, L):
     """K1j over 16-bit units (codepoint documents below U+10000): the fq
-    arithmetic with c5 = 2^-3 passed at launch, two windows per word, <= 80
-    registers and no local memory"""
+    arithmetic with c5 = 2^-3 passed at launch, two windows per word, 32
+    functions per pass within 4 CTAs' registers (<= 128) and no local memory"""
     lib = _lib.load()
     fam = minhash.derive_family(5, 128, L, minhash.ShingleUnit.CODEPOINT)
     n = lib.nd_k1j_source_units(fam.functions, 128, L, 2, None, 0)
@@ -125,5 +125,5 @@ def test_k1j_u16_source_compiles_without_spills(tmp_path, L):
                         "-Xptxas", "-v", str(src), "-o", str(tmp_path / "k.cubin")],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:]
-    assert int(re.search(r"Used (\d+) registers", r.stderr).group(1)) <= 80
+    assert int(re.search(r"Used (\d+) registers", r.stderr).group(1)) <= 128
     assert "0 bytes spill stores" in r.stderr
