@@ -141,35 +141,10 @@ __global__ void k_fill_multi(const uint32_t* __restrict__ multi_docs, uint32_t n
   }
 }
 
-// Codepoint documents whose units are all < 256 (ASCII / Latin-1 text) hash
-// exactly like bytes, and those whose units are all < 2^16 (the BMP) run K1j
-// over 16-bit units: wide[d] = 0 (< 256), 1 (< 2^16) or 2 (a supplementary
-// code point); cnt[0] counts classes >= 1, cnt[1] class 2
-__global__ void k_wide_docs(const uint32_t* __restrict__ units, const uint64_t* __restrict__ uoff,
-                            uint64_t n, uint32_t* __restrict__ wide, uint32_t* __restrict__ cnt) {
-  const uint64_t d = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / 32;
-  const int lane = threadIdx.x & 31;
-  if (d >= n) return;
-  uint32_t mx = 0;
-  for (uint64_t i = uoff[d] + lane; i < uoff[d + 1] && mx < 0x10000u; i += 32) mx = max(mx, units[i]);
-  mx = __reduce_max_sync(0xFFFFFFFFu, mx);
-  if (lane == 0) {
-    const uint32_t c = mx >= 0x10000u ? 2u : mx >= 256u ? 1u : 0u;
-    wide[d] = c;
-    if (c) atomicAdd(cnt, 1u);
-    if (c == 2) atomicAdd(cnt + 1, 1u);
-  }
-}
-
-__global__ void k_units_to_u16(const uint32_t* __restrict__ units, uint64_t m,
-                               uint16_t* __restrict__ out) {
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    out[i] = static_cast<uint16_t>(units[i]);
-}
-
-__global__ void k_units_to_u8(const uint32_t* __restrict__ units, uint64_t m,
-                              uint8_t* __restrict__ out) {
+// class-0 codepoint documents (all units < 256) run the byte kernels over
+// their units narrowed to bytes
+__global__ void k_u16_to_u8(const uint16_t* __restrict__ units, uint64_t m,
+                            uint8_t* __restrict__ out) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     out[i] = static_cast<uint8_t>(units[i]);
@@ -950,45 +925,40 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   if (fam.unit == 1) {
     // codepoint units: decode, then plan and sign over the u32 unit arrays;
     // unit counts are only known on the device, so the short check runs there
+    const char* nv = getenv("ND_K1_NARROW");  // 0: every codepoint document through K1w
+    const bool narrow = fam.narrow_ok && !(nv && nv[0] == '0');
+    // Documents whose code points are all < 256 hash exactly like bytes (the
+    // fq arithmetic's domain: units < 256, 2^21 <= p < 2^23) and run the byte
+    // kernels; those below 2^16 run K1j over 16-bit units; the rest K1w.  The
+    // decode classifies every document (count pass) and writes 16-bit units
+    // for the narrow classes, u32 units only for the documents K1w takes.
+    CodepointClasses cc;
+    cc.cls_buf = &sc.wide;
+    cc.cnt_buf = &sc.cls_cnt;
+    cc.u16_buf = &sc.units16;
+    cc.wide_from = fam.jit16 ? 2u : 1u;
     const uint32_t* units = nullptr;
     const uint64_t* uoff = nullptr;
     decode_codepoints_device(d_bytes, d_offsets, n, sc.units, sc.unit_off, sc.unit_cnt,
-                             sc.scan_tmp, s, &units, &uoff);
+                             sc.scan_tmp, s, &units, &uoff, narrow ? &cc : nullptr);
     d_text = units;
     d_offsets = uoff;
     h_offsets = nullptr;
     check_short = true;
-    static const bool narrow_on = [] {
-      const char* v = getenv("ND_K1_NARROW");  // 0: every codepoint document through K1w
-      return !(v && v[0] == '0');
-    }();
-    if (fam.narrow_ok && narrow_on) {
-      // Documents whose code points are all < 256 hash exactly like bytes
-      // (the fq arithmetic's domain: units < 256, 2^21 <= p < 2^23): narrow
-      // every unit to a byte and run the byte kernels (K1j / fq) over those
-      // documents; those below 2^16 run K1j over 16-bit units, the rest K1w.
-      uint32_t* wide = sc.wide.as<uint32_t>(n);
-      uint32_t* cnt = sc.flags.as<uint32_t>(4);
-      ND_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), s));
-      k_wide_docs<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, s>>>(units, uoff, n, wide,
-                                                                              cnt);
-      ND_CHECK_LAUNCH();
-      uint32_t nwide = 0;
-      uint64_t total = 0;
-      uint32_t nastral = 0;
-      ND_CUDA(cudaMemcpyAsync(&nwide, cnt, 4, cudaMemcpyDeviceToHost, s));
-      ND_CUDA(cudaMemcpyAsync(&nastral, cnt + 1, 4, cudaMemcpyDeviceToHost, s));
-      ND_CUDA(cudaMemcpyAsync(&total, uoff + n, 8, cudaMemcpyDeviceToHost, s));
-      ND_CUDA(cudaStreamSynchronize(s));
+    if (narrow) {
+      const uint32_t* wide = cc.cls;
+      const uint32_t nwide = cc.n_wide, nastral = cc.n_astral;
+      const uint64_t total = cc.total;
       // K1w below: the documents with a code point >= 2^16 when the u16 pass
-      // ran, else every document with one >= 256
-      class_lo = fam.jit16 ? 2u : 1u;
+      // runs, else every document with one >= 256
+      class_lo = cc.wide_from;
       class_hi = 2u;
       if (nwide < n) {
         uint8_t* u8 = sc.units8.as<uint8_t>(total + 16);
-        if (total)
-          k_units_to_u8<<<4 * sm_count(), 256, 0, s>>>(units, total, u8);
-        ND_CHECK_LAUNCH();
+        if (total) {
+          k_u16_to_u8<<<4 * sm_count(), 256, 0, s>>>(cc.u16, total, u8);
+          ND_CHECK_LAUNCH();
+        }
         DevFamily byte_view = fam;
         byte_view.unit = 0;
         byte_view.narrow_ok = false;
@@ -1000,17 +970,12 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
       }
       if (fam.jit16 && nwide > nastral) {
         // K1j over 16-bit units for the documents of class 1 (code points
-        // < 2^16, some >= 256); their rows from the byte pass are overwritten
-        uint16_t* u16 = sc.units16.as<uint16_t>(total + 16);
-        if (total) {
-          k_units_to_u16<<<4 * sm_count(), 256, 0, s>>>(units, total, u16);
-          ND_CHECK_LAUNCH();
-        }
+        // < 2^16, some >= 256)
         DevFamily v16 = fam;
         v16.unit = 2;
         v16.narrow_ok = false;
-        launch_signatures(v16, reinterpret_cast<const uint8_t*>(u16), uoff, n, bands, rows, K, d_sig,
-                          d_band, sc, s, /*check_short=*/true, nullptr, nullptr, wide, 1u, 1u);
+        launch_signatures(v16, reinterpret_cast<const uint8_t*>(cc.u16), uoff, n, bands, rows, K,
+                          d_sig, d_band, sc, s, /*check_short=*/true, nullptr, nullptr, wide, 1u, 1u);
         if (nastral == 0) return;
       }
       wide_mask = wide;  // K1w below: the documents of classes [class_lo, 2]

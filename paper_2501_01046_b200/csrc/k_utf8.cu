@@ -211,10 +211,14 @@ __device__ __forceinline__ uint32_t step_units(const uint32_t* aw, int64_t pos0,
   return m & valid;
 }
 
-// pass 1: units per document (one warp per document)
+// pass 1: units per document (one warp per document); CLS: also the
+// document's class by its largest code point (0: < 256, 1: < 2^16, 2: above),
+// cls_cnt[0] counting classes >= 1 and cls_cnt[1] class 2
+template <bool CLS>
 __global__ void __launch_bounds__(kWarps * 32)
     k_utf8_count(const uint8_t* __restrict__ text, const uint64_t* __restrict__ offsets,
-                 uint64_t n, uint32_t* __restrict__ units) {
+                 uint64_t n, uint32_t* __restrict__ units, uint32_t* __restrict__ cls,
+                 uint32_t* __restrict__ cls_cnt) {
   const uint64_t d = static_cast<uint64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (d >= n) return;
@@ -222,19 +226,39 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int64_t len = static_cast<int64_t>(offsets[d + 1] - offsets[d]);
   const uint32_t* aw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s) & ~uintptr_t{3});
   int64_t pos0 = -static_cast<int64_t>(reinterpret_cast<uintptr_t>(s) & 3);
-  uint32_t count = 0, carry = 0, lcarry = 01111u << 0;
+  uint32_t count = 0, carry = 0, lcarry = 01111u, mx = 0;
   uint32_t cp[4];
-  for (; pos0 < len; pos0 += 128, aw += 32)
-    count += __popc(step_units(aw, pos0, len, lane, carry, lcarry, cp));
+  for (; pos0 < len; pos0 += 128, aw += 32) {
+    const uint32_t m = step_units(aw, pos0, len, lane, carry, lcarry, cp);
+    count += __popc(m);
+    if (CLS) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (m & (1u << k)) mx = max(mx, cp[k]);
+    }
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) count += __shfl_xor_sync(0xFFFFFFFFu, count, o);
-  if (lane == 0) units[d] = count;
+  if (CLS) mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+  if (lane == 0) {
+    units[d] = count;
+    if (CLS) {
+      const uint32_t c = mx >= 0x10000u ? 2u : mx >= 256u ? 1u : 0u;
+      cls[d] = c;
+      if (c) atomicAdd(cls_cnt, 1u);
+      if (c == 2) atomicAdd(cls_cnt + 1, 1u);
+    }
+  }
 }
 
-// pass 2: the units themselves, at unit_off[d] (exclusive scan of pass 1)
+// pass 2: the units themselves, at unit_off[d] (exclusive scan of pass 1):
+// as u32, or -- cls given -- as u16 (out16) for the documents of class
+// < wide_from and u32 for the others
 __global__ void __launch_bounds__(kWarps * 32)
     k_utf8_decode(const uint8_t* __restrict__ text, const uint64_t* __restrict__ offsets,
-                  uint64_t n, const uint64_t* __restrict__ unit_off, uint32_t* __restrict__ out) {
+                  uint64_t n, const uint64_t* __restrict__ unit_off, uint32_t* __restrict__ out,
+                  const uint32_t* __restrict__ cls, uint32_t wide_from,
+                  uint16_t* __restrict__ out16) {
   const uint64_t d = static_cast<uint64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (d >= n) return;
@@ -243,6 +267,8 @@ __global__ void __launch_bounds__(kWarps * 32)
   const uint32_t* aw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s) & ~uintptr_t{3});
   int64_t pos0 = -static_cast<int64_t>(reinterpret_cast<uintptr_t>(s) & 3);
   uint32_t* o = out + unit_off[d];
+  uint16_t* o16 = out16 ? out16 + unit_off[d] : nullptr;
+  const bool narrow = cls && cls[d] < wide_from;
   const unsigned below = (1u << lane) - 1u;
   uint64_t written = 0;
   uint32_t carry = 0, lcarry = 01111u;
@@ -254,10 +280,17 @@ __global__ void __launch_bounds__(kWarps * 32)
     const unsigned b1 = __ballot_sync(0xFFFFFFFFu, cnt & 2u);
     const unsigned b2 = __ballot_sync(0xFFFFFFFFu, cnt & 4u);
     uint32_t at = __popc(b0 & below) + 2 * __popc(b1 & below) + 4 * __popc(b2 & below);
-    uint32_t* dst = o + written;
+    if (narrow) {
+      uint16_t* dst = o16 + written;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (m & (1u << k)) dst[at++] = cp[k];
+      for (int k = 0; k < 4; ++k)
+        if (m & (1u << k)) dst[at++] = static_cast<uint16_t>(cp[k]);
+    } else {
+      uint32_t* dst = o + written;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (m & (1u << k)) dst[at++] = cp[k];
+    }
     written += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
   }
 }
@@ -267,18 +300,40 @@ __global__ void __launch_bounds__(kWarps * 32)
 void decode_codepoints_device(const uint8_t* d_text, const uint64_t* d_offsets, uint64_t n,
                               DevBuf& units_buf, DevBuf& unit_off_buf, DevBuf& count_buf,
                               DevBuf& scan_tmp, cudaStream_t s, const uint32_t** units_out,
-                              const uint64_t** unit_off_out) {
+                              const uint64_t** unit_off_out, CodepointClasses* classes) {
   uint32_t* cnt = count_buf.as<uint32_t>(n);
   uint64_t* uoff = unit_off_buf.as<uint64_t>(n + 1);
   const unsigned blocks = static_cast<unsigned>((n + kWarps - 1) / kWarps);
-  k_utf8_count<<<blocks, kWarps * 32, 0, s>>>(d_text, d_offsets, n, cnt);
+  uint32_t* cls = nullptr;
+  uint32_t* cls_cnt = nullptr;
+  if (classes) {
+    cls = classes->cls_buf->as<uint32_t>(n);
+    cls_cnt = classes->cnt_buf->as<uint32_t>(4);
+    ND_CUDA(cudaMemsetAsync(cls_cnt, 0, 4 * sizeof(uint32_t), s));
+    k_utf8_count<true><<<blocks, kWarps * 32, 0, s>>>(d_text, d_offsets, n, cnt, cls, cls_cnt);
+  } else {
+    k_utf8_count<false><<<blocks, kWarps * 32, 0, s>>>(d_text, d_offsets, n, cnt, nullptr, nullptr);
+  }
   ND_CHECK_LAUNCH();
   scan_u32_to_u64(cnt, uoff, n, scan_tmp, s);
-  uint64_t total = 0;
-  ND_CUDA(cudaMemcpyAsync(&total, uoff + n, sizeof total, cudaMemcpyDeviceToHost, s));
+  uint64_t h[2] = {0, 0};
+  uint32_t hc[2] = {0, 0};
+  ND_CUDA(cudaMemcpyAsync(&h[0], uoff + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  if (classes) ND_CUDA(cudaMemcpyAsync(hc, cls_cnt, sizeof hc, cudaMemcpyDeviceToHost, s));
   ND_CUDA(cudaStreamSynchronize(s));
+  const uint64_t total = h[0];
   uint32_t* units = units_buf.as<uint32_t>(total + 1);
-  k_utf8_decode<<<blocks, kWarps * 32, 0, s>>>(d_text, d_offsets, n, uoff, units);
+  uint16_t* u16 = nullptr;
+  if (classes) {
+    classes->total = total;
+    classes->n_wide = hc[0];
+    classes->n_astral = hc[1];
+    classes->cls = cls;
+    u16 = classes->u16_buf->as<uint16_t>(total + 16);
+    classes->u16 = u16;
+  }
+  k_utf8_decode<<<blocks, kWarps * 32, 0, s>>>(d_text, d_offsets, n, uoff, units, cls,
+                                                classes ? classes->wide_from : 0u, u16);
   ND_CHECK_LAUNCH();
   *units_out = units;
   *unit_off_out = uoff;

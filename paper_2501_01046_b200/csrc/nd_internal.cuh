@@ -123,12 +123,12 @@ struct SortScratch {
 };
 struct SigScratch {
   DevBuf seg_count, item_off, item_doc, flags, multi_docs, scan_tmp, units, unit_off, unit_cnt,
-      item_counter, order_keys, order_vals, units8, units16, wide;
+      item_counter, order_keys, order_vals, units8, units16, wide, cls_cnt;
   SortScratch sort;  // K1j: items ordered by length
   void release() {
     for (DevBuf* b : {&seg_count, &item_off, &item_doc, &flags, &multi_docs, &scan_tmp, &units,
                       &unit_off, &unit_cnt, &item_counter, &order_keys, &order_vals, &units8,
-                      &units16, &wide})
+                      &units16, &wide, &cls_cnt})
       b->release();
     sort.release();
   }
@@ -156,10 +156,24 @@ void k1_jit_launch(const void* handle, const uint8_t* d_text, const uint64_t* d_
                    unsigned long long* counter, cudaStream_t s, const K1Gate* gate = nullptr);
 // UTF-8 -> codepoint units (k_utf8.cu): units_out[unit_off_out[d] ..
 // unit_off_out[d+1]) are document d's units (decode_codepoints, text.cpp:101-113).
+// Codepoint classes of a decoded batch (k_utf8.cu): per document 0 (all
+// code points < 256), 1 (< 2^16) or 2; the documents of class < wide_from
+// get 16-bit units in u16 (at the same unit offsets), the others u32 units.
+struct CodepointClasses {
+  DevBuf* cls_buf = nullptr;
+  DevBuf* cnt_buf = nullptr;
+  DevBuf* u16_buf = nullptr;
+  uint32_t wide_from = 1;
+  // outputs
+  const uint32_t* cls = nullptr;
+  const uint16_t* u16 = nullptr;
+  uint64_t total = 0;
+  uint32_t n_wide = 0, n_astral = 0;  // documents of class >= 1 / class 2
+};
 void decode_codepoints_device(const uint8_t* d_text, const uint64_t* d_offsets, uint64_t n,
                               DevBuf& units_buf, DevBuf& unit_off_buf, DevBuf& count_buf,
                               DevBuf& scan_tmp, cudaStream_t s, const uint32_t** units_out,
-                              const uint64_t** unit_off_out);
+                              const uint64_t** unit_off_out, CodepointClasses* classes = nullptr);
 // h_offsets: optional host copy of d_offsets; when given, planning happens on
 // the host and the launch is fully asynchronous for single-item documents.
 void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint64_t* d_offsets,
