@@ -141,6 +141,28 @@ __global__ void k_fill_multi(const uint32_t* __restrict__ multi_docs, uint32_t n
   }
 }
 
+// any byte >= 0x80 in text[lo, hi)?  (a codepoint batch of pure ASCII has
+// units == bytes: it runs the byte path on the text as it is)
+__global__ void k_any_high(const uint8_t* __restrict__ text, uint64_t lo, uint64_t hi,
+                           unsigned int* __restrict__ flag) {
+  const uint64_t a = (lo + 15) & ~uint64_t{15}, b = hi & ~uint64_t{15};
+  const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint32_t acc = 0;
+  if (a < b) {
+    const uint4* v = reinterpret_cast<const uint4*>(text + a);
+    for (uint64_t i = tid; i < (b - a) / 16; i += stride) {
+      const uint4 w = __ldg(v + i);
+      acc |= w.x | w.y | w.z | w.w;
+    }
+    for (uint64_t i = lo + tid; i < a; i += stride) acc |= text[i];
+    for (uint64_t i = b + tid; i < hi; i += stride) acc |= text[i];
+  } else {
+    for (uint64_t i = lo + tid; i < hi; i += stride) acc |= text[i];
+  }
+  if (__any_sync(0xFFFFFFFFu, (acc & 0x80808080u) != 0) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 // class-0 codepoint documents (all units < 256) run the byte kernels over
 // their units narrowed to bytes
 __global__ void k_u16_to_u8(const uint16_t* __restrict__ units, uint64_t m,
@@ -922,6 +944,39 @@ void launch_signatures(const DevFamily& fam, const uint8_t* d_bytes, const uint6
   // only the documents whose class lies in [class_lo, class_hi] (codepoint
   // batches: the u16 pass and K1w each take their own documents)
   const uint32_t* wide_mask = doc_class;
+  if (fam.unit == 1 && fam.narrow_ok) {
+    // pure ASCII batch: units are the bytes -- the byte path on the text as it
+    // is (no decode); one pass over the text decides
+    const char* nv = getenv("ND_K1_NARROW");
+    if (!(nv && nv[0] == '0')) {
+      uint64_t ends[2];
+      if (h_offsets) {
+        ends[0] = h_offsets[0];
+        ends[1] = h_offsets[n];
+      } else {
+        ND_CUDA(cudaMemcpyAsync(&ends[0], d_offsets, 8, cudaMemcpyDeviceToHost, s));
+        ND_CUDA(cudaMemcpyAsync(&ends[1], d_offsets + n, 8, cudaMemcpyDeviceToHost, s));
+      }
+      unsigned int* flag = sc.flags.as<unsigned int>(4);
+      ND_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned int), s));
+      ND_CUDA(cudaStreamSynchronize(s));
+      unsigned int high = 1;
+      if (ends[1] > ends[0]) {
+        k_any_high<<<8 * sm_count(), 256, 0, s>>>(d_bytes, ends[0], ends[1], flag);
+        ND_CHECK_LAUNCH();
+        ND_CUDA(cudaMemcpyAsync(&high, flag, sizeof high, cudaMemcpyDeviceToHost, s));
+        ND_CUDA(cudaStreamSynchronize(s));
+      }
+      if (!high) {
+        DevFamily byte_view = fam;
+        byte_view.unit = 0;
+        byte_view.narrow_ok = false;
+        launch_signatures(byte_view, d_bytes, d_offsets, n, bands, rows, K, d_sig, d_band, sc, s,
+                          /*check_short=*/true, h_offsets, gate, doc_class, class_lo, class_hi);
+        return;
+      }
+    }
+  }
   if (fam.unit == 1) {
     // codepoint units: decode, then plan and sign over the u32 unit arrays;
     // unit counts are only known on the device, so the short check runs there

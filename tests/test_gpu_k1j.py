@@ -312,3 +312,35 @@ def test_codepoint_bmp_documents_take_k1j16(ctx, oracle, monkeypatch, L, H, kind
     want = oracle.signatures(data, offs, oracle.derive_family(7, H, L), L=L, unit=1)
     assert np.array_equal(res["1"][0], want)
     assert np.array_equal(res["1"][0], res["0"][0]) and np.array_equal(res["1"][1], res["0"][1])
+
+
+@pytest.mark.parametrize("layout", ["ascii", "ascii_short", "one_high_byte", "small_batch"])
+def test_codepoint_pure_ascii_batch_runs_the_byte_path(ctx, oracle, monkeypatch, layout):
+    """a codepoint batch without a byte >= 0x80 has units == bytes: it runs
+    the byte path on the text as it is (no decode); one byte >= 0x80 anywhere
+    sends the batch through the decode.  Both equal the oracle and the
+    all-K1w path; documents shorter than L still raise ShortDocumentError"""
+    rng = np.random.default_rng(7)
+    texts = ["".join(rng.choice(_ASCII, size=int(k))) for k in rng.integers(5, 4000, size=300)]
+    texts.append("x" * 20000)  # multi-item
+    if layout == "one_high_byte":
+        texts[150] = texts[150][:40] + "\u00e9" + texts[150][40:]
+    if layout == "small_batch":
+        texts = texts[:3]
+    raw = [t.encode() for t in texts]
+    if layout == "ascii_short":
+        raw[7] = b"abc"
+    offs = np.zeros(len(raw) + 1, np.uint64)
+    offs[1:] = np.cumsum([len(b) for b in raw])
+    data = np.frombuffer(b"".join(raw), np.uint8).copy()
+    fam = minhash.derive_family(5, 128, 5, minhash.ShingleUnit.CODEPOINT)
+    if layout == "ascii_short":
+        with pytest.raises(minhash.ShortDocumentError):
+            minhash.signatures_packed(data, offs, fam, 16, 8, 1000, ctx=ctx)
+        return
+    got = minhash.signatures_packed(data, offs, fam, 16, 8, 1000, ctx=ctx)
+    monkeypatch.setenv("ND_K1_NARROW", "0")
+    wide = minhash.signatures_packed(data, offs, fam, 16, 8, 1000, ctx=ctx)
+    monkeypatch.delenv("ND_K1_NARROW")
+    assert np.array_equal(got[0], wide[0]) and np.array_equal(got[1], wide[1])
+    assert np.array_equal(got[0], oracle.signatures(data, offs, oracle.derive_family(5, 128), unit=1))
