@@ -133,9 +133,17 @@ uint64_t h2d_chunk_bytes(const DevFamily& fam, size_t chunk_index) {
     const char* v = getenv("ND_H2D_MAX_MB");  // tuning
     return v ? std::max(1, atoi(v)) : 512;
   }();
+  // growth per chunk in percent (ND_H2D_GROWTH, tuning): a chunk's copy must
+  // land before the kernels of the chunks before it finish
+  static const uint64_t growth = [] {
+    const char* v = getenv("ND_H2D_GROWTH");
+    return static_cast<uint64_t>(v ? std::max(110, std::min(400, atoi(v))) : 200);
+  }();
   constexpr uint64_t kSmall = 64ull << 20;
   if (!fam.jit) return kSmall;
-  return std::min<uint64_t>(max_mb << 20, (first_mb << 20) << std::min<size_t>(chunk_index, 6));
+  uint64_t b = first_mb << 20;
+  for (size_t c = 0; c < chunk_index && b < (max_mb << 20); ++c) b = b * growth / 100;
+  return std::min<uint64_t>(max_mb << 20, b);
 }
 
 // Host-pipelined signatures: chunks of documents are copied in (h2d stream),

@@ -513,12 +513,24 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
       return;
     }
     cudaStream_t s = ctx->stream;
+    // ND_DEDUP_TRACE=1: host milliseconds of the call's phases on stderr
+    const char* tr = getenv("ND_DEDUP_TRACE");
+    const bool trace = tr && tr[0] == '1';
+    const auto h0 = std::chrono::steady_clock::now();
+    auto ms = [&] {
+      return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    };
     EventTimer t(s);
     t.mark();  // 0
+    const double a = ms();
     h2d_signatures(ctx, st, bytes, offsets, n, p.bands, p.rows, st.K,
                    st.sig.as<uint32_t>(n * p.hash_count), st.band.as<uint32_t>(n * p.bands));
+    const double b = ms();
     t.mark();  // 1
     dedup_tail(ctx, st, p, n, stats, t);
+    if (trace)
+      std::fprintf(stderr, "nd_dedup host ms: setup %.2f, enqueue K1 %.2f, tail (waits for K1) %.2f\n",
+                   a, b - a, ms() - b);
   });
 }
 

@@ -55,7 +55,7 @@ def main():
     for spec in args:
         name, _, kv = spec.partition(":")
         envs[name] = dict(x.split("=", 1) for x in kv.split(",") if x)
-    reps = 2
+    reps = int(os.environ.get("PROBE_REPS", "2"))
     res = {k: [] for k in envs}
     for _ in range(reps):
         for name, extra in envs.items():
