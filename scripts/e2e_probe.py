@@ -12,7 +12,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 PROBE = r"""
-import json, os, sys
+import gc, json, os, sys
 import numpy as np, torch
 sys.path.insert(0, os.environ['ROOT'])
 import bench
@@ -39,6 +39,7 @@ def run():
         minhash.signatures_packed(data, op, fam, 16, 8, 2000, ctx=ctx, sig_out=sig, band_out=band)
 for _ in range(3): run()
 torch.cuda.synchronize()
+gc.collect(); gc.freeze(); gc.disable()  # as bench.py
 ts = []
 for _ in range(8):
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
