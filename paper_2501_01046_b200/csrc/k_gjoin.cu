@@ -30,6 +30,7 @@
 // (candidate pairs = sum n(n-1)/2, non-singleton cells, their records,
 // pipeline.cpp:406-411): one histogram over band * K + bucket (k_cell_hist).
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 #include <string>
 
@@ -203,6 +204,27 @@ void gj_fps_launch(const uint32_t* sig, uint64_t n, uint32_t H, uint32_t NB, uin
 
 }  // namespace
 
+// Free device memory for the budget decisions.  cudaMemGetInfo measured
+// 0.1-125 ms per call on B200 (profiles/r2_dedup_e2e_variance.txt), so the
+// value is cached per device and re-queried only when a decision is within a
+// factor of `margin` of the cached limit (a decision far from the limit does
+// not depend on the exact figure; nd_set_hbm_budget overrides the budget).
+uint64_t device_free_bytes(uint64_t need, uint64_t num, uint64_t den) {
+  static std::mutex mu;
+  static uint64_t cached[64] = {};
+  int dev = 0;
+  ND_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  uint64_t& c = cached[dev & 63];
+  // usable = c * num / den; re-query unless need < usable / 2
+  if (c == 0 || need >= c / den * num / 2) {
+    size_t free_b = 0, total_b = 0;
+    ND_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    c = free_b;
+  }
+  return c;
+}
+
 bool global_join_eligible(uint64_t n, uint32_t H, uint32_t B, uint32_t K, uint32_t mm) {
   const char* e = getenv("ND_K3");  // "cells": the per-cell join for every dedup
   if (e && std::string(e) == "cells") return false;
@@ -212,11 +234,9 @@ bool global_join_eligible(uint64_t n, uint32_t H, uint32_t B, uint32_t K, uint32
   if (mm <= H) join_block_shape(H, mm, &NB, &BW);
   if (NB > kGJoinMaxBlocks) return false;
   // fingerprints + links + table must fit next to what is already resident
-  size_t free_b = 0, total_b = 0;
-  ND_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const uint64_t need = n * (4ull * NB + 8) + (uint64_t{8} << std::max(10, bits_for(n))) +
                         4ull * B * K;
-  return need < free_b / 10 * 8;
+  return need < device_free_bytes(need, 8, 10) / 10 * 8;
 }
 
 void gj_cell_hist(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint32_t K,

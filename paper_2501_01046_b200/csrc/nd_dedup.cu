@@ -302,11 +302,11 @@ void dedup_tail(nd_ctx* ctx, DedupState& st, const nd_params& p, uint64_t n, nd_
   }
 }
 
-uint64_t hbm_budget_of(nd_ctx* ctx) {
+// need: the bytes the caller is about to compare against the budget (the
+// free-memory query is skipped when need is far below it)
+uint64_t hbm_budget_of(nd_ctx* ctx, uint64_t need) {
   if (ctx->hbm_budget) return ctx->hbm_budget;
-  size_t fr = 0, tot = 0;
-  ND_CUDA(cudaMemGetInfo(&fr, &tot));
-  return static_cast<uint64_t>(fr) / 10 * 7;
+  return device_free_bytes(need, 7, 10) / 10 * 7;
 }
 
 // Device bytes of the in-memory dedup per document: signature + band ids +
@@ -488,6 +488,13 @@ extern "C" {
 int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const uint64_t* doc_ids,
              uint64_t n, const nd_params* params, nd_dedup_stats* stats) {
   return guarded_impl(ctx, [&] {
+    // ND_DEDUP_TRACE=1: host milliseconds of the call's phases on stderr
+    const char* tr = getenv("ND_DEDUP_TRACE");
+    const bool trace = tr && tr[0] == '1';
+    const auto h0 = std::chrono::steady_clock::now();
+    auto ms = [&] {
+      return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    };
     const nd_params p = *params;
     validate(p);
     if (is_group(ctx)) {  // sharded over the group's devices (nd_multi.cu)
@@ -495,6 +502,7 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
       return;
     }
     ensure_family(ctx, p);
+    const double f_ms = ms();
     DedupState& st = ctx->dedup;
     st.valid = false;
     set_doc_ids(st, doc_ids, n);
@@ -504,8 +512,10 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
     st.host_sig.clear();
     st.host_band.clear();
     st.intervals = 1;
-    const uint64_t budget = hbm_budget_of(ctx);
-    if (n * row_bytes_of(p) + n * p.bands * kRecBytes > budget) {
+    const uint64_t need = n * row_bytes_of(p) + n * p.bands * kRecBytes;
+    const uint64_t budget = hbm_budget_of(ctx, need);
+    const double b_ms = ms();
+    if (need > budget) {
       for (uint64_t i = 0; i < n; ++i)
         if (offsets[i + 1] < offsets[i] || offsets[i + 1] - offsets[i] < p.shingle_len)
           fail(ND_ERR_SHORT, "document " + std::to_string(i) + " has fewer units than the shingle length");
@@ -513,13 +523,6 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
       return;
     }
     cudaStream_t s = ctx->stream;
-    // ND_DEDUP_TRACE=1: host milliseconds of the call's phases on stderr
-    const char* tr = getenv("ND_DEDUP_TRACE");
-    const bool trace = tr && tr[0] == '1';
-    const auto h0 = std::chrono::steady_clock::now();
-    auto ms = [&] {
-      return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-    };
     EventTimer t(s);
     t.mark();  // 0
     const double a = ms();
@@ -529,8 +532,8 @@ int nd_dedup(nd_ctx* ctx, const uint8_t* bytes, const uint64_t* offsets, const u
     t.mark();  // 1
     dedup_tail(ctx, st, p, n, stats, t);
     if (trace)
-      std::fprintf(stderr, "nd_dedup host ms: setup %.2f, enqueue K1 %.2f, tail (waits for K1) %.2f\n",
-                   a, b - a, ms() - b);
+      std::fprintf(stderr, "nd_dedup host ms: family %.2f, budget %.2f, timers %.2f, enqueue K1 %.2f, "
+                   "tail (waits for K1) %.2f\n", f_ms, b_ms - f_ms, a - b_ms, b - a, ms() - b);
   });
 }
 

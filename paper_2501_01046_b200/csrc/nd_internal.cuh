@@ -358,6 +358,9 @@ struct GJoinCounts {
   uint64_t candidate_pairs, ncells, cell_records, emitted;
 };
 bool global_join_eligible(uint64_t n, uint32_t H, uint32_t B, uint32_t K, uint32_t mm);
+// free device memory (cudaMemGetInfo), cached per device; re-queried when
+// `need` is at least half of free * num / den (k_gjoin.cu)
+uint64_t device_free_bytes(uint64_t need, uint64_t num, uint64_t den);
 // reference counters from a histogram of the cells (async, into g.acc_d)
 void gj_cell_counts(GJoin& g, const uint32_t* band, uint64_t n, uint32_t B, uint32_t K,
                     cudaStream_t s);
